@@ -1,0 +1,162 @@
+/*
+ * rsf.h -- C ABI of librsf: Gaussian-process log-likelihood l(theta) and score
+ * g(theta) through the recursive skeletonization factorization (RSF) of
+ * Sigma(theta) and weak-admissibility matrix peeling of Tr(Sigma^-1 Sigma_i),
+ * hand-written FP64 CUDA for sm_100a (B200).
+ *
+ * Citations: "P:n" = line n of the paper's text (arXiv:1603.08057, PAPER.md).
+ *   problem statement   P:14-18 (Eq. normaldist), P:37-39 (Eq. loglikelihood),
+ *                       P:43-47 (Eq. gradient)
+ *   RSF                 P:201-283 (Eq. rskelf), Def. id P:205-210,
+ *                       proxy trick P:299-308, operators P:381-389
+ *   peeling             P:438-595 (Eq. lowrankapprox, levels, extraction)
+ *   Alg. 1
+ * Readings of ambiguous passages (R-*) are listed in DESIGN.md §3.
+ *
+ * Conventions (all functions):
+ *   - every call returns rsf_status; RSF_OK == 0; no C++ exception or exit()
+ *     crosses the ABI.  On error the outputs are unspecified, no handle is
+ *     created, and rsf_last_error() describes the failure (level/box on a
+ *     numerical failure).
+ *   - points: xy is n x 2, row-major (x0,y0,x1,y1,...), FP64, every coordinate
+ *     finite and inside the unit square [0,1]^2 (root box, reading R-S);
+ *     device OR host memory (host buffers are staged by the library).
+ *   - vectors / blocks: column-major n x nrhs with leading dimension ld >= n,
+ *     in the CALLER's original point order (the library applies its Morton
+ *     permutation internally); device or host memory.
+ *   - the caller owns every buffer it passes; the library owns handles and
+ *     their device memory until *_destroy.  Handles are immutable after
+ *     creation; concurrent solve/apply calls on one handle must use the same
+ *     context stream (calls are stream-ordered on it).
+ *   - results are bitwise reproducible for a fixed (input, seed, build, GPU).
+ */
+#ifndef RSF_H_
+#define RSF_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  RSF_OK = 0,
+  RSF_EINVAL = 1,    /* invalid argument (null pointer, n < 1, eps <= 0, leaf < 1, rho/sigma2/alpha <= 0,
+                        nugget < 0, p out of range, point outside [0,1]^2 or non-finite, logdet of a
+                        Sigma_i handle, ...) */
+  RSF_ENUMERIC = 2,  /* Cholesky of a redundant block X_RR or of the top block failed (Remark P:285-287) */
+  RSF_ECUDA = 3,     /* CUDA runtime error */
+  RSF_ENOMEM = 4,    /* device allocation failed */
+  RSF_ENCCL = 5      /* collective failure (multi-GPU) */
+} rsf_status;
+
+/* covariance families: Sigma_jk = sigma2 * k(r_jk) + nugget * [j == k] (index delta, R-H/R-I) */
+typedef enum {
+  RSF_RQ = 0,        /* (1 + r^2/(2 alpha rho^2))^-alpha */
+  RSF_MATERN12 = 1,  /* exp(-r/rho) */
+  RSF_MATERN32 = 2,  /* (1 + sqrt3 r/rho) exp(-sqrt3 r/rho) */
+  RSF_MATERN52 = 3,  /* (1 + s + s^2/3) exp(-s), s = sqrt5 r/rho */
+  RSF_SQEXP = 4      /* exp(-r^2/(2 rho^2)) (alpha -> inf limit; test family) */
+} rsf_family;
+
+/* theta components (order of the gradient is the order given in rsf_kernel.theta) */
+typedef enum { RSF_RHO = 0, RSF_SIGMA2 = 1, RSF_NUGGET = 2, RSF_ALPHA = 3 } rsf_param;
+
+typedef struct {
+  int32_t family;      /* rsf_family */
+  double rho, sigma2, nugget, alpha;   /* current values; alpha used by RSF_RQ only */
+  int32_t p;           /* number of theta components, 0 <= p <= 4 */
+  int32_t theta[4];    /* rsf_param values, distinct; RSF_ALPHA only with RSF_RQ */
+} rsf_kernel;
+
+typedef struct {
+  double eps_peel;     /* peeling tolerance (CPQR truncation of the sketches; R-N). default 1e-6 */
+  int32_t oversample;  /* c of W in R^{n x (r+c)} (R-K). default 8 */
+  int32_t probe_block; /* max columns per G-apply block (memory bound). default 512 */
+  int32_t peel_start;  /* initial probe columns per group at level 1 (adaptive, R-M). default 64 */
+  int32_t max_depth;   /* quadtree depth cap (degenerate leaves). default 30 */
+  double r_near;       /* near radius / box half-width (R-C). default 1.8 */
+  double r_in, r_out;  /* proxy annulus radii / half-width (R-C; 4 rings x 64 angles, n_prox=256). 1.75, 2.45 */
+  uint64_t seed;       /* Philox4x32-10 key of the peeling probes (stream 3). default 1603080570 */
+} rsf_opts;            /* pass NULL for all defaults; rsf_opts_default() fills the defaults */
+
+typedef struct rsf_ctx_s* rsf_ctx;     /* device, stream, optional NCCL communicator */
+typedef struct rsf_fact_s* rsf_fact;   /* an RSF of Sigma, or the apply-only compression of Sigma_i */
+
+typedef struct {
+  int32_t levels;            /* quadtree depth L */
+  int32_t top_size;          /* |I_0| (dense top block) */
+  int32_t level_boxes[32];   /* boxes per level 1..L (index = level) */
+  int32_t level_active[32];  /* sum |I_b| per level */
+  int32_t level_skel[32];    /* sum |S_b| per level */
+  int32_t level_maxI[32];    /* max |I_b| per level */
+  double flops_id, flops_elim, flops_top;   /* algorithmic FP64 flops */
+  double factor_bytes;       /* stored factor bytes (read twice by a 1-RHS solve) */
+  double seconds;            /* wall time of the factorization (device-synchronised) */
+} rsf_fact_diag;
+
+typedef struct {
+  int32_t levels;
+  int32_t cols[32];          /* probe columns per group at level l (index = level), after adaptivity */
+  int32_t rank_max[32];      /* max eps_peel-rank of the sibling blocks at level l */
+  int32_t nL;                /* extraction columns (max leaf size) */
+  double cancellation;       /* sum |diag(H)| / |Tr| (P:597-599 diagnostic) */
+  double applies;            /* operator columns applied (G X column count) */
+  double seconds;
+} rsf_peel_diag;
+
+typedef struct {
+  double logdet, quad;       /* log|F| and z^T F^-1 z */
+  double q[4], trace[4];     /* z^T F^-1 F_i F^-1 z and Tr(F^-1 F_i) per theta component */
+  double t_tree, t_factor, t_compress, t_solve, t_peel, t_total;  /* seconds */
+  double flops_factor;       /* algorithmic flops of all factorizations */
+  double kernel_launches;    /* CUDA kernels launched by the call */
+  rsf_fact_diag fact;        /* the Sigma factor */
+  rsf_peel_diag peel[4];     /* per theta component (sigma2/nugget share the F^-1 peel) */
+} rsf_eval_diag;
+
+void rsf_opts_default(rsf_opts* out);
+
+/* context on CUDA device `device`; cuda_stream may be NULL (library creates a stream);
+ * nccl_comm is reserved (NULL = single GPU). */
+rsf_status rsf_ctx_create(int device, void* cuda_stream, void* nccl_comm, rsf_ctx* out);
+void rsf_ctx_destroy(rsf_ctx ctx);
+
+/* Build F ~ Sigma (which = -1) with ID tolerance eps (Def. id: |R'_jj| <= eps |R'_11| truncation,
+ * reading R-A), leaf capacity `leaf` (n_occ), or (which = i in [0,p)) the apply-only
+ * compression of Sigma_i = dSigma/dtheta_i (reading R-F).  xy: n x 2 (see conventions). */
+rsf_status rsf_factor(rsf_ctx ctx, const double* xy, int64_t n, const rsf_kernel* kernel, int32_t which,
+                      double eps, int32_t leaf, const rsf_opts* opts, rsf_fact* out);
+void rsf_fact_destroy(rsf_fact f);
+rsf_status rsf_fact_info(rsf_fact f, rsf_fact_diag* out);
+
+/* log|F| = 2 log|C| plus the redundant-block terms; Sigma handles only. out: host. */
+rsf_status rsf_logdet(rsf_fact f, double* out);
+/* x = F^-1 b; b and x may alias; Sigma handles only */
+rsf_status rsf_solve(rsf_fact f, const double* b, double* x, int64_t nrhs, int64_t ld);
+/* y = F x; for a Sigma_i handle, y = F_i x */
+rsf_status rsf_apply(rsf_fact f, const double* x, double* y, int64_t nrhs, int64_t ld);
+/* z = F^{1/2} w with F^{1/2} (F^{1/2})^T = F; Sigma handles only */
+rsf_status rsf_sample(rsf_fact f, const double* w, double* z, int64_t nrhs, int64_t ld);
+
+/* Tr(F^-1 F_i) by peeling G = 1/2 (F^-1 F_i + F_i F^-1) (R-Z); Fi == NULL peels G = F^-1.
+ * trace_id selects the probe counter stream. trace: host. diag nullable. */
+rsf_status peel_trace(rsf_fact F, rsf_fact Fi, double eps_peel, const rsf_opts* opts, int32_t trace_id,
+                      double* trace, rsf_peel_diag* diag);
+
+/* Alg. 1: l-hat and g-hat at theta = kernel values.  eps is the ID tolerance of every
+ * factorization (eps_fact), opts->eps_peel the peeling tolerance.  ell: host scalar; grad: host
+ * array of p doubles.  xy, z device or host.  diag nullable. */
+rsf_status gp_mle_eval(rsf_ctx ctx, const double* xy, const double* z, int64_t n, const rsf_kernel* kernel,
+                       double eps, int32_t leaf, const rsf_opts* opts, double* ell, double* grad,
+                       rsf_eval_diag* diag);
+
+/* message of the last failing call on this thread ("" if none) */
+const char* rsf_last_error(void);
+/* number of CUDA kernels launched by this thread so far (diagnostics) */
+int64_t rsf_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RSF_H_ */

@@ -1,0 +1,200 @@
+"""B200-native GP likelihood engine: l(theta), g(theta) via RSF + weak peeling.
+
+Thin Python binding over librsf.so (include/rsf.h).  Every step of the path
+runs in the CUDA library; this module only marshals arguments.  Arrays may be
+torch tensors (CUDA or CPU) or numpy arrays (host); they must be float64 and
+contiguous.  PyTorch is used only for device memory and streams.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+from . import _lib
+from ._lib import FAMILY, PARAM, rsf_eval_diag, rsf_fact_diag, rsf_kernel, rsf_opts, rsf_peel_diag
+
+__all__ = ["Context", "Kernel", "Opts", "Factor", "peel_trace", "gp_mle_eval", "RsfError", "lib",
+           "kernel_launches"]
+
+lib = _lib.load()
+
+
+class RsfError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"rsf status {code}: {msg}")
+        self.code = code
+
+
+def _check(st):
+    if st != 0:
+        raise RsfError(st, lib.rsf_last_error().decode())
+
+
+def kernel_launches() -> int:
+    return int(lib.rsf_kernel_launches())
+
+
+def _ptr(a, dtype_ok=True):
+    """(address, keepalive) of a float64 contiguous torch tensor or numpy array."""
+    try:
+        import torch
+        if isinstance(a, torch.Tensor):
+            if a.dtype != torch.float64 or not a.is_contiguous():
+                raise TypeError("tensors must be contiguous float64")
+            return a.data_ptr(), a
+    except ImportError:  # pragma: no cover
+        pass
+    import numpy as np
+    if isinstance(a, np.ndarray):
+        if a.dtype != np.float64 or not a.flags["C_CONTIGUOUS"]:
+            raise TypeError("arrays must be C-contiguous float64")
+        return a.ctypes.data, a
+    raise TypeError(f"unsupported array type {type(a)}")
+
+
+@dataclass
+class Kernel:
+    family: str
+    rho: float
+    sigma2: float = 1.0
+    nugget: float = 0.0
+    alpha: float = 1.0
+    theta: tuple = ("rho",)
+
+    def c(self) -> rsf_kernel:
+        k = rsf_kernel()
+        k.family = FAMILY[self.family]
+        k.rho, k.sigma2, k.nugget, k.alpha = self.rho, self.sigma2, self.nugget, self.alpha
+        k.p = len(self.theta)
+        for i, t in enumerate(self.theta):
+            k.theta[i] = PARAM[t]
+        return k
+
+
+@dataclass
+class Opts:
+    eps_peel: float = 1e-6
+    oversample: int = 8
+    probe_block: int = 512
+    peel_start: int = 64
+    max_depth: int = 30
+    r_near: float = 1.8
+    r_in: float = 1.75
+    r_out: float = 2.45
+    seed: int = 1603080570
+
+    def c(self) -> rsf_opts:
+        o = rsf_opts()
+        for f, _ in rsf_opts._fields_:
+            setattr(o, f, getattr(self, f))
+        return o
+
+
+class Context:
+    def __init__(self, device: int = 0, stream=None):
+        h = C.c_void_p()
+        s = None
+        if stream is not None:
+            s = C.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+        _check(lib.rsf_ctx_create(device, s, None, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            lib.rsf_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Factor:
+    """rsf_factor: which=None -> F ~ Sigma; which=i -> apply-only compression of Sigma_i."""
+
+    def __init__(self, ctx: Context, xy, kernel: Kernel, eps: float, leaf: int = 64,
+                 which: int | None = None, opts: Opts | None = None):
+        p, keep = _ptr(xy)
+        n = (xy.shape[0])
+        h = C.c_void_p()
+        kc = kernel.c()
+        oc = (opts or Opts()).c()
+        _check(lib.rsf_factor(ctx.h, p, n, C.byref(kc), -1 if which is None else which, eps, leaf,
+                              C.byref(oc), C.byref(h)))
+        self.h, self.ctx, self.n, self.which = h, ctx, n, which
+
+    def close(self):
+        if self.h:
+            lib.rsf_fact_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def logdet(self) -> float:
+        v = C.c_double()
+        _check(lib.rsf_logdet(self.h, C.byref(v)))
+        return v.value
+
+    def info(self) -> rsf_fact_diag:
+        d = rsf_fact_diag()
+        _check(lib.rsf_fact_info(self.h, C.byref(d)))
+        return d
+
+    def _op(self, fn, b, out):
+        pb, kb = _ptr(b)
+        po, ko = _ptr(out)
+        nrhs = 1 if b.ndim == 1 else b.shape[0]
+        # (nrhs, n) row-major == column-major n x nrhs with ld = n
+        _check(fn(self.h, pb, po, nrhs, self.n))
+        return out
+
+    def solve(self, b, out=None):
+        """x = F^-1 b; b is (n,) or (nrhs, n) (each row a right-hand side)."""
+        out = b.clone() if out is None and hasattr(b, "clone") else (b.copy() if out is None else out)
+        return self._op(lib.rsf_solve, b, out)
+
+    def apply(self, x, out=None):
+        out = x.clone() if out is None and hasattr(x, "clone") else (x.copy() if out is None else out)
+        return self._op(lib.rsf_apply, x, out)
+
+    def sample(self, w, out=None):
+        out = w.clone() if out is None and hasattr(w, "clone") else (w.copy() if out is None else out)
+        return self._op(lib.rsf_sample, w, out)
+
+
+def peel_trace(F: Factor, Fi: Factor | None, eps_peel: float = 1e-6, opts: Opts | None = None,
+               trace_id: int = 0):
+    v = C.c_double()
+    d = rsf_peel_diag()
+    oc = (opts or Opts()).c()
+    _check(lib.peel_trace(F.h, Fi.h if Fi is not None else None, eps_peel, C.byref(oc), trace_id,
+                          C.byref(v), C.byref(d)))
+    return v.value, d
+
+
+@dataclass
+class EvalResult:
+    ell: float
+    grad: list
+    diag: rsf_eval_diag = field(repr=False)
+
+
+def gp_mle_eval(ctx: Context, xy, z, kernel: Kernel, eps: float, leaf: int = 64,
+                opts: Opts | None = None) -> EvalResult:
+    px, kx = _ptr(xy)
+    pz, kz = _ptr(z)
+    n = xy.shape[0]
+    kc = kernel.c()
+    oc = (opts or Opts()).c()
+    ell = C.c_double()
+    grad = (C.c_double * 4)()
+    d = rsf_eval_diag()
+    _check(lib.gp_mle_eval(ctx.h, px, pz, n, C.byref(kc), eps, leaf, C.byref(oc), C.byref(ell), grad,
+                           C.byref(d)))
+    return EvalResult(ell.value, [grad[i] for i in range(len(kernel.theta))], d)

@@ -1,0 +1,333 @@
+// C ABI of librsf (include/rsf.h): argument checking, host/device staging,
+// exception -> status translation.
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+#include "../../include/rsf.h"
+#include "peel.cuh"
+#include "rsf_impl.cuh"
+
+struct rsf_ctx_s {
+  rsf::Ctx ctx;
+};
+struct rsf_fact_s {
+  std::unique_ptr<rsf::Fact> F;
+  rsf_ctx_s* owner = nullptr;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+rsf_status fail(int code, const std::string& msg) {
+  g_err = msg;
+  return (rsf_status)code;
+}
+
+template <class Fn>
+rsf_status guard(Fn&& fn) {
+  try {
+    g_err.clear();
+    fn();
+    return RSF_OK;
+  } catch (const rsf::Error& e) {
+    return fail(e.code, e.what());
+  } catch (const std::bad_alloc&) {
+    return fail(RSF_ENOMEM, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(RSF_ECUDA, e.what());
+  }
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+rsf::Opts make_opts(const rsf_opts* o) {
+  rsf::Opts r;
+  if (!o) return r;
+  if (o->eps_peel > 0) r.eps_peel = o->eps_peel;
+  if (o->oversample > 0) r.oversample = o->oversample;
+  if (o->probe_block > 0) r.probe_block = o->probe_block;
+  if (o->peel_start > 0) r.peel_start = o->peel_start;
+  if (o->max_depth > 0) r.max_depth = o->max_depth;
+  if (o->r_near > 0) r.r_near = o->r_near;
+  if (o->r_in > 0) r.r_in = o->r_in;
+  if (o->r_out > 0) r.r_out = o->r_out;
+  r.seed = o->seed;
+  return r;
+}
+
+rsf::KParams check_kernel(const rsf_kernel* k) {
+  RSF_REQUIRE(k != nullptr, rsf::ST_EINVAL, "kernel is NULL");
+  RSF_REQUIRE(k->family >= 0 && k->family <= 4, rsf::ST_EINVAL, "unknown kernel family");
+  RSF_REQUIRE(std::isfinite(k->rho) && k->rho > 0, rsf::ST_EINVAL, "rho must be > 0");
+  RSF_REQUIRE(std::isfinite(k->sigma2) && k->sigma2 > 0, rsf::ST_EINVAL, "sigma2 must be > 0");
+  RSF_REQUIRE(std::isfinite(k->nugget) && k->nugget >= 0, rsf::ST_EINVAL, "nugget must be >= 0");
+  RSF_REQUIRE(std::isfinite(k->alpha) && (k->family != rsf::FAM_RQ || k->alpha > 0), rsf::ST_EINVAL,
+              "alpha must be > 0");
+  RSF_REQUIRE(k->p >= 0 && k->p <= 4, rsf::ST_EINVAL, "p out of range");
+  for (int i = 0; i < k->p; ++i) {
+    RSF_REQUIRE(k->theta[i] >= 0 && k->theta[i] <= 3, rsf::ST_EINVAL, "unknown theta component");
+    RSF_REQUIRE(k->theta[i] != RSF_ALPHA || k->family == RSF_RQ, rsf::ST_EINVAL, "alpha is an RQ parameter");
+    for (int j = 0; j < i; ++j) RSF_REQUIRE(k->theta[i] != k->theta[j], rsf::ST_EINVAL, "repeated theta component");
+  }
+  return rsf::KParams{k->family, k->rho, k->sigma2, k->nugget, k->alpha};
+}
+
+// device copy of a (possibly host) n x 2 point array
+const double* stage_points(rsf::Ctx& c, const double* xy, int64_t n, rsf::DBuf<double>& keep) {
+  if (is_device_ptr(xy)) return xy;
+  keep.alloc(2 * n, c.stream);
+  keep.upload(xy, 2 * n);
+  return keep.p;
+}
+
+// run op on X' chunks of at most kmax columns; in/out in caller layout
+template <class Op>
+void blocked_op(const rsf::Fact& F, const double* in, double* out, int64_t nrhs, int64_t ld, Op op) {
+  rsf::Ctx& c = *F.ctx;
+  cudaStream_t s = c.stream;
+  const int n = F.n();
+  RSF_REQUIRE(in && out, rsf::ST_EINVAL, "null vector");
+  RSF_REQUIRE(nrhs >= 0, rsf::ST_EINVAL, "nrhs < 0");
+  RSF_REQUIRE(ld >= n, rsf::ST_EINVAL, "ld < n");
+  if (nrhs == 0) return;
+  const bool din = is_device_ptr(in), dout = is_device_ptr(out);
+  const int kmax = 256;
+  for (int64_t j0 = 0; j0 < nrhs; j0 += kmax) {
+    const int k = (int)std::min<int64_t>(kmax, nrhs - j0);
+    rsf::DBuf<double> stage;
+    const double* src = in + j0 * ld;
+    long long lds = ld;
+    if (!din) {
+      stage.alloc((size_t)n * k, s);
+      for (int j = 0; j < k; ++j)
+        RSF_CUDA(cudaMemcpyAsync(stage.p + (size_t)j * n, src + j * ld, n * sizeof(double), cudaMemcpyHostToDevice, s));
+      src = stage.p;
+      lds = n;
+    }
+    rsf::DBuf<double> X((size_t)n * k, s);
+    rsf::to_internal(s, *F.tree, src, lds, k, X.p);
+    op(X.p, k);
+    if (dout) {
+      rsf::to_external(s, *F.tree, X.p, k, out + j0 * ld, ld);
+    } else {
+      rsf::DBuf<double> o((size_t)n * k, s);
+      rsf::to_external(s, *F.tree, X.p, k, o.p, n);
+      for (int j = 0; j < k; ++j)
+        RSF_CUDA(cudaMemcpyAsync(out + (j0 + j) * ld, o.p + (size_t)j * n, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+      RSF_CUDA(cudaStreamSynchronize(s));
+    }
+  }
+  RSF_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace
+
+extern "C" {
+
+void rsf_opts_default(rsf_opts* o) {
+  if (!o) return;
+  rsf::Opts d;
+  o->eps_peel = d.eps_peel;
+  o->oversample = d.oversample;
+  o->probe_block = d.probe_block;
+  o->peel_start = d.peel_start;
+  o->max_depth = d.max_depth;
+  o->r_near = d.r_near;
+  o->r_in = d.r_in;
+  o->r_out = d.r_out;
+  o->seed = d.seed;
+}
+
+rsf_status rsf_ctx_create(int device, void* cuda_stream, void* nccl_comm, rsf_ctx* out) {
+  return guard([&] {
+    RSF_REQUIRE(out != nullptr, rsf::ST_EINVAL, "out is NULL");
+    int ndev = 0;
+    RSF_CUDA(cudaGetDeviceCount(&ndev));
+    RSF_REQUIRE(device >= 0 && device < ndev, rsf::ST_EINVAL, "no such CUDA device");
+    RSF_CUDA(cudaSetDevice(device));
+    auto* c = new rsf_ctx_s;
+    c->ctx.device = device;
+    c->ctx.nccl = nccl_comm;
+    if (cuda_stream) {
+      c->ctx.stream = (cudaStream_t)cuda_stream;
+    } else {
+      RSF_CUDA(cudaStreamCreateWithFlags(&c->ctx.stream, cudaStreamNonBlocking));
+      c->ctx.own_stream = true;
+    }
+    // keep freed device blocks cached in the stream-ordered pool across evaluations
+    cudaMemPool_t pool;
+    RSF_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = UINT64_MAX;
+    RSF_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    *out = c;
+  });
+}
+
+void rsf_ctx_destroy(rsf_ctx ctx) {
+  if (!ctx) return;
+  cudaStreamSynchronize(ctx->ctx.stream);
+  if (ctx->ctx.own_stream) cudaStreamDestroy(ctx->ctx.stream);
+  delete ctx;
+}
+
+rsf_status rsf_factor(rsf_ctx ctx, const double* xy, int64_t n, const rsf_kernel* kernel, int32_t which,
+                      double eps, int32_t leaf, const rsf_opts* opts, rsf_fact* out) {
+  return guard([&] {
+    RSF_REQUIRE(ctx && xy && out, rsf::ST_EINVAL, "null argument");
+    RSF_REQUIRE(n >= 1 && n < (1ll << 31), rsf::ST_EINVAL, "n out of range");
+    RSF_REQUIRE(eps > 0 && std::isfinite(eps), rsf::ST_EINVAL, "eps must be > 0");
+    RSF_REQUIRE(leaf >= 1, rsf::ST_EINVAL, "leaf must be >= 1");
+    rsf::KParams kp = check_kernel(kernel);
+    int w = rsf::W_SIGMA;
+    if (which >= 0) {
+      RSF_REQUIRE(which < kernel->p, rsf::ST_EINVAL, "which out of range");
+      w = kernel->theta[which];
+    } else {
+      RSF_REQUIRE(which == -1, rsf::ST_EINVAL, "which must be -1 or a theta index");
+    }
+    RSF_CUDA(cudaSetDevice(ctx->ctx.device));
+    rsf::Opts o = make_opts(opts);
+    rsf::DBuf<double> keep;
+    const double* dxy = stage_points(ctx->ctx, xy, n, keep);
+    auto tree = rsf::build_tree(ctx->ctx, dxy, (int)n, leaf, o.max_depth);
+    auto F = rsf::factor(ctx->ctx, tree, kp, w, eps, o);
+    auto* h = new rsf_fact_s;
+    h->F = std::move(F);
+    h->owner = ctx;
+    *out = h;
+  });
+}
+
+void rsf_fact_destroy(rsf_fact f) {
+  if (!f) return;
+  cudaStreamSynchronize(f->owner->ctx.stream);
+  delete f;
+}
+
+rsf_status rsf_fact_info(rsf_fact f, rsf_fact_diag* out) {
+  return guard([&] {
+    RSF_REQUIRE(f && out, rsf::ST_EINVAL, "null argument");
+    std::memset(out, 0, sizeof(*out));
+    const rsf::Fact& F = *f->F;
+    out->levels = F.tree->L;
+    out->top_size = F.n0;
+    const auto& d = F.diag;
+    for (size_t i = 0; i < d.level_boxes.size() && i < 32; ++i) {
+      int lev = F.tree->L - (int)i;   // recorded from L down to 1
+      if (lev < 0 || lev >= 32) continue;
+      out->level_boxes[lev] = d.level_boxes[i];
+      out->level_active[lev] = d.level_I[i];
+      out->level_skel[lev] = d.level_S[i];
+      out->level_maxI[lev] = d.level_maxI[i];
+    }
+    out->flops_id = d.flops_id;
+    out->flops_elim = d.flops_elim;
+    out->flops_top = d.flops_top;
+    out->factor_bytes = d.bytes_factor;
+    out->seconds = d.t_factor;
+  });
+}
+
+rsf_status rsf_logdet(rsf_fact f, double* out) {
+  return guard([&] {
+    RSF_REQUIRE(f && out, rsf::ST_EINVAL, "null argument");
+    RSF_REQUIRE(f->F->which == rsf::W_SIGMA, rsf::ST_EINVAL, "logdet of a Sigma_i handle");
+    *out = f->F->logdet;
+  });
+}
+
+rsf_status rsf_solve(rsf_fact f, const double* b, double* x, int64_t nrhs, int64_t ld) {
+  return guard([&] {
+    RSF_REQUIRE(f, rsf::ST_EINVAL, "null handle");
+    RSF_REQUIRE(f->F->which == rsf::W_SIGMA, rsf::ST_EINVAL, "solve with a Sigma_i handle");
+    RSF_CUDA(cudaSetDevice(f->owner->ctx.device));
+    const rsf::Fact& F = *f->F;
+    blocked_op(F, b, x, nrhs, ld, [&](double* X, int k) {
+      rsf::DBuf<double> tmp((size_t)std::max<long long>(F.tmp_cols, 1) * k, F.ctx->stream);
+      rsf::solve_internal(F, X, k, tmp.p);
+    });
+  });
+}
+
+rsf_status rsf_apply(rsf_fact f, const double* x, double* y, int64_t nrhs, int64_t ld) {
+  return guard([&] {
+    RSF_REQUIRE(f, rsf::ST_EINVAL, "null handle");
+    RSF_CUDA(cudaSetDevice(f->owner->ctx.device));
+    const rsf::Fact& F = *f->F;
+    blocked_op(F, x, y, nrhs, ld, [&](double* X, int k) {
+      cudaStream_t s = F.ctx->stream;
+      if (F.which == rsf::W_SIGMA) {
+        rsf::DBuf<double> tmp((size_t)std::max<long long>(F.tmp_cols, 1) * k, s);
+        rsf::apply_internal(F, X, k, tmp.p);
+      } else {
+        rsf::DBuf<double> Y((size_t)F.n() * k, s);
+        rsf::apply_only_internal(F, X, Y.p, k);
+        RSF_CUDA(cudaMemcpyAsync(X, Y.p, (size_t)F.n() * k * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      }
+    });
+  });
+}
+
+rsf_status rsf_sample(rsf_fact f, const double* w, double* z, int64_t nrhs, int64_t ld) {
+  return guard([&] {
+    RSF_REQUIRE(f, rsf::ST_EINVAL, "null handle");
+    RSF_REQUIRE(f->F->which == rsf::W_SIGMA, rsf::ST_EINVAL, "sample with a Sigma_i handle");
+    RSF_CUDA(cudaSetDevice(f->owner->ctx.device));
+    const rsf::Fact& F = *f->F;
+    blocked_op(F, w, z, nrhs, ld, [&](double* X, int k) {
+      rsf::DBuf<double> tmp((size_t)std::max<long long>(F.tmp_cols, 1) * k, F.ctx->stream);
+      rsf::sqrt_internal(F, X, k, tmp.p);
+    });
+  });
+}
+
+rsf_status peel_trace(rsf_fact F, rsf_fact Fi, double eps_peel, const rsf_opts* opts, int32_t trace_id,
+                      double* trace, rsf_peel_diag* diag) {
+  return guard([&] {
+    RSF_REQUIRE(F && trace, rsf::ST_EINVAL, "null argument");
+    RSF_REQUIRE(F->F->which == rsf::W_SIGMA, rsf::ST_EINVAL, "F must be a Sigma factor");
+    RSF_REQUIRE(!Fi || Fi->F->which != rsf::W_SIGMA, rsf::ST_EINVAL, "Fi must be a Sigma_i compression");
+    RSF_REQUIRE(!Fi || Fi->F->n() == F->F->n(), rsf::ST_EINVAL, "dimension mismatch");
+    RSF_REQUIRE(eps_peel > 0, rsf::ST_EINVAL, "eps_peel must be > 0");
+    RSF_CUDA(cudaSetDevice(F->owner->ctx.device));
+    rsf::Opts o = opts ? make_opts(opts) : F->F->opts;
+    o.eps_peel = eps_peel;
+    rsf::PeelDiag pd;
+    *trace = rsf::peel(*F->F, Fi ? Fi->F.get() : nullptr, o, trace_id, &pd);
+    if (diag) rsf::fill_peel_diag(pd, diag);
+  });
+}
+
+rsf_status gp_mle_eval(rsf_ctx ctx, const double* xy, const double* z, int64_t n, const rsf_kernel* kernel,
+                       double eps, int32_t leaf, const rsf_opts* opts, double* ell, double* grad,
+                       rsf_eval_diag* diag) {
+  return guard([&] {
+    RSF_REQUIRE(ctx && xy && z && ell, rsf::ST_EINVAL, "null argument");
+    RSF_REQUIRE(n >= 1 && n < (1ll << 31), rsf::ST_EINVAL, "n out of range");
+    RSF_REQUIRE(eps > 0 && std::isfinite(eps), rsf::ST_EINVAL, "eps must be > 0");
+    RSF_REQUIRE(leaf >= 1, rsf::ST_EINVAL, "leaf must be >= 1");
+    rsf::KParams kp = check_kernel(kernel);
+    RSF_REQUIRE(kernel->p == 0 || grad != nullptr, rsf::ST_EINVAL, "grad is NULL");
+    RSF_CUDA(cudaSetDevice(ctx->ctx.device));
+    rsf::Opts o = make_opts(opts);
+    rsf::EvalResult r = rsf::mle_eval(ctx->ctx, xy, z, (int)n, kp, kernel->p, kernel->theta, eps, leaf, o);
+    *ell = r.ell;
+    for (int i = 0; i < kernel->p; ++i) grad[i] = r.grad[i];
+    if (diag) rsf::fill_eval_diag(r, diag);
+  });
+}
+
+const char* rsf_last_error(void) { return g_err.c_str(); }
+
+int64_t rsf_kernel_launches(void) { return rsf::g_launches; }
+
+}  // extern "C"

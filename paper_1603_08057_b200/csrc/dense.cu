@@ -1,0 +1,732 @@
+// Batched dense FP64 factorizations (see dense.cuh).
+#include <algorithm>
+
+#include "dense.cuh"
+
+namespace rsf {
+
+namespace {
+
+constexpr int NT = 256;
+constexpr size_t SMEM_BUDGET = 200 * 1024;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// block-wide sum; sh must hold >= 32 doubles; all threads get the result
+__device__ double block_sum(double v, double* sh) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  double r = (threadIdx.x < (blockDim.x >> 5)) ? sh[threadIdx.x] : 0.0;
+  if (w == 0) r = warp_sum(r);
+  if (threadIdx.x == 0) sh[0] = r;
+  __syncthreads();
+  return sh[0];
+}
+
+// LAPACK dlarfg-style reflector: given alpha = x0 and sigma = ||x(1:)||^2,
+// H = I - tau v v^T with v0 = 1 maps x to beta e1.
+__device__ __forceinline__ void householder(double alpha, double sigma, double& tau, double& beta,
+                                            double& scale) {
+  if (sigma == 0.0) {
+    tau = 0.0; beta = alpha; scale = 0.0;
+    return;
+  }
+  double mu = sqrt(alpha * alpha + sigma);
+  beta = (alpha >= 0.0) ? -mu : mu;
+  tau = (beta - alpha) / beta;
+  scale = 1.0 / (alpha - beta);
+}
+
+// ------------------------------------------------------------------ QR panel
+struct PanelDesc {
+  double* A;       // points at A(j0, j0)
+  long long lda;
+  int rows, ncol;  // rows = m - j0, ncol = panel width
+  double* V;       // explicit unit-lower V, rows x ncol, ld = rows
+  double* T;       // ncol x ncol, ld = QR_NB
+  double* tau;     // ncol (may be null)
+  int smem;        // panel staged in shared memory
+};
+
+__global__ void __launch_bounds__(NT) qr_panel_kernel(const PanelDesc* __restrict__ descs) {
+  extern __shared__ double sm[];
+  const PanelDesc d = descs[blockIdx.x];
+  double* red = sm;                 // 32
+  double* scal = sm + 32;           // 8
+  double* taus = sm + 40;           // QR_NB
+  double* G = taus + QR_NB;         // QR_NB * QR_NB
+  double* Ts = G + QR_NB * QR_NB;   // QR_NB * QR_NB
+  double* pan = Ts + QR_NB * QR_NB;
+  const int rows = d.rows, ncol = d.ncol;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  double* P;
+  long long ldp;
+  if (d.smem) {
+    P = pan;
+    ldp = rows;
+    for (long long e = tid; e < (long long)rows * ncol; e += NT) {
+      int r = (int)(e % rows), c = (int)(e / rows);
+      P[e] = d.A[c * d.lda + r];
+    }
+    __syncthreads();
+  } else {
+    P = d.A;
+    ldp = d.lda;
+  }
+  for (int jj = 0; jj < ncol; ++jj) {
+    const int len = rows - jj;
+    double* x = P + jj * ldp + jj;
+    double s = 0.0;
+    for (int r = 1 + tid; r < len; r += NT) s += x[r] * x[r];
+    s = block_sum(s, red);
+    if (tid == 0) {
+      double tau, beta, scale;
+      householder(len > 0 ? x[0] : 0.0, s, tau, beta, scale);
+      scal[0] = tau; scal[1] = beta; scal[2] = scale;
+      taus[jj] = tau;
+    }
+    __syncthreads();
+    const double tau = scal[0], scale = scal[2];
+    if (tau != 0.0)
+      for (int r = 1 + tid; r < len; r += NT) x[r] *= scale;
+    __syncthreads();
+    if (tid == 0 && len > 0) x[0] = scal[1];
+    // apply H to the remaining panel columns
+    if (tau != 0.0) {
+      for (int col = jj + 1 + warp; col < ncol; col += NT / 32) {
+        double* y = P + col * ldp + jj;
+        double dot = 0.0;
+        for (int r = 1 + lane; r < len; r += 32) dot += x[r] * y[r];
+        dot = warp_sum(dot);
+        dot += y[0];
+        const double w = tau * dot;
+        for (int r = 1 + lane; r < len; r += 32) y[r] -= w * x[r];
+        __syncwarp();
+        if (lane == 0) y[0] -= w;
+      }
+    }
+    __syncthreads();
+  }
+  if (d.smem) {
+    for (long long e = tid; e < (long long)rows * ncol; e += NT) {
+      int r = (int)(e % rows), c = (int)(e / rows);
+      d.A[c * d.lda + r] = P[e];
+    }
+  }
+  // explicit V
+  for (long long e = tid; e < (long long)rows * ncol; e += NT) {
+    int r = (int)(e % rows), c = (int)(e / rows);
+    d.V[e] = (r < c) ? 0.0 : (r == c ? 1.0 : P[c * ldp + r]);
+  }
+  // G(l, i) = v_l . v_i for l < i
+  const int npair = ncol * (ncol - 1) / 2;
+  for (int pidx = warp; pidx < npair; pidx += NT / 32) {
+    // decode pair (l, i), l < i
+    int i = 1, acc = 0;
+    while (acc + i <= pidx) { acc += i; ++i; }
+    int l = pidx - acc;
+    const double* vl = P + l * ldp;
+    const double* vi = P + i * ldp;
+    double dot = 0.0;
+    for (int r = i + 1 + lane; r < rows; r += 32) dot += vl[r] * vi[r];
+    dot = warp_sum(dot);
+    if (lane == 0) G[l * QR_NB + i] = dot + vl[i];
+  }
+  __syncthreads();
+  // T (forward, columnwise): T(i,i) = tau_i; T(0:i,i) = -tau_i T(0:i,0:i) G(0:i,i)
+  if (warp == 0) {
+    for (int i = 0; i < ncol; ++i) {
+      double v = 0.0;
+      if (lane < i) {
+        for (int l2 = lane; l2 < i; ++l2) v += Ts[lane + l2 * QR_NB] * G[l2 * QR_NB + i];
+      }
+      __syncwarp();
+      if (lane < i) Ts[lane + i * QR_NB] = -taus[i] * v;
+      for (int r = i + 1 + lane; r < QR_NB; r += 32) Ts[r + i * QR_NB] = 0.0;
+      if (lane == 0) Ts[i + i * QR_NB] = taus[i];
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < QR_NB * QR_NB; e += NT) {
+    int r = e % QR_NB, c = e / QR_NB;
+    d.T[e] = (r < ncol && c < ncol) ? Ts[e] : 0.0;
+  }
+  if (d.tau)
+    for (int e = tid; e < ncol; e += NT) d.tau[e] = taus[e];
+}
+
+// explicit V for an already-factored panel (ormqr)
+struct VDesc { const double* A; long long lda; int rows, ncol; double* V; };
+__global__ void build_v_kernel(const VDesc* __restrict__ descs) {
+  const VDesc d = descs[blockIdx.y];
+  for (long long e = blockIdx.x * (long long)NT + threadIdx.x; e < (long long)d.rows * d.ncol;
+       e += (long long)gridDim.x * NT) {
+    int r = (int)(e % d.rows), c = (int)(e / d.rows);
+    d.V[e] = (r < c) ? 0.0 : (r == c ? 1.0 : d.A[c * d.lda + r]);
+  }
+}
+
+// ------------------------------------------------------------------ CPQR + T
+struct CPQRDesc {
+  const double* R; long long ldr; int q, c;
+  double* W; long long ldw; int smem;
+  double* T; int* piv; int* kout;
+  double* Rout; double* tau;
+  double eps; int want_T;
+};
+
+__global__ void __launch_bounds__(NT) cpqr_kernel(const CPQRDesc* __restrict__ descs) {
+  extern __shared__ double sm[];
+  const CPQRDesc d = descs[blockIdx.x];
+  const int q = d.q, c = d.c;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  double* red = sm;          // 64
+  double* scal = sm + 64;    // 8
+  double* nrm = sm + 72;     // c
+  int* ipiv = reinterpret_cast<int*>(nrm + c);   // c ints
+  int* redi = ipiv + c;                           // 32 ints
+  size_t off = 72 + c + ((size_t)c + 32 + 1) / 2 + 1;
+  double* W = d.smem ? (sm + off) : d.W;
+  const long long ldw = d.smem ? q : d.ldw;
+  double* taus = d.tau;
+
+  for (long long e = tid; e < (long long)q * c; e += NT) {
+    int i = (int)(e % q), j = (int)(e / q);
+    W[j * ldw + i] = (i <= j) ? d.R[j * d.ldr + i] : 0.0;
+  }
+  for (int j = tid; j < c; j += NT) ipiv[j] = j;
+  __syncthreads();
+  for (int j = warp; j < c; j += NT / 32) {
+    double s = 0.0;
+    for (int i = lane; i < q; i += 32) { double v = W[j * ldw + i]; s += v * v; }
+    s = warp_sum(s);
+    if (lane == 0) nrm[j] = s;
+  }
+  __syncthreads();
+  const int kmax = min(q, c);
+  double ref = 0.0;
+  int k = 0;
+  for (int i = 0; i < kmax; ++i) {
+    // argmax over nrm[i..c), lowest position on ties
+    double bv = -1.0;
+    int bi = c;
+    for (int j = i + tid; j < c; j += NT) {
+      double v = nrm[j];
+      if (v > bv) { bv = v; bi = j; }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    __syncthreads();
+    if (lane == 0) { red[warp] = bv; redi[warp] = bi; }
+    __syncthreads();
+    if (tid == 0) {
+      double v = red[0]; int b = redi[0];
+      for (int w = 1; w < NT / 32; ++w)
+        if (red[w] > v || (red[w] == v && redi[w] < b)) { v = red[w]; b = redi[w]; }
+      scal[0] = v;
+      redi[0] = b;
+    }
+    __syncthreads();
+    const double nr = sqrt(fmax(scal[0], 0.0));
+    const int p = redi[0];
+    if (i == 0) ref = nr;
+    if (!(ref > 0.0) || !(nr > d.eps * ref)) break;
+    if (p != i) {
+      for (int r = tid; r < q; r += NT) {
+        double t = W[i * ldw + r]; W[i * ldw + r] = W[p * ldw + r]; W[p * ldw + r] = t;
+      }
+      if (tid == 0) {
+        double t = nrm[i]; nrm[i] = nrm[p]; nrm[p] = t;
+        int ti = ipiv[i]; ipiv[i] = ipiv[p]; ipiv[p] = ti;
+      }
+      __syncthreads();
+    }
+    double* x = W + i * ldw + i;
+    const int len = q - i;
+    double s = 0.0;
+    for (int r = 1 + tid; r < len; r += NT) s += x[r] * x[r];
+    s = block_sum(s, red);
+    if (tid == 0) {
+      double tau, beta, scale;
+      householder(x[0], s, tau, beta, scale);
+      scal[2] = tau; scal[3] = beta; scal[4] = scale;
+      if (taus) taus[i] = tau;
+    }
+    __syncthreads();
+    const double tau = scal[2], scale = scal[4];
+    if (tau != 0.0)
+      for (int r = 1 + tid; r < len; r += NT) x[r] *= scale;
+    __syncthreads();
+    if (tid == 0) x[0] = scal[3];
+    for (int j = i + 1 + warp; j < c; j += NT / 32) {
+      double* y = W + j * ldw + i;
+      double dot = 0.0;
+      if (tau != 0.0) {
+        for (int r = 1 + lane; r < len; r += 32) dot += x[r] * y[r];
+        dot = warp_sum(dot);
+        dot += y[0];
+      }
+      const double w = tau * dot;
+      double ss = 0.0;
+      for (int r = 1 + lane; r < len; r += 32) {
+        double v = y[r] - w * x[r];
+        y[r] = v;
+        ss += v * v;
+      }
+      ss = warp_sum(ss);
+      __syncwarp();
+      if (lane == 0) { y[0] -= w; nrm[j] = ss; }
+    }
+    __syncthreads();
+    k = i + 1;
+  }
+  __syncthreads();
+  if (tid == 0) d.kout[0] = k;
+  for (int j = tid; j < c; j += NT) d.piv[j] = ipiv[j];
+  if (d.want_T) {
+    // T = R11^-1 R12, back substitution per column (warp per column)
+    for (int j = k + warp; j < c; j += NT / 32) {
+      double* y = W + j * ldw;
+      for (int i = k - 1; i >= 0; --i) {
+        __syncwarp();
+        const double xi = y[i] / W[i * ldw + i];
+        __syncwarp();
+        if (lane == 0) y[i] = xi;
+        for (int r = lane; r < i; r += 32) y[r] -= W[i * ldw + r] * xi;
+      }
+      __syncwarp();
+      for (int r = lane; r < k; r += 32) d.T[(long long)(j - k) * c + r] = y[r];
+    }
+  }
+  if (d.Rout) {
+    __syncthreads();
+    for (long long e = tid; e < (long long)q * c; e += NT) {
+      int i = (int)(e % q), j = (int)(e / q);
+      d.Rout[j * (long long)q + i] = W[j * ldw + i];
+    }
+  }
+}
+
+// ------------------------------------------------------------------ Cholesky
+struct DiagDesc {
+  double* A; long long lda;   // points at A(j0, j0)
+  int nb;                     // block size actually used (<= CH_NB)
+  double* Dinv;               // CH_NB x CH_NB scratch (ld CH_NB)
+  double* Linv; long long ldi;  // optional: Linv(j0, j0)
+  double* logsum; int* info; int col0;
+};
+
+__global__ void __launch_bounds__(NT) potrf_diag_kernel(const DiagDesc* __restrict__ descs) {
+  extern __shared__ double dsm[];
+  double* S = dsm;
+  double* X = dsm + CH_NB * CH_NB;
+  __shared__ int fail;
+  __shared__ double red[32];
+  const DiagDesc d = descs[blockIdx.x];
+  if (*d.info) return;
+  const int nb = d.nb, tid = threadIdx.x;
+  for (int e = tid; e < nb * nb; e += NT) {
+    int i = e % nb, j = e / nb;
+    S[e] = (i >= j) ? d.A[j * d.lda + i] : 0.0;
+  }
+  if (tid == 0) fail = 0;
+  __syncthreads();
+  for (int j = 0; j < nb; ++j) {
+    double djj = S[j * nb + j];
+    if (!(djj > 0.0)) {
+      if (tid == 0) fail = j + 1;
+      break;
+    }
+    djj = sqrt(djj);
+    __syncthreads();
+    for (int i = j + 1 + tid; i < nb; i += NT) S[j * nb + i] /= djj;
+    if (tid == 0) S[j * nb + j] = djj;
+    __syncthreads();
+    const int m = nb - j - 1;
+    for (int e = tid; e < m * m; e += NT) {
+      int i = j + 1 + e % m, l = j + 1 + e / m;
+      if (i >= l) S[l * nb + i] -= S[j * nb + i] * S[j * nb + l];
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  if (fail) {
+    if (tid == 0) *d.info = d.col0 + fail;
+    return;
+  }
+  // inverse of the lower-triangular block, one column per thread
+  if (tid < nb) {
+    const int c = tid;
+    for (int i = 0; i < c; ++i) X[c * nb + i] = 0.0;
+    X[c * nb + c] = 1.0 / S[c * nb + c];
+    for (int i = c + 1; i < nb; ++i) {
+      double s = 0.0;
+      for (int l = c; l < i; ++l) s += S[l * nb + i] * X[c * nb + l];
+      X[c * nb + i] = -s / S[i * nb + i];
+    }
+  }
+  double ls = 0.0;
+  for (int j = tid; j < nb; j += NT) ls += log(S[j * nb + j]);
+  ls = block_sum(ls, red);
+  if (tid == 0) *d.logsum += ls;
+  __syncthreads();
+  for (int e = tid; e < nb * nb; e += NT) {
+    int i = e % nb, j = e / nb;
+    d.A[j * d.lda + i] = (i >= j) ? S[e] : 0.0;
+    d.Dinv[j * CH_NB + i] = X[e];
+    if (d.Linv) d.Linv[j * d.ldi + i] = X[e];
+  }
+}
+
+struct ZDesc { double* A; long long lda; int n; };
+__global__ void zero_upper_kernel(const ZDesc* __restrict__ descs) {
+  const ZDesc d = descs[blockIdx.y];
+  const long long tot = (long long)d.n * d.n;
+  for (long long e = blockIdx.x * (long long)NT + threadIdx.x; e < tot; e += (long long)gridDim.x * NT) {
+    int i = (int)(e % d.n), j = (int)(e / d.n);
+    if (i < j) d.A[j * d.lda + i] = 0.0;
+  }
+}
+
+__global__ void zero_all_kernel(const ZDesc* __restrict__ descs) {
+  const ZDesc d = descs[blockIdx.y];
+  const long long tot = (long long)d.n * d.n;
+  for (long long e = blockIdx.x * (long long)NT + threadIdx.x; e < tot; e += (long long)gridDim.x * NT) {
+    int i = (int)(e % d.n), j = (int)(e / d.n);
+    d.A[j * d.lda + i] = 0.0;
+  }
+}
+
+__global__ void copy_kernel(const CopyProb* __restrict__ descs) {
+  const CopyProb d = descs[blockIdx.y];
+  const long long tot = (long long)d.rows * d.cols;
+  for (long long e = blockIdx.x * (long long)NT + threadIdx.x; e < tot; e += (long long)gridDim.x * NT) {
+    int i = (int)(e % d.rows), j = (int)(e / d.rows);
+    d.dst[j * d.ldd + i] = d.alpha * d.src[j * d.lds + i];
+  }
+}
+
+template <class D>
+DBuf<D> upload_descs(const std::vector<D>& v, cudaStream_t s) {
+  DBuf<D> b(v.size(), s);
+  b.upload(v);
+  return b;
+}
+
+int grid_x_for(long long maxelems) {
+  long long g = (maxelems + NT - 1) / NT;
+  return (int)std::max<long long>(1, std::min<long long>(g, 256));
+}
+
+// launch a per-problem elementwise kernel with grid.y = problems (chunked to 65535)
+template <class D, class K>
+void launch_y(cudaStream_t s, const std::vector<D>& v, long long maxelems, K kern) {
+  if (v.empty()) return;
+  auto d = upload_descs(v, s);
+  const int gx = grid_x_for(maxelems);
+  for (size_t o = 0; o < v.size(); o += 65535) {
+    int ny = (int)std::min<size_t>(65535, v.size() - o);
+    kern<<<dim3(gx, ny), NT, 0, s>>>(d.p + o);
+    count_launch();
+    RSF_LAUNCH_CHECK();
+  }
+}
+
+}  // namespace
+
+void copy_batched(cudaStream_t s, const std::vector<CopyProb>& probs) {
+  long long mx = 0;
+  for (auto& p : probs) mx = std::max(mx, (long long)p.rows * p.cols);
+  if (mx == 0) return;
+  launch_y(s, probs, mx, copy_kernel);
+}
+
+// ------------------------------------------------------------------ geqrf
+void geqrf_batched(cudaStream_t s, const std::vector<QRProb>& probs, bool keep_q) {
+  if (probs.empty()) return;
+  static bool attr = false;
+  if (!attr) {
+    RSF_CUDA(cudaFuncSetAttribute(qr_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(SMEM_BUDGET + 16 * 1024)));
+    attr = true;
+  }
+  const int P = (int)probs.size();
+  // workspace: V (m x QR_NB), T (QR_NB^2), W and W2 (QR_NB x c)
+  std::vector<long long> voff(P), woff(P), toff(P);
+  long long vtot = 0, wtot = 0;
+  int maxk = 0;
+  for (int i = 0; i < P; ++i) {
+    voff[i] = vtot; vtot += (long long)probs[i].m * QR_NB;
+    woff[i] = wtot; wtot += (long long)QR_NB * probs[i].c;
+    toff[i] = (long long)i * QR_NB * QR_NB;
+    maxk = std::max(maxk, std::min(probs[i].m, probs[i].c));
+  }
+  DBuf<double> V(vtot, s), W(wtot, s), W2(wtot, s), Tscr(keep_q ? 0 : (size_t)P * QR_NB * QR_NB, s);
+  const size_t base_smem = (40 + QR_NB + 2 * QR_NB * QR_NB) * sizeof(double);
+  for (int j0 = 0; j0 < maxk; j0 += QR_NB) {
+    std::vector<PanelDesc> pd;
+    GemmBatch g1(true, false), g2(true, false), g3(false, false);
+    size_t smem_need = base_smem;
+    for (int i = 0; i < P; ++i) {
+      const QRProb& q = probs[i];
+      const int kk = std::min(q.m, q.c);
+      if (j0 >= kk) continue;
+      const int nbp = std::min(QR_NB, kk - j0);
+      const int rows = q.m - j0;
+      PanelDesc d;
+      d.A = q.A + j0 * q.lda + j0;
+      d.lda = q.lda;
+      d.rows = rows;
+      d.ncol = nbp;
+      d.V = V.p + voff[i];
+      d.T = keep_q ? q.Tws + (long long)(j0 / QR_NB) * QR_NB * QR_NB : Tscr.p + toff[i];
+      d.tau = keep_q && q.tau ? q.tau + j0 : nullptr;
+      const size_t pbytes = (size_t)rows * nbp * sizeof(double);
+      d.smem = (pbytes <= SMEM_BUDGET) ? 1 : 0;
+      if (d.smem) smem_need = std::max(smem_need, base_smem + pbytes);
+      pd.push_back(d);
+      const int j1 = j0 + nbp;
+      const int c2 = q.c - j1;
+      if (c2 > 0) {
+        GemmDesc a = gdesc(nbp, c2, rows);          // W = V^T A2
+        a.A = d.V; a.lda = rows;
+        a.B = q.A + (long long)j1 * q.lda + j0; a.ldb = (int)q.lda;
+        a.C = W.p + woff[i]; a.ldc = QR_NB;
+        g1.add(a);
+        GemmDesc b = gdesc(nbp, c2, nbp);           // W2 = T^T W
+        b.A = d.T; b.lda = QR_NB;
+        b.B = W.p + woff[i]; b.ldb = QR_NB;
+        b.C = W2.p + woff[i]; b.ldc = QR_NB;
+        g2.add(b);
+        GemmDesc c = gdesc(rows, c2, nbp);          // A2 -= V W2
+        c.A = d.V; c.lda = rows;
+        c.B = W2.p + woff[i]; c.ldb = QR_NB;
+        c.C = q.A + (long long)j1 * q.lda + j0; c.ldc = (int)q.lda;
+        c.alpha = -1.0; c.beta = 1.0;
+        g3.add(c);
+      }
+    }
+    if (pd.empty()) continue;
+    auto dd = upload_descs(pd, s);
+    qr_panel_kernel<<<(unsigned)pd.size(), NT, smem_need, s>>>(dd.p);
+    count_launch();
+    RSF_LAUNCH_CHECK();
+    g1.run(s);
+    g2.run(s);
+    g3.run(s);
+  }
+}
+
+void ormqr_batched(cudaStream_t s, const std::vector<QApplyProb>& probs, bool trans) {
+  if (probs.empty()) return;
+  const int P = (int)probs.size();
+  std::vector<long long> voff(P), woff(P);
+  long long vtot = 0, wtot = 0;
+  int maxk = 0;
+  for (int i = 0; i < P; ++i) {
+    voff[i] = vtot; vtot += (long long)probs[i].m * QR_NB;
+    woff[i] = wtot; wtot += (long long)QR_NB * probs[i].nc;
+    maxk = std::max(maxk, std::min(probs[i].m, probs[i].c));
+  }
+  DBuf<double> V(vtot, s), W(wtot, s), W2(wtot, s);
+  const int npan = (maxk + QR_NB - 1) / QR_NB;
+  for (int pi = 0; pi < npan; ++pi) {
+    const int pp = trans ? pi : (npan - 1 - pi);
+    const int j0 = pp * QR_NB;
+    std::vector<VDesc> vd;
+    GemmBatch g1(true, false), g2(!trans ? false : true, false), g3(false, false);
+    long long mx = 0;
+    for (int i = 0; i < P; ++i) {
+      const QApplyProb& q = probs[i];
+      const int kk = std::min(q.m, q.c);
+      if (j0 >= kk || q.nc <= 0) continue;
+      const int nbp = std::min(QR_NB, kk - j0);
+      const int rows = q.m - j0;
+      VDesc v{q.A + j0 * q.lda + j0, q.lda, rows, nbp, V.p + voff[i]};
+      vd.push_back(v);
+      mx = std::max(mx, (long long)rows * nbp);
+      const double* Tp = q.Tws + (long long)pp * QR_NB * QR_NB;
+      GemmDesc a = gdesc(nbp, q.nc, rows);          // W = V^T C
+      a.A = V.p + voff[i]; a.lda = rows;
+      a.B = q.C + j0; a.ldb = (int)q.ldc;
+      a.C = W.p + woff[i]; a.ldc = QR_NB;
+      g1.add(a);
+      GemmDesc b = gdesc(nbp, q.nc, nbp);           // W2 = T^T W (Q^T) or T W (Q)
+      b.A = Tp; b.lda = QR_NB;
+      b.B = W.p + woff[i]; b.ldb = QR_NB;
+      b.C = W2.p + woff[i]; b.ldc = QR_NB;
+      g2.add(b);
+      GemmDesc c = gdesc(rows, q.nc, nbp);          // C -= V W2
+      c.A = V.p + voff[i]; c.lda = rows;
+      c.B = W2.p + woff[i]; c.ldb = QR_NB;
+      c.C = q.C + j0; c.ldc = (int)q.ldc;
+      c.alpha = -1.0; c.beta = 1.0;
+      g3.add(c);
+    }
+    if (vd.empty()) continue;
+    launch_y(s, vd, mx, build_v_kernel);
+    g1.run(s);
+    g2.run(s);
+    g3.run(s);
+  }
+}
+
+// ------------------------------------------------------------------ cpqr
+void cpqr_id_batched(cudaStream_t s, const std::vector<CPQRProb>& probs, double eps, int* d_k,
+                     bool want_T) {
+  if (probs.empty()) return;
+  static bool attr = false;
+  if (!attr) {
+    RSF_CUDA(cudaFuncSetAttribute(cpqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(SMEM_BUDGET + 24 * 1024)));
+    attr = true;
+  }
+  std::vector<CPQRDesc> dv;
+  size_t smem_need = 0;
+  for (size_t i = 0; i < probs.size(); ++i) {
+    const CPQRProb& p = probs[i];
+    CPQRDesc d;
+    d.R = p.R; d.ldr = p.ldr; d.q = p.q; d.c = p.c;
+    size_t hdr = (72 + p.c + ((size_t)p.c + 32 + 1) / 2 + 1) * sizeof(double);
+    size_t wbytes = (size_t)p.q * p.c * sizeof(double);
+    if (hdr + wbytes <= SMEM_BUDGET) {
+      d.smem = 1; d.W = nullptr; d.ldw = p.q;
+      smem_need = std::max(smem_need, hdr + wbytes);
+    } else {
+      RSF_REQUIRE(p.W != nullptr, ST_ECUDA, "cpqr: workspace required");
+      RSF_REQUIRE(hdr <= SMEM_BUDGET + 16 * 1024, ST_EINVAL, "cpqr: block too wide");
+      d.smem = 0; d.W = p.W; d.ldw = p.q;
+      smem_need = std::max(smem_need, hdr);
+    }
+    d.T = p.T; d.piv = p.piv; d.kout = d_k + i;
+    d.Rout = p.Rout; d.tau = p.tau;
+    d.eps = eps; d.want_T = want_T ? 1 : 0;
+    dv.push_back(d);
+  }
+  auto dd = upload_descs(dv, s);
+  for (size_t o = 0; o < dv.size(); o += 65535) {
+    unsigned nb = (unsigned)std::min<size_t>(65535, dv.size() - o);
+    cpqr_kernel<<<nb, NT, smem_need, s>>>(dd.p + o);
+    count_launch();
+    RSF_LAUNCH_CHECK();
+  }
+}
+
+// ------------------------------------------------------------------ potrf (+ inverse)
+void potrf_batched(cudaStream_t s, const std::vector<PotrfProb>& probs, double* d_logsum, int* d_info) {
+  if (probs.empty()) return;
+  static bool attr = false;
+  if (!attr) {
+    RSF_CUDA(cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(2 * CH_NB * CH_NB * sizeof(double))));
+    attr = true;
+  }
+  const int P = (int)probs.size();
+  RSF_CUDA(cudaMemsetAsync(d_logsum, 0, P * sizeof(double), s));
+  RSF_CUDA(cudaMemsetAsync(d_info, 0, P * sizeof(int), s));
+  int maxn = 0;
+  std::vector<long long> woff(P);
+  long long wtot = 0;
+  for (int i = 0; i < P; ++i) {
+    maxn = std::max(maxn, probs[i].n);
+    woff[i] = wtot;
+    wtot += (long long)CH_NB * probs[i].n;
+  }
+  if (maxn == 0) return;
+  DBuf<double> Dinv((size_t)P * CH_NB * CH_NB, s), Wb(wtot, s);
+  {  // Linv starts at zero (upper triangle and not-yet-written blocks)
+    std::vector<ZDesc> z;
+    long long mx = 0;
+    for (auto& p : probs)
+      if (p.Linv && p.n) { z.push_back(ZDesc{p.Linv, p.ldi, p.n}); mx = std::max(mx, (long long)p.n * p.n); }
+    launch_y(s, z, mx, zero_all_kernel);
+  }
+  for (int j0 = 0; j0 < maxn; j0 += CH_NB) {
+    std::vector<DiagDesc> dd;
+    std::vector<CopyProb> cp;
+    GemmBatch gp(false, true), gt(false, true);
+    for (int i = 0; i < P; ++i) {
+      const PotrfProb& p = probs[i];
+      if (p.n <= j0) continue;
+      const int nb = std::min(CH_NB, p.n - j0);
+      DiagDesc d;
+      d.A = p.A + j0 * p.lda + j0; d.lda = p.lda; d.nb = nb;
+      d.Dinv = Dinv.p + (long long)i * CH_NB * CH_NB;
+      d.Linv = p.Linv ? p.Linv + j0 * p.ldi + j0 : nullptr; d.ldi = p.ldi;
+      d.logsum = d_logsum + i; d.info = d_info + i; d.col0 = j0;
+      dd.push_back(d);
+      const int j1 = j0 + nb, r = p.n - j1;
+      if (r > 0) {
+        GemmDesc a = gdesc(r, nb, nb);            // W = A21 Dinv^T
+        a.A = p.A + j0 * p.lda + j1; a.lda = (int)p.lda;
+        a.B = d.Dinv; a.ldb = CH_NB;
+        a.C = Wb.p + woff[i]; a.ldc = r;
+        gp.add(a);
+        cp.push_back(CopyProb{Wb.p + woff[i], r, p.A + j0 * p.lda + j1, p.lda, r, nb, 1.0});
+        GemmDesc t = gdesc(r, r, nb);             // A22 -= L21 L21^T (lower tiles)
+        t.A = p.A + j0 * p.lda + j1; t.lda = (int)p.lda;
+        t.B = p.A + j0 * p.lda + j1; t.ldb = (int)p.lda;
+        t.C = p.A + j1 * p.lda + j1; t.ldc = (int)p.lda;
+        t.alpha = -1.0; t.beta = 1.0; t.lower = 1;
+        gt.add(t);
+      }
+    }
+    if (dd.empty()) continue;
+    auto ddev = upload_descs(dd, s);
+    for (size_t o = 0; o < dd.size(); o += 65535) {
+      unsigned nb = (unsigned)std::min<size_t>(65535, dd.size() - o);
+      potrf_diag_kernel<<<nb, NT, 2 * CH_NB * CH_NB * sizeof(double), s>>>(ddev.p + o);
+      count_launch();
+      RSF_LAUNCH_CHECK();
+    }
+    gp.run(s);
+    copy_batched(s, cp);
+    gt.run(s);
+  }
+  // zero the strict upper triangle (the SYRK tiles straddle the diagonal)
+  std::vector<ZDesc> zd;
+  long long mx = 0;
+  for (auto& p : probs)
+    if (p.n > 0) { zd.push_back(ZDesc{p.A, p.lda, p.n}); mx = std::max(mx, (long long)p.n * p.n); }
+  launch_y(s, zd, mx, zero_upper_kernel);
+  // explicit inverse: block rows  X(r0:, 0:r0) = -Dinv_rr * (L(r0:, 0:r0) X(0:r0, 0:r0))
+  bool want_inv = false;
+  for (auto& p : probs) want_inv |= (p.Linv != nullptr);
+  if (!want_inv) return;
+  DBuf<double> tmp(wtot, s);
+  for (int r0 = CH_NB; r0 < maxn; r0 += CH_NB) {
+    GemmBatch g1(false, false), g2(false, false);
+    for (int i = 0; i < P; ++i) {
+      const PotrfProb& p = probs[i];
+      if (!p.Linv || p.n <= r0) continue;
+      const int rb = std::min(CH_NB, p.n - r0);
+      GemmDesc a = gdesc(rb, r0, r0);
+      a.A = p.A + r0; a.lda = (int)p.lda;
+      a.B = p.Linv; a.ldb = (int)p.ldi;
+      a.C = tmp.p + woff[i]; a.ldc = rb;
+      g1.add(a);
+      GemmDesc b = gdesc(rb, r0, rb);
+      b.A = p.Linv + r0 * p.ldi + r0; b.lda = (int)p.ldi;
+      b.B = tmp.p + woff[i]; b.ldb = rb;
+      b.C = p.Linv + r0; b.ldc = (int)p.ldi;
+      b.alpha = -1.0;
+      g2.add(b);
+    }
+    g1.run(s);
+    g2.run(s);
+  }
+}
+
+}  // namespace rsf

@@ -1,0 +1,62 @@
+// Variable-size batched FP64 GEMM with column gather/scatter maps.
+//
+//   C_b[:, mapC] = alpha * op(A_b)[:, :] * op(B_b) + beta * C_b[:, mapC]
+//
+// All matrices column-major.  A "map" replaces the stored-column index j by
+// map[j] (gather for A/B, scatter for C); the multi-RHS sweeps of the RSF use
+// it to read/write the per-box DOF columns of X' (k x n, the transpose of the
+// n x k right-hand-side block) without packing.  Operands may be absolute
+// pointers (factor storage) or offsets into two per-call base pointers X0/X1
+// with leading dimension ldx, so descriptor arrays are built once per factor
+// and reused by every solve/apply.
+#pragma once
+#include "common.cuh"
+
+namespace rsf {
+
+struct GemmDesc {
+  int M, N, K;                 // M < 0: use the per-call M (number of RHS)
+  int selA, selB, selC;        // 0: absolute pointer (+off elements), 1: X0, 2: X1 (+off columns, ld = ldx)
+  const double* A; long long offA; int lda; const int* mapA;
+  const double* B; long long offB; int ldb; const int* mapB;
+  double* C; long long offC; int ldc; const int* mapC;
+  double alpha, beta;
+  int lower;                   // 1: only tiles touching the lower triangle of C (SYRK-style)
+};
+
+inline GemmDesc gdesc(int M, int N, int K) {
+  GemmDesc d{};
+  d.M = M; d.N = N; d.K = K;
+  d.alpha = 1.0; d.beta = 0.0;
+  return d;
+}
+
+class GemmBatch {
+ public:
+  GemmBatch() = default;
+  GemmBatch(bool ta, bool tb) : ta_(ta), tb_(tb) {}
+  void reset(bool ta, bool tb) { ta_ = ta; tb_ = tb; h_.clear(); ready_ = false; }
+  void add(const GemmDesc& d) { h_.push_back(d); ready_ = false; }
+  size_t size() const { return h_.size(); }
+  bool empty() const { return h_.empty(); }
+  void finalize(cudaStream_t s) const;
+  // Launch; X0/X1/ldx/Mglob resolve the per-call operands.
+  void run(cudaStream_t s, double* X0 = nullptr, double* X1 = nullptr, int ldx = 0, int Mglob = 0) const;
+  // flops of one run (2*M*N*K summed), for diagnostics
+  double flops(int Mglob = 0) const;
+
+ private:
+  bool ta_ = false, tb_ = false;
+  mutable bool ready_ = false;
+  std::vector<GemmDesc> h_;
+  mutable DBuf<GemmDesc> d_;
+  mutable DBuf<int> prefix_;
+  mutable int totalN_ = 0, maxM_ = 0;
+  mutable bool glob_ = false;
+};
+
+// one-shot helper: single problem
+void gemm1(cudaStream_t s, bool ta, bool tb, int M, int N, int K, double alpha, const double* A,
+           int lda, const double* B, int ldb, double beta, double* C, int ldc);
+
+}  // namespace rsf

@@ -1,0 +1,44 @@
+// Weak-admissibility matrix peeling (PAPER §3.2) and Alg. 1.
+#pragma once
+#include "../../include/rsf.h"
+#include "rsf_impl.cuh"
+
+namespace rsf {
+
+struct PeelDiag {
+  std::vector<int> cols, rank_max;   // per level (index = level)
+  int nL = 0;
+  double cancellation = 0;
+  double applies = 0;
+  double seconds = 0;
+  double flops = 0;
+};
+
+// Tr(G) with G = 1/2 (F^-1 Fi + Fi F^-1) (Fi != null) or G = F^-1 (Fi == null).
+double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag* diag);
+void fill_peel_diag(const PeelDiag& d, rsf_peel_diag* out);
+
+struct EvalResult {
+  double ell = 0, logdet = 0, quad = 0;
+  double grad[4] = {0, 0, 0, 0}, q[4] = {0, 0, 0, 0}, trace[4] = {0, 0, 0, 0};
+  double t_tree = 0, t_factor = 0, t_compress = 0, t_solve = 0, t_peel = 0, t_total = 0;
+  double flops_factor = 0;
+  long long launches = 0;
+  FactDiag fdiag;
+  int L = 0, n0 = 0;
+  PeelDiag pd[4];
+};
+
+EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KParams& kp, int p,
+                    const int* theta, double eps, int leaf, const Opts& o);
+void fill_eval_diag(const EvalResult& r, rsf_eval_diag* out);
+
+// deterministic dot product of two device vectors (n doubles)
+double ddot(cudaStream_t s, const double* a, const double* b, long long n);
+
+// Philox4x32-10 N(0,1) probe entries: X'(j, t) = qmap[t] == g ?
+// normal(perm[t], col0 + j, level, trace) : 0, X' is k x n (ld k)
+void gen_probes(cudaStream_t s, double* X, int k, int n, const int* perm, const int* qmap, int g,
+                int col0, int level, int trace, unsigned long long seed);
+
+}  // namespace rsf

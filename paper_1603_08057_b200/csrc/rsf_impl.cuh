@@ -1,0 +1,127 @@
+// Internal data structures of librsf: context, quadtree, factor handle.
+#pragma once
+#include <array>
+#include <memory>
+#include <unordered_map>
+
+#include "common.cuh"
+#include "covariance.cuh"
+#include "gemm.cuh"
+
+namespace rsf {
+
+struct Opts {
+  double eps_peel = 1e-6;
+  int oversample = 8;        // c in (r + c) (R-K)
+  int probe_block = 512;     // max probe columns per G-apply chunk
+  int peel_start = 64;       // initial probe columns per group at level 1 (R-M adaptivity)
+  int max_depth = 30;
+  double r_near = 1.8, r_in = 1.75, r_out = 2.45;   // R-C (in units of the box half-width)
+  unsigned long long seed = 1603080570ull;
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = 0;
+  bool own_stream = false;
+  void* nccl = nullptr;
+  std::string last_error;
+};
+
+// ------------------------------------------------------------------ quadtree
+// Points are sorted by 60-bit Morton key (30 bits per axis on the root [0,1]^2);
+// every node owns a contiguous range [begin, end) of the sorted order ("tree
+// index").  Children are in quadrant order SW, SE, NW, NE (q = bx + 2 by).
+struct Tree {
+  int n = 0, leaf = 0, L = 0;
+  std::vector<int> perm;        // tree index -> original index
+  std::vector<int> lev, parent, quad, begin, end;
+  std::vector<std::array<int, 4>> child;    // by quadrant, -1 if absent
+  std::vector<int> ix, iy;      // cell coordinates at the node's level
+  std::vector<std::vector<int>> levels;     // node ids per level (Morton order)
+  std::unordered_map<unsigned long long, int> cell;   // (level, ix, iy) -> node
+  DBuf<double> xs, ys;          // coordinates in tree order (device)
+  std::vector<double> hx, hy;   // same, host copy (near-list scheduling)
+  DBuf<int> d_perm;             // tree index -> original index (device)
+  bool is_leaf(int b) const { return child[b][0] < 0 && child[b][1] < 0 && child[b][2] < 0 && child[b][3] < 0; }
+  double cx(int b) const { return (ix[b] + 0.5) / double(1u << lev[b]); }
+  double cy(int b) const { return (iy[b] + 0.5) / double(1u << lev[b]); }
+  double h(int b) const { return 0.5 / double(1u << lev[b]); }
+  static unsigned long long cell_key(int l, int x, int y) {
+    return ((unsigned long long)l << 58) | ((unsigned long long)x << 29) | (unsigned long long)y;
+  }
+  int find(int l, int x, int y) const {
+    auto it = cell.find(cell_key(l, x, y));
+    return it == cell.end() ? -1 : it->second;
+  }
+};
+
+std::shared_ptr<Tree> build_tree(Ctx& ctx, const double* d_xy, int n, int leaf, int max_depth);
+
+// ------------------------------------------------------------------ factor
+struct Level {
+  int lev = 0;
+  int nbox = 0;
+  std::vector<int> node;             // node ids
+  std::vector<int> c, k, r;          // |I|, |S|, |R|
+  std::vector<long long> soff, roff; // offsets into S/R index arrays
+  DBuf<int> S, R;                    // tree indices
+  // persistent blocks (offsets in doubles)
+  std::vector<long long> toff, loff, eoff;
+  DBuf<double> T;      // k x r (ld k)
+  DBuf<double> L, Linv;  // r x r (Sigma) | XRR r x r (Sigma_i, in L)
+  DBuf<double> E;      // k x r (Sigma: E; Sigma_i: X_SR)
+  long long rtot = 0;  // sum r (tmp columns)
+  // sweep GEMM batches (M = number of RHS, per call)
+  GemmBatch fs1, fs2, fs3;            // forward solve
+  GemmBatch bs2, bs3, bs4;            // backward solve
+  GemmBatch up1, up2, up3;            // apply, up
+  GemmBatch dn1, dn2, dn4;            // apply, down
+  GemmBatch ao1, ao2a, ao2b, ao3, ao4;  // apply-only (Sigma_i)
+};
+
+struct FactDiag {
+  double flops_id = 0, flops_elim = 0, flops_top = 0;   // algorithmic (formulas of DESIGN.md)
+  double bytes_factor = 0;                              // stored factor bytes
+  double t_tree = 0, t_factor = 0;
+  std::vector<int> level_boxes, level_I, level_S, level_maxI;
+};
+
+struct Fact {
+  Ctx* ctx = nullptr;
+  int which = W_SIGMA;
+  KParams kp{};
+  double eps = 0;
+  Opts opts;
+  std::shared_ptr<Tree> tree;
+  std::vector<Level> levels;         // indexed by level number (0 unused)
+  int n0 = 0;
+  DBuf<int> I0;
+  DBuf<double> C, Cinv;              // Sigma: top Cholesky and inverse; Sigma_i: C = B0
+  double logdet = 0;
+  long long tmp_cols = 0;            // max(sum r per level, n0)
+  GemmBatch top_s1, top_s2, top_a1, top_a2, top_q1, top_ao;
+  FactDiag diag;
+  int n() const { return tree->n; }
+};
+
+std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams& kp, int which,
+                             double eps, const Opts& opts);
+
+// operations on X' (k x n column-major, tree order, ld = k): in place
+void solve_internal(const Fact& F, double* X, int k, double* tmp);
+void apply_internal(const Fact& F, double* X, int k, double* tmp);
+void sqrt_internal(const Fact& F, double* X, int k, double* tmp);
+// apply-only Sigma_i: Y = F_i X (X is overwritten)
+void apply_only_internal(const Fact& F, double* X, double* Y, int k);
+// any operator: out = op(X) with X preserved? (helpers in rsf.cu)
+
+// layout conversions between the caller's n x k (ld) original order and X'
+void to_internal(cudaStream_t s, const Tree& t, const double* b, long long ld, int k, double* X);
+void to_external(cudaStream_t s, const Tree& t, const double* X, int k, double* b, long long ld);
+
+// kernel launch helpers (rsf_kernels.cu)
+void colcopy(cudaStream_t s, double* dst, const double* src, int ldx, int M, const int* dmap,
+             const int* smap, long long count, double alpha = 1.0, double beta = 0.0);
+
+}  // namespace rsf
