@@ -1,0 +1,326 @@
+#!/usr/bin/env python
+"""bench.py -- l(theta)+g(theta) evaluations per second through the CUDA path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl cuda|reference]
+                    [--config 4] [--n N]
+
+A "step" is one full evaluation of Alg. 1 -- quadtree, RSF of
+Sigma, compression of each Sigma_i, solve, and the peeled traces -- at the
+metric workload of BASELINE.json (config 4: n = 2^20 clustered points,
+Matern 1/2), inputs resident in HBM.  Multi-GPU (torchrun): every rank
+evaluates its own independent replica ("replicas"), the time is
+the max over ranks, value = evaluations of all ranks / time.
+
+--impl reference times the CPU oracle (oracle/, the only other place bench.py
+runs it) on rank 0 on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "l+g evals/sec at n=2^20 (1/2/4/8 B200); RSF FP64 TFLOP/s vs peak"
+UNIT = "evals/s"
+# FP64 FMA-pipe peak derived from unit counts and clocks:
+# 148 SMs x 64 FP64 FMA/clk x 2 flop x 1.965 GHz
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
+
+
+def _env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+        self.th = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.th:
+            self.th.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                smax.append(float(p[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def workload(cid: int, n: int | None):
+    from workloads import config, points_for, w_for
+    c = config(cid)
+    n = n or c.n
+    return c, n, points_for(c, n), w_for(c, n)
+
+
+def run_reference(args, rank):
+    """CPU oracle (O2: serial numpy RSF + weak peeling) on a bounded sample."""
+    if rank != 0:
+        return
+    from oracle.kernels import Kernel as OK
+    from oracle.mle import rsf_mle_eval
+    from workloads import philox_normal
+    c, n_full, _, _ = workload(args.config, args.n)
+    n_s = args.ref_n
+    c_s, _, xy, w = workload(args.config, n_s)
+    ok = OK(c.family, c.rho, c.sigma2, c.nugget, c.alpha, c.theta)
+    # z = w (a valid observation vector for timing; the time does not depend on z)
+    times = []
+    for it in range(args.warmup + args.steps):
+        t = time.perf_counter()
+        rsf_mle_eval(ok, xy, w, c.eps_fact, c.eps_peel, c.leaf, c.seed, philox_normal, block=8)
+        dt = time.perf_counter() - t
+        if it >= args.warmup:
+            times.append(dt)
+        if sum(times) > args.ref_budget:
+            break
+    t_s = float(np.mean(times))
+    # extrapolation to n_full by the paper's observed n^1.6 scaling of one evaluation
+    t_full = t_s * (n_full / n_s) ** 1.6
+    value = 1.0 / t_full
+    cores = len(os.sched_getaffinity(0))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": len(times), "warmup": args.warmup, "ms_per_step": t_full * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": _config_dict(c, n_full, args),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"O2 oracle (numpy RSF + weak peeling) full l+g evaluation of config "
+                                   f"{c.cid}'s recipe at n={n_s}, mean {t_s:.2f} s over {len(times)} "
+                                   f"step(s); extrapolated to n={n_full} by the paper's n^1.6 (P:830)",
+                         "sample_seconds": t_s},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _config_dict(c, n, args):
+    return {"workload": f"config{c.cid}: n={n} {c.points} points, {c.family}, rho={c.rho}, "
+                        f"nugget={c.nugget}, theta={list(c.theta)}, leaf={c.leaf}",
+            "n": n, "eps": c.eps, "eps_fact": c.eps_fact, "eps_peel": c.eps_peel, "leaf": c.leaf,
+            "theta": list(c.theta), "parallelism": f"replicas x{args.gpus}",
+            "l2": "working set (factor + probe blocks, GBs) >> 126 MB L2; no flush"}
+
+
+def cpu_baseline_sample(args, c):
+    """The oracle as it stands on a bounded sample (rank 0, N=1 only)."""
+    from oracle.kernels import Kernel as OK
+    from oracle.mle import rsf_mle_eval
+    from workloads import philox_normal
+    n_s = args.ref_n
+    _, _, xy, w = workload(args.config, n_s)
+    ok = OK(c.family, c.rho, c.sigma2, c.nugget, c.alpha, c.theta)
+    t = time.perf_counter()
+    rsf_mle_eval(ok, xy, w, c.eps_fact, c.eps_peel, c.leaf, c.seed, philox_normal, block=8)
+    t_s = time.perf_counter() - t
+    n_full = args.n or c.n
+    t_full = t_s * (n_full / n_s) ** 1.6
+    return {"value": 1.0 / t_full, "unit": UNIT, "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
+            "sample": f"O2 oracle (numpy RSF + weak peeling) one full l+g evaluation of config {c.cid}'s "
+                      f"recipe at n={n_s} took {t_s:.2f} s; extrapolated to n={n_full} by the paper's "
+                      f"n^1.6 (P:830)", "sample_seconds": t_s}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--ref-n", type=int, default=4096)
+    ap.add_argument("--ref-budget", type=float, default=120.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = _env_int("WORLD_SIZE", 1)
+    rank = _env_int("RANK", 0)
+    local = _env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_1603_08057_b200 as R
+    from workloads import config
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    c, n, xy_h, w_h = workload(args.config, args.n)
+    ctx = R.Context(local)
+    K = R.Kernel(c.family, c.rho, c.sigma2, c.nugget, c.alpha, c.theta)
+    opts = R.Opts(eps_peel=c.eps_peel, seed=c.seed + 1000 * rank)
+    xy = torch.from_numpy(xy_h).to(dev)
+    w = torch.from_numpy(w_h).to(dev)
+    # z = F^{1/2} w through the CUDA path (input recipe R-V), before timing
+    F = R.Factor(ctx, xy, K, c.eps_fact, c.leaf, opts=opts)
+    z = F.sample(w)
+    F.close()
+    torch.cuda.synchronize()
+
+    def step(xyb, zb):
+        return R.gp_mle_eval(ctx, xyb, zb, K, c.eps_fact, c.leaf, opts)
+
+    for _ in range(args.warmup):
+        r = step(xy, z)
+    torch.cuda.synchronize()
+    barrier()
+
+    # ---- timed region: device-resident inputs
+    R.lib.rsf_stats_reset()
+    R.lib.rsf_stats_enable(1)
+    clk = ClockSampler(local)
+    clk.start()
+    l0 = R.kernel_launches()
+    torch.cuda.synchronize()
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    t0 = time.perf_counter()
+    diags = []
+    for _ in range(args.steps):
+        r = step(xy, z)
+        diags.append(r.diag)
+    e1.record()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    barrier()
+    clocks = clk.stop()
+    R.lib.rsf_stats_enable(0)
+    launches = R.kernel_launches() - l0
+    st = (R.C if hasattr(R, "C") else __import__("ctypes")).c_double * 4
+    stats = st()
+    R.lib.rsf_stats_get(stats)
+    # the library synchronises its own stream at the end of every evaluation, so the
+    # wall time brackets exactly the device work; torch events on the default stream
+    # see only the torch part, hence max(device-synchronised wall, event time)
+    ev_ms = e0.elapsed_time(e1)
+    t_local = max(wall, ev_ms / 1e3)
+    t_all = t_local
+    if world > 1:
+        tt = torch.tensor([t_local], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_all = float(tt.item())
+    value = world * args.steps / t_all
+
+    # ---- e2e: same metric through the C ABI with pinned HOST buffers (H2D inside the call)
+    xy_p = torch.from_numpy(xy_h).pin_memory()
+    z_p = z.cpu().pin_memory()
+    torch.cuda.synchronize()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step(xy_p, z_p)
+    torch.cuda.synchronize()
+    te = time.perf_counter() - t0
+    if world > 1:
+        tt = torch.tensor([te], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        te = float(tt.item())
+    e2e = {"value": world * args.steps / te, "unit": UNIT,
+           "h2d_bytes_per_step": int(xy_h.nbytes + z_p.numel() * 8),
+           "d2h_bytes_per_step": int(8 * (1 + len(c.theta)))}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    d = diags[-1]
+    gl, gsec, gfl, gby = stats[0], stats[1], stats[2], stats[3]
+    achieved = gfl / gsec / 1e12 if gsec > 0 else 0.0
+    roofline = {"bound": "alu", "kernel": "gemm_vb_kernel (batched FP64 GEMM: RSF sweeps, Schur "
+                                          "updates, WY updates)",
+                "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": achieved / FP64_PEAK_TFLOPS,
+                "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md §5)",
+                "traffic": None, "launches": int(gl), "kernel_seconds": gsec,
+                "share_of_step": gsec / (t_local) if t_local > 0 else None,
+                "algorithmic_flops_per_launch": gfl / gl if gl else None}
+    fl_factor = d.flops_factor
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * t_all / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": _config_dict(c, n, args), "clocks": clocks, "gpu_launches": int(launches),
+        "e2e": e2e, "roofline": roofline,
+        "rsf_factor_tflops": fl_factor / max(d.t_factor + d.t_compress, 1e-9) / 1e12,
+        "phases_s": {"tree": d.t_tree, "factor": d.t_factor, "compress": d.t_compress,
+                     "solve": d.t_solve, "peel": d.t_peel, "total": d.t_total},
+        "ell": r.ell, "grad": r.grad,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_sample(args, c)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -155,6 +155,14 @@ rsf_status gp_mle_eval(rsf_ctx ctx, const double* xy, const double* z, int64_t n
 const char* rsf_last_error(void);
 /* number of CUDA kernels launched by this thread so far (diagnostics) */
 int64_t rsf_kernel_launches(void);
+/* phase timings "name=seconds;..." collected when RSF_PROFILE=1 (stream-synchronising; diagnostics only) */
+const char* rsf_profile_dump(void);
+void rsf_profile_reset(void);
+/* batched-GEMM statistics for the roofline: CUDA events around every launch on its stream.
+ * rsf_stats_get fills {launches, seconds, algorithmic flops, compulsory bytes}. */
+void rsf_stats_enable(int on);
+void rsf_stats_get(double* out4);
+void rsf_stats_reset(void);
 
 #ifdef __cplusplus
 }

@@ -53,7 +53,8 @@ class rsf_eval_diag(C.Structure):
 
 EXPORTS = ["rsf_opts_default", "rsf_ctx_create", "rsf_ctx_destroy", "rsf_factor", "rsf_fact_destroy",
            "rsf_fact_info", "rsf_logdet", "rsf_solve", "rsf_apply", "rsf_sample", "peel_trace",
-           "gp_mle_eval", "rsf_last_error", "rsf_kernel_launches"]
+           "gp_mle_eval", "rsf_last_error", "rsf_kernel_launches", "rsf_profile_dump",
+           "rsf_profile_reset", "rsf_stats_enable", "rsf_stats_get", "rsf_stats_reset"]
 
 
 def load(path: str = LIB_PATH) -> C.CDLL:
@@ -82,8 +83,19 @@ def load(path: str = LIB_PATH) -> C.CDLL:
     lib.rsf_last_error.restype = C.c_char_p
     lib.rsf_kernel_launches.argtypes = []
     lib.rsf_kernel_launches.restype = C.c_int64
+    lib.rsf_profile_dump.argtypes = []
+    lib.rsf_profile_dump.restype = C.c_char_p
+    lib.rsf_profile_reset.argtypes = []
+    lib.rsf_profile_reset.restype = None
+    lib.rsf_stats_enable.argtypes = [C.c_int]
+    lib.rsf_stats_enable.restype = None
+    lib.rsf_stats_get.argtypes = [C.POINTER(C.c_double)]
+    lib.rsf_stats_get.restype = None
+    lib.rsf_stats_reset.argtypes = []
+    lib.rsf_stats_reset.restype = None
     for f in EXPORTS:
         if f not in ("rsf_ctx_destroy", "rsf_fact_destroy", "rsf_opts_default", "rsf_last_error",
-                     "rsf_kernel_launches"):
+                     "rsf_kernel_launches", "rsf_profile_dump", "rsf_profile_reset", "rsf_stats_enable",
+                     "rsf_stats_get", "rsf_stats_reset"):
             getattr(lib, f).restype = C.c_int
     return lib

@@ -330,4 +330,15 @@ const char* rsf_last_error(void) { return g_err.c_str(); }
 
 int64_t rsf_kernel_launches(void) { return rsf::g_launches; }
 
+const char* rsf_profile_dump(void) {
+  static thread_local std::string s;
+  s = rsf::Prof::dump();
+  return s.c_str();
+}
+void rsf_profile_reset(void) { rsf::Prof::reset(); }
+
+void rsf_stats_enable(int on) { rsf::KStats::on = on != 0; }
+void rsf_stats_get(double* out4) { rsf::KStats::collect(out4); }
+void rsf_stats_reset(void) { rsf::KStats::reset(); }
+
 }  // extern "C"

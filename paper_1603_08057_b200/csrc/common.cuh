@@ -85,6 +85,37 @@ struct DBuf {
 extern thread_local long long g_launches;
 inline void count_launch(long long k = 1) { g_launches += k; }
 
+// Phase profiler (enabled by RSF_PROFILE=1): synchronises the stream at the
+// scope boundaries and accumulates wall time per named phase.
+struct Prof {
+  static bool enabled();
+  static void add(const char* name, double sec);
+  static std::string dump();
+  static void reset();
+};
+struct PhaseTimer {
+  const char* name;
+  cudaStream_t s;
+  double t0 = 0;
+  bool on;
+  PhaseTimer(const char* n, cudaStream_t st);
+  ~PhaseTimer();
+};
+#define RSF_CAT2(a, b) a##b
+#define RSF_CAT(a, b) RSF_CAT2(a, b)
+#define RSF_PHASE(name, stream) ::rsf::PhaseTimer RSF_CAT(_rsf_pt_, __LINE__)(name, stream)
+
+// Kernel statistics for the roofline (enabled by rsf_stats_enable): CUDA events
+// around every batched-GEMM launch on its own stream, plus algorithmic flops.
+struct KStats {
+  static bool on;
+  static void record(cudaStream_t s, cudaEvent_t* e0, cudaEvent_t* e1);
+  static void push(cudaEvent_t e0, cudaEvent_t e1, double flops, double bytes);
+  // returns {launches, seconds, flops, bytes}; synchronises pending events
+  static void collect(double out[4]);
+  static void reset();
+};
+
 inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 
 }  // namespace rsf

@@ -9,6 +9,7 @@ namespace {
 
 constexpr int NT = 256;
 constexpr size_t SMEM_BUDGET = 200 * 1024;
+constexpr size_t SMEM_MAX = 227 * 1024;   // sm_100 opt-in dynamic shared memory per CTA
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -459,7 +460,7 @@ void geqrf_batched(cudaStream_t s, const std::vector<QRProb>& probs, bool keep_q
   static bool attr = false;
   if (!attr) {
     RSF_CUDA(cudaFuncSetAttribute(qr_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(SMEM_BUDGET + 16 * 1024)));
+                                  (int)SMEM_MAX));
     attr = true;
   }
   const int P = (int)probs.size();
@@ -494,7 +495,7 @@ void geqrf_batched(cudaStream_t s, const std::vector<QRProb>& probs, bool keep_q
       d.T = keep_q ? q.Tws + (long long)(j0 / QR_NB) * QR_NB * QR_NB : Tscr.p + toff[i];
       d.tau = keep_q && q.tau ? q.tau + j0 : nullptr;
       const size_t pbytes = (size_t)rows * nbp * sizeof(double);
-      d.smem = (pbytes <= SMEM_BUDGET) ? 1 : 0;
+      d.smem = (base_smem + pbytes <= SMEM_MAX) ? 1 : 0;
       if (d.smem) smem_need = std::max(smem_need, base_smem + pbytes);
       pd.push_back(d);
       const int j1 = j0 + nbp;
@@ -527,6 +528,51 @@ void geqrf_batched(cudaStream_t s, const std::vector<QRProb>& probs, bool keep_q
     g2.run(s);
     g3.run(s);
   }
+}
+
+void panel_step_batched(cudaStream_t s, const std::vector<PanelStep>& v) {
+  if (v.empty()) return;
+  static bool attr = false;
+  if (!attr) {
+    RSF_CUDA(cudaFuncSetAttribute(qr_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_MAX));
+    attr = true;
+  }
+  const size_t base_smem = (40 + QR_NB + 2 * QR_NB * QR_NB) * sizeof(double);
+  size_t smem_need = base_smem;
+  std::vector<PanelDesc> pd;
+  GemmBatch g1(true, false), g2(true, false), g3(false, false);
+  for (const PanelStep& q : v) {
+    PanelDesc d;
+    d.A = q.A; d.lda = q.lda; d.rows = q.rows; d.ncol = q.ncol;
+    d.V = q.V; d.T = q.T; d.tau = nullptr;
+    const size_t pbytes = (size_t)q.rows * q.ncol * sizeof(double);
+    d.smem = (base_smem + pbytes <= SMEM_MAX) ? 1 : 0;
+    if (d.smem) smem_need = std::max(smem_need, base_smem + pbytes);
+    pd.push_back(d);
+    if (q.c2 > 0) {
+      double* A2 = q.A + (long long)q.ncol * q.lda;
+      GemmDesc a = gdesc(q.ncol, q.c2, q.rows);
+      a.A = q.V; a.lda = q.rows; a.B = A2; a.ldb = (int)q.lda; a.C = q.W; a.ldc = QR_NB;
+      g1.add(a);
+      GemmDesc b = gdesc(q.ncol, q.c2, q.ncol);
+      b.A = q.T; b.lda = QR_NB; b.B = q.W; b.ldb = QR_NB; b.C = q.W2; b.ldc = QR_NB;
+      g2.add(b);
+      GemmDesc c = gdesc(q.rows, q.c2, q.ncol);
+      c.A = q.V; c.lda = q.rows; c.B = q.W2; c.ldb = QR_NB; c.C = A2; c.ldc = (int)q.lda;
+      c.alpha = -1.0; c.beta = 1.0;
+      g3.add(c);
+    }
+  }
+  auto dd = upload_descs(pd, s);
+  for (size_t o = 0; o < pd.size(); o += 65535) {
+    unsigned nb = (unsigned)std::min<size_t>(65535, pd.size() - o);
+    qr_panel_kernel<<<nb, NT, smem_need, s>>>(dd.p + o);
+    count_launch();
+    RSF_LAUNCH_CHECK();
+  }
+  g1.run(s);
+  g2.run(s);
+  g3.run(s);
 }
 
 void ormqr_batched(cudaStream_t s, const std::vector<QApplyProb>& probs, bool trans) {

@@ -57,6 +57,17 @@ struct PotrfProb {
 // d_logsum[i] = sum_j log L_jj; d_info[i] = 0 or (1 + first failing column).
 void potrf_batched(cudaStream_t s, const std::vector<PotrfProb>& probs, double* d_logsum, int* d_info);
 
+// One Householder panel step: factor the panel A(j0:m, j0:j0+ncol) (A points at
+// A(j0, j0)), then apply Q^T of the panel to the c2 trailing columns (compact WY
+// on the batched GEMM).  V (rows x ncol), T (QR_NB^2), W/W2 (QR_NB x c2) are
+// caller workspaces; T is kept if the caller needs Q later.
+struct PanelStep {
+  double* A; long long lda;
+  int rows, ncol, c2;
+  double* V; double* T; double* W; double* W2;
+};
+void panel_step_batched(cudaStream_t s, const std::vector<PanelStep>& v);
+
 struct CopyProb {
   const double* src; long long lds;
   double* dst; long long ldd;

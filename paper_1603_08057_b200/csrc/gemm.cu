@@ -2,11 +2,88 @@
 // 256 threads, CTA tile BM x 64, BK = 16, each thread TM x 4 outputs with an
 // interleaved (bank-conflict-free) column pattern; global->register prefetch
 // of the next K-slab overlaps the FMA loop.
+#include <ctime>
+#include <cstdlib>
+
 #include "gemm.cuh"
 
 namespace rsf {
 
 thread_local long long g_launches = 0;
+
+namespace {
+std::vector<std::pair<std::string, double>>& prof_table() {
+  static std::vector<std::pair<std::string, double>> t;
+  return t;
+}
+double wall() {
+  timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return ts.tv_sec + 1e-9 * ts.tv_nsec;
+}
+}  // namespace
+
+bool KStats::on = false;
+namespace {
+struct KRec { cudaEvent_t a, b; double flops, bytes; };
+std::vector<KRec>& krecs() { static std::vector<KRec> v; return v; }
+std::vector<cudaEvent_t>& kpool() { static std::vector<cudaEvent_t> v; return v; }
+double k_launch = 0, k_sec = 0, k_flops = 0, k_bytes = 0;
+cudaEvent_t get_ev() {
+  auto& p = kpool();
+  if (!p.empty()) { cudaEvent_t e = p.back(); p.pop_back(); return e; }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+void drain() {
+  for (auto& r : krecs()) {
+    cudaEventSynchronize(r.b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    k_launch += 1; k_sec += ms * 1e-3; k_flops += r.flops; k_bytes += r.bytes;
+    kpool().push_back(r.a);
+    kpool().push_back(r.b);
+  }
+  krecs().clear();
+}
+}  // namespace
+void KStats::record(cudaStream_t s, cudaEvent_t* e0, cudaEvent_t* e1) {
+  if (e0) { *e0 = get_ev(); cudaEventRecord(*e0, s); }
+  if (e1) { *e1 = get_ev(); cudaEventRecord(*e1, s); }
+}
+void KStats::push(cudaEvent_t e0, cudaEvent_t e1, double flops, double bytes) {
+  krecs().push_back(KRec{e0, e1, flops, bytes});
+  if (krecs().size() > 4096) drain();
+}
+void KStats::collect(double out[4]) {
+  drain();
+  out[0] = k_launch; out[1] = k_sec; out[2] = k_flops; out[3] = k_bytes;
+}
+void KStats::reset() { drain(); k_launch = k_sec = k_flops = k_bytes = 0; }
+
+bool Prof::enabled() {
+  static int e = -1;
+  if (e < 0) { const char* v = getenv("RSF_PROFILE"); e = (v && v[0] == '1') ? 1 : 0; }
+  return e == 1;
+}
+void Prof::add(const char* name, double sec) {
+  for (auto& p : prof_table())
+    if (p.first == name) { p.second += sec; return; }
+  prof_table().emplace_back(name, sec);
+}
+std::string Prof::dump() {
+  std::string r;
+  for (auto& p : prof_table()) r += p.first + "=" + std::to_string(p.second) + ";";
+  return r;
+}
+void Prof::reset() { prof_table().clear(); }
+PhaseTimer::PhaseTimer(const char* n, cudaStream_t st) : name(n), s(st), on(Prof::enabled()) {
+  if (on) { cudaStreamSynchronize(s); t0 = wall(); }
+}
+PhaseTimer::~PhaseTimer() {
+  if (on) { cudaStreamSynchronize(s); Prof::add(name, wall() - t0); }
+}
 
 namespace {
 
@@ -213,12 +290,25 @@ void GemmBatch::run(cudaStream_t s, double* X0, double* X1, int ldx, int Mglob) 
   if (totalN_ == 0) return;
   int M = std::max(maxM_, glob_ ? Mglob : 0);
   if (M <= 0) return;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (KStats::on) KStats::record(s, &e0, nullptr);
   if (M <= 16) {
     dim3 grid(totalN_, ceil_div(M, 16));
     launch_variant<16, 1>(ta_, tb_, grid, s, d_.p, prefix_.p, (int)h_.size(), X0, X1, ldx, Mglob);
   } else {
     dim3 grid(totalN_, ceil_div(M, 64));
     launch_variant<64, 4>(ta_, tb_, grid, s, d_.p, prefix_.p, (int)h_.size(), X0, X1, ldx, Mglob);
+  }
+  if (KStats::on) {
+    KStats::record(s, nullptr, &e1);
+    // algorithmic flops 2MNK; compulsory bytes: A, B read once, C written (and read if beta != 0)
+    double f = 0, b = 0;
+    for (const auto& d : h_) {
+      const double m = d.M < 0 ? Mglob : d.M;
+      f += 2.0 * m * d.N * d.K;
+      b += 8.0 * (m * d.K + (double)d.K * d.N + m * d.N * (d.beta != 0.0 ? 2.0 : 1.0));
+    }
+    KStats::push(e0, e1, f, b);
   }
   count_launch();
   RSF_LAUNCH_CHECK();

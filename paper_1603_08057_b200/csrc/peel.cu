@@ -20,6 +20,7 @@
 
 #include "dense.cuh"
 #include "peel.cuh"
+#include "rrqr.cuh"
 #include "rsf_kernels.cuh"
 
 namespace rsf {
@@ -95,34 +96,13 @@ __global__ void transpose_kernel(const TrDesc* __restrict__ descs) {
   }
 }
 
-// U (ni x k, ld ni) <- Q_R E_k padded: identity, then the CPQR reflectors in reverse
-struct URDesc { double* U; int ni, q, k; const double* Rv; const double* tau; };
-__global__ void form_qr_columns_kernel(const URDesc* __restrict__ descs) {
-  const URDesc d = descs[blockIdx.x];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (long long e = tid; e < (long long)d.ni * d.k; e += NT) {
+// U (ni x k, ld ni) <- [I_k; 0]
+struct EyeDesc { double* U; int ni, k; };
+__global__ void eye_kernel(const EyeDesc* __restrict__ descs) {
+  const EyeDesc d = descs[blockIdx.y];
+  for (long long e = blockIdx.x * (long long)NT + threadIdx.x; e < (long long)d.ni * d.k; e += (long long)gridDim.x * NT) {
     const int r = (int)(e % d.ni), c = (int)(e / d.ni);
     d.U[e] = (r == c) ? 1.0 : 0.0;
-  }
-  __syncthreads();
-  for (int i = d.k - 1; i >= 0; --i) {
-    const double tau = d.tau[i];
-    if (tau != 0.0) {
-      const double* v = d.Rv + (long long)i * d.q;   // v(i) = 1, v(r>i) = Rv(r, i)
-      for (int j = i + warp; j < d.k; j += NT / 32) {
-        double* y = d.U + (long long)j * d.ni;
-        double dot = 0.0;
-        for (int r = i + 1 + lane; r < d.q; r += 32) dot += v[r] * y[r];
-#pragma unroll
-        for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-        dot += y[i];
-        const double w = tau * dot;
-        for (int r = i + 1 + lane; r < d.q; r += 32) y[r] -= w * v[r];
-        __syncwarp();
-        if (lane == 0) y[i] -= w;
-      }
-    }
-    __syncthreads();
   }
 }
 
@@ -206,6 +186,7 @@ struct GOp {
   }
   // Y = G X (X preserved), X and Y are k x n
   void apply(const double* X, double* Y, int k) {
+    RSF_PHASE("p.G_apply", s);
     reserve(k);
     const size_t bytes = (size_t)F.n() * k * sizeof(double);
     columns += k;
@@ -239,15 +220,17 @@ struct PairLR {
 struct PeelLevel {
   std::vector<PairLR> pairs;
   DBuf<double> U, M;
+  std::vector<DBuf<double>> Ubufs;
   GemmBatch g1, g2, g3;
+  std::vector<GemmBatch> g3s;
   long long tcols = 0;   // temp columns per probe column
   bool empty() const { return g1.empty(); }
   // Y' -= G^(m) X'   (X', Y' are k x n; tmp has k * tcols doubles)
   void subtract(cudaStream_t s, const double* X, double* Y, int k, double* tmp) const {
-    if (g1.empty()) return;
+    if (g2.empty()) return;
     g1.run(s, const_cast<double*>(X), tmp, k, k);
     g2.run(s, nullptr, tmp, k, k);
-    g3.run(s, Y, tmp, k, k);
+    for (const auto& g : g3s) g.run(s, Y, tmp, k, k);
   }
 };
 
@@ -279,6 +262,7 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
   const Tree& t = *F.tree;
   const int n = t.n, L = t.L;
   const unsigned long long seed = o.seed;
+  const unsigned seed32 = (unsigned)(seed & 0xffffffffull);
   GOp G(F, Fi);
   std::vector<PeelLevel> peeled(L + 1);
   long long max_tcols = 0;
@@ -287,37 +271,43 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
   pd.rank_max.assign(L + 1, 0);
   int prev_rank = -1;
   const int kb = std::max(16, o.probe_block);
+  const double budget = 24.0 * (1ull << 30);   // bytes of transient per-batch buffers
 
   auto residual = [&](const double* W, double* Y, int k, int upto) {
     G.apply(W, Y, k);
     DBuf<double> tmp((size_t)std::max<long long>(max_tcols, 1) * k, s);
+    RSF_PHASE("p.subtract", s);
     for (int m = 1; m < upto; ++m) peeled[m].subtract(s, W, Y, k, tmp.p);
   };
 
   for (int lev = 1; lev <= L; ++lev) {
     const std::vector<int>& nodes = t.levels[lev];
     const int nb = (int)nodes.size();
-    // ordered sibling pairs (Def. sibs)
+    // ordered sibling pairs (Def. sibs), grouped by the probe group quad(j)
     std::vector<PairLR> pairs;
     std::unordered_map<int, std::vector<int>> fam;
     for (int b = 0; b < nb; ++b) fam[t.parent[nodes[b]]].push_back(b);
     for (int b = 0; b < nb; ++b) {
-      const auto& sib = fam[t.parent[nodes[b]]];
-      for (int c : sib) {
-        if (c == b) continue;
+      for (int c2 : fam[t.parent[nodes[b]]]) {
+        if (c2 == b) continue;
         PairLR p;
-        p.i = b; p.j = c;
+        p.i = b; p.j = c2;
         p.ib = t.begin[nodes[b]]; p.ni = t.end[nodes[b]] - p.ib;
-        p.jb = t.begin[nodes[c]]; p.nj = t.end[nodes[c]] - p.jb;
+        p.jb = t.begin[nodes[c2]]; p.nj = t.end[nodes[c2]] - p.jb;
         pairs.push_back(p);
       }
     }
     if (pairs.empty()) continue;
+    const size_t P = pairs.size();
     {
       std::unordered_map<long long, int> idx;
-      for (int q = 0; q < (int)pairs.size(); ++q) idx[(long long)pairs[q].i * nb + pairs[q].j] = q;
+      for (int q = 0; q < (int)P; ++q) idx[(long long)pairs[q].i * nb + pairs[q].j] = q;
       for (auto& p : pairs) p.rev = idx[(long long)p.j * nb + p.i];
     }
+    std::vector<std::vector<int>> grp(4);
+    for (size_t q = 0; q < P; ++q) grp[t.quad[nodes[pairs[q].j]]].push_back((int)q);
+    std::vector<int> gorder = {0, 1, 2, 3};
+    std::stable_sort(gorder.begin(), gorder.end(), [&](int a2, int b2) { return grp[a2].size() > grp[b2].size(); });
     std::vector<int> hq(n, -1);
     int maxni = 0;
     for (int b = 0; b < nb; ++b) {
@@ -326,207 +316,195 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
       maxni = std::max(maxni, t.end[nd] - t.begin[nd]);
     }
     DBuf<int> qmap = up(hq, s);
-    const int cmax = maxni + o.oversample;
-    int c = (prev_rank < 0) ? o.peel_start : (int)std::ceil(0.7 * prev_rank) + o.oversample;
+    const int cmax = ((maxni + o.oversample) + 7) / 8 * 8;
+    // initial width: level 1 from the factor's level-1 skeleton sizes (ranks of Sigma's
+    // off-diagonal blocks at eps_fact); deeper levels from the previous level's ranks (R-M)
+    int hint = o.peel_start;
+    if (prev_rank < 0 && F.levels.size() > 1)
+      for (int kk : F.levels[1].k) hint = std::max(hint, kk);
+    int c = (prev_rank < 0) ? hint : prev_rank + o.oversample;
     c = std::min(std::max(c, o.oversample + 8), cmax);
     c = (c + 7) / 8 * 8;
-    int cap = 0, have = 0;
-    DBuf<double> Yg[4];
-    std::vector<int> kp(pairs.size(), 0);
-    // QR factors of the final sketches (kept when they fit one batch)
-    DBuf<double> Qws, Tws, Rout, tau;
-    std::vector<long long> qoff(pairs.size()), toffv(pairs.size()), roff(pairs.size()), tauoff(pairs.size());
+
+    PeelLevel& PL = peeled[lev];
+    std::vector<DBuf<double>> keep;          // U, A1, P buffers of this level
+    std::vector<double*> Up(P, nullptr), A1p(P, nullptr), Pp(P, nullptr);
+    std::vector<int> kp(P, 0);
+    int mr = 0;
     while (true) {
-      if (c > cap) {   // grow the sketch buffers (keep computed rows)
-        int ncap = c;
-        for (int g = 0; g < 4; ++g) {
-          DBuf<double> nbuf((size_t)ncap * n, s);
-          if (have > 0) {   // keep the computed rows [0, have)
-            std::vector<CopyProb> cp{CopyProb{Yg[g].p, cap, nbuf.p, ncap, have, n, 1.0}};
-            copy_batched(s, cp);
-          }
-          Yg[g] = std::move(nbuf);
-        }
-        cap = ncap;
-      }
-      // new probe columns [have, c) for every group
-      for (int g = 0; g < 4; ++g) {
-        for (int c0 = have; c0 < c; c0 += kb) {
+      keep.clear();
+      bool fail = false;
+      mr = 0;
+      for (int g : gorder) {
+        if (grp[g].empty()) continue;
+        // sketch Y_g = (G - sum_{m<l} G^(m)) W_g in column chunks
+        std::vector<DBuf<double>> ych;
+        std::vector<int> ycs, ykk;
+        for (int c0 = 0; c0 < c; c0 += kb) {
           const int k = std::min(kb, c - c0);
           DBuf<double> W((size_t)n * k, s), Y((size_t)n * k, s);
           gen_probes(s, W.p, k, n, t.d_perm.p, qmap.p, g, c0, lev, trace_id, seed);
           residual(W.p, Y.p, k, lev);
-          rowblock_copy_kernel<<<gxx((long long)n * k), NT, 0, s>>>(Yg[g].p, cap, c0, Y.p, k, n);
-          count_launch();
-          RSF_LAUNCH_CHECK();
+          ych.push_back(std::move(Y));
+          ycs.push_back(c0);
+          ykk.push_back(k);
         }
+        // pair batches under the byte budget
+        const std::vector<int>& gq = grp[g];
+        size_t q0 = 0;
+        while (q0 < gq.size() && !fail) {
+          size_t q1 = q0;
+          double bytes = 0;
+          while (q1 < gq.size()) {
+            const auto& p = pairs[gq[q1]];
+            const double bb = 8.0 * (2.0 * p.ni * (double)c + 2.0 * (double)c * c);
+            if (q1 > q0 && bytes + bb > budget) break;
+            bytes += bb;
+            ++q1;
+          }
+          const size_t B = q1 - q0;
+          std::vector<long long> qo(B), to(B), wo(B), po(B);
+          long long qt = 0, tt = 0, wt = 0, pt = 0;
+          for (size_t x = 0; x < B; ++x) {
+            const auto& p = pairs[gq[q0 + x]];
+            const int qq = std::min(p.ni, c);
+            qo[x] = qt; qt += (long long)p.ni * c;
+            to[x] = tt; tt += (long long)((qq + QR_NB - 1) / QR_NB) * QR_NB * QR_NB;
+            wo[x] = wt; wt += (long long)c * p.ni;
+            po[x] = pt; pt += (long long)c * c;
+          }
+          DBuf<double> Qws(qt, s), Tws(std::max<long long>(tt, 1), s), Wi(wt, s);
+          DBuf<double> Pb(pt, s);
+          DBuf<int> dpv((size_t)c * B, s);
+          std::vector<int> kk;
+          std::vector<int> kdone;
+          {
+            RSF_PHASE("p.orth_rank", s);
+            std::vector<TrDesc> td;
+            for (size_t x = 0; x < B; ++x) {
+              const auto& p = pairs[gq[q0 + x]];
+              for (size_t ci = 0; ci < ych.size(); ++ci)
+                td.push_back(TrDesc{ych[ci].p + (long long)p.ib * ykk[ci], ykk[ci],
+                                    Qws.p + qo[x] + (long long)ycs[ci] * p.ni, p.ni, ykk[ci]});
+              // W_i^T (c x n_i): the same Philox entries as in the sketches
+              probes_kernel<<<gxx((long long)p.ni * c), NT, 0, s>>>(Wi.p + wo[x], c, p.ib, p.ib + p.ni, t.d_perm.p,
+                                                                  nullptr, 0, 0, lev, trace_id, seed32, c);
+              count_launch();
+            }
+            auto dtd = up(td, s);
+            for (size_t o2 = 0; o2 < td.size(); o2 += 65535) {
+              unsigned nz = (unsigned)std::min<size_t>(65535, td.size() - o2);
+              transpose_kernel<<<dim3(64, 1, nz), NT, 0, s>>>(dtd.p + o2);
+              count_launch();
+              RSF_LAUNCH_CHECK();
+            }
+            GemmBatch gp(false, false);   // P_ij = W_i^T Y_ij (c x c)
+            for (size_t x = 0; x < B; ++x) {
+              const auto& p = pairs[gq[q0 + x]];
+              GemmDesc d = gdesc(c, c, p.ni);
+              d.A = Wi.p + wo[x]; d.lda = c; d.B = Qws.p + qo[x]; d.ldb = p.ni; d.C = Pb.p + po[x]; d.ldc = c;
+              gp.add(d);
+              pd.flops += 2.0 * c * (double)c * p.ni;
+            }
+            gp.run(s);
+            std::vector<RRQRProb> rp;
+            for (size_t x = 0; x < B; ++x) {
+              const auto& p = pairs[gq[q0 + x]];
+              rp.push_back(RRQRProb{Qws.p + qo[x], p.ni, p.ni, c, dpv.p + (long long)x * c, Tws.p + to[x], nullptr, 0});
+            }
+            RRQRResult rr = rrqr_batched(s, rp, o.eps_peel,
+                                         seed ^ (0xD1B54A32D192ED03ull * (unsigned long long)(lev + 64 * (trace_id + 1))));
+            kk = rr.k;
+            kdone = rr.done;
+          }
+          for (size_t x = 0; x < B; ++x) mr = std::max(mr, kk[x]);
+          if (mr > c - o.oversample && c < cmax) { fail = true; break; }
+          // U_ij = Q [I_k; 0] (orth) and A1_ij = W_i^T U_ij
+          long long ut = 0, at = 0;
+          std::vector<long long> uo(B), ao(B);
+          for (size_t x = 0; x < B; ++x) {
+            uo[x] = ut; ut += (long long)pairs[gq[q0 + x]].ni * kk[x];
+            ao[x] = at; at += (long long)c * kk[x];
+          }
+          DBuf<double> Ub(std::max<long long>(ut, 1), s), Ab(std::max<long long>(at, 1), s);
+          {
+            RSF_PHASE("p.form_U", s);
+            std::vector<EyeDesc> ed;
+            std::vector<QApplyProb> ap;
+            GemmBatch ga(false, false);
+            long long mx = 0;
+            for (size_t x = 0; x < B; ++x) {
+              const auto& p = pairs[gq[q0 + x]];
+              if (kk[x] == 0) continue;
+              ed.push_back(EyeDesc{Ub.p + uo[x], p.ni, kk[x]});
+              mx = std::max(mx, (long long)p.ni * kk[x]);
+              ap.push_back(QApplyProb{Qws.p + qo[x], p.ni, p.ni, kdone[x], Tws.p + to[x], Ub.p + uo[x], p.ni, kk[x]});
+              GemmDesc d = gdesc(c, kk[x], p.ni);
+              d.A = Wi.p + wo[x]; d.lda = c; d.B = Ub.p + uo[x]; d.ldb = p.ni; d.C = Ab.p + ao[x]; d.ldc = c;
+              ga.add(d);
+            }
+            if (!ed.empty()) {
+              auto de = up(ed, s);
+              for (size_t o2 = 0; o2 < ed.size(); o2 += 65535) {
+                unsigned nz = (unsigned)std::min<size_t>(65535, ed.size() - o2);
+                eye_kernel<<<dim3(gxx(mx), nz), NT, 0, s>>>(de.p + o2);
+                count_launch();
+                RSF_LAUNCH_CHECK();
+              }
+              ormqr_batched(s, ap, false);
+              ga.run(s);
+            }
+          }
+          for (size_t x = 0; x < B; ++x) {
+            const int q = gq[q0 + x];
+            kp[q] = kk[x];
+            Up[q] = Ub.p + uo[x];
+            A1p[q] = Ab.p + ao[x];
+            Pp[q] = Pb.p + po[x];
+          }
+          keep.push_back(std::move(Ub));
+          keep.push_back(std::move(Ab));
+          keep.push_back(std::move(Pb));
+          q0 = q1;
+        }
+        if (fail) break;
       }
-      have = c;
-      // sketches Y_ij = Y_{quad(j)}(I_i, 0:c) -> QR -> truncated CPQR (ranks)
-      long long qtot = 0, ttot = 0, rtot = 0, tautot = 0;
-      for (size_t q = 0; q < pairs.size(); ++q) {
-        const auto& p = pairs[q];
-        const int qq = std::min(p.ni, c);
-        qoff[q] = qtot; qtot += (long long)p.ni * c;
-        toffv[q] = ttot; ttot += (long long)((qq + QR_NB - 1) / QR_NB) * QR_NB * QR_NB;
-        roff[q] = rtot; rtot += (long long)qq * c;
-        tauoff[q] = tautot; tautot += std::max(qq, 1);
-      }
-      Qws.alloc(qtot, s);
-      Tws.alloc(std::max<long long>(ttot, 1), s);
-      Rout.alloc(std::max<long long>(rtot, 1), s);
-      tau.alloc(std::max<long long>(tautot * 2, 1), s);
-      {
-        std::vector<TrDesc> td;
-        std::vector<QRProb> qp;
-        for (size_t q = 0; q < pairs.size(); ++q) {
-          const auto& p = pairs[q];
-          const int gj = t.quad[nodes[p.j]];
-          td.push_back(TrDesc{Yg[gj].p + (long long)p.ib * cap, cap, Qws.p + qoff[q], p.ni, c});
-          qp.push_back(QRProb{Qws.p + qoff[q], p.ni, p.ni, c, Tws.p + toffv[q], tau.p + tautot + tauoff[q]});
-        }
-        auto dtd = up(td, s);
-        for (size_t o2 = 0; o2 < td.size(); o2 += 65535) {
-          unsigned nz = (unsigned)std::min<size_t>(65535, td.size() - o2);
-          transpose_kernel<<<dim3(64, 1, nz), NT, 0, s>>>(dtd.p + o2);
-          count_launch();
-          RSF_LAUNCH_CHECK();
-        }
-        geqrf_batched(s, qp, true);
-        std::vector<CPQRProb> cp;
-        DBuf<int> dpv((size_t)c * pairs.size(), s), dk(pairs.size(), s);
-        long long wtot = 0;
-        std::vector<long long> wo(pairs.size(), -1);
-        for (size_t q = 0; q < pairs.size(); ++q) {
-          const int qq = std::min(pairs[q].ni, c);
-          if ((size_t)qq * c * 8 + (72 + 2 * (size_t)c + 64) * 8 > 200 * 1024) { wo[q] = wtot; wtot += (long long)qq * c; }
-        }
-        DBuf<double> W(std::max<long long>(wtot, 1), s);
-        for (size_t q = 0; q < pairs.size(); ++q) {
-          const auto& p = pairs[q];
-          CPQRProb pr;
-          pr.R = Qws.p + qoff[q]; pr.ldr = p.ni; pr.q = std::min(p.ni, c); pr.c = c;
-          pr.W = wo[q] >= 0 ? W.p + wo[q] : nullptr;
-          pr.T = nullptr; pr.piv = dpv.p + (long long)q * c;
-          pr.Rout = Rout.p + roff[q]; pr.tau = tau.p + tauoff[q];
-          cp.push_back(pr);
-        }
-        cpqr_id_batched(s, cp, o.eps_peel, dk.p, false);
-        kp = dk.to_host(pairs.size());
-      }
-      int mr = 0;
-      for (int v : kp) mr = std::max(mr, v);
-      if (mr <= c - o.oversample || c >= cmax) {
-        pd.rank_max[lev] = mr;
-        break;
-      }
-      int nc = (mr >= c - 1) ? 2 * c : std::max(c + 8, (int)std::ceil(1.25 * mr) + o.oversample);
-      nc = std::min((nc + 7) / 8 * 8, (cmax + 7) / 8 * 8);
-      c = std::max(nc, c + 8);
+      if (!fail) break;
+      int nc = (mr >= c - 1) ? (int)std::ceil(1.5 * c) : std::max(c + 8, (int)std::ceil(1.2 * mr) + o.oversample);
+      c = std::max(std::min((nc + 7) / 8 * 8, cmax), c + 8);
     }
     pd.cols[lev] = c;
-    prev_rank = pd.rank_max[lev];
+    pd.rank_max[lev] = mr;
+    prev_rank = mr;
 
-    // ---- U_ij = Q [Q_R E_k ; 0]
-    PeelLevel& PL = peeled[lev];
-    long long utot = 0;
-    for (size_t q = 0; q < pairs.size(); ++q) {
-      pairs[q].kij = kp[q];
-      pairs[q].uoff = utot;
-      utot += (long long)pairs[q].ni * kp[q];
-    }
-    PL.U.alloc(std::max<long long>(utot, 1), s);
+    // ---- cores M_ij = (A1_ij)^+ P_ij (A1_ji^T)^+   (Eq. lowrankapprox; U_ji^T W_j = A1_ji^T)
+    DBuf<double> Mbuf;
+    std::vector<long long> moff(P, -1);
     {
-      std::vector<URDesc> ud;
-      std::vector<QApplyProb> ap;
-      for (size_t q = 0; q < pairs.size(); ++q) {
-        const auto& p = pairs[q];
-        if (p.kij == 0) continue;
-        ud.push_back(URDesc{PL.U.p + p.uoff, p.ni, std::min(p.ni, c), p.kij, Rout.p + roff[q], tau.p + tauoff[q]});
-        ap.push_back(QApplyProb{Qws.p + qoff[q], p.ni, p.ni, c, Tws.p + toffv[q], PL.U.p + p.uoff, p.ni, p.kij});
-      }
-      if (!ud.empty()) {
-        auto dud = up(ud, s);
-        for (size_t o2 = 0; o2 < ud.size(); o2 += 65535) {
-          unsigned nz = (unsigned)std::min<size_t>(65535, ud.size() - o2);
-          form_qr_columns_kernel<<<nz, NT, 0, s>>>(dud.p + o2);
-          count_launch();
-          RSF_LAUNCH_CHECK();
-        }
-        ormqr_batched(s, ap, false);
-      }
-    }
-    Qws.release(); Tws.release(); Rout.release(); tau.release();
-
-    // ---- cores M_ij (Eq. lowrankapprox) via normal equations of the Gaussian sketches
-    {
-      const size_t P = pairs.size();
-      std::vector<long long> woff(P), a1off(P), poff(P), b2off(P), g1off(P), g2off(P), t1off(P), t2off(P), moff(P);
-      long long wt = 0, a1t = 0, pt = 0, b2t = 0, g1t = 0, g2t = 0, t1t = 0, t2t = 0, mt = 0;
-      std::vector<long long> boxw(nb, -1);
-      for (int b = 0; b < nb; ++b) { boxw[b] = wt; wt += (long long)c * (t.end[nodes[b]] - t.begin[nodes[b]]); }
+      RSF_PHASE("p.cores", s);
+      std::vector<long long> g1o(P), t1o(P), t2o(P);
+      long long g1t = 0, t1t = 0, t2t = 0, mt = 0;
       for (size_t q = 0; q < P; ++q) {
-        const auto& p = pairs[q];
-        const int k1 = p.kij, k2 = pairs[p.rev].kij;
-        a1off[q] = a1t; a1t += (long long)c * k1;
-        poff[q] = pt; pt += (long long)c * c;
-        b2off[q] = b2t; b2t += (long long)k2 * c;
-        g1off[q] = g1t; g1t += (long long)k1 * k1;
-        g2off[q] = g2t; g2t += (long long)k2 * k2;
-        t1off[q] = t1t; t1t += (long long)k1 * c;
-        t2off[q] = t2t; t2t += (long long)k1 * k2;
-        moff[q] = mt; mt += (long long)k1 * k2;
+        const int k1 = kp[q], k2 = kp[pairs[q].rev];
+        g1o[q] = g1t; g1t += (long long)k1 * k1;
+        t1o[q] = t1t; t1t += (long long)k1 * c;
+        t2o[q] = t2t; t2t += (long long)k1 * k2;
+        if (k1 > 0 && k2 > 0) { moff[q] = mt; mt += (long long)k1 * k2; }
       }
-      DBuf<double> Wb(std::max<long long>(wt, 1), s), A1(std::max<long long>(a1t, 1), s), Pm(std::max<long long>(pt, 1), s),
-          B2(std::max<long long>(b2t, 1), s), G1(std::max<long long>(g1t, 1), s), G1i(std::max<long long>(g1t, 1), s),
-          G2(std::max<long long>(g2t, 1), s), G2i(std::max<long long>(g2t, 1), s), T1(std::max<long long>(t1t, 1), s),
-          T2(std::max<long long>(t2t, 1), s), T3(std::max<long long>(t2t, 1), s);
-      PL.M.alloc(std::max<long long>(mt, 1), s);
-      // probes of every box: W_b^T as (c x n_b), the same Philox entries as in the sketches
-      for (int b = 0; b < nb; ++b) {
-        const int nd = nodes[b];
-        const int ni = t.end[nd] - t.begin[nd];
-        probes_kernel<<<gxx((long long)ni * c), NT, 0, s>>>(Wb.p + boxw[b], c, t.begin[nd], t.end[nd], t.d_perm.p,
-                                                            nullptr, 0, 0, lev, trace_id,
-                                                            (unsigned)(seed & 0xffffffffull), c);
-        count_launch();
-      }
-      RSF_LAUNCH_CHECK();
-      GemmBatch ga1(false, false), gp(false, true), gb2(true, true), gg1(true, false), gg2(false, true);
+      DBuf<double> G1(std::max<long long>(g1t, 1), s), G1i(std::max<long long>(g1t, 1), s),
+          T1(std::max<long long>(t1t, 1), s), T2(std::max<long long>(t2t, 1), s), T3(std::max<long long>(t2t, 1), s);
+      Mbuf.alloc(std::max<long long>(mt, 1), s);
+      GemmBatch gg(true, false);
       std::vector<PotrfProb> pp;
-      std::vector<int> ppq;
       for (size_t q = 0; q < P; ++q) {
-        const auto& p = pairs[q];
-        const int k1 = p.kij, k2 = pairs[p.rev].kij;
-        if (k1 == 0 || k2 == 0) continue;
-        const double* Wi = Wb.p + boxw[p.i];
-        const double* Wj = Wb.p + boxw[p.j];
-        const int gj = t.quad[nodes[p.j]];
-        GemmDesc a = gdesc(c, k1, p.ni);            // A1 = W_i^T U_ij
-        a.A = Wi; a.lda = c; a.B = PL.U.p + p.uoff; a.ldb = p.ni; a.C = A1.p + a1off[q]; a.ldc = c;
-        ga1.add(a);
-        GemmDesc b = gdesc(c, c, p.ni);             // P = W_i^T Y_ij   (Y_ij^T stored c x ni)
-        b.A = Wi; b.lda = c; b.B = Yg[gj].p + (long long)p.ib * cap; b.ldb = cap; b.C = Pm.p + poff[q]; b.ldc = c;
-        gp.add(b);
-        GemmDesc d = gdesc(k2, c, p.nj);            // B2 = U_ji^T W_j
-        d.A = PL.U.p + pairs[p.rev].uoff; d.lda = p.nj; d.B = Wj; d.ldb = c; d.C = B2.p + b2off[q]; d.ldc = k2;
-        gb2.add(d);
+        const int k1 = kp[q];
+        if (k1 == 0) continue;
         GemmDesc e = gdesc(k1, k1, c);              // G1 = A1^T A1
-        e.A = A1.p + a1off[q]; e.lda = c; e.B = A1.p + a1off[q]; e.ldb = c; e.C = G1.p + g1off[q]; e.ldc = k1;
-        gg1.add(e);
-        GemmDesc f = gdesc(k2, k2, c);              // G2 = B2 B2^T
-        f.A = B2.p + b2off[q]; f.lda = k2; f.B = B2.p + b2off[q]; f.ldb = k2; f.C = G2.p + g2off[q]; f.ldc = k2;
-        gg2.add(f);
-        pp.push_back(PotrfProb{G1.p + g1off[q], k1, k1, G1i.p + g1off[q], k1});
-        pp.push_back(PotrfProb{G2.p + g2off[q], k2, k2, G2i.p + g2off[q], k2});
-        ppq.push_back((int)q);
-        pd.flops += 2.0 * c * k1 * p.ni + 2.0 * c * c * p.ni + 2.0 * k2 * c * p.nj;
+        e.A = A1p[q]; e.lda = c; e.B = A1p[q]; e.ldb = c; e.C = G1.p + g1o[q]; e.ldc = k1;
+        gg.add(e);
+        pp.push_back(PotrfProb{G1.p + g1o[q], k1, k1, G1i.p + g1o[q], k1});
       }
-      ga1.run(s);
-      gp.run(s);
-      gb2.run(s);
-      gg1.run(s);
-      gg2.run(s);
+      gg.run(s);
       DBuf<double> ls(std::max<size_t>(pp.size(), 1), s);
       DBuf<int> inf(std::max<size_t>(pp.size(), 1), s);
       potrf_batched(s, pp, ls.p, inf.p);
@@ -535,82 +513,99 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
         for (size_t x = 0; x < hi.size(); ++x)
           if (hi[x]) throw Error(ST_ENUMERIC, "peeling: rank-deficient sketch product at level " + std::to_string(lev));
       }
-      GemmBatch m1(true, false), m2(false, true), m3(false, false), m4(true, false), m5(false, true), m6(false, false);
-      for (size_t q : ppq) {
-        const auto& p = pairs[q];
-        const int k1 = p.kij, k2 = pairs[p.rev].kij;
-        GemmDesc a = gdesc(k1, c, c);     // T1 = A1^T P
-        a.A = A1.p + a1off[q]; a.lda = c; a.B = Pm.p + poff[q]; a.ldb = c; a.C = T1.p + t1off[q]; a.ldc = k1;
+      GemmBatch m1(true, false), m2(false, false), m3(false, false), m4(true, false), m5(false, true), m6(false, false);
+      for (size_t q = 0; q < P; ++q) {
+        const int k1 = kp[q], rq = pairs[q].rev, k2 = kp[rq];
+        if (moff[q] < 0) continue;
+        const double* L1i = G1i.p + g1o[q];
+        const double* L2i = G1i.p + g1o[rq];
+        GemmDesc a = gdesc(k1, c, c);     // T1 = A1_ij^T P_ij
+        a.A = A1p[q]; a.lda = c; a.B = Pp[q]; a.ldb = c; a.C = T1.p + t1o[q]; a.ldc = k1;
         m1.add(a);
-        GemmDesc b = gdesc(k1, k2, c);    // T2 = T1 B2^T
-        b.A = T1.p + t1off[q]; b.lda = k1; b.B = B2.p + b2off[q]; b.ldb = k2; b.C = T2.p + t2off[q]; b.ldc = k1;
+        GemmDesc b = gdesc(k1, k2, c);    // T2 = T1 A1_ji
+        b.A = T1.p + t1o[q]; b.lda = k1; b.B = A1p[rq]; b.ldb = c; b.C = T2.p + t2o[q]; b.ldc = k1;
         m2.add(b);
         GemmDesc d = gdesc(k1, k2, k1);   // T3 = L1^-1 T2
-        d.A = G1i.p + g1off[q]; d.lda = k1; d.B = T2.p + t2off[q]; d.ldb = k1; d.C = T3.p + t2off[q]; d.ldc = k1;
+        d.A = L1i; d.lda = k1; d.B = T2.p + t2o[q]; d.ldb = k1; d.C = T3.p + t2o[q]; d.ldc = k1;
         m3.add(d);
         GemmDesc e = gdesc(k1, k2, k1);   // T2 = L1^-T T3
-        e.A = G1i.p + g1off[q]; e.lda = k1; e.B = T3.p + t2off[q]; e.ldb = k1; e.C = T2.p + t2off[q]; e.ldc = k1;
+        e.A = L1i; e.lda = k1; e.B = T3.p + t2o[q]; e.ldb = k1; e.C = T2.p + t2o[q]; e.ldc = k1;
         m4.add(e);
         GemmDesc f = gdesc(k1, k2, k2);   // T3 = T2 L2^-T
-        f.A = T2.p + t2off[q]; f.lda = k1; f.B = G2i.p + g2off[q]; f.ldb = k2; f.C = T3.p + t2off[q]; f.ldc = k1;
+        f.A = T2.p + t2o[q]; f.lda = k1; f.B = L2i; f.ldb = k2; f.C = T3.p + t2o[q]; f.ldc = k1;
         m5.add(f);
-        GemmDesc g = gdesc(k1, k2, k2);   // M = T3 L2^-1
-        g.A = T3.p + t2off[q]; g.lda = k1; g.B = G2i.p + g2off[q]; g.ldb = k2; g.C = PL.M.p + moff[q]; g.ldc = k1;
-        m6.add(g);
-        pairs[q].moff = moff[q];
+        GemmDesc g2 = gdesc(k1, k2, k2);  // M = T3 L2^-1
+        g2.A = T3.p + t2o[q]; g2.lda = k1; g2.B = L2i; g2.ldb = k2; g2.C = Mbuf.p + moff[q]; g2.ldc = k1;
+        m6.add(g2);
+        pd.flops += 2.0 * k1 * (double)c * c + 2.0 * k1 * (double)k2 * c;
       }
       m1.run(s); m2.run(s); m3.run(s); m4.run(s); m5.run(s); m6.run(s);
     }
-    for (int g = 0; g < 4; ++g) Yg[g].release();
+    // keep U (persistent) and M; drop A1 / P
+    std::vector<DBuf<double>> Ukeep;
+    for (size_t x = 0; x < keep.size(); x += 3) Ukeep.push_back(std::move(keep[x]));
+    keep.clear();
 
     // ---- subtraction batches for G^(lev):  Y'(I_i) -= sum_j X'(I_j) U_ji M_ij^T U_ij^T
-    //      (one final GEMM per row box i over its concatenated [U_ij1 | U_ij2 | ...])
+    //      one final GEMM per (row box i, U buffer) over its concatenated [U_ij1 | U_ij2 | ...]
+    for (size_t q = 0; q < P; ++q) { pairs[q].kij = kp[q]; pairs[q].moff = moff[q]; }
     PL.pairs = pairs;
+    PL.U = DBuf<double>();
+    PL.M = std::move(Mbuf);
+    PL.Ubufs = std::move(Ukeep);
     PL.g1.reset(false, false);
     PL.g2.reset(false, true);
     PL.g3.reset(false, true);
     long long tc = 0;
-    std::vector<long long> t1o(pairs.size(), -1), t2o(pairs.size(), -1);
-    for (size_t q = 0; q < pairs.size(); ++q) {
-      const auto& p = PL.pairs[q];
-      const int k1 = p.kij, k2 = PL.pairs[p.rev].kij;
+    std::vector<long long> t1o(P, -1), t2o(P, -1);
+    for (size_t q = 0; q < P; ++q) {
+      const int k1 = kp[q], k2 = kp[pairs[q].rev];
       if (k1 > 0 && k2 > 0) { t1o[q] = tc; tc += k2; }
     }
-    for (size_t q = 0; q < pairs.size(); ++q)
-      if (PL.pairs[q].kij > 0) { t2o[q] = tc; tc += PL.pairs[q].kij; }
-    for (size_t q = 0; q < pairs.size(); ++q) {
+    // t2 columns grouped by row box i (pairs are generated in row-box order)
+    for (size_t q = 0; q < P; ++q)
+      if (kp[q] > 0) { t2o[q] = tc; tc += kp[q]; }
+    for (size_t q = 0; q < P; ++q) {
       const auto& p = PL.pairs[q];
-      const int k1 = p.kij, k2 = PL.pairs[p.rev].kij;
+      const int k1 = kp[q], k2 = kp[p.rev];
       if (k1 == 0) continue;
       if (k2 > 0) {
         GemmDesc a = gdesc(-1, k2, p.nj);                 // t1 = X'(I_j) U_ji
-        a.selA = 1; a.offA = p.jb; a.B = PL.U.p + PL.pairs[p.rev].uoff; a.ldb = p.nj; a.selC = 2; a.offC = t1o[q];
+        a.selA = 1; a.offA = p.jb; a.B = Up[p.rev]; a.ldb = p.nj; a.selC = 2; a.offC = t1o[q];
         PL.g1.add(a);
       }
       GemmDesc b = gdesc(-1, k1, k2);                     // t2 = t1 M_ij^T  (zero if k2 == 0)
-      b.selA = 2; b.offA = k2 > 0 ? t1o[q] : 0; b.B = k2 > 0 ? PL.M.p + p.moff : PL.M.p; b.ldb = k1;
+      b.selA = 2; b.offA = k2 > 0 ? t1o[q] : 0; b.B = k2 > 0 ? PL.M.p + moff[q] : PL.M.p; b.ldb = k1;
       b.selC = 2; b.offC = t2o[q];
       PL.g2.add(b);
     }
-    for (size_t q = 0; q < pairs.size();) {
-      size_t e = q;
-      int ksum = 0;
-      while (e < pairs.size() && PL.pairs[e].i == PL.pairs[q].i) { ksum += PL.pairs[e].kij; ++e; }
-      if (ksum > 0) {
-        size_t f = q;
-        while (PL.pairs[f].kij == 0) ++f;
-        const auto& p = PL.pairs[f];
-        GemmDesc d = gdesc(-1, p.ni, ksum);               // Y'(I_i) -= [t2 ...] [U_ij ...]^T
-        d.selA = 2; d.offA = t2o[f]; d.B = PL.U.p + p.uoff; d.ldb = p.ni; d.selC = 1; d.offC = p.ib;
-        d.alpha = -1.0; d.beta = 1.0;
-        PL.g3.add(d);
+    // Y'(I_i) -= t2 U_ij^T: one GEMM per row box i when its U_ij are contiguous, else per pair
+    // (pairs of one row box live in different group buffers, so they are never contiguous;
+    //  the per-pair GEMMs of one row box are issued in separate batches to avoid races)
+    {
+      std::vector<std::vector<int>> byrow(nb);
+      for (size_t q = 0; q < P; ++q) if (kp[q] > 0) byrow[pairs[q].i].push_back((int)q);
+      size_t maxdeg = 0;
+      for (auto& v : byrow) maxdeg = std::max(maxdeg, v.size());
+      PL.g3s.clear();
+      for (size_t r = 0; r < maxdeg; ++r) {
+        PL.g3s.emplace_back(false, true);
+        for (int b = 0; b < nb; ++b) {
+          if (r >= byrow[b].size()) continue;
+          const int q = byrow[b][r];
+          const auto& p = PL.pairs[q];
+          GemmDesc d = gdesc(-1, p.ni, kp[q]);
+          d.selA = 2; d.offA = t2o[q]; d.B = Up[q]; d.ldb = p.ni; d.selC = 1; d.offC = p.ib;
+          d.alpha = -1.0; d.beta = 1.0;
+          PL.g3s.back().add(d);
+        }
       }
-      q = e;
     }
     PL.tcols = tc;
     max_tcols = std::max(max_tcols, tc);
-    for (GemmBatch* g : {&PL.g1, &PL.g2, &PL.g3})
+    for (GemmBatch* g : {&PL.g1, &PL.g2})
       if (!g->empty()) g->finalize(s);
+    for (auto& g : PL.g3s) if (!g.empty()) g.finalize(s);
   }
 
   // ---- extraction
@@ -622,6 +617,7 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
     nL = std::max(nL, t.end[nd] - t.begin[nd]);
   }
   DBuf<int> dlb = up(lb, s);
+  RSF_PHASE("p.extract", s);
   double tr = 0.0, tra = 0.0;
   const int GB = 256;
   for (int e0 = 0; e0 < nL; e0 += kb) {

@@ -1,0 +1,526 @@
+// Blocked randomized rank-revealing QR truncated at the eps-rank (see rrqr.cuh).
+#include <algorithm>
+#include <cmath>
+
+#include "rrqr.cuh"
+
+namespace rsf {
+
+namespace {
+
+constexpr int NT = 256;
+constexpr int SP = QR_NB + 8;   // sketch rows (block + oversampling)
+
+__device__ __forceinline__ double wsum(double v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ uint4 philox10(uint4 c, uint2 k) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) { k.x += 0x9E3779B9u; k.y += 0xBB67AE85u; }
+    const unsigned hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    const unsigned hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+  }
+  return c;
+}
+
+struct RDesc {
+  double* A; long long lda; int m, c;
+  double* G;       // SP x m
+  double* Y;       // SP x c
+  double* Z;       // SP x c scratch (sketch CPQR)
+  double* zn;      // c scratch (sketch column norms)
+  double* nrm2;    // c: squared trailing column norms
+  int* piv;
+  int* sw;         // QR_NB swap targets
+  double* ref;     // max column norm
+  int* flag;       // [0] done, [1] k
+  double* R11i;    // QR_NB x QR_NB
+  int J, nbp, id;
+  double eps;
+};
+
+// ref = max_j ||A(:, j)||, piv = identity
+__global__ void ref_kernel(const RDesc* __restrict__ d0) {
+  const RDesc d = d0[blockIdx.x];
+  __shared__ double red[NT / 32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double mx = 0.0;
+  for (int j = warp; j < d.c; j += NT / 32) {
+    const double* a = d.A + (long long)j * d.lda;
+    double s = 0.0;
+    for (int r = lane; r < d.m; r += 32) s += a[r] * a[r];
+    s = wsum(s);
+    mx = fmax(mx, s);
+  }
+  for (int j = threadIdx.x; j < d.c; j += NT) d.piv[j] = j;
+  if (lane == 0) red[warp] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v = 0.0;
+    for (int w = 0; w < NT / 32; ++w) v = fmax(v, red[w]);
+    *d.ref = sqrt(v);
+    d.flag[0] = (v > 0.0) ? 0 : 1;
+    d.flag[1] = 0;
+  }
+}
+
+__global__ void gauss_kernel(const RDesc* __restrict__ d0, unsigned seed) {
+  const RDesc d = d0[blockIdx.y];
+  const long long tot = (long long)SP * d.m;
+  for (long long e = blockIdx.x * (long long)NT + threadIdx.x; e < tot; e += (long long)gridDim.x * NT) {
+    const int r = (int)(e % SP), col = (int)(e / SP);
+    uint4 x = philox10(make_uint4((unsigned)d.id, (unsigned)r, (unsigned)col, 0x51u), make_uint2(seed, 4u));
+    const double u1 = ((double)(x.x >> 5) * 67108864.0 + (double)(x.y >> 6)) * (1.0 / 9007199254740992.0);
+    const double u2 = ((double)(x.z >> 5) * 67108864.0 + (double)(x.w >> 6)) * (1.0 / 9007199254740992.0);
+    d.G[e] = sqrt(-2.0 * log1p(-u1)) * cos(6.283185307179586 * u2);
+  }
+}
+
+// greedy CPQR of a copy of the sketch Y(:, J:c) for nbp steps -> swap list
+__global__ void __launch_bounds__(NT) sketch_cpqr_kernel(const RDesc* __restrict__ d0) {
+  const RDesc d = d0[blockIdx.x];
+  const int J = d.J, cr = d.c - J, nbp = d.nbp;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  __shared__ double redv[NT / 32];
+  __shared__ int redi[NT / 32];
+  __shared__ double sc[4];
+  __shared__ int sp;
+  double* Z = d.Z;
+  double* zn = d.zn;
+  for (long long e = tid; e < (long long)SP * cr; e += NT) Z[e] = d.Y[(long long)J * SP + e];
+  __syncthreads();
+  for (int j = warp; j < cr; j += NT / 32) {
+    double v = (lane < SP) ? Z[(long long)j * SP + lane] : 0.0;
+    double s = v * v;
+    if (lane + 32 < SP) { double w = Z[(long long)j * SP + lane + 32]; s += w * w; }
+    s = wsum(s);
+    if (lane == 0) zn[j] = s;
+  }
+  __syncthreads();
+  for (int t = 0; t < nbp; ++t) {
+    double bv = -1.0;
+    int bi = cr;
+    for (int j = t + tid; j < cr; j += NT) {
+      const double v = zn[j];
+      if (v > bv) { bv = v; bi = j; }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    if (lane == 0) { redv[warp] = bv; redi[warp] = bi; }
+    __syncthreads();
+    if (tid == 0) {
+      double v = redv[0]; int b = redi[0];
+      for (int w = 1; w < NT / 32; ++w)
+        if (redv[w] > v || (redv[w] == v && redi[w] < b)) { v = redv[w]; b = redi[w]; }
+      if (b >= cr) b = t;
+      sp = b;
+      d.sw[t] = b;
+    }
+    __syncthreads();
+    const int p = sp;
+    if (p != t) {
+      for (int r = tid; r < SP; r += NT) {
+        double a = Z[(long long)t * SP + r];
+        Z[(long long)t * SP + r] = Z[(long long)p * SP + r];
+        Z[(long long)p * SP + r] = a;
+      }
+      if (tid == 0) { double a = zn[t]; zn[t] = zn[p]; zn[p] = a; }
+    }
+    __syncthreads();
+    // Householder on Z(t:SP, t)
+    double* x = Z + (long long)t * SP;
+    if (warp == 0) {
+      double s = 0.0;
+      for (int r = t + 1 + lane; r < SP; r += 32) s += x[r] * x[r];
+      s = wsum(s);
+      if (lane == 0) {
+        const double alpha = x[t];
+        double tau = 0.0, beta = alpha, scale = 0.0;
+        if (s != 0.0) {
+          const double mu = sqrt(alpha * alpha + s);
+          beta = (alpha >= 0.0) ? -mu : mu;
+          tau = (beta - alpha) / beta;
+          scale = 1.0 / (alpha - beta);
+        }
+        sc[0] = tau; sc[1] = beta; sc[2] = scale;
+      }
+    }
+    __syncthreads();
+    const double tau = sc[0], scale = sc[2];
+    if (tau != 0.0)
+      for (int r = t + 1 + tid; r < SP; r += NT) x[r] *= scale;
+    __syncthreads();
+    if (tid == 0) x[t] = sc[1];
+    for (int j = t + 1 + warp; j < cr; j += NT / 32) {
+      double* y = Z + (long long)j * SP;
+      double dot = 0.0;
+      for (int r = t + 1 + lane; r < SP; r += 32) dot += x[r] * y[r];
+      dot = wsum(dot) + y[t];
+      const double w = tau * dot;
+      double ss = 0.0;
+      for (int r = t + 1 + lane; r < SP; r += 32) {
+        const double v = y[r] - w * x[r];
+        y[r] = v;
+        ss += v * v;
+      }
+      ss = wsum(ss);
+      __syncwarp();
+      if (lane == 0) { y[t] -= w; zn[j] = ss; }
+    }
+    __syncthreads();
+  }
+}
+
+// apply the swap list to A (m rows), Y (SP rows) and piv
+__global__ void apply_swaps_kernel(const RDesc* __restrict__ d0) {
+  const RDesc d = d0[blockIdx.x];
+  for (int t = 0; t < d.nbp; ++t) {
+    const int a = d.J + t, b = d.J + d.sw[t];
+    if (a != b) {
+      double* ca = d.A + (long long)a * d.lda;
+      double* cb = d.A + (long long)b * d.lda;
+      for (int r = threadIdx.x; r < d.m; r += NT) { double v = ca[r]; ca[r] = cb[r]; cb[r] = v; }
+      double* ya = d.Y + (long long)a * SP;
+      double* yb = d.Y + (long long)b * SP;
+      for (int r = threadIdx.x; r < SP; r += NT) { double v = ya[r]; ya[r] = yb[r]; yb[r] = v; }
+      if (threadIdx.x == 0) { int v = d.piv[a]; d.piv[a] = d.piv[b]; d.piv[b] = v; }
+    }
+    __syncthreads();
+  }
+}
+
+// squared norms of the trailing columns A(j1:m, j) for j >= j1 (warp per column, many CTAs)
+__global__ void trail_norm_kernel(const RDesc* __restrict__ d0) {
+  const RDesc d = d0[blockIdx.y];
+  const int j1 = d.J + d.nbp;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int j = j1 + blockIdx.x * (NT / 32) + warp; j < d.c; j += gridDim.x * (NT / 32)) {
+    const double* a = d.A + (long long)j * d.lda;
+    double s = 0.0;
+    for (int r = j1 + lane; r < d.m; r += 32) s += a[r] * a[r];
+    s = wsum(s);
+    if (lane == 0) d.nrm2[j] = s;
+  }
+}
+
+// smallest k' in [J, j1] with max trailing column norm <= eps * ref (exact, from R and nrm2)
+__global__ void __launch_bounds__(NT) rank_kernel(const RDesc* __restrict__ d0) {
+  const RDesc d = d0[blockIdx.x];
+  const int J = d.J, nbp = d.nbp, j1 = J + nbp;
+  __shared__ double red[QR_NB + 1][NT / 32];
+  double mx[QR_NB + 1];
+#pragma unroll
+  for (int q = 0; q <= QR_NB; ++q) mx[q] = 0.0;
+  for (int j = J + threadIdx.x; j < d.c; j += NT) {
+    const double* a = d.A + (long long)j * d.lda;
+    if (j < j1) {
+      double acc = 0.0;   // sum_{r=k'}^{j} R(r,j)^2 for k' = j, j-1, ..., J
+      for (int r = j; r >= J; --r) {
+        acc += a[r] * a[r];
+        const int q = r - J;
+        mx[q] = fmax(mx[q], acc);
+      }
+    } else {
+      double acc = d.nrm2[j];
+      mx[nbp] = fmax(mx[nbp], acc);
+      for (int r = j1 - 1; r >= J; --r) {
+        acc += a[r] * a[r];
+        const int q = r - J;
+        mx[q] = fmax(mx[q], acc);
+      }
+    }
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int q = 0; q <= QR_NB; ++q) {
+    double v = mx[q];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) red[q][warp] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const double thr = d.eps * (*d.ref);
+    int k = -1;
+    for (int q = 0; q <= nbp; ++q) {
+      double v = 0.0;
+      for (int w = 0; w < NT / 32; ++w) v = fmax(v, red[q][w]);
+      if (sqrt(v) <= thr) { k = J + q; break; }
+    }
+    if (k < 0 && j1 >= min(d.m, d.c)) k = j1;
+    if (k >= 0) { d.flag[0] = 1; d.flag[1] = k; }
+  }
+}
+
+// inverse of the upper-triangular block R(J:j1, J:j1) -> R11i (ld QR_NB)
+__global__ void r11_inv_kernel(const RDesc* __restrict__ d0) {
+  const RDesc d = d0[blockIdx.x];
+  __shared__ double S[QR_NB * QR_NB];
+  const int nb = d.nbp;
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+    const int i = e % nb, j = e / nb;
+    S[e] = (i <= j) ? d.A[(long long)(d.J + j) * d.lda + d.J + i] : 0.0;
+  }
+  __syncthreads();
+  if (threadIdx.x < nb) {
+    const int c = threadIdx.x;   // column c of the inverse: back substitution
+    double x[QR_NB];
+#pragma unroll
+    for (int i = 0; i < QR_NB; ++i) x[i] = 0.0;
+    for (int i = c; i >= 0; --i) {
+      double s = (i == c) ? 1.0 : 0.0;
+      for (int l = i + 1; l <= c; ++l) s -= S[l * nb + i] * x[l];
+      x[i] = s / S[i * nb + i];
+    }
+    for (int i = 0; i < QR_NB; ++i) d.R11i[c * QR_NB + i] = (i <= c && i < nb) ? x[i] : 0.0;
+  }
+}
+
+template <class D>
+DBuf<D> upd(const std::vector<D>& v, cudaStream_t s) {
+  DBuf<D> b(std::max<size_t>(v.size(), 1), s);
+  b.upload(v);
+  return b;
+}
+
+// ----------------------------------------------------------------- trsm helpers
+constexpr int TB = 64;
+struct DInvDesc { const double* U; long long ldu; int nb; double* out; };   // out ld TB
+__global__ void upper_inv64_kernel(const DInvDesc* __restrict__ d0) {
+  const DInvDesc d = d0[blockIdx.x];
+  __shared__ double S[TB * TB];
+  const int nb = d.nb;
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+    const int i = e % nb, j = e / nb;
+    S[e] = (i <= j) ? d.U[(long long)j * d.ldu + i] : 0.0;
+  }
+  __syncthreads();
+  if (threadIdx.x < nb) {
+    const int c = threadIdx.x;
+    for (int i = c; i >= 0; --i) {
+      double s = (i == c) ? 1.0 : 0.0;
+      for (int l = i + 1; l <= c; ++l) s -= S[l * nb + i] * d.out[c * TB + l];
+      d.out[c * TB + i] = s / S[i * nb + i];
+    }
+    for (int i = c + 1; i < TB; ++i) d.out[c * TB + i] = 0.0;
+  }
+}
+
+}  // namespace
+
+void trsm_upper_batched(cudaStream_t s, const std::vector<TrsmProb>& probs) {
+  if (probs.empty()) return;
+  const int P = (int)probs.size();
+  std::vector<long long> ioff(P), woff(P);
+  long long it = 0, wt = 0;
+  int maxblk = 0;
+  std::vector<DInvDesc> dv;
+  for (int i = 0; i < P; ++i) {
+    const int nblk = (probs[i].k + TB - 1) / TB;
+    ioff[i] = it; it += (long long)nblk * TB * TB;
+    woff[i] = wt; wt += (long long)TB * probs[i].nrhs;
+    maxblk = std::max(maxblk, nblk);
+  }
+  DBuf<double> inv(std::max<long long>(it, 1), s), W(std::max<long long>(wt, 1), s);
+  for (int i = 0; i < P; ++i) {
+    const auto& p = probs[i];
+    const int nblk = (p.k + TB - 1) / TB;
+    for (int b = 0; b < nblk; ++b) {
+      const int r0 = b * TB, rb = std::min(TB, p.k - r0);
+      dv.push_back(DInvDesc{p.U + (long long)r0 * p.ldu + r0, p.ldu, rb, inv.p + ioff[i] + (long long)b * TB * TB});
+    }
+  }
+  if (!dv.empty()) {
+    auto dd = upd(dv, s);
+    for (size_t o = 0; o < dv.size(); o += 65535) {
+      unsigned nb = (unsigned)std::min<size_t>(65535, dv.size() - o);
+      upper_inv64_kernel<<<nb, 64, 0, s>>>(dd.p + o);
+      count_launch();
+      RSF_LAUNCH_CHECK();
+    }
+  }
+  for (int st = 0; st < maxblk; ++st) {
+    GemmBatch g1(false, false), g2(false, false);
+    std::vector<CopyProb> cp;
+    for (int i = 0; i < P; ++i) {
+      const auto& p = probs[i];
+      const int nblk = (p.k + TB - 1) / TB;
+      const int b = nblk - 1 - st;
+      if (b < 0 || p.nrhs <= 0) continue;
+      const int r0 = b * TB, rb = std::min(TB, p.k - r0), r1 = r0 + rb;
+      if (r1 < p.k) {   // B_b -= U(b, r1:k) X(r1:k)
+        GemmDesc a = gdesc(rb, p.nrhs, p.k - r1);
+        a.A = p.U + (long long)r1 * p.ldu + r0; a.lda = (int)p.ldu;
+        a.B = p.B + r1; a.ldb = (int)p.ldb;
+        a.C = p.B + r0; a.ldc = (int)p.ldb;
+        a.alpha = -1.0; a.beta = 1.0;
+        g1.add(a);
+      }
+      GemmDesc c = gdesc(rb, p.nrhs, rb);   // W = Uinv_bb B_b
+      c.A = inv.p + ioff[i] + (long long)b * TB * TB; c.lda = TB;
+      c.B = p.B + r0; c.ldb = (int)p.ldb;
+      c.C = W.p + woff[i]; c.ldc = rb;
+      g2.add(c);
+      cp.push_back(CopyProb{W.p + woff[i], rb, p.B + r0, p.ldb, rb, p.nrhs, 1.0});
+    }
+    g1.run(s);
+    g2.run(s);
+    copy_batched(s, cp);
+  }
+}
+
+RRQRResult rrqr_batched(cudaStream_t s, const std::vector<RRQRProb>& probs, double eps,
+                        unsigned long long seed) {
+  RRQRResult res;
+  const int P = (int)probs.size();
+  res.k.assign(P, 0);
+  res.done.assign(P, 0);
+  if (P == 0) return res;
+  // workspaces
+  std::vector<long long> goff(P), yoff(P), coff(P), voff(P), woff(P);
+  long long gt = 0, yt = 0, ct = 0, vt = 0, wt = 0;
+  for (int i = 0; i < P; ++i) {
+    goff[i] = gt; gt += (long long)SP * probs[i].m;
+    yoff[i] = yt; yt += (long long)SP * probs[i].c;
+    coff[i] = ct; ct += probs[i].c;
+    voff[i] = vt; vt += (long long)probs[i].m * QR_NB;
+    woff[i] = wt; wt += (long long)QR_NB * probs[i].c;
+  }
+  DBuf<double> Y(yt, s), Z(yt, s), zn(ct, s), nrm2(ct, s), V(vt, s), W(wt, s), W2(wt, s), Wt(wt, s);
+  DBuf<double> Tsc((size_t)P * QR_NB * QR_NB, s), R11i((size_t)P * QR_NB * QR_NB, s), ref(P, s);
+  DBuf<int> sw((size_t)P * QR_NB, s), flag((size_t)2 * P, s);
+  std::vector<RDesc> base(P);
+  for (int i = 0; i < P; ++i) {
+    const auto& p = probs[i];
+    RDesc d{};
+    d.A = p.A; d.lda = p.lda; d.m = p.m; d.c = p.c;
+    d.Y = Y.p + yoff[i]; d.Z = Z.p + yoff[i]; d.zn = zn.p + coff[i]; d.nrm2 = nrm2.p + coff[i];
+    d.piv = p.piv; d.sw = sw.p + (long long)i * QR_NB; d.ref = ref.p + i; d.flag = flag.p + 2 * i;
+    d.R11i = R11i.p + (long long)i * QR_NB * QR_NB;
+    d.id = i; d.eps = eps;
+    base[i] = d;
+  }
+  {
+    DBuf<double> G(gt, s);
+    for (int i = 0; i < P; ++i) base[i].G = G.p + goff[i];
+    auto db = upd(base, s);
+    ref_kernel<<<P, NT, 0, s>>>(db.p);
+    long long mx = 0;
+    for (auto& p : probs) mx = std::max(mx, (long long)SP * p.m);
+    gauss_kernel<<<dim3((unsigned)std::min<long long>(1024, (mx + NT - 1) / NT), P), NT, 0, s>>>(
+        db.p, (unsigned)(seed & 0xffffffffu));
+    count_launch(2);
+    RSF_LAUNCH_CHECK();
+    GemmBatch gy(false, false);   // Y = G A
+    for (int i = 0; i < P; ++i) {
+      GemmDesc g = gdesc(SP, probs[i].c, probs[i].m);
+      g.A = base[i].G; g.lda = SP; g.B = probs[i].A; g.ldb = (int)probs[i].lda; g.C = base[i].Y; g.ldc = SP;
+      gy.add(g);
+    }
+    gy.run(s);
+    for (int i = 0; i < P; ++i) base[i].G = nullptr;
+  }
+  std::vector<int> hflag = flag.to_host(2 * P);
+  std::vector<int> active;
+  for (int i = 0; i < P; ++i) {
+    if (hflag[2 * i]) { res.k[i] = 0; res.done[i] = 0; }
+    else active.push_back(i);
+  }
+  for (int J = 0; !active.empty(); J += QR_NB) {
+    std::vector<RDesc> dv;
+    for (int i : active) {
+      RDesc d = base[i];
+      d.J = J;
+      d.nbp = std::min(QR_NB, std::min(probs[i].m, probs[i].c) - J);
+      dv.push_back(d);
+    }
+    auto dd = upd(dv, s);
+    const unsigned na = (unsigned)dv.size();
+    sketch_cpqr_kernel<<<na, NT, 0, s>>>(dd.p);
+    apply_swaps_kernel<<<na, NT, 0, s>>>(dd.p);
+    count_launch(2);
+    RSF_LAUNCH_CHECK();
+    std::vector<PanelStep> ps;
+    for (size_t a = 0; a < dv.size(); ++a) {
+      const int i = active[a];
+      const auto& p = probs[i];
+      PanelStep st;
+      st.A = p.A + (long long)J * p.lda + J; st.lda = p.lda;
+      st.rows = p.m - J; st.ncol = dv[a].nbp; st.c2 = p.c - J - dv[a].nbp;
+      st.V = V.p + voff[i];
+      st.T = p.Tws ? p.Tws + (long long)(J / QR_NB) * QR_NB * QR_NB : Tsc.p + (long long)i * QR_NB * QR_NB;
+      st.W = W.p + woff[i]; st.W2 = W2.p + woff[i];
+      ps.push_back(st);
+    }
+    panel_step_batched(s, ps);
+    int maxc = 0;
+    for (auto& d : dv) maxc = std::max(maxc, d.c - d.J - d.nbp);
+    if (maxc > 0) {
+      trail_norm_kernel<<<dim3((unsigned)std::min(256, (maxc + 7) / 8), na), NT, 0, s>>>(dd.p);
+      count_launch();
+    }
+    rank_kernel<<<na, NT, 0, s>>>(dd.p);
+    count_launch();
+    RSF_LAUNCH_CHECK();
+    hflag = flag.to_host(2 * P);
+    std::vector<int> next;
+    std::vector<RDesc> cont;
+    for (size_t a = 0; a < dv.size(); ++a) {
+      const int i = active[a];
+      if (hflag[2 * i]) {
+        res.k[i] = hflag[2 * i + 1];
+        res.done[i] = J + dv[a].nbp;
+      } else {
+        next.push_back(i);
+        cont.push_back(dv[a]);
+      }
+    }
+    if (!cont.empty()) {   // sketch downdate: Y2 -= Y1 R11^-1 R12
+      auto dc = upd(cont, s);
+      r11_inv_kernel<<<(unsigned)cont.size(), 64, 0, s>>>(dc.p);
+      count_launch();
+      RSF_LAUNCH_CHECK();
+      GemmBatch g1(false, false), g2(false, false);
+      for (auto& d : cont) {
+        const int j1 = d.J + d.nbp, rest = d.c - j1;
+        if (rest <= 0) continue;
+        const int i = d.id;
+        GemmDesc a = gdesc(d.nbp, rest, d.nbp);   // Wt = R11^-1 R12
+        a.A = d.R11i; a.lda = QR_NB; a.B = d.A + (long long)j1 * d.lda + d.J; a.ldb = (int)d.lda;
+        a.C = Wt.p + woff[i]; a.ldc = QR_NB;
+        g1.add(a);
+        GemmDesc b = gdesc(SP, rest, d.nbp);      // Y2 -= Y1 Wt
+        b.A = d.Y + (long long)d.J * SP; b.lda = SP; b.B = Wt.p + woff[i]; b.ldb = QR_NB;
+        b.C = d.Y + (long long)j1 * SP; b.ldc = SP; b.alpha = -1.0; b.beta = 1.0;
+        g2.add(b);
+      }
+      g1.run(s);
+      g2.run(s);
+    }
+    active.swap(next);
+  }
+  // T = R11^-1 R12
+  std::vector<TrsmProb> tp;
+  std::vector<CopyProb> cp;
+  for (int i = 0; i < P; ++i) {
+    const auto& p = probs[i];
+    const int k = res.k[i];
+    if (!p.T || k == 0 || k >= p.c) continue;
+    cp.push_back(CopyProb{p.A + (long long)k * p.lda, p.lda, p.T, p.ldt, k, p.c - k, 1.0});
+    tp.push_back(TrsmProb{p.A, p.lda, p.T, p.ldt, k, p.c - k});
+  }
+  copy_batched(s, cp);
+  trsm_upper_batched(s, tp);
+  return res;
+}
+
+}  // namespace rsf

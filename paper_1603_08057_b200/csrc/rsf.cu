@@ -20,6 +20,7 @@
 
 #include "dense.cuh"
 #include "rsf_impl.cuh"
+#include "rrqr.cuh"
 #include "rsf_kernels.cuh"
 
 namespace rsf {
@@ -28,6 +29,7 @@ namespace {
 
 constexpr int N_RINGS = 4, N_ANGLES = 64;   // n_prox = 256, R-C
 constexpr long long CHUNK_ELEMS = 1ll << 28; // max doubles of ID matrices per launch group
+constexpr int SMALL_C = 128;                 // |I| <= SMALL_C: exact greedy CPQR in shared memory
 
 double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -96,6 +98,8 @@ std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams
     }
     // ---- near lists (R-C, R-E): active DOFs outside b within r_near * h of its center
     std::vector<std::vector<int>> N(nb);
+    {
+    RSF_PHASE("f.near_host", s);
     for (int b = 0; b < nb; ++b) {
       const int nd = nodes[b];
       const double cx = t.cx(nd), cy = t.cy(nd), h = t.h(nd);
@@ -133,6 +137,7 @@ std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams
         }
     }
 
+    }
     // ---- interpolative decompositions, in chunks of boxes
     std::vector<int> cvec(nb), kvec(nb, 0);
     std::vector<std::vector<int>> piv(nb);
@@ -178,13 +183,14 @@ std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams
       for (int b = b0; b < b1; ++b) {
         const int m = (int)N[b].size() + N_RINGS * N_ANGLES, c = cvec[b];
         const int q = std::min(m, c);
-        if ((size_t)q * c * 8 + (72 + 2 * (size_t)c + 64) * 8 > 200 * 1024) {
+        if (c <= SMALL_C && (size_t)q * c * 8 + (72 + 2 * (size_t)c + 64) * 8 > 200 * 1024) {
           woff[b - b0] = wtot;
           wtot += (long long)q * c;
         }
       }
       DBuf<double> Wcp(std::max<long long>(wtot, 1), s);
-      DBuf<int> dpiv(std::max<size_t>(hI.size(), 1), s), dk(b1 - b0, s);
+      DBuf<int> dpiv(std::max<size_t>(hI.size(), 1), s);
+      std::vector<int> big, sm;   // boxes on the blocked randomized RRQR path / greedy smem path
       for (int b = b0; b < b1; ++b) {
         const int nd = nodes[b];
         const int m = (int)N[b].size() + N_RINGS * N_ANGLES, c = cvec[b];
@@ -196,26 +202,51 @@ std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams
         d.I = dI.p + ioff[b - b0];
         d.cx = t.cx(nd); d.cy = t.cy(nd); d.h = t.h(nd);
         ad.push_back(d);
-        qp.push_back(QRProb{A.p + aoff[b - b0], m, m, c, nullptr, nullptr});
-        CPQRProb p;
-        p.R = A.p + aoff[b - b0]; p.ldr = m; p.q = std::min(m, c); p.c = c;
-        p.W = woff[b - b0] >= 0 ? Wcp.p + woff[b - b0] : nullptr;
-        p.T = Tfull.p + tfoff[b];
-        p.piv = dpiv.p + ioff[b - b0];
-        p.Rout = nullptr; p.tau = nullptr;
-        cp.push_back(p);
-        F->diag.flops_id += 2.0 * m * (double)c * c - (2.0 / 3.0) * (double)c * c * c + (4.0 / 3.0) * (double)c * c * c;
+        if (c > SMALL_C) {
+          big.push_back(b);
+        } else {
+          sm.push_back(b);
+          qp.push_back(QRProb{A.p + aoff[b - b0], m, m, c, nullptr, nullptr});
+          CPQRProb p;
+          p.R = A.p + aoff[b - b0]; p.ldr = m; p.q = std::min(m, c); p.c = c;
+          p.W = woff[b - b0] >= 0 ? Wcp.p + woff[b - b0] : nullptr;
+          p.T = Tfull.p + tfoff[b];
+          p.piv = dpiv.p + ioff[b - b0];
+          p.Rout = nullptr; p.tau = nullptr;
+          cp.push_back(p);
+          F->diag.flops_id += 2.0 * m * (double)c * c - (2.0 / 3.0) * (double)c * c * c + (4.0 / 3.0) * (double)c * c * c;
+        }
       }
-      assemble_id(s, ad, kp, which, opts, t.xs.p, t.ys.p, N_RINGS, N_ANGLES);
-      geqrf_batched(s, qp, false);
-      cpqr_id_batched(s, cp, eps, dk.p, true);
-      std::vector<int> hk = dk.to_host(b1 - b0);
+      { RSF_PHASE("f.assemble_id", s); assemble_id(s, ad, kp, which, opts, t.xs.p, t.ys.p, N_RINGS, N_ANGLES); }
+      std::vector<int> hk(b1 - b0, 0);
+      if (!cp.empty()) {
+        DBuf<int> dks(cp.size(), s);
+        { RSF_PHASE("f.geqrf", s); geqrf_batched(s, qp, false); }
+        { RSF_PHASE("f.cpqr", s); cpqr_id_batched(s, cp, eps, dks.p, true); }
+        std::vector<int> h = dks.to_host(cp.size());
+        for (size_t q = 0; q < sm.size(); ++q) hk[sm[q] - b0] = h[q];
+      }
+      if (!big.empty()) {
+        RSF_PHASE("f.rrqr", s);
+        std::vector<RRQRProb> rp;
+        for (int b : big) {
+          const int m = (int)N[b].size() + N_RINGS * N_ANGLES, c = cvec[b];
+          rp.push_back(RRQRProb{A.p + aoff[b - b0], m, m, c, dpiv.p + ioff[b - b0], nullptr, Tfull.p + tfoff[b], c});
+        }
+        RRQRResult rr = rrqr_batched(s, rp, eps, opts.seed ^ (0x9E3779B97F4A7C15ull * (unsigned long long)(lev + 17 * (which + 2))));
+        for (size_t q = 0; q < big.size(); ++q) {
+          const int b = big[q];
+          const int m = (int)N[b].size() + N_RINGS * N_ANGLES, c = cvec[b];
+          hk[b - b0] = rr.k[q];
+          F->diag.flops_id += 2.0 * m * (double)c * rr.done[q] + (double)rr.k[q] * rr.k[q] * (c - rr.k[q]);
+        }
+      }
       std::vector<int> hp = dpiv.to_host(hI.size());
       for (int b = b0; b < b1; ++b) {
         kvec[b] = hk[b - b0];
         piv[b].assign(hp.begin() + ioff[b - b0], hp.begin() + ioff[b - b0] + cvec[b]);
         const double kk = kvec[b];
-        F->diag.flops_id += kk * kk * (cvec[b] - kk);
+        if (cvec[b] <= SMALL_C) F->diag.flops_id += kk * kk * (cvec[b] - kk);
       }
       b0 = b1;
     }
@@ -279,6 +310,7 @@ std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams
         }
         sd.push_back(d);
       }
+      RSF_PHASE("f.self_perm", s);
       assemble_self(s, sd, kp, which, t.xs.p, t.ys.p);
       std::vector<PermDesc> pd;
       for (int b = 0; b < nb; ++b) pd.push_back(PermDesc{Bcur.p + bsz[b], Bp.p + bsz[b], cvec[b], dpv.p + poff[b]});
@@ -326,9 +358,7 @@ std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams
         F->diag.flops_elim += sig ? (3.0 * k * k * r + 5.0 * k * (double)r * r + (double)r * r * r / 3.0)
                                   : (2.0 * k * k * r + 4.0 * k * (double)r * r);
       }
-      e1.run(s);
-      e2.run(s);
-      e3.run(s);
+      { RSF_PHASE("f.elim_gemm", s); e1.run(s); e2.run(s); e3.run(s); }
       copy_batched(s, tcopy);
       if (sig) {
         std::vector<PotrfProb> pp;
@@ -341,7 +371,7 @@ std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams
         }
         DBuf<double> lsum(std::max<size_t>(pp.size(), 1), s);
         DBuf<int> info(std::max<size_t>(pp.size(), 1), s);
-        potrf_batched(s, pp, lsum.p, info.p);
+        { RSF_PHASE("f.potrf", s); potrf_batched(s, pp, lsum.p, info.p); }
         std::vector<double> hl = lsum.to_host(pp.size());
         std::vector<int> hi = info.to_host(pp.size());
         for (size_t i = 0; i < pp.size(); ++i) {
@@ -368,6 +398,7 @@ std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams
           d5.C = B; d5.ldc = c; d5.alpha = -1.0; d5.beta = 1.0;
           e5.add(d5);
         }
+        RSF_PHASE("f.elim_gemm", s);
         copy_batched(s, lc);
         e4.run(s);
         e5.run(s);
@@ -456,6 +487,7 @@ std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams
 
   // ---- top (level 0, R-Y): B_0 and its dense Cholesky
   {
+    RSF_PHASE("f.top", s);
     const int root = t.levels[0][0];
     std::vector<int> I0;
     std::array<int, 5> co{};
