@@ -101,6 +101,19 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def aggregate(t_local: float, steps: int, world: int, device=None):
+    """Max-over-ranks time and whole-job throughput (every rank evaluates `steps`
+    independent replicas).  Used by the timed region and by tests/test_multirank.py."""
+    t_all = t_local
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        tt = torch.tensor([t_local], dtype=torch.float64, device=device)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_all = float(tt.item())
+    return t_all, world * steps / t_all
+
+
 def workload(cid: int, n: int | None):
     from workloads import config, points_for, w_for
     c = config(cid)
@@ -262,12 +275,7 @@ def main():
     # see only the torch part, hence max(device-synchronised wall, event time)
     ev_ms = e0.elapsed_time(e1)
     t_local = max(wall, ev_ms / 1e3)
-    t_all = t_local
-    if world > 1:
-        tt = torch.tensor([t_local], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_all = float(tt.item())
-    value = world * args.steps / t_all
+    t_all, value = aggregate(t_local, args.steps, world, dev)
 
     # ---- e2e: same metric through the C ABI with pinned HOST buffers (H2D inside the call)
     xy_p = torch.from_numpy(xy_h).pin_memory()
@@ -278,12 +286,8 @@ def main():
     for _ in range(args.steps):
         step(xy_p, z_p)
     torch.cuda.synchronize()
-    te = time.perf_counter() - t0
-    if world > 1:
-        tt = torch.tensor([te], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        te = float(tt.item())
-    e2e = {"value": world * args.steps / te, "unit": UNIT,
+    te, e2e_value = aggregate(time.perf_counter() - t0, args.steps, world, dev)
+    e2e = {"value": e2e_value, "unit": UNIT,
            "h2d_bytes_per_step": int(xy_h.nbytes + z_p.numel() * 8),
            "d2h_bytes_per_step": int(8 * (1 + len(c.theta)))}
 

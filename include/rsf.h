@@ -161,6 +161,8 @@ void rsf_profile_reset(void);
 /* batched-GEMM statistics for the roofline: CUDA events around every launch on its stream.
  * rsf_stats_get fills {launches, seconds, algorithmic flops, compulsory bytes}. */
 void rsf_stats_enable(int on);
+/* diagnostics: TFLOP/s of the batched FP64 GEMM on batch x (M x N x K), transposes ta/tb */
+double rsf_debug_gemm_bench(int M, int N, int K, int batch, int ta, int tb, int reps);
 void rsf_stats_get(double* out4);
 void rsf_stats_reset(void);
 

@@ -337,6 +337,41 @@ const char* rsf_profile_dump(void) {
 }
 void rsf_profile_reset(void) { rsf::Prof::reset(); }
 
+double rsf_debug_gemm_bench(int M, int N, int K, int batch, int ta, int tb, int reps) {
+  // diagnostics: TFLOP/s of the batched FP64 GEMM on `batch` independent M x N x K problems
+  try {
+    cudaStream_t s = 0;   // legacy default stream (buffers are released before return)
+    const size_t sa = (size_t)M * K, sb = (size_t)K * N, sc = (size_t)M * N;
+    rsf::DBuf<double> A(sa * batch, s), B(sb * batch, s), C(sc * batch, s);
+    A.zero(); B.zero(); C.zero();
+    rsf::GemmBatch g(ta != 0, tb != 0);
+    for (int i = 0; i < batch; ++i) {
+      rsf::GemmDesc d = rsf::gdesc(M, N, K);
+      d.A = A.p + sa * i; d.lda = ta ? K : M;
+      d.B = B.p + sb * i; d.ldb = tb ? N : K;
+      d.C = C.p + sc * i; d.ldc = M;
+      g.add(d);
+    }
+    g.finalize(s);
+    g.run(s);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, s);
+    for (int r = 0; r < reps; ++r) g.run(s);
+    cudaEventRecord(e1, s);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaStreamSynchronize(s);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return 2.0 * M * N * (double)K * batch * reps / (ms * 1e-3) / 1e12;
+  } catch (...) {
+    return -1.0;
+  }
+}
+
 void rsf_stats_enable(int on) { rsf::KStats::on = on != 0; }
 void rsf_stats_get(double* out4) { rsf::KStats::collect(out4); }
 void rsf_stats_reset(void) { rsf::KStats::reset(); }

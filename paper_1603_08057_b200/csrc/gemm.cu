@@ -264,6 +264,306 @@ void launch_variant(bool ta, bool tb, dim3 grid, cudaStream_t s, const GemmDesc*
   else gemm_vb_kernel<BM, TM, true, true><<<grid, NT, 0, s>>>(d, pre, np, X0, X1, ldx, Mg);
 }
 
+
+// ---------------------------------------------------------------------------
+// DMMA variant: mma.sync.m8n8k4 f64 (SASS DMMA.8x8x4 on sm_100a). 128 threads,
+// CTA tile 64x64, warps 2x2 with 32x32 warp tiles (4x4 mma tiles), BK = 16.
+// Fragments (PTX m8n8k4 .f64): A[g][t], B[t][g], C[g][2t..2t+1] with g = lane>>2,
+// t = lane&3.  Smem rows padded to 72 doubles (2 wavefronts per 32-lane f64 load).
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(128) gemm_dmma_kernel(const GemmDesc* __restrict__ descs,
+                                                        const int* __restrict__ prefix, int nprob,
+                                                        double* X0, double* X1, int ldx, int Mglob) {
+  constexpr int BM = 64, LDS = 72, NTD = 128;
+  __shared__ __align__(16) double As[BK][LDS];
+  __shared__ __align__(16) double Bs[BK][LDS];
+  const int p = find_prob(prefix, nprob, blockIdx.x);
+  const GemmDesc& dd = descs[p];
+  const int M = dd.M < 0 ? Mglob : dd.M;
+  const int N = dd.N, K = dd.K;
+  const int m0 = blockIdx.y * BM;
+  if (m0 >= M) return;
+  const int n0 = (blockIdx.x - __ldg(prefix + p)) * BN;
+  if (dd.lower && n0 >= m0 + BM) return;
+  const double* A = dd.selA == 0 ? dd.A + dd.offA : (dd.selA == 1 ? X0 : X1) + dd.offA * (long long)ldx;
+  const double* B = dd.selB == 0 ? dd.B + dd.offB : (dd.selB == 1 ? X0 : X1) + dd.offB * (long long)ldx;
+  double* C = dd.selC == 0 ? dd.C + dd.offC : (dd.selC == 1 ? X0 : X1) + dd.offC * (long long)ldx;
+  const long long lda = dd.selA ? ldx : dd.lda;
+  const long long ldb = dd.selB ? ldx : dd.ldb;
+  const long long ldc = dd.selC ? ldx : dd.ldc;
+  const int* mapA = dd.mapA;
+  const int* mapB = dd.mapB;
+  const int* mapC = dd.mapC;
+  const double alpha = dd.alpha, beta = dd.beta;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, tq = lane & 3;
+  const int wm = warp & 1, wn = warp >> 1;
+  constexpr int AE = BM * BK / NTD, BE = BK * BN / NTD;   // 8 each
+  double ra[AE], rb[BE];
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int r = 0; r < AE; ++r) {
+      int e = tid + r * NTD, i, l;
+      if (!TA) { i = e % BM; l = e / BM; } else { l = e % BK; i = e / BK; }
+      int gi = m0 + i, gl = k0 + l;
+      double v = 0.0;
+      if (gi < M && gl < K) {
+        if (!TA) { long long c = mapA ? __ldg(mapA + gl) : gl; v = A[c * lda + gi]; }
+        else { long long c = mapA ? __ldg(mapA + gi) : gi; v = A[c * lda + gl]; }
+      }
+      ra[r] = v;
+    }
+#pragma unroll
+    for (int r = 0; r < BE; ++r) {
+      int e = tid + r * NTD, l, j;
+      if (!TB) { l = e % BK; j = e / BK; } else { j = e % BN; l = e / BN; }
+      int gl = k0 + l, gj = n0 + j;
+      double v = 0.0;
+      if (gl < K && gj < N) {
+        if (!TB) { long long c = mapB ? __ldg(mapB + gj) : gj; v = B[c * ldb + gl]; }
+        else { long long c = mapB ? __ldg(mapB + gl) : gl; v = B[c * ldb + gj]; }
+      }
+      rb[r] = v;
+    }
+  };
+  auto store = [&]() {
+#pragma unroll
+    for (int r = 0; r < AE; ++r) {
+      int e = tid + r * NTD, i, l;
+      if (!TA) { i = e % BM; l = e / BM; } else { l = e % BK; i = e / BK; }
+      As[l][i] = ra[r];
+    }
+#pragma unroll
+    for (int r = 0; r < BE; ++r) {
+      int e = tid + r * NTD, l, j;
+      if (!TB) { l = e % BK; j = e / BK; } else { j = e % BN; l = e / BN; }
+      Bs[l][j] = rb[r];
+    }
+  };
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) { acc[a][b][0] = 0.0; acc[a][b][1] = 0.0; }
+  if (K > 0) load(0);
+  for (int k0 = 0; k0 < K; k0 += BK) {
+    store();
+    __syncthreads();
+    if (k0 + BK < K) load(k0 + BK);
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) af[mi] = As[kk + tq][wm * 32 + mi * 8 + g];
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) bf[ni] = Bs[kk + tq][wn * 32 + ni * 8 + g];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                       : "+d"(acc[mi][ni][0]), "+d"(acc[mi][ni][1])
+                       : "d"(af[mi]), "d"(bf[ni]));
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int ni = 0; ni < 4; ++ni) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int gj = n0 + wn * 32 + ni * 8 + 2 * tq + h;
+      if (gj >= N) continue;
+      const long long cc = mapC ? __ldg(mapC + gj) : gj;
+      double* Cc = C + cc * ldc;
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) {
+        const int gi = m0 + wm * 32 + mi * 8 + g;
+        if (gi >= M) continue;
+        double r = alpha * acc[mi][ni][h];
+        if (beta != 0.0) r = fma(beta, Cc[gi], r);
+        Cc[gi] = r;
+      }
+    }
+  }
+}
+
+void launch_dmma(bool ta, bool tb, dim3 grid, cudaStream_t s, const GemmDesc* d, const int* pre, int np,
+                 double* X0, double* X1, int ldx, int Mg) {
+  if (!ta && !tb) gemm_dmma_kernel<false, false><<<grid, 128, 0, s>>>(d, pre, np, X0, X1, ldx, Mg);
+  else if (ta && !tb) gemm_dmma_kernel<true, false><<<grid, 128, 0, s>>>(d, pre, np, X0, X1, ldx, Mg);
+  else if (!ta && tb) gemm_dmma_kernel<false, true><<<grid, 128, 0, s>>>(d, pre, np, X0, X1, ldx, Mg);
+  else gemm_dmma_kernel<true, true><<<grid, 128, 0, s>>>(d, pre, np, X0, X1, ldx, Mg);
+}
+
+
+// ---------------------------------------------------------------------------
+// Pipelined DMMA variant: CTA tile 128 x 64, BK = 16, 256 threads (8 warps as
+// 4 x 2, warp tile 32 x 32 = 4 x 4 DMMA.8x8x4 tiles), 4-stage cp.async (LDGSTS)
+// pipeline with zero-fill for the ragged edges, gathered columns via maps.
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+constexpr int P_BM = 128, P_BN = 64, P_BK = 16, P_ST = 4, P_NT = 256;
+constexpr int P_LDA = P_BM + 8, P_LDB = P_BN + 8;
+constexpr size_t P_SMEM = (size_t)P_ST * P_BK * (P_LDA + P_LDB) * sizeof(double);
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(P_NT, 2) gemm_pipe_kernel(const GemmDesc* __restrict__ descs,
+                                                            const int* __restrict__ prefix, int nprob,
+                                                            double* X0, double* X1, int ldx, int Mglob) {
+  extern __shared__ __align__(16) double psm[];
+  double* As = psm;                              // [ST][BK][LDA]
+  double* Bs = psm + P_ST * P_BK * P_LDA;        // [ST][BK][LDB]
+  const int p = find_prob(prefix, nprob, blockIdx.x);
+  const GemmDesc& dd = descs[p];
+  const int M = dd.M < 0 ? Mglob : dd.M;
+  const int N = dd.N, K = dd.K;
+  const int m0 = blockIdx.y * P_BM;
+  if (m0 >= M) return;
+  const int n0 = (blockIdx.x - __ldg(prefix + p)) * P_BN;
+  if (dd.lower && n0 >= m0 + P_BM) return;
+  const double* A = dd.selA == 0 ? dd.A + dd.offA : (dd.selA == 1 ? X0 : X1) + dd.offA * (long long)ldx;
+  const double* B = dd.selB == 0 ? dd.B + dd.offB : (dd.selB == 1 ? X0 : X1) + dd.offB * (long long)ldx;
+  double* C = dd.selC == 0 ? dd.C + dd.offC : (dd.selC == 1 ? X0 : X1) + dd.offC * (long long)ldx;
+  const long long lda = dd.selA ? ldx : dd.lda;
+  const long long ldb = dd.selB ? ldx : dd.ldb;
+  const long long ldc = dd.selC ? ldx : dd.ldc;
+  const int* mapA = dd.mapA;
+  const int* mapB = dd.mapB;
+  const int* mapC = dd.mapC;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, tq = lane & 3;
+  const int wm = warp & 3, wn = warp >> 2;
+
+  auto load_stage = [&](int st, int k0) {
+    double* as = As + st * P_BK * P_LDA;
+    double* bs = Bs + st * P_BK * P_LDB;
+#pragma unroll
+    for (int r = 0; r < (P_BM * P_BK) / P_NT; ++r) {
+      const int e = tid + r * P_NT;
+      int i, l;
+      if (!TA) { i = e % P_BM; l = e / P_BM; } else { l = e % P_BK; i = e / P_BK; }
+      const int gi = m0 + i, gl = k0 + l;
+      const bool v = gi < M && gl < K;
+      const double* src = A;
+      if (v) {
+        if (!TA) { const long long c = mapA ? __ldg(mapA + gl) : gl; src = A + c * lda + gi; }
+        else { const long long c = mapA ? __ldg(mapA + gi) : gi; src = A + c * lda + gl; }
+      }
+      cp_async8(as + l * P_LDA + i, src, v);
+    }
+#pragma unroll
+    for (int r = 0; r < (P_BK * P_BN) / P_NT; ++r) {
+      const int e = tid + r * P_NT;
+      int l, j;
+      if (!TB) { l = e % P_BK; j = e / P_BK; } else { j = e % P_BN; l = e / P_BN; }
+      const int gl = k0 + l, gj = n0 + j;
+      const bool v = gl < K && gj < N;
+      const double* src = B;
+      if (v) {
+        if (!TB) { const long long c = mapB ? __ldg(mapB + gj) : gj; src = B + c * ldb + gl; }
+        else { const long long c = mapB ? __ldg(mapB + gl) : gl; src = B + c * ldb + gj; }
+      }
+      cp_async8(bs + l * P_LDB + j, src, v);
+    }
+  };
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) { acc[a][b][0] = 0.0; acc[a][b][1] = 0.0; }
+
+  const int nk = (K + P_BK - 1) / P_BK;
+#pragma unroll
+  for (int st = 0; st < P_ST - 1; ++st) {
+    if (st < nk) load_stage(st, st * P_BK);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<P_ST - 2>();
+    __syncthreads();
+    const int pf = kt + P_ST - 1;
+    if (pf < nk) load_stage(pf % P_ST, pf * P_BK);
+    cp_async_commit();
+    const double* as = As + (kt % P_ST) * P_BK * P_LDA;
+    const double* bs = Bs + (kt % P_ST) * P_BK * P_LDB;
+#pragma unroll
+    for (int kk = 0; kk < P_BK; kk += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) af[mi] = as[(kk + tq) * P_LDA + wm * 32 + mi * 8 + g];
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) bf[ni] = bs[(kk + tq) * P_LDB + wn * 32 + ni * 8 + g];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                       : "+d"(acc[mi][ni][0]), "+d"(acc[mi][ni][1])
+                       : "d"(af[mi]), "d"(bf[ni]));
+    }
+  }
+  cp_async_wait<0>();
+  const double alpha = dd.alpha, beta = dd.beta;
+#pragma unroll
+  for (int ni = 0; ni < 4; ++ni) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int gj = n0 + wn * 32 + ni * 8 + 2 * tq + h;
+      if (gj >= N) continue;
+      const long long cc = mapC ? __ldg(mapC + gj) : gj;
+      double* Cc = C + cc * ldc;
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) {
+        const int gi = m0 + wm * 32 + mi * 8 + g;
+        if (gi >= M) continue;
+        double r = alpha * acc[mi][ni][h];
+        if (beta != 0.0) r = fma(beta, Cc[gi], r);
+        Cc[gi] = r;
+      }
+    }
+  }
+}
+
+void launch_pipe(bool ta, bool tb, dim3 grid, cudaStream_t s, const GemmDesc* d, const int* pre, int np,
+                 double* X0, double* X1, int ldx, int Mg) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gemm_pipe_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P_SMEM);
+    cudaFuncSetAttribute(gemm_pipe_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P_SMEM);
+    cudaFuncSetAttribute(gemm_pipe_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P_SMEM);
+    cudaFuncSetAttribute(gemm_pipe_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P_SMEM);
+    attr = true;
+  }
+  if (!ta && !tb) gemm_pipe_kernel<false, false><<<grid, P_NT, P_SMEM, s>>>(d, pre, np, X0, X1, ldx, Mg);
+  else if (ta && !tb) gemm_pipe_kernel<true, false><<<grid, P_NT, P_SMEM, s>>>(d, pre, np, X0, X1, ldx, Mg);
+  else if (!ta && tb) gemm_pipe_kernel<false, true><<<grid, P_NT, P_SMEM, s>>>(d, pre, np, X0, X1, ldx, Mg);
+  else gemm_pipe_kernel<true, true><<<grid, P_NT, P_SMEM, s>>>(d, pre, np, X0, X1, ldx, Mg);
+}
+
+int gemm_mode() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RSF_GEMM");
+    std::string m = e ? e : "pipe";
+    v = m == "dfma" ? 0 : (m == "dmma" ? 1 : 2);
+  }
+  return v;
+}
+
+bool use_dmma() {
+  static int v = -1;
+  if (v < 0) { const char* e = getenv("RSF_GEMM"); v = (e && std::string(e) == "dfma") ? 0 : 1; }
+  return v == 1;
+}
+
 }  // namespace
 
 void GemmBatch::finalize(cudaStream_t s) const {
@@ -295,6 +595,13 @@ void GemmBatch::run(cudaStream_t s, double* X0, double* X1, int ldx, int Mglob) 
   if (M <= 16) {
     dim3 grid(totalN_, ceil_div(M, 16));
     launch_variant<16, 1>(ta_, tb_, grid, s, d_.p, prefix_.p, (int)h_.size(), X0, X1, ldx, Mglob);
+  } else if (gemm_mode() == 2) {
+    // tiles are 64 wide in N for every variant (prefix computed with BN = 64)
+    dim3 grid(totalN_, ceil_div(M, P_BM));
+    launch_pipe(ta_, tb_, grid, s, d_.p, prefix_.p, (int)h_.size(), X0, X1, ldx, Mglob);
+  } else if (gemm_mode() == 1) {
+    dim3 grid(totalN_, ceil_div(M, 64));
+    launch_dmma(ta_, tb_, grid, s, d_.p, prefix_.p, (int)h_.size(), X0, X1, ldx, Mglob);
   } else {
     dim3 grid(totalN_, ceil_div(M, 64));
     launch_variant<64, 4>(ta_, tb_, grid, s, d_.p, prefix_.p, (int)h_.size(), X0, X1, ldx, Mglob);

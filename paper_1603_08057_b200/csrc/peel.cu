@@ -106,6 +106,20 @@ __global__ void eye_kernel(const EyeDesc* __restrict__ descs) {
   }
 }
 
+// Y_k (n_i x k, ld n_i) <- probe columns piv[0:k] of the sketch rows of box i,
+// read from the column chunks of Y_g (chunk c holds probe columns [c*kb, ...), X' layout)
+struct GatherDesc { double* Yk; const int* piv; int ib, ni, k; };
+__global__ void gather_cols_kernel(const GatherDesc* __restrict__ descs, double* const* __restrict__ chunks,
+                                   const int* __restrict__ chw, int kb) {
+  const GatherDesc d = descs[blockIdx.y];
+  const long long tot = (long long)d.ni * d.k;
+  for (long long e = blockIdx.x * (long long)NT + threadIdx.x; e < tot; e += (long long)gridDim.x * NT) {
+    const int t = (int)(e % d.ni), j = (int)(e / d.ni);
+    const int col = __ldg(d.piv + j), ch = col / kb, w = __ldg(chw + ch);
+    d.Yk[e] = chunks[ch][(long long)(d.ib + t) * w + (col - ch * kb)];
+  }
+}
+
 // E' (k x n): 1 where t - leafbegin[t] == e0 + j
 __global__ void extract_probe_kernel(double* X, int k, int n, const int* __restrict__ lb, int e0) {
   const long long tot = (long long)n * k;
@@ -322,7 +336,7 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
     int hint = o.peel_start;
     if (prev_rank < 0 && F.levels.size() > 1)
       for (int kk : F.levels[1].k) hint = std::max(hint, kk);
-    int c = (prev_rank < 0) ? hint : prev_rank + o.oversample;
+    int c = (prev_rank < 0) ? (int)std::ceil(0.6 * hint) : prev_rank + o.oversample;
     c = std::min(std::max(c, o.oversample + 8), cmax);
     c = (c + 7) / 8 * 8;
 
@@ -357,101 +371,147 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
           double bytes = 0;
           while (q1 < gq.size()) {
             const auto& p = pairs[gq[q1]];
-            const double bb = 8.0 * (2.0 * p.ni * (double)c + 2.0 * (double)c * c);
+            const double bb = 8.0 * (3.0 * p.ni * (double)c + 3.0 * (double)c * c);
             if (q1 > q0 && bytes + bb > budget) break;
             bytes += bb;
             ++q1;
           }
           const size_t B = q1 - q0;
-          std::vector<long long> qo(B), to(B), wo(B), po(B);
-          long long qt = 0, tt = 0, wt = 0, pt = 0;
+          // per pair: W_i^T (c x n_i), P = W_i^T Y_ij (c x c), Pc (RRQR copy)
+          std::vector<long long> wo(B), po(B);
+          long long wt = 0, pt = 0;
           for (size_t x = 0; x < B; ++x) {
             const auto& p = pairs[gq[q0 + x]];
-            const int qq = std::min(p.ni, c);
-            qo[x] = qt; qt += (long long)p.ni * c;
-            to[x] = tt; tt += (long long)((qq + QR_NB - 1) / QR_NB) * QR_NB * QR_NB;
             wo[x] = wt; wt += (long long)c * p.ni;
             po[x] = pt; pt += (long long)c * c;
           }
-          DBuf<double> Qws(qt, s), Tws(std::max<long long>(tt, 1), s), Wi(wt, s);
-          DBuf<double> Pb(pt, s);
+          DBuf<double> Wi(wt, s), Pb(pt, s), Pc(pt, s);
           DBuf<int> dpv((size_t)c * B, s);
           std::vector<int> kk;
-          std::vector<int> kdone;
           {
-            RSF_PHASE("p.orth_rank", s);
-            std::vector<TrDesc> td;
+            RSF_PHASE("p.sketch_rank", s);
+            GemmBatch gp(false, true);   // P_ij(:, chunk cols) = W_i^T (Y_chunk(:, I_i))^T
             for (size_t x = 0; x < B; ++x) {
               const auto& p = pairs[gq[q0 + x]];
-              for (size_t ci = 0; ci < ych.size(); ++ci)
-                td.push_back(TrDesc{ych[ci].p + (long long)p.ib * ykk[ci], ykk[ci],
-                                    Qws.p + qo[x] + (long long)ycs[ci] * p.ni, p.ni, ykk[ci]});
-              // W_i^T (c x n_i): the same Philox entries as in the sketches
+              // W_i^T: the same Philox entries as in the sketches
               probes_kernel<<<gxx((long long)p.ni * c), NT, 0, s>>>(Wi.p + wo[x], c, p.ib, p.ib + p.ni, t.d_perm.p,
                                                                   nullptr, 0, 0, lev, trace_id, seed32, c);
               count_launch();
-            }
-            auto dtd = up(td, s);
-            for (size_t o2 = 0; o2 < td.size(); o2 += 65535) {
-              unsigned nz = (unsigned)std::min<size_t>(65535, td.size() - o2);
-              transpose_kernel<<<dim3(64, 1, nz), NT, 0, s>>>(dtd.p + o2);
-              count_launch();
-              RSF_LAUNCH_CHECK();
-            }
-            GemmBatch gp(false, false);   // P_ij = W_i^T Y_ij (c x c)
-            for (size_t x = 0; x < B; ++x) {
-              const auto& p = pairs[gq[q0 + x]];
-              GemmDesc d = gdesc(c, c, p.ni);
-              d.A = Wi.p + wo[x]; d.lda = c; d.B = Qws.p + qo[x]; d.ldb = p.ni; d.C = Pb.p + po[x]; d.ldc = c;
-              gp.add(d);
+              for (size_t ci = 0; ci < ych.size(); ++ci) {
+                GemmDesc d = gdesc(c, ykk[ci], p.ni);
+                d.A = Wi.p + wo[x]; d.lda = c;
+                d.B = ych[ci].p + (long long)p.ib * ykk[ci]; d.ldb = ykk[ci];
+                d.C = Pb.p + po[x] + (long long)ycs[ci] * c; d.ldc = c;
+                gp.add(d);
+              }
               pd.flops += 2.0 * c * (double)c * p.ni;
             }
+            RSF_LAUNCH_CHECK();
             gp.run(s);
+            RSF_CUDA(cudaMemcpyAsync(Pc.p, Pb.p, pt * sizeof(double), cudaMemcpyDeviceToDevice, s));
+            // rank and column pivots of Y_ij from its Gaussian row sketch P_ij (R-N)
             std::vector<RRQRProb> rp;
-            for (size_t x = 0; x < B; ++x) {
-              const auto& p = pairs[gq[q0 + x]];
-              rp.push_back(RRQRProb{Qws.p + qo[x], p.ni, p.ni, c, dpv.p + (long long)x * c, Tws.p + to[x], nullptr, 0});
-            }
+            for (size_t x = 0; x < B; ++x)
+              rp.push_back(RRQRProb{Pc.p + po[x], c, c, c, dpv.p + (long long)x * c, nullptr, nullptr, 0});
             RRQRResult rr = rrqr_batched(s, rp, o.eps_peel,
                                          seed ^ (0xD1B54A32D192ED03ull * (unsigned long long)(lev + 64 * (trace_id + 1))));
             kk = rr.k;
-            kdone = rr.done;
           }
           for (size_t x = 0; x < B; ++x) mr = std::max(mr, kk[x]);
           if (mr > c - o.oversample && c < cmax) { fail = true; break; }
-          // U_ij = Q [I_k; 0] (orth) and A1_ij = W_i^T U_ij
-          long long ut = 0, at = 0;
-          std::vector<long long> uo(B), ao(B);
+          // U_ij = orth(Y_ij(:, piv[0:k])): preconditioned CholeskyQR2
+          //   U0 = Y_k R11^-1 (R11 from the sketch RRQR; W_i^T U0 has orthonormal columns),
+          //   then twice U <- U chol(U^T U)^-T
+          long long ut = 0, at = 0, kt = 0, rt = 0;
+          std::vector<long long> uo(B), ao(B), ko(B), ro(B);
           for (size_t x = 0; x < B; ++x) {
-            uo[x] = ut; ut += (long long)pairs[gq[q0 + x]].ni * kk[x];
+            const auto& p = pairs[gq[q0 + x]];
+            uo[x] = ut; ut += (long long)p.ni * kk[x];
             ao[x] = at; at += (long long)c * kk[x];
+            ko[x] = kt; kt += (long long)kk[x] * kk[x];
           }
           DBuf<double> Ub(std::max<long long>(ut, 1), s), Ab(std::max<long long>(at, 1), s);
           {
             RSF_PHASE("p.form_U", s);
+            DBuf<double> Yk(std::max<long long>(ut, 1), s), U0(std::max<long long>(ut, 1), s);
+            DBuf<double> Ri(std::max<long long>(kt, 1), s), G1(std::max<long long>(kt, 1), s), G1i(std::max<long long>(kt, 1), s);
+            // gather Y_k from the chunks
+            std::vector<double*> chp;
+            std::vector<int> chw;
+            for (size_t ci = 0; ci < ych.size(); ++ci) { chp.push_back(ych[ci].p); chw.push_back(ykk[ci]); }
+            DBuf<double*> dchp = up(chp, s);
+            DBuf<int> dchw = up(chw, s);
+            std::vector<GatherDesc> gd;
             std::vector<EyeDesc> ed;
-            std::vector<QApplyProb> ap;
-            GemmBatch ga(false, false);
+            std::vector<TrsmProb> tp;
             long long mx = 0;
             for (size_t x = 0; x < B; ++x) {
               const auto& p = pairs[gq[q0 + x]];
               if (kk[x] == 0) continue;
-              ed.push_back(EyeDesc{Ub.p + uo[x], p.ni, kk[x]});
+              gd.push_back(GatherDesc{Yk.p + uo[x], dpv.p + (long long)x * c, p.ib, p.ni, kk[x]});
+              ed.push_back(EyeDesc{Ri.p + ko[x], kk[x], kk[x]});
+              tp.push_back(TrsmProb{Pc.p + po[x], c, Ri.p + ko[x], kk[x], kk[x], kk[x]});
               mx = std::max(mx, (long long)p.ni * kk[x]);
-              ap.push_back(QApplyProb{Qws.p + qo[x], p.ni, p.ni, kdone[x], Tws.p + to[x], Ub.p + uo[x], p.ni, kk[x]});
-              GemmDesc d = gdesc(c, kk[x], p.ni);
-              d.A = Wi.p + wo[x]; d.lda = c; d.B = Ub.p + uo[x]; d.ldb = p.ni; d.C = Ab.p + ao[x]; d.ldc = c;
-              ga.add(d);
             }
-            if (!ed.empty()) {
+            if (!gd.empty()) {
+              auto dg = up(gd, s);
+              for (size_t o2 = 0; o2 < gd.size(); o2 += 65535) {
+                unsigned nz = (unsigned)std::min<size_t>(65535, gd.size() - o2);
+                gather_cols_kernel<<<dim3(gxx(mx), nz), NT, 0, s>>>(dg.p + o2, dchp.p, dchw.p, kb);
+                count_launch();
+              }
               auto de = up(ed, s);
               for (size_t o2 = 0; o2 < ed.size(); o2 += 65535) {
                 unsigned nz = (unsigned)std::min<size_t>(65535, ed.size() - o2);
                 eye_kernel<<<dim3(gxx(mx), nz), NT, 0, s>>>(de.p + o2);
                 count_launch();
-                RSF_LAUNCH_CHECK();
               }
-              ormqr_batched(s, ap, false);
+              RSF_LAUNCH_CHECK();
+              trsm_upper_batched(s, tp);                 // Ri = R11^-1
+              GemmBatch g0(false, false);
+              for (size_t x = 0; x < B; ++x) {
+                const auto& p = pairs[gq[q0 + x]];
+                if (kk[x] == 0) continue;
+                GemmDesc d = gdesc(p.ni, kk[x], kk[x]);   // U0 = Y_k R11^-1
+                d.A = Yk.p + uo[x]; d.lda = p.ni; d.B = Ri.p + ko[x]; d.ldb = kk[x]; d.C = U0.p + uo[x]; d.ldc = p.ni;
+                g0.add(d);
+              }
+              g0.run(s);
+              for (int pass = 0; pass < 2; ++pass) {
+                double* src = pass == 0 ? U0.p : Yk.p;   // U1 lives in Yk, U in Ub
+                double* dst = pass == 0 ? Yk.p : Ub.p;
+                GemmBatch gg(true, false), gu(false, true);
+                std::vector<PotrfProb> pp;
+                for (size_t x = 0; x < B; ++x) {
+                  const auto& p = pairs[gq[q0 + x]];
+                  if (kk[x] == 0) continue;
+                  GemmDesc d = gdesc(kk[x], kk[x], p.ni);     // Gram = U^T U
+                  d.A = src + uo[x]; d.lda = p.ni; d.B = src + uo[x]; d.ldb = p.ni; d.C = G1.p + ko[x]; d.ldc = kk[x];
+                  gg.add(d);
+                  pp.push_back(PotrfProb{G1.p + ko[x], kk[x], kk[x], G1i.p + ko[x], kk[x]});
+                  GemmDesc e = gdesc(p.ni, kk[x], kk[x]);     // U <- U L^-T
+                  e.A = src + uo[x]; e.lda = p.ni; e.B = G1i.p + ko[x]; e.ldb = kk[x]; e.C = dst + uo[x]; e.ldc = p.ni;
+                  gu.add(e);
+                  pd.flops += 4.0 * p.ni * (double)kk[x] * kk[x];
+                }
+                gg.run(s);
+                DBuf<double> ls(std::max<size_t>(pp.size(), 1), s);
+                DBuf<int> inf(std::max<size_t>(pp.size(), 1), s);
+                potrf_batched(s, pp, ls.p, inf.p);
+                auto hi = inf.to_host(pp.size());
+                for (int v : hi)
+                  if (v) throw Error(ST_ENUMERIC, "peeling: CholeskyQR of the skeleton sketch columns failed at level " +
+                                                      std::to_string(lev));
+                gu.run(s);
+              }
+              GemmBatch ga(false, false);
+              for (size_t x = 0; x < B; ++x) {
+                const auto& p = pairs[gq[q0 + x]];
+                if (kk[x] == 0) continue;
+                GemmDesc d = gdesc(c, kk[x], p.ni);            // A1 = W_i^T U_ij
+                d.A = Wi.p + wo[x]; d.lda = c; d.B = Ub.p + uo[x]; d.ldb = p.ni; d.C = Ab.p + ao[x]; d.ldc = c;
+                ga.add(d);
+              }
               ga.run(s);
             }
           }
@@ -470,7 +530,7 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
         if (fail) break;
       }
       if (!fail) break;
-      int nc = (mr >= c - 1) ? (int)std::ceil(1.5 * c) : std::max(c + 8, (int)std::ceil(1.2 * mr) + o.oversample);
+      int nc = (mr >= c - 1) ? (int)std::ceil(1.4 * c) : std::max(c + 8, (int)std::ceil(1.1 * mr) + o.oversample);
       c = std::max(std::min((nc + 7) / 8 * 8, cmax), c + 8);
     }
     pd.cols[lev] = c;

@@ -403,7 +403,7 @@ def test_P13_peel_recovers_exact_low_rank_off_diagonal():
 def test_P13_peel_duplicate_parameter_gives_n(cfg1_case):
     c, xy, K, z, F = cfg1_case
     G = lambda X: 0.5 * (F.solve(F.apply(X)) + F.apply(F.solve(X)))  # noqa: E731
-    assert peel_trace(G, F.tree, 1e-6, _probe()) == pytest.approx(len(xy), rel=1e-9)
+    assert peel_trace(G, F.tree, 1e-6, _probe(), block=64) == pytest.approx(len(xy), rel=1e-9)
 
 
 def test_P13_peel_smooth_operator_vs_dense_trace():

@@ -1,0 +1,8 @@
+import os, sys
+sys.path.insert(0, '/root/repo')
+import paper_1603_08057_b200 as R
+shapes = [(512, 512, 512, 64), (512, 64, 64, 4096), (512, 32, 32, 8192), (4096, 4096, 4096, 1), (8192, 8192, 64, 1), (512, 2048, 2048, 8)]
+for (M, N, K, b) in shapes:
+    for ta, tb in [(0, 0), (0, 1)]:
+        v = R.lib.rsf_debug_gemm_bench(M, N, K, b, ta, tb, 5)
+        print(f"{os.environ.get('RSF_GEMM','pipe')} M={M} N={N} K={K} batch={b} ta={ta} tb={tb}: {v:.2f} TFLOP/s")
