@@ -222,31 +222,124 @@ struct GOp {
   }
 };
 
-// ----------------------------------------------------------------- G^(m) storage
-struct PairLR {
-  int i, j;          // level-box indices
-  int ib, ni, jb, nj;
-  int kij = 0;
-  long long uoff = -1, moff = -1;
-  int rev = -1;      // index of the pair (j, i)
-};
-
+// ----------------------------------------------------------------- G^(m): shared row bases
+// The peeled level-m operator G^(m) is stored with one
+// orthonormal row basis per box:  G^(m)_ij ~= V_i B_ij V_j^T for every ordered
+// sibling pair (i, j).  V_i spans the sketches of all three blocks of box row i
+// (grown group by group, truncated at eps_peel relative to each block's own
+// scale), the per-pair bases of Eq. lowrankapprox are
+// U_ij = V_i Z_ij, and B_ij = Z_ij M_ij Z_ji^T with B_ji = B_ij^T.
+// Storage is n * r_i per level instead of 3 n k_ij.
 struct PeelLevel {
-  std::vector<PairLR> pairs;
-  DBuf<double> U, M;
-  std::vector<DBuf<double>> Ubufs;
+  std::vector<DBuf<double>> V;   // per box: V_i (n_i x r_i, ld n_i)
+  DBuf<double> Brow;
+  long long tcols = 0;   // tmp columns per probe column: sum r (T') + sum r (S')
   GemmBatch g1, g2, g3;
-  std::vector<GemmBatch> g3s;
-  long long tcols = 0;   // temp columns per probe column
-  bool empty() const { return g1.empty(); }
   // Y' -= G^(m) X'   (X', Y' are k x n; tmp has k * tcols doubles)
   void subtract(cudaStream_t s, const double* X, double* Y, int k, double* tmp) const {
-    if (g2.empty()) return;
-    g1.run(s, const_cast<double*>(X), tmp, k, k);
-    g2.run(s, nullptr, tmp, k, k);
-    for (const auto& g : g3s) g.run(s, Y, tmp, k, k);
+    if (g3.empty()) return;
+    g1.run(s, const_cast<double*>(X), tmp, k, k);   // T'_j = X'(:, I_j) V_j
+    g2.run(s, nullptr, tmp, k, k);                  // S'_i = [T'_f]_{f in family(i)} Brow_i^T
+    g3.run(s, Y, tmp, k, k);                        // Y'(:, I_i) -= S'_i V_i^T
   }
 };
+
+// out (rows x q, ld rows) = transpose of rows piv[0:q] of src (c x rows, ld lds)
+struct GatherTDesc { const double* src; long long lds; const int* piv; double* out; int rows, q; };
+__global__ void gather_t_kernel(const GatherTDesc* __restrict__ descs) {
+  const GatherTDesc d = descs[blockIdx.y];
+  const long long tot = (long long)d.rows * d.q;
+  for (long long e = blockIdx.x * (long long)NT + threadIdx.x; e < tot; e += (long long)gridDim.x * NT) {
+    const int t = (int)(e % d.rows), j = (int)(e / d.rows);
+    d.out[e] = d.src[(long long)t * d.lds + __ldg(d.piv + j)];
+  }
+}
+
+// out = max(out, max_j ||A(:, j)||)   (one CTA per problem)
+struct ColMaxDesc { const double* A; long long lda; int rows, cols; double* out; };
+__global__ void colmax_kernel(const ColMaxDesc* __restrict__ descs) {
+  const ColMaxDesc d = descs[blockIdx.x];
+  __shared__ double red[NT / 32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double mx = 0.0;
+  for (int j = warp; j < d.cols; j += NT / 32) {
+    const double* a = d.A + (long long)j * d.lda;
+    double v = 0.0;
+    for (int r = lane; r < d.rows; r += 32) v += a[r] * a[r];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    mx = fmax(mx, v);
+  }
+  if (lane == 0) red[warp] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v = 0.0;
+    for (int w = 0; w < NT / 32; ++w) v = fmax(v, red[w]);
+    *d.out = fmax(*d.out, sqrt(v));
+  }
+}
+
+void launch_colmax(cudaStream_t s, const std::vector<ColMaxDesc>& v) {
+  if (v.empty()) return;
+  auto d = up(v, s);
+  for (size_t o = 0; o < v.size(); o += 65535) {
+    colmax_kernel<<<(unsigned)std::min<size_t>(65535, v.size() - o), NT, 0, s>>>(d.p + o);
+    count_launch();
+  }
+  RSF_LAUNCH_CHECK();
+}
+
+template <class D, class K>
+void launch_descs(cudaStream_t s, const std::vector<D>& v, long long maxelems, K kern) {
+  if (v.empty() || maxelems <= 0) return;
+  auto d = up(v, s);
+  for (size_t o = 0; o < v.size(); o += 65535) {
+    const unsigned nz = (unsigned)std::min<size_t>(65535, v.size() - o);
+    kern<<<dim3(gxx(maxelems), nz), NT, 0, s>>>(d.p + o);
+    count_launch();
+  }
+  RSF_LAUNCH_CHECK();
+}
+
+// U <- orth(U) by two passes of U <- U chol(U^T U)^-T (CholeskyQR2), in place.
+struct CQProb { double* U; int rows, k; };
+void cholqr2_batched(cudaStream_t s, const std::vector<CQProb>& v, int lev, double* flops) {
+  std::vector<CQProb> w;
+  for (auto& p : v) if (p.k > 0 && p.rows > 0) w.push_back(p);
+  if (w.empty()) return;
+  long long st = 0, gt = 0;
+  std::vector<long long> so(w.size()), go(w.size());
+  for (size_t x = 0; x < w.size(); ++x) {
+    so[x] = st; st += (long long)w[x].rows * w[x].k;
+    go[x] = gt; gt += (long long)w[x].k * w[x].k;
+  }
+  DBuf<double> S(st, s), G(gt, s), Gi(gt, s), ls(w.size(), s);
+  DBuf<int> inf(w.size(), s);
+  for (int pass = 0; pass < 2; ++pass) {
+    GemmBatch gg(true, false), gu(false, true);
+    std::vector<PotrfProb> pp;
+    for (size_t x = 0; x < w.size(); ++x) {
+      const auto& p = w[x];
+      double* src = pass == 0 ? p.U : S.p + so[x];
+      double* dst = pass == 0 ? S.p + so[x] : p.U;
+      GemmDesc d = gdesc(p.k, p.k, p.rows);        // Gram = U^T U
+      d.A = src; d.lda = p.rows; d.B = src; d.ldb = p.rows; d.C = G.p + go[x]; d.ldc = p.k;
+      gg.add(d);
+      pp.push_back(PotrfProb{G.p + go[x], p.k, p.k, Gi.p + go[x], p.k});
+      GemmDesc e = gdesc(p.rows, p.k, p.k);        // U <- U L^-T
+      e.A = src; e.lda = p.rows; e.B = Gi.p + go[x]; e.ldb = p.k; e.C = dst; e.ldc = p.rows;
+      gu.add(e);
+      if (flops) *flops += 4.0 * p.rows * (double)p.k * p.k;
+    }
+    gg.run(s);
+    potrf_batched(s, pp, ls.p, inf.p);
+    for (int v2 : inf.to_host(w.size()))
+      if (v2) throw Error(ST_ENUMERIC, "peeling: CholeskyQR of a sketch basis failed at level " + std::to_string(lev));
+    gu.run(s);
+  }
+}
+
+struct PBox { int node, ib, ni, fam0, fam1, quad; };
 
 }  // namespace
 
@@ -285,7 +378,7 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
   pd.rank_max.assign(L + 1, 0);
   int prev_rank = -1;
   const int kb = std::max(16, o.probe_block);
-  const double budget = 24.0 * (1ull << 30);   // bytes of transient per-batch buffers
+  const double budget = 16.0 * (1ull << 30);   // bytes of transient per-batch buffers
 
   auto residual = [&](const double* W, double* Y, int k, int upto) {
     G.apply(W, Y, k);
@@ -294,45 +387,40 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
     for (int m = 1; m < upto; ++m) peeled[m].subtract(s, W, Y, k, tmp.p);
   };
 
-  for (int lev = 1; lev <= L; ++lev) {
+  static const int verbose = getenv("RSF_VERBOSE") ? atoi(getenv("RSF_VERBOSE")) : 0;
+  static const int max_lev = getenv("RSF_PEEL_LEVELS") ? atoi(getenv("RSF_PEEL_LEVELS")) : 1 << 30;
+  for (int lev = 1; lev <= std::min(L, max_lev); ++lev) {
     const std::vector<int>& nodes = t.levels[lev];
     const int nb = (int)nodes.size();
-    // ordered sibling pairs (Def. sibs), grouped by the probe group quad(j)
-    std::vector<PairLR> pairs;
-    std::unordered_map<int, std::vector<int>> fam;
-    for (int b = 0; b < nb; ++b) fam[t.parent[nodes[b]]].push_back(b);
-    for (int b = 0; b < nb; ++b) {
-      for (int c2 : fam[t.parent[nodes[b]]]) {
-        if (c2 == b) continue;
-        PairLR p;
-        p.i = b; p.j = c2;
-        p.ib = t.begin[nodes[b]]; p.ni = t.end[nodes[b]] - p.ib;
-        p.jb = t.begin[nodes[c2]]; p.nj = t.end[nodes[c2]] - p.jb;
-        pairs.push_back(p);
-      }
-    }
-    if (pairs.empty()) continue;
-    const size_t P = pairs.size();
-    {
-      std::unordered_map<long long, int> idx;
-      for (int q = 0; q < (int)P; ++q) idx[(long long)pairs[q].i * nb + pairs[q].j] = q;
-      for (auto& p : pairs) p.rev = idx[(long long)p.j * nb + p.i];
-    }
-    std::vector<std::vector<int>> grp(4);
-    for (size_t q = 0; q < P; ++q) grp[t.quad[nodes[pairs[q].j]]].push_back((int)q);
-    std::vector<int> gorder = {0, 1, 2, 3};
-    std::stable_sort(gorder.begin(), gorder.end(), [&](int a2, int b2) { return grp[a2].size() > grp[b2].size(); });
-    std::vector<int> hq(n, -1);
+    // boxes and families (siblings are consecutive in Morton order; Def. sibs)
+    std::vector<PBox> bx(nb);
     int maxni = 0;
     for (int b = 0; b < nb; ++b) {
       const int nd = nodes[b];
-      for (int x = t.begin[nd]; x < t.end[nd]; ++x) hq[x] = t.quad[nd];
-      maxni = std::max(maxni, t.end[nd] - t.begin[nd]);
+      bx[b].node = nd; bx[b].ib = t.begin[nd]; bx[b].ni = t.end[nd] - t.begin[nd]; bx[b].quad = t.quad[nd];
+      maxni = std::max(maxni, bx[b].ni);
     }
+    int npairs = 0;
+    for (int b = 0; b < nb;) {
+      int e = b;
+      while (e < nb && t.parent[nodes[e]] == t.parent[nodes[b]]) ++e;
+      for (int x = b; x < e; ++x) { bx[x].fam0 = b; bx[x].fam1 = e; }
+      npairs += (e - b) * (e - b - 1);
+      b = e;
+    }
+    if (npairs == 0) continue;
+    // probe groups: W_g on the boxes with quadrant g (R-R), largest groups first
+    std::vector<int> gcount(4, 0);
+    for (auto& b : bx) if (b.fam1 - b.fam0 > 1) gcount[b.quad]++;
+    std::vector<int> gorder = {0, 1, 2, 3};
+    std::stable_sort(gorder.begin(), gorder.end(), [&](int a2, int b2) { return gcount[a2] > gcount[b2]; });
+    std::vector<int> hq(n, -1);
+    for (auto& b : bx)
+      for (int x = b.ib; x < b.ib + b.ni; ++x) hq[x] = b.quad;
     DBuf<int> qmap = up(hq, s);
     const int cmax = ((maxni + o.oversample) + 7) / 8 * 8;
-    // initial width: level 1 from the factor's level-1 skeleton sizes (ranks of Sigma's
-    // off-diagonal blocks at eps_fact); deeper levels from the previous level's ranks (R-M)
+    // initial width (R-M): level 1 from the factor's level-1 skeleton sizes, deeper levels
+    // from the previous level's ranks
     int hint = o.peel_start;
     if (prev_rank < 0 && F.levels.size() > 1)
       for (int kk : F.levels[1].k) hint = std::max(hint, kk);
@@ -340,194 +428,348 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
     c = std::min(std::max(c, o.oversample + 8), cmax);
     c = (c + 7) / 8 * 8;
 
-    PeelLevel& PL = peeled[lev];
-    std::vector<DBuf<double>> keep;          // U, A1, P buffers of this level
-    std::vector<double*> Up(P, nullptr), A1p(P, nullptr), Pp(P, nullptr);
-    std::vector<int> kp(P, 0);
+    // per-level state (reset when the width grows)
+    std::vector<int> rb(nb, 0);                   // basis size r_i
+    std::vector<DBuf<double>> Vb(nb), Ab(nb);     // V_i (n_i x r_i, ld n_i), A_i = W_i^T V_i (c x r_i, ld c)
+    // per ordered pair (index: b * 4 + position of the sibling in the family)
+    struct PairData { int k = 0, rz = 0; double *Z = nullptr, *X = nullptr, *Lm = nullptr, *Gi = nullptr; };
+    std::vector<PairData> pdat((size_t)nb * 4);
+    std::vector<DBuf<double>> arenas;
     int mr = 0;
     while (true) {
-      keep.clear();
+      std::fill(rb.begin(), rb.end(), 0);
+      for (auto& v : Vb) v.release();
+      for (auto& v : Ab) v.release();
+      arenas.clear();
+      for (auto& q : pdat) q = PairData{};
       bool fail = false;
       mr = 0;
       for (int g : gorder) {
-        if (grp[g].empty()) continue;
-        // sketch Y_g = (G - sum_{m<l} G^(m)) W_g in column chunks
-        std::vector<DBuf<double>> ych;
-        std::vector<int> ycs, ykk;
+        if (gcount[g] == 0) continue;
+        // boxes i with a sibling j in quadrant g (at most one per family)
+        std::vector<int> act, partner;
+        for (int b = 0; b < nb; ++b) {
+          if (bx[b].quad == g) continue;
+          for (int x = bx[b].fam0; x < bx[b].fam1; ++x)
+            if (bx[x].quad == g) { act.push_back(b); partner.push_back(x); break; }
+        }
+        if (act.empty()) continue;
+        const size_t NA = act.size();
+        // per act box, for the whole group: P_ij = W_i^T Y_ij (c x c), C_ij' = Y_ij^T [V_i ...]
+        // (c x (r_i + c) upper bound, ld c), the block scale ref_ij = max_j ||W_i^T Y_ij(:, j)||
+        std::vector<long long> po(NA), cco(NA), cccap(NA);
+        long long pt = 0, cct = 0;
+        for (size_t x = 0; x < NA; ++x) {
+          const int i = act[x];
+          po[x] = pt; pt += (long long)c * c;
+          cccap[x] = std::min<long long>(bx[i].ni, (long long)rb[i] + c);
+          cco[x] = cct; cct += (long long)c * cccap[x];
+        }
+        DBuf<double> P(pt, s), CC(std::max<long long>(cct, 1), s), ref(NA, s);
+        ref.zero();
+        CC.zero();
+        // sketch Y'_g = ((G - sum_{m<l} G^(m)) W_g)^T in chunks of kb probe columns;
+        // every chunk extends the bases V_i of the boxes that see it
+        DBuf<double> W((size_t)n * std::min(kb, c), s), Y((size_t)n * std::min(kb, c), s);
         for (int c0 = 0; c0 < c; c0 += kb) {
           const int k = std::min(kb, c - c0);
-          DBuf<double> W((size_t)n * k, s), Y((size_t)n * k, s);
           gen_probes(s, W.p, k, n, t.d_perm.p, qmap.p, g, c0, lev, trace_id, seed);
           residual(W.p, Y.p, k, lev);
-          ych.push_back(std::move(Y));
-          ycs.push_back(c0);
-          ykk.push_back(k);
-        }
-        // pair batches under the byte budget
-        const std::vector<int>& gq = grp[g];
-        size_t q0 = 0;
-        while (q0 < gq.size() && !fail) {
-          size_t q1 = q0;
-          double bytes = 0;
-          while (q1 < gq.size()) {
-            const auto& p = pairs[gq[q1]];
-            const double bb = 8.0 * (3.0 * p.ni * (double)c + 3.0 * (double)c * c);
-            if (q1 > q0 && bytes + bb > budget) break;
-            bytes += bb;
-            ++q1;
-          }
-          const size_t B = q1 - q0;
-          // per pair: W_i^T (c x n_i), P = W_i^T Y_ij (c x c), Pc (RRQR copy)
-          std::vector<long long> wo(B), po(B);
-          long long wt = 0, pt = 0;
-          for (size_t x = 0; x < B; ++x) {
-            const auto& p = pairs[gq[q0 + x]];
-            wo[x] = wt; wt += (long long)c * p.ni;
-            po[x] = pt; pt += (long long)c * c;
-          }
-          DBuf<double> Wi(wt, s), Pb(pt, s), Pc(pt, s);
-          DBuf<int> dpv((size_t)c * B, s);
-          std::vector<int> kk;
-          {
-            RSF_PHASE("p.sketch_rank", s);
-            GemmBatch gp(false, true);   // P_ij(:, chunk cols) = W_i^T (Y_chunk(:, I_i))^T
+          RSF_PHASE("p.basis", s);
+          size_t x0 = 0;
+          while (x0 < NA) {
+            size_t x1 = x0;
+            double bytes = 0;
+            while (x1 < NA) {
+              const PBox& b = bx[act[x1]];
+              const double bb = 8.0 * ((double)b.ni * (c + 3.0 * k) + 3.0 * (double)c * k + 2.0 * (double)k * (rb[act[x1]] + k));
+              if (x1 > x0 && bytes + bb > budget) break;
+              bytes += bb;
+              ++x1;
+            }
+            const size_t B = x1 - x0;
+            std::vector<long long> wo(B), c1o(B), pro(B);
+            long long wt = 0, c1t = 0, prt = 0;
             for (size_t x = 0; x < B; ++x) {
-              const auto& p = pairs[gq[q0 + x]];
-              // W_i^T: the same Philox entries as in the sketches
-              probes_kernel<<<gxx((long long)p.ni * c), NT, 0, s>>>(Wi.p + wo[x], c, p.ib, p.ib + p.ni, t.d_perm.p,
+              const int i = act[x0 + x];
+              wo[x] = wt; wt += (long long)c * bx[i].ni;
+              c1o[x] = c1t; c1t += (long long)k * rb[i];
+              pro[x] = prt; prt += (long long)c * k;
+            }
+            DBuf<double> Wi(wt, s), C1(std::max<long long>(c1t, 1), s), Pr(prt, s);
+            DBuf<int> pivr((size_t)k * B, s);
+            GemmBatch gp(false, true), gc(false, false), gr(false, true), gpr(false, true);
+            std::vector<ColMaxDesc> cm;
+            for (size_t x = 0; x < B; ++x) {
+              const size_t xa = x0 + x;
+              const int i = act[xa];
+              const PBox& b = bx[i];
+              // W_i^T (c x n_i): the same Philox entries as box i's rows of its own group's probes
+              probes_kernel<<<gxx((long long)b.ni * c), NT, 0, s>>>(Wi.p + wo[x], c, b.ib, b.ib + b.ni, t.d_perm.p,
                                                                   nullptr, 0, 0, lev, trace_id, seed32, c);
               count_launch();
-              for (size_t ci = 0; ci < ych.size(); ++ci) {
-                GemmDesc d = gdesc(c, ykk[ci], p.ni);
-                d.A = Wi.p + wo[x]; d.lda = c;
-                d.B = ych[ci].p + (long long)p.ib * ykk[ci]; d.ldb = ykk[ci];
-                d.C = Pb.p + po[x] + (long long)ycs[ci] * c; d.ldc = c;
-                gp.add(d);
+              double* Yi = Y.p + (long long)b.ib * k;
+              GemmDesc d = gdesc(c, k, b.ni);              // P_ij(:, chunk) = W_i^T Y_ij(:, chunk)
+              d.A = Wi.p + wo[x]; d.lda = c; d.B = Yi; d.ldb = k; d.C = P.p + po[xa] + (long long)c * c0; d.ldc = c;
+              gp.add(d);
+              cm.push_back(ColMaxDesc{P.p + po[xa] + (long long)c * c0, c, c, k, ref.p + xa});
+              pd.flops += 2.0 * c * (double)k * b.ni;
+              if (rb[i] > 0) {                             // Res = (I - V_i V_i^T) Y_ij(:, chunk)
+                GemmDesc e = gdesc(k, rb[i], b.ni);
+                e.A = Yi; e.lda = k; e.B = Vb[i].p; e.ldb = b.ni; e.C = C1.p + c1o[x]; e.ldc = k;
+                gc.add(e);
+                GemmDesc f = gdesc(k, b.ni, rb[i]);
+                f.A = C1.p + c1o[x]; f.lda = k; f.B = Vb[i].p; f.ldb = b.ni; f.C = Yi; f.ldc = k;
+                f.alpha = -1.0; f.beta = 1.0;
+                gr.add(f);
+                pd.flops += 4.0 * k * (double)rb[i] * b.ni;
               }
-              pd.flops += 2.0 * c * (double)c * p.ni;
+              GemmDesc h = gdesc(c, k, b.ni);              // W_i^T Res
+              h.A = Wi.p + wo[x]; h.lda = c; h.B = Yi; h.ldb = k; h.C = Pr.p + pro[x]; h.ldc = c;
+              gpr.add(h);
             }
             RSF_LAUNCH_CHECK();
             gp.run(s);
-            RSF_CUDA(cudaMemcpyAsync(Pc.p, Pb.p, pt * sizeof(double), cudaMemcpyDeviceToDevice, s));
-            // rank and column pivots of Y_ij from its Gaussian row sketch P_ij (R-N)
+            launch_colmax(s, cm);
+            gc.run(s); gr.run(s); gpr.run(s);
             std::vector<RRQRProb> rp;
-            for (size_t x = 0; x < B; ++x)
-              rp.push_back(RRQRProb{Pc.p + po[x], c, c, c, dpv.p + (long long)x * c, nullptr, nullptr, 0});
-            RRQRResult rr = rrqr_batched(s, rp, o.eps_peel,
-                                         seed ^ (0xD1B54A32D192ED03ull * (unsigned long long)(lev + 64 * (trace_id + 1))));
-            kk = rr.k;
-          }
-          for (size_t x = 0; x < B; ++x) mr = std::max(mr, kk[x]);
-          if (mr > c - o.oversample && c < cmax) { fail = true; break; }
-          // U_ij = orth(Y_ij(:, piv[0:k])): preconditioned CholeskyQR2
-          //   U0 = Y_k R11^-1 (R11 from the sketch RRQR; W_i^T U0 has orthonormal columns),
-          //   then twice U <- U chol(U^T U)^-T
-          long long ut = 0, at = 0, kt = 0, rt = 0;
-          std::vector<long long> uo(B), ao(B), ko(B), ro(B);
-          for (size_t x = 0; x < B; ++x) {
-            const auto& p = pairs[gq[q0 + x]];
-            uo[x] = ut; ut += (long long)p.ni * kk[x];
-            ao[x] = at; at += (long long)c * kk[x];
-            ko[x] = kt; kt += (long long)kk[x] * kk[x];
-          }
-          DBuf<double> Ub(std::max<long long>(ut, 1), s), Ab(std::max<long long>(at, 1), s);
-          {
-            RSF_PHASE("p.form_U", s);
-            DBuf<double> Yk(std::max<long long>(ut, 1), s), U0(std::max<long long>(ut, 1), s);
-            DBuf<double> Ri(std::max<long long>(kt, 1), s), G1(std::max<long long>(kt, 1), s), G1i(std::max<long long>(kt, 1), s);
-            // gather Y_k from the chunks
-            std::vector<double*> chp;
-            std::vector<int> chw;
-            for (size_t ci = 0; ci < ych.size(); ++ci) { chp.push_back(ych[ci].p); chw.push_back(ykk[ci]); }
-            DBuf<double*> dchp = up(chp, s);
-            DBuf<int> dchw = up(chw, s);
-            std::vector<GatherDesc> gd;
+            for (size_t x = 0; x < B; ++x) {
+              RRQRProb r{Pr.p + pro[x], c, c, k, pivr.p + (long long)x * k, nullptr, nullptr, 0};
+              r.ref_in = ref.p + x0 + x;                   // threshold eps_peel * ||Y_ij|| (the block's scale)
+              rp.push_back(r);
+            }
+            std::vector<int> qq = rrqr_batched(s, rp, o.eps_peel,
+                                               seed ^ (0x9E3779B97F4A7C15ull * (unsigned long long)(lev + 64 * (trace_id + 3) + 4096 * c0))).k;
+            // new orthonormal directions Q_i = orth(Res(:, pivr[0:q])), re-orthogonalized against V_i
+            long long qt = 0, rt = 0;
+            std::vector<long long> qo(B), ro(B);
+            for (size_t x = 0; x < B; ++x) {
+              const int i = act[x0 + x];
+              qq[x] = std::min<int>(qq[x], (int)(cccap[x0 + x] - rb[i]));
+              qo[x] = qt; qt += (long long)bx[i].ni * qq[x];
+              ro[x] = rt; rt += (long long)qq[x] * qq[x];
+            }
+            DBuf<double> Qb(std::max<long long>(qt, 1), s), Q0(std::max<long long>(qt, 1), s), Ri(std::max<long long>(rt, 1), s);
+            std::vector<GatherTDesc> gd;
             std::vector<EyeDesc> ed;
             std::vector<TrsmProb> tp;
             long long mx = 0;
             for (size_t x = 0; x < B; ++x) {
-              const auto& p = pairs[gq[q0 + x]];
-              if (kk[x] == 0) continue;
-              gd.push_back(GatherDesc{Yk.p + uo[x], dpv.p + (long long)x * c, p.ib, p.ni, kk[x]});
-              ed.push_back(EyeDesc{Ri.p + ko[x], kk[x], kk[x]});
-              tp.push_back(TrsmProb{Pc.p + po[x], c, Ri.p + ko[x], kk[x], kk[x], kk[x]});
-              mx = std::max(mx, (long long)p.ni * kk[x]);
+              const int i = act[x0 + x];
+              if (qq[x] == 0) continue;
+              gd.push_back(GatherTDesc{Y.p + (long long)bx[i].ib * k, k, pivr.p + (long long)x * k, Q0.p + qo[x], bx[i].ni, qq[x]});
+              ed.push_back(EyeDesc{Ri.p + ro[x], qq[x], qq[x]});
+              tp.push_back(TrsmProb{Pr.p + pro[x], c, Ri.p + ro[x], qq[x], qq[x], qq[x]});
+              mx = std::max(mx, (long long)bx[i].ni * qq[x]);
             }
-            if (!gd.empty()) {
-              auto dg = up(gd, s);
-              for (size_t o2 = 0; o2 < gd.size(); o2 += 65535) {
-                unsigned nz = (unsigned)std::min<size_t>(65535, gd.size() - o2);
-                gather_cols_kernel<<<dim3(gxx(mx), nz), NT, 0, s>>>(dg.p + o2, dchp.p, dchw.p, kb);
-                count_launch();
-              }
-              auto de = up(ed, s);
-              for (size_t o2 = 0; o2 < ed.size(); o2 += 65535) {
-                unsigned nz = (unsigned)std::min<size_t>(65535, ed.size() - o2);
-                eye_kernel<<<dim3(gxx(mx), nz), NT, 0, s>>>(de.p + o2);
-                count_launch();
-              }
-              RSF_LAUNCH_CHECK();
-              trsm_upper_batched(s, tp);                 // Ri = R11^-1
-              GemmBatch g0(false, false);
-              for (size_t x = 0; x < B; ++x) {
-                const auto& p = pairs[gq[q0 + x]];
-                if (kk[x] == 0) continue;
-                GemmDesc d = gdesc(p.ni, kk[x], kk[x]);   // U0 = Y_k R11^-1
-                d.A = Yk.p + uo[x]; d.lda = p.ni; d.B = Ri.p + ko[x]; d.ldb = kk[x]; d.C = U0.p + uo[x]; d.ldc = p.ni;
-                g0.add(d);
-              }
-              g0.run(s);
-              for (int pass = 0; pass < 2; ++pass) {
-                double* src = pass == 0 ? U0.p : Yk.p;   // U1 lives in Yk, U in Ub
-                double* dst = pass == 0 ? Yk.p : Ub.p;
-                GemmBatch gg(true, false), gu(false, true);
-                std::vector<PotrfProb> pp;
-                for (size_t x = 0; x < B; ++x) {
-                  const auto& p = pairs[gq[q0 + x]];
-                  if (kk[x] == 0) continue;
-                  GemmDesc d = gdesc(kk[x], kk[x], p.ni);     // Gram = U^T U
-                  d.A = src + uo[x]; d.lda = p.ni; d.B = src + uo[x]; d.ldb = p.ni; d.C = G1.p + ko[x]; d.ldc = kk[x];
-                  gg.add(d);
-                  pp.push_back(PotrfProb{G1.p + ko[x], kk[x], kk[x], G1i.p + ko[x], kk[x]});
-                  GemmDesc e = gdesc(p.ni, kk[x], kk[x]);     // U <- U L^-T
-                  e.A = src + uo[x]; e.lda = p.ni; e.B = G1i.p + ko[x]; e.ldb = kk[x]; e.C = dst + uo[x]; e.ldc = p.ni;
-                  gu.add(e);
-                  pd.flops += 4.0 * p.ni * (double)kk[x] * kk[x];
-                }
-                gg.run(s);
-                DBuf<double> ls(std::max<size_t>(pp.size(), 1), s);
-                DBuf<int> inf(std::max<size_t>(pp.size(), 1), s);
-                potrf_batched(s, pp, ls.p, inf.p);
-                auto hi = inf.to_host(pp.size());
-                for (int v : hi)
-                  if (v) throw Error(ST_ENUMERIC, "peeling: CholeskyQR of the skeleton sketch columns failed at level " +
-                                                      std::to_string(lev));
-                gu.run(s);
-              }
-              GemmBatch ga(false, false);
-              for (size_t x = 0; x < B; ++x) {
-                const auto& p = pairs[gq[q0 + x]];
-                if (kk[x] == 0) continue;
-                GemmDesc d = gdesc(c, kk[x], p.ni);            // A1 = W_i^T U_ij
-                d.A = Wi.p + wo[x]; d.lda = c; d.B = Ub.p + uo[x]; d.ldb = p.ni; d.C = Ab.p + ao[x]; d.ldc = c;
-                ga.add(d);
-              }
-              ga.run(s);
+            launch_descs(s, gd, mx, gather_t_kernel);
+            launch_descs(s, ed, mx, eye_kernel);
+            trsm_upper_batched(s, tp);                    // R11^-1 of the residual sketch
+            GemmBatch g0(false, false);
+            std::vector<CQProb> cq;
+            for (size_t x = 0; x < B; ++x) {
+              const int i = act[x0 + x];
+              if (qq[x] == 0) continue;
+              GemmDesc d = gdesc(bx[i].ni, qq[x], qq[x]);   // Q0 R11^-1 (well conditioned)
+              d.A = Q0.p + qo[x]; d.lda = bx[i].ni; d.B = Ri.p + ro[x]; d.ldb = qq[x]; d.C = Qb.p + qo[x]; d.ldc = bx[i].ni;
+              g0.add(d);
+              cq.push_back(CQProb{Qb.p + qo[x], bx[i].ni, qq[x]});
             }
+            g0.run(s);
+            Q0.release();
+            cholqr2_batched(s, cq, lev, &pd.flops);
+            {
+              GemmBatch gh(true, false), gq(false, false);
+              long long ht = 0;
+              std::vector<long long> hoff(B);
+              for (size_t x = 0; x < B; ++x) { hoff[x] = ht; ht += (long long)rb[act[x0 + x]] * qq[x]; }
+              DBuf<double> H(std::max<long long>(ht, 1), s);
+              for (size_t x = 0; x < B; ++x) {
+                const int i = act[x0 + x];
+                if (qq[x] == 0 || rb[i] == 0) continue;
+                GemmDesc d = gdesc(rb[i], qq[x], bx[i].ni);  // H = V^T Q
+                d.A = Vb[i].p; d.lda = bx[i].ni; d.B = Qb.p + qo[x]; d.ldb = bx[i].ni; d.C = H.p + hoff[x]; d.ldc = rb[i];
+                gh.add(d);
+                GemmDesc e = gdesc(bx[i].ni, qq[x], rb[i]);  // Q -= V H
+                e.A = Vb[i].p; e.lda = bx[i].ni; e.B = H.p + hoff[x]; e.ldb = rb[i]; e.C = Qb.p + qo[x]; e.ldc = bx[i].ni;
+                e.alpha = -1.0; e.beta = 1.0;
+                gq.add(e);
+              }
+              if (!gh.empty()) {
+                gh.run(s); gq.run(s);
+                cholqr2_batched(s, cq, lev, &pd.flops);
+              }
+            }
+            // C_ij'(chunk, :) = Y_ij(:, chunk)^T [V_i, Q_i] = [C1, Res^T Q_i]; V_i <- [V_i, Q_i],
+            // A_i <- [A_i, W_i^T Q_i] (per-box buffers, regrown)
+            GemmBatch gcq(false, false);
+            std::vector<CopyProb> cc1;
+            std::vector<DBuf<double>> nV(B), nA(B);
+            for (size_t x = 0; x < B; ++x) {
+              const size_t xa = x0 + x;
+              const int i = act[xa];
+              const long long ni = bx[i].ni;
+              if (rb[i] > 0) cc1.push_back(CopyProb{C1.p + c1o[x], k, CC.p + cco[xa] + c0, c, k, rb[i], 1.0});
+              if (qq[x] == 0) continue;
+              GemmDesc d = gdesc(k, qq[x], bx[i].ni);
+              d.A = Y.p + (long long)bx[i].ib * k; d.lda = k; d.B = Qb.p + qo[x]; d.ldb = bx[i].ni;
+              d.C = CC.p + cco[xa] + c0 + (long long)c * rb[i]; d.ldc = c;
+              gcq.add(d);
+              nV[x].alloc((size_t)ni * (rb[i] + qq[x]), s);
+              nA[x].alloc((size_t)c * (rb[i] + qq[x]), s);
+              pd.flops += 4.0 * c * (double)qq[x] * bx[i].ni;
+            }
+            copy_batched(s, cc1);
+            gcq.run(s);
+            GemmBatch gan(false, false);
+            std::vector<CopyProb> cpv;
+            for (size_t x = 0; x < B; ++x) {
+              const int i = act[x0 + x];
+              const long long ni = bx[i].ni;
+              if (qq[x] == 0) continue;
+              if (rb[i] > 0) {
+                cpv.push_back(CopyProb{Vb[i].p, ni, nV[x].p, ni, (int)ni, rb[i], 1.0});
+                cpv.push_back(CopyProb{Ab[i].p, c, nA[x].p, c, c, rb[i], 1.0});
+              }
+              cpv.push_back(CopyProb{Qb.p + qo[x], ni, nV[x].p + ni * rb[i], ni, (int)ni, qq[x], 1.0});
+              GemmDesc e = gdesc(c, qq[x], bx[i].ni);
+              e.A = Wi.p + wo[x]; e.lda = c; e.B = Qb.p + qo[x]; e.ldb = bx[i].ni;
+              e.C = nA[x].p + (long long)c * rb[i]; e.ldc = c;
+              gan.add(e);
+            }
+            copy_batched(s, cpv);
+            gan.run(s);
+            for (size_t x = 0; x < B; ++x) {
+              const int i = act[x0 + x];
+              if (qq[x] == 0) continue;
+              Vb[i] = std::move(nV[x]);
+              Ab[i] = std::move(nA[x]);
+              rb[i] += qq[x];
+            }
+            x0 = x1;
           }
-          for (size_t x = 0; x < B; ++x) {
-            const int q = gq[q0 + x];
-            kp[q] = kk[x];
-            Up[q] = Ub.p + uo[x];
-            A1p[q] = Ab.p + ao[x];
-            Pp[q] = Pb.p + po[x];
-          }
-          keep.push_back(std::move(Ub));
-          keep.push_back(std::move(Ab));
-          keep.push_back(std::move(Pb));
-          q0 = q1;
         }
-        if (fail) break;
+        W.release();
+        Y.release();
+        // eps_peel-rank of every sibling block from its Gaussian sketch P_ij (R-N); adaptivity (R-M)
+        DBuf<double> Pc(pt, s);
+        DBuf<int> piv((size_t)c * NA, s);
+        std::vector<int> kk;
+        {
+          RSF_PHASE("p.sketch_rank", s);
+          RSF_CUDA(cudaMemcpyAsync(Pc.p, P.p, pt * sizeof(double), cudaMemcpyDeviceToDevice, s));
+          std::vector<RRQRProb> rp;
+          for (size_t x = 0; x < NA; ++x)
+            rp.push_back(RRQRProb{Pc.p + po[x], c, c, c, piv.p + (long long)x * c, nullptr, nullptr, 0});
+          kk = rrqr_batched(s, rp, o.eps_peel, seed ^ (0xD1B54A32D192ED03ull * (unsigned long long)(lev + 64 * (trace_id + 1)))).k;
+        }
+        for (size_t x = 0; x < NA; ++x) mr = std::max(mr, kk[x]);
+        if (mr > c - o.oversample && c < cmax) { fail = true; break; }
+        // per-pair basis Z_ij = orth(C_ij(:, piv[0:k])) in the coordinates of V_i
+        // (U_ij = V_i Z_ij = orth(Y_ij), R-N) and the left core factor
+        //   X_ij = W_i^T U_ij,  Lm_ij = X_ij^+ (W_i^T Y_ij)       (Eq. lowrankapprox)
+        RSF_PHASE("p.pair_core", s);
+        size_t x0 = 0;
+        while (x0 < NA) {
+          size_t x1 = x0;
+          double bytes = 0;
+          while (x1 < NA) {
+            const double bb = 8.0 * (3.0 * rb[act[x1]] * (double)c + 6.0 * (double)c * c);
+            if (x1 > x0 && bytes + bb > budget) break;
+            bytes += bb;
+            ++x1;
+          }
+          const size_t B = x1 - x0;
+          long long zt = 0;
+          std::vector<long long> zo(B), xo(B), lo(B), go(B);
+          for (size_t x = 0; x < B; ++x) {
+            const size_t xa = x0 + x;
+            const int i = act[xa];
+            kk[xa] = std::min(kk[xa], rb[i]);
+            const long long k = kk[xa];
+            zo[x] = zt; zt += (long long)rb[i] * k;
+            xo[x] = zt; zt += (long long)c * k;
+            lo[x] = zt; zt += k * c;
+            go[x] = zt; zt += k * k;
+          }
+          DBuf<double> arena(std::max<long long>(zt, 1), s);
+          DBuf<double> Z0(std::max<long long>(zt, 1), s), Ri2(std::max<long long>(zt, 1), s), T1(std::max<long long>(zt, 1), s);
+          std::vector<GatherTDesc> gz;
+          std::vector<EyeDesc> ez;
+          std::vector<TrsmProb> tz;
+          long long mz = 0;
+          for (size_t x = 0; x < B; ++x) {
+            const size_t xa = x0 + x;
+            const int i = act[xa];
+            const int k = kk[xa];
+            if (k == 0) continue;
+            gz.push_back(GatherTDesc{CC.p + cco[xa], c, piv.p + (long long)xa * c, Z0.p + zo[x], rb[i], k});
+            ez.push_back(EyeDesc{Ri2.p + go[x], k, k});
+            tz.push_back(TrsmProb{Pc.p + po[xa], c, Ri2.p + go[x], k, k, k});
+            mz = std::max(mz, (long long)rb[i] * k);
+          }
+          launch_descs(s, gz, mz, gather_t_kernel);
+          launch_descs(s, ez, mz, eye_kernel);
+          trsm_upper_batched(s, tz);
+          GemmBatch gz1(false, false);
+          std::vector<CQProb> cz;
+          for (size_t x = 0; x < B; ++x) {
+            const size_t xa = x0 + x;
+            const int i = act[xa];
+            const int k = kk[xa];
+            if (k == 0) continue;
+            GemmDesc d = gdesc(rb[i], k, k);
+            d.A = Z0.p + zo[x]; d.lda = rb[i]; d.B = Ri2.p + go[x]; d.ldb = k; d.C = arena.p + zo[x]; d.ldc = rb[i];
+            gz1.add(d);
+            cz.push_back(CQProb{arena.p + zo[x], rb[i], k});
+          }
+          gz1.run(s);
+          cholqr2_batched(s, cz, lev, &pd.flops);
+          GemmBatch gx(false, false), gg(true, false), gt1(true, false), gt2(false, false), gt3(true, false);
+          std::vector<PotrfProb> pp;
+          for (size_t x = 0; x < B; ++x) {
+            const size_t xa = x0 + x;
+            const int i = act[xa];
+            const int k = kk[xa];
+            if (k == 0) continue;
+            GemmDesc a = gdesc(c, k, rb[i]);               // X = A_i Z
+            a.A = Ab[i].p; a.lda = c; a.B = arena.p + zo[x]; a.ldb = rb[i]; a.C = arena.p + xo[x]; a.ldc = c;
+            gx.add(a);
+            GemmDesc d = gdesc(k, k, c);                   // X^T X
+            d.A = arena.p + xo[x]; d.lda = c; d.B = arena.p + xo[x]; d.ldb = c; d.C = T1.p + go[x]; d.ldc = k;
+            gg.add(d);
+            pp.push_back(PotrfProb{T1.p + go[x], k, k, arena.p + go[x], k});
+            GemmDesc e = gdesc(k, c, c);                   // X^T P
+            e.A = arena.p + xo[x]; e.lda = c; e.B = P.p + po[xa]; e.ldb = c; e.C = Z0.p + lo[x]; e.ldc = k;
+            gt1.add(e);
+            GemmDesc f = gdesc(k, c, k);                   // L^-1 (X^T P)
+            f.A = arena.p + go[x]; f.lda = k; f.B = Z0.p + lo[x]; f.ldb = k; f.C = Ri2.p + lo[x]; f.ldc = k;
+            gt2.add(f);
+            GemmDesc h = gdesc(k, c, k);                   // Lm = L^-T L^-1 X^T P
+            h.A = arena.p + go[x]; h.lda = k; h.B = Ri2.p + lo[x]; h.ldb = k; h.C = arena.p + lo[x]; h.ldc = k;
+            gt3.add(h);
+            pd.flops += 2.0 * c * (double)k * rb[i] + 4.0 * k * (double)c * c;
+          }
+          gx.run(s);
+          gg.run(s);
+          {
+            DBuf<double> ls(std::max<size_t>(pp.size(), 1), s);
+            DBuf<int> inf(std::max<size_t>(pp.size(), 1), s);
+            potrf_batched(s, pp, ls.p, inf.p);
+            for (int v2 : inf.to_host(pp.size()))
+              if (v2) throw Error(ST_ENUMERIC, "peeling: rank-deficient sketch product at level " + std::to_string(lev));
+          }
+          gt1.run(s); gt2.run(s); gt3.run(s);
+          for (size_t x = 0; x < B; ++x) {
+            const size_t xa = x0 + x;
+            const int i = act[xa], j = partner[xa];
+            PairData& q = pdat[(size_t)i * 4 + (j - bx[i].fam0)];
+            q.k = kk[xa]; q.rz = rb[i];
+            q.Z = arena.p + zo[x]; q.X = arena.p + xo[x]; q.Lm = arena.p + lo[x]; q.Gi = arena.p + go[x];
+          }
+          arenas.push_back(std::move(arena));
+          x0 = x1;
+        }
       }
       if (!fail) break;
       int nc = (mr >= c - 1) ? (int)std::ceil(1.4 * c) : std::max(c + 8, (int)std::ceil(1.1 * mr) + o.oversample);
@@ -536,136 +778,123 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
     pd.cols[lev] = c;
     pd.rank_max[lev] = mr;
     prev_rank = mr;
+    for (auto& v : Ab) v.release();
 
-    // ---- cores M_ij = (A1_ij)^+ P_ij (A1_ji^T)^+   (Eq. lowrankapprox; U_ji^T W_j = A1_ji^T)
-    DBuf<double> Mbuf;
-    std::vector<long long> moff(P, -1);
+    // ---- cores: M_ij = Lm_ij (X_ji^T)^+ = Lm_ij X_ji (X_ji^T X_ji)^-1, B_ij = Z_ij M_ij Z_ji^T,
+    //      B_ji = B_ij^T; Brow_i = [B_ij]_{j in family(i)} (r_i x R_fam, zero self block)
+    PeelLevel& PL = peeled[lev];
+    std::vector<long long> fo(nb), bo(nb);     // column offset of box b inside its family row; Brow offsets
+    long long brt = 0;
+    for (int b = 0; b < nb; ++b) {
+      long long off = 0, tot = 0;
+      for (int x = bx[b].fam0; x < bx[b].fam1; ++x) { if (x < b) off += rb[x]; tot += rb[x]; }
+      fo[b] = off;
+      bo[b] = brt; brt += (long long)rb[b] * tot;
+    }
+    PL.Brow.alloc(std::max<long long>(brt, 1), s);
+    PL.Brow.zero();
     {
       RSF_PHASE("p.cores", s);
-      std::vector<long long> g1o(P), t1o(P), t2o(P);
-      long long g1t = 0, t1t = 0, t2t = 0, mt = 0;
-      for (size_t q = 0; q < P; ++q) {
-        const int k1 = kp[q], k2 = kp[pairs[q].rev];
-        g1o[q] = g1t; g1t += (long long)k1 * k1;
-        t1o[q] = t1t; t1t += (long long)k1 * c;
-        t2o[q] = t2t; t2t += (long long)k1 * k2;
-        if (k1 > 0 && k2 > 0) { moff[q] = mt; mt += (long long)k1 * k2; }
+      long long mt = 0;
+      std::vector<std::array<long long, 3>> mo;
+      std::vector<std::pair<int, int>> pl;
+      for (int i = 0; i < nb; ++i)
+        for (int j = bx[i].fam0; j < bx[i].fam1; ++j) {
+          if (j <= i) continue;
+          const PairData& a = pdat[(size_t)i * 4 + (j - bx[i].fam0)];
+          const PairData& b2 = pdat[(size_t)j * 4 + (i - bx[j].fam0)];
+          if (a.k == 0 || b2.k == 0) continue;
+          std::array<long long, 3> m{};
+          m[0] = mt; mt += (long long)a.k * b2.k;                 // T1, then M
+          m[1] = mt; mt += (long long)a.k * b2.k;                 // T2
+          m[2] = mt; mt += (long long)std::max(a.rz, b2.rz) * std::max(a.k, b2.k) * 2;  // T3 / T4
+          mo.push_back(m);
+          pl.emplace_back(i, j);
+        }
+      DBuf<double> Mw(std::max<long long>(mt, 1), s);
+      GemmBatch m1(false, false), m2(false, true), m3(false, false), m4(false, false), m5(false, true),
+          m6(false, true), m7(false, true);
+      for (size_t q = 0; q < pl.size(); ++q) {
+        const int i = pl[q].first, j = pl[q].second;
+        const PairData& a = pdat[(size_t)i * 4 + (j - bx[i].fam0)];
+        const PairData& b2 = pdat[(size_t)j * 4 + (i - bx[j].fam0)];
+        const int k1 = a.k, k2 = b2.k;
+        double* T1p = Mw.p + mo[q][0];
+        double* T2p = Mw.p + mo[q][1];
+        double* T3p = Mw.p + mo[q][2];
+        double* T4p = T3p + (long long)std::max(a.rz, b2.rz) * std::max(k1, k2);
+        GemmDesc d1 = gdesc(k1, k2, c);     // T1 = Lm_ij X_ji
+        d1.A = a.Lm; d1.lda = k1; d1.B = b2.X; d1.ldb = c; d1.C = T1p; d1.ldc = k1;
+        m1.add(d1);
+        GemmDesc d2 = gdesc(k1, k2, k2);    // T2 = T1 Gi_ji^T
+        d2.A = T1p; d2.lda = k1; d2.B = b2.Gi; d2.ldb = k2; d2.C = T2p; d2.ldc = k1;
+        m2.add(d2);
+        GemmDesc d3 = gdesc(k1, k2, k2);    // M = T2 Gi_ji   (into T1)
+        d3.A = T2p; d3.lda = k1; d3.B = b2.Gi; d3.ldb = k2; d3.C = T1p; d3.ldc = k1;
+        m3.add(d3);
+        GemmDesc d4 = gdesc(a.rz, k2, k1);  // T3 = Z_ij M
+        d4.A = a.Z; d4.lda = a.rz; d4.B = T1p; d4.ldb = k1; d4.C = T3p; d4.ldc = a.rz;
+        m4.add(d4);
+        GemmDesc d5 = gdesc(a.rz, b2.rz, k2);   // B_ij = T3 Z_ji^T  -> Brow_i
+        d5.A = T3p; d5.lda = a.rz; d5.B = b2.Z; d5.ldb = b2.rz;
+        d5.C = PL.Brow.p + bo[i] + (long long)rb[i] * fo[j]; d5.ldc = rb[i];
+        m5.add(d5);
+        GemmDesc d6 = gdesc(b2.rz, k1, k2);     // T4 = Z_ji M^T
+        d6.A = b2.Z; d6.lda = b2.rz; d6.B = T1p; d6.ldb = k1; d6.C = T4p; d6.ldc = b2.rz;
+        m6.add(d6);
+        GemmDesc d7 = gdesc(b2.rz, a.rz, k1);   // B_ji = T4 Z_ij^T  -> Brow_j
+        d7.A = T4p; d7.lda = b2.rz; d7.B = a.Z; d7.ldb = a.rz;
+        d7.C = PL.Brow.p + bo[j] + (long long)rb[j] * fo[i]; d7.ldc = rb[j];
+        m7.add(d7);
+        pd.flops += 2.0 * k1 * (double)k2 * c + 2.0 * a.rz * (double)b2.rz * (k1 + k2);
       }
-      DBuf<double> G1(std::max<long long>(g1t, 1), s), G1i(std::max<long long>(g1t, 1), s),
-          T1(std::max<long long>(t1t, 1), s), T2(std::max<long long>(t2t, 1), s), T3(std::max<long long>(t2t, 1), s);
-      Mbuf.alloc(std::max<long long>(mt, 1), s);
-      GemmBatch gg(true, false);
-      std::vector<PotrfProb> pp;
-      for (size_t q = 0; q < P; ++q) {
-        const int k1 = kp[q];
-        if (k1 == 0) continue;
-        GemmDesc e = gdesc(k1, k1, c);              // G1 = A1^T A1
-        e.A = A1p[q]; e.lda = c; e.B = A1p[q]; e.ldb = c; e.C = G1.p + g1o[q]; e.ldc = k1;
-        gg.add(e);
-        pp.push_back(PotrfProb{G1.p + g1o[q], k1, k1, G1i.p + g1o[q], k1});
-      }
-      gg.run(s);
-      DBuf<double> ls(std::max<size_t>(pp.size(), 1), s);
-      DBuf<int> inf(std::max<size_t>(pp.size(), 1), s);
-      potrf_batched(s, pp, ls.p, inf.p);
-      {
-        auto hi = inf.to_host(pp.size());
-        for (size_t x = 0; x < hi.size(); ++x)
-          if (hi[x]) throw Error(ST_ENUMERIC, "peeling: rank-deficient sketch product at level " + std::to_string(lev));
-      }
-      GemmBatch m1(true, false), m2(false, false), m3(false, false), m4(true, false), m5(false, true), m6(false, false);
-      for (size_t q = 0; q < P; ++q) {
-        const int k1 = kp[q], rq = pairs[q].rev, k2 = kp[rq];
-        if (moff[q] < 0) continue;
-        const double* L1i = G1i.p + g1o[q];
-        const double* L2i = G1i.p + g1o[rq];
-        GemmDesc a = gdesc(k1, c, c);     // T1 = A1_ij^T P_ij
-        a.A = A1p[q]; a.lda = c; a.B = Pp[q]; a.ldb = c; a.C = T1.p + t1o[q]; a.ldc = k1;
-        m1.add(a);
-        GemmDesc b = gdesc(k1, k2, c);    // T2 = T1 A1_ji
-        b.A = T1.p + t1o[q]; b.lda = k1; b.B = A1p[rq]; b.ldb = c; b.C = T2.p + t2o[q]; b.ldc = k1;
-        m2.add(b);
-        GemmDesc d = gdesc(k1, k2, k1);   // T3 = L1^-1 T2
-        d.A = L1i; d.lda = k1; d.B = T2.p + t2o[q]; d.ldb = k1; d.C = T3.p + t2o[q]; d.ldc = k1;
-        m3.add(d);
-        GemmDesc e = gdesc(k1, k2, k1);   // T2 = L1^-T T3
-        e.A = L1i; e.lda = k1; e.B = T3.p + t2o[q]; e.ldb = k1; e.C = T2.p + t2o[q]; e.ldc = k1;
-        m4.add(e);
-        GemmDesc f = gdesc(k1, k2, k2);   // T3 = T2 L2^-T
-        f.A = T2.p + t2o[q]; f.lda = k1; f.B = L2i; f.ldb = k2; f.C = T3.p + t2o[q]; f.ldc = k1;
-        m5.add(f);
-        GemmDesc g2 = gdesc(k1, k2, k2);  // M = T3 L2^-1
-        g2.A = T3.p + t2o[q]; g2.lda = k1; g2.B = L2i; g2.ldb = k2; g2.C = Mbuf.p + moff[q]; g2.ldc = k1;
-        m6.add(g2);
-        pd.flops += 2.0 * k1 * (double)c * c + 2.0 * k1 * (double)k2 * c;
-      }
-      m1.run(s); m2.run(s); m3.run(s); m4.run(s); m5.run(s); m6.run(s);
+      m1.run(s); m2.run(s); m3.run(s); m4.run(s); m5.run(s); m6.run(s); m7.run(s);
+      RSF_CUDA(cudaStreamSynchronize(s));
     }
-    // keep U (persistent) and M; drop A1 / P
-    std::vector<DBuf<double>> Ukeep;
-    for (size_t x = 0; x < keep.size(); x += 3) Ukeep.push_back(std::move(keep[x]));
-    keep.clear();
+    arenas.clear();
+    for (auto& q : pdat) q = PairData{};
 
-    // ---- subtraction batches for G^(lev):  Y'(I_i) -= sum_j X'(I_j) U_ji M_ij^T U_ij^T
-    //      one final GEMM per (row box i, U buffer) over its concatenated [U_ij1 | U_ij2 | ...]
-    for (size_t q = 0; q < P; ++q) { pairs[q].kij = kp[q]; pairs[q].moff = moff[q]; }
-    PL.pairs = pairs;
-    PL.U = DBuf<double>();
-    PL.M = std::move(Mbuf);
-    PL.Ubufs = std::move(Ukeep);
+    // ---- subtraction batches of G^(lev)
+    PL.V = std::move(Vb);
+    double vbytes = 0;
+    for (auto& v : PL.V) vbytes += 8.0 * v.n;
     PL.g1.reset(false, false);
     PL.g2.reset(false, true);
     PL.g3.reset(false, true);
     long long tc = 0;
-    std::vector<long long> t1o(P, -1), t2o(P, -1);
-    for (size_t q = 0; q < P; ++q) {
-      const int k1 = kp[q], k2 = kp[pairs[q].rev];
-      if (k1 > 0 && k2 > 0) { t1o[q] = tc; tc += k2; }
-    }
-    // t2 columns grouped by row box i (pairs are generated in row-box order)
-    for (size_t q = 0; q < P; ++q)
-      if (kp[q] > 0) { t2o[q] = tc; tc += kp[q]; }
-    for (size_t q = 0; q < P; ++q) {
-      const auto& p = PL.pairs[q];
-      const int k1 = kp[q], k2 = kp[p.rev];
-      if (k1 == 0) continue;
-      if (k2 > 0) {
-        GemmDesc a = gdesc(-1, k2, p.nj);                 // t1 = X'(I_j) U_ji
-        a.selA = 1; a.offA = p.jb; a.B = Up[p.rev]; a.ldb = p.nj; a.selC = 2; a.offC = t1o[q];
-        PL.g1.add(a);
-      }
-      GemmDesc b = gdesc(-1, k1, k2);                     // t2 = t1 M_ij^T  (zero if k2 == 0)
-      b.selA = 2; b.offA = k2 > 0 ? t1o[q] : 0; b.B = k2 > 0 ? PL.M.p + moff[q] : PL.M.p; b.ldb = k1;
-      b.selC = 2; b.offC = t2o[q];
-      PL.g2.add(b);
-    }
-    // Y'(I_i) -= t2 U_ij^T: one GEMM per row box i when its U_ij are contiguous, else per pair
-    // (pairs of one row box live in different group buffers, so they are never contiguous;
-    //  the per-pair GEMMs of one row box are issued in separate batches to avoid races)
-    {
-      std::vector<std::vector<int>> byrow(nb);
-      for (size_t q = 0; q < P; ++q) if (kp[q] > 0) byrow[pairs[q].i].push_back((int)q);
-      size_t maxdeg = 0;
-      for (auto& v : byrow) maxdeg = std::max(maxdeg, v.size());
-      PL.g3s.clear();
-      for (size_t r = 0; r < maxdeg; ++r) {
-        PL.g3s.emplace_back(false, true);
-        for (int b = 0; b < nb; ++b) {
-          if (r >= byrow[b].size()) continue;
-          const int q = byrow[b][r];
-          const auto& p = PL.pairs[q];
-          GemmDesc d = gdesc(-1, p.ni, kp[q]);
-          d.selA = 2; d.offA = t2o[q]; d.B = Up[q]; d.ldb = p.ni; d.selC = 1; d.offC = p.ib;
-          d.alpha = -1.0; d.beta = 1.0;
-          PL.g3s.back().add(d);
-        }
-      }
+    std::vector<long long> toff(nb), soff(nb);
+    for (int b = 0; b < nb; ++b) { toff[b] = tc; tc += rb[b]; }
+    for (int b = 0; b < nb; ++b) { soff[b] = tc; tc += rb[b]; }
+    for (int b = 0; b < nb; ++b) {
+      if (rb[b] == 0) continue;
+      long long tot = 0;
+      for (int x = bx[b].fam0; x < bx[b].fam1; ++x) tot += rb[x];
+      GemmDesc a = gdesc(-1, rb[b], bx[b].ni);            // T'_b = X'(:, I_b) V_b
+      a.selA = 1; a.offA = bx[b].ib; a.B = PL.V[b].p; a.ldb = bx[b].ni; a.selC = 2; a.offC = toff[b];
+      PL.g1.add(a);
+      GemmDesc d = gdesc(-1, rb[b], (int)tot);            // S'_b = T'_fam Brow_b^T
+      d.selA = 2; d.offA = toff[bx[b].fam0]; d.B = PL.Brow.p + bo[b]; d.ldb = rb[b]; d.selC = 2; d.offC = soff[b];
+      PL.g2.add(d);
+      GemmDesc e = gdesc(-1, bx[b].ni, rb[b]);            // Y'(:, I_b) -= S'_b V_b^T
+      e.selA = 2; e.offA = soff[b]; e.B = PL.V[b].p; e.ldb = bx[b].ni; e.selC = 1; e.offC = bx[b].ib;
+      e.alpha = -1.0; e.beta = 1.0;
+      PL.g3.add(e);
     }
     PL.tcols = tc;
     max_tcols = std::max(max_tcols, tc);
-    for (GemmBatch* g : {&PL.g1, &PL.g2})
+    for (GemmBatch* g : {&PL.g1, &PL.g2, &PL.g3})
       if (!g->empty()) g->finalize(s);
-    for (auto& g : PL.g3s) if (!g.empty()) g.finalize(s);
+    if (verbose) {
+      RSF_CUDA(cudaStreamSynchronize(s));
+      size_t fr = 0, tot = 0;
+      cudaMemGetInfo(&fr, &tot);
+      long long rsum = 0;
+      int rmax = 0;
+      for (int b = 0; b < nb; ++b) { rsum += rb[b]; rmax = std::max(rmax, rb[b]); }
+      fprintf(stderr, "[peel tr%d] level %d boxes %d pairs %d cols %d rank_max %d basis sum %lld max %d V %.2f GB "
+                      "dev_used %.2f GB t %.2f s\n",
+              trace_id, lev, nb, npairs, c, mr, rsum, rmax, 1e-9 * vbytes, 1e-9 * (tot - fr), now_s() - t0);
+    }
   }
 
   // ---- extraction
@@ -736,7 +965,7 @@ EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KP
   auto tree = build_tree(ctx, dxy, n, leaf, o.max_depth);
   R.t_tree = now_s() - t;
   t = now_s();
-  auto F = factor(ctx, tree, kp, W_SIGMA, eps, o);
+  auto F = factor(ctx, tree, kp, W_SIGMA, eps, o, /*solve_only=*/true);
   R.t_factor = now_s() - t;
   R.fdiag = F->diag;
   R.L = tree->L;

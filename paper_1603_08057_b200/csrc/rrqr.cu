@@ -40,6 +40,8 @@ struct RDesc {
   double* ref;     // max column norm
   int* flag;       // [0] done, [1] k
   double* R11i;    // QR_NB x QR_NB
+  const double* ref_in;
+  double* ref_out;
   int J, nbp, id;
   double eps;
 };
@@ -63,8 +65,11 @@ __global__ void ref_kernel(const RDesc* __restrict__ d0) {
   if (threadIdx.x == 0) {
     double v = 0.0;
     for (int w = 0; w < NT / 32; ++w) v = fmax(v, red[w]);
-    *d.ref = sqrt(v);
-    d.flag[0] = (v > 0.0) ? 0 : 1;
+    if (d.ref_out) *d.ref_out = sqrt(v);
+    const double rf = d.ref_in ? *d.ref_in : sqrt(v);
+    *d.ref = rf;
+    // nothing to factor: an all-zero matrix, or every column already below the absolute threshold
+    d.flag[0] = (v > 0.0 && rf > 0.0 && sqrt(v) > d.eps * rf) ? 0 : 1;
     d.flag[1] = 0;
   }
 }
@@ -407,6 +412,7 @@ RRQRResult rrqr_batched(cudaStream_t s, const std::vector<RRQRProb>& probs, doub
     d.piv = p.piv; d.sw = sw.p + (long long)i * QR_NB; d.ref = ref.p + i; d.flag = flag.p + 2 * i;
     d.R11i = R11i.p + (long long)i * QR_NB * QR_NB;
     d.id = i; d.eps = eps;
+    d.ref_in = p.ref_in; d.ref_out = p.ref_out;
     base[i] = d;
   }
   {

@@ -22,6 +22,9 @@ struct RRQRProb {
   double* Tws;      // optional: WY T factors, one QR_NB^2 block per panel (for ormqr / U formation)
   double* T;        // optional: out T = R11^-1 R12, k x (c-k), leading dimension ldt
   long long ldt;
+  const double* ref_in = nullptr;  // optional (device scalar): absolute reference norm; the
+                                   // truncation becomes ||trailing col|| <= eps * (*ref_in)
+  double* ref_out = nullptr;       // optional (device scalar): max_j ||A(:, j)|| of the input
 };
 
 struct RRQRResult {

@@ -44,13 +44,14 @@ struct BRef {
 }  // namespace
 
 std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams& kp, int which,
-                             double eps, const Opts& opts) {
+                             double eps, const Opts& opts, bool solve_only) {
   RSF_REQUIRE(eps > 0.0, ST_EINVAL, "eps must be > 0");
   const double t0 = now_s();
   cudaStream_t s = ctx.stream;
   auto F = std::make_unique<Fact>();
   F->ctx = &ctx;
   F->which = which;
+  F->solve_only = solve_only && which == W_SIGMA;
   F->kp = kp;
   F->eps = eps;
   F->opts = opts;
@@ -331,7 +332,8 @@ std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams
     }
     LV.T.alloc(std::max<long long>(ttot, 1), s);
     LV.E.alloc(std::max<long long>(ttot, 1), s);
-    LV.L.alloc(std::max<long long>(ltot, 1), s);
+    // L is needed by apply / sample only; a solve-only factor (Alg. 1) keeps L^-1
+    if (!(sig && solve_only)) LV.L.alloc(std::max<long long>(ltot, 1), s);
     if (sig) LV.Linv.alloc(std::max<long long>(ltot, 1), s);
     {
       GemmBatch e1(false, false), e2(false, false), e3(true, false);
@@ -387,7 +389,7 @@ std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams
           const int c = cvec[b], k = kvec[b], r = LV.r[b];
           if (r == 0) continue;
           double* B = Bp.p + bsz[b];
-          lc.push_back(CopyProb{B + (long long)k * c + k, c, LV.L.p + LV.loff[b], r, r, r, 1.0});
+          if (!solve_only) lc.push_back(CopyProb{B + (long long)k * c + k, c, LV.L.p + LV.loff[b], r, r, r, 1.0});
           if (k == 0) continue;
           GemmDesc d4 = gdesc(k, r, r);      // E = X_SR L^-T
           d4.A = B + (long long)k * c; d4.lda = c; d4.B = LV.Linv.p + LV.loff[b]; d4.ldb = r;
@@ -417,7 +419,7 @@ std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams
         copy_batched(s, lc);
       }
     }
-    F->diag.bytes_factor += 8.0 * (sig ? (2.0 * ttot + 2.0 * ltot) : (2.0 * ttot + ltot));
+    F->diag.bytes_factor += 8.0 * (sig ? (2.0 * ttot + (solve_only ? 1.0 : 2.0) * ltot) : (2.0 * ttot + ltot));
     F->diag.level_boxes.push_back(nb);
     long long Isum = 0, Ssum = 0;
     int Imax = 0;
@@ -465,6 +467,7 @@ std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams
         if (k > 0) LV.bs2.add(mk(r, k, 1, Sb, 0, Eb, k, 2, nullptr, tc[b], -1.0, 1.0));
         LV.bs3.add(mk(r, r, 2, nullptr, tc[b], Lib, r, 1, Rb, 0, 1.0, 0.0));
         if (k > 0) LV.bs4.add(mk(k, r, 1, Rb, 0, Tb, k, 1, Sb, 0, -1.0, 1.0));
+        if (solve_only) continue;
         if (k > 0) LV.up1.add(mk(k, r, 1, Rb, 0, Tb, k, 1, Sb, 0, 1.0, 1.0));
         LV.up2.add(mk(r, r, 1, Rb, 0, Lb, r, 2, nullptr, tc[b], 1.0, 0.0));
         if (k > 0) LV.up3.add(mk(r, k, 1, Sb, 0, Eb, k, 2, nullptr, tc[b], 1.0, 1.0));
@@ -532,7 +535,7 @@ std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams
         logdet += 2.0 * hl;
         F->diag.flops_top = (double)n0 * n0 * n0 / 3.0;
       }
-      F->diag.bytes_factor += 8.0 * (double)n0 * n0 * (sig ? 2 : 1);
+      F->diag.bytes_factor += 8.0 * (double)n0 * n0 * (sig && !solve_only ? 2 : 1);
     }
     Bp_prev.release();
     auto mk = [&](int N, int K, int selA, const int* mapA, const double* Bm, int ldb, int selC,
@@ -549,9 +552,13 @@ std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams
       if (sig) {
         F->top_s1.add(mk(n0, n0, 1, m0, F->Cinv.p, n0, 2, nullptr, 0.0));   // tmp = X(I0) Cinv^T
         F->top_s2.add(mk(n0, n0, 2, nullptr, F->Cinv.p, n0, 1, m0, 0.0));   // X(I0) = tmp Cinv
-        F->top_a1.add(mk(n0, n0, 1, m0, F->C.p, n0, 2, nullptr, 0.0));      // tmp = X(I0) C
-        F->top_a2.add(mk(n0, n0, 2, nullptr, F->C.p, n0, 1, m0, 0.0));      // X(I0) = tmp C^T
-        F->top_q1.add(mk(n0, n0, 1, m0, F->C.p, n0, 2, nullptr, 0.0));      // tmp = X(I0) C^T
+        if (!solve_only) {
+          F->top_a1.add(mk(n0, n0, 1, m0, F->C.p, n0, 2, nullptr, 0.0));      // tmp = X(I0) C
+          F->top_a2.add(mk(n0, n0, 2, nullptr, F->C.p, n0, 1, m0, 0.0));      // X(I0) = tmp C^T
+          F->top_q1.add(mk(n0, n0, 1, m0, F->C.p, n0, 2, nullptr, 0.0));      // tmp = X(I0) C^T
+        } else {
+          F->C.release();
+        }
       } else {
         F->top_ao.add(mk(n0, n0, 1, m0, F->C.p, n0, 2, m0, 0.0));           // Y(I0) = X(I0) B0
       }
@@ -600,7 +607,7 @@ static void down_sweep(const Fact& F, double* X, int k, double* tmp) {
 }
 
 void apply_internal(const Fact& F, double* X, int k, double* tmp) {
-  RSF_REQUIRE(F.which == W_SIGMA, ST_EINVAL, "apply_internal needs a Sigma factor");
+  RSF_REQUIRE(F.which == W_SIGMA && !F.solve_only, ST_EINVAL, "apply_internal needs a full Sigma factor");
   cudaStream_t s = F.ctx->stream;
   for (int lev = F.tree->L; lev >= 1; --lev) {
     const Level& LV = F.levels[lev];
@@ -615,7 +622,7 @@ void apply_internal(const Fact& F, double* X, int k, double* tmp) {
 }
 
 void sqrt_internal(const Fact& F, double* X, int k, double* tmp) {
-  RSF_REQUIRE(F.which == W_SIGMA, ST_EINVAL, "sample needs a Sigma factor");
+  RSF_REQUIRE(F.which == W_SIGMA && !F.solve_only, ST_EINVAL, "sample needs a full Sigma factor");
   cudaStream_t s = F.ctx->stream;
   if (F.n0 > 0) {
     F.top_q1.run(s, X, tmp, k, k);

@@ -90,6 +90,7 @@ struct FactDiag {
 struct Fact {
   Ctx* ctx = nullptr;
   int which = W_SIGMA;
+  bool solve_only = false;           // Sigma factor without L / C (Alg. 1: only solves are needed)
   KParams kp{};
   double eps = 0;
   Opts opts;
@@ -106,7 +107,7 @@ struct Fact {
 };
 
 std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams& kp, int which,
-                             double eps, const Opts& opts);
+                             double eps, const Opts& opts, bool solve_only = false);
 
 // operations on X' (k x n column-major, tree order, ld = k): in place
 void solve_internal(const Fact& F, double* X, int k, double* tmp);

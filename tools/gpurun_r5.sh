@@ -1,0 +1,4 @@
+cd $GRAFT_REPO_ROOT
+timeout 900 python -m pytest tests -m gpu -q -x -k "not full_size" > gpurun_out/r5_pytest.log 2>&1; echo "pytest exit $?" >> gpurun_out/r5_pytest.log
+RSF_PROFILE=1 RSF_VERBOSE=1 timeout 400 python tools/dev_scale.py 3 > gpurun_out/r5_scale3.log 2>&1; echo "exit $?" >> gpurun_out/r5_scale3.log
+RSF_PROFILE=1 RSF_VERBOSE=1 timeout 1200 python tools/dev_scale.py 4 > gpurun_out/r5_scale4.log 2>&1; echo "exit $?" >> gpurun_out/r5_scale4.log
