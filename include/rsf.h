@@ -164,6 +164,9 @@ void rsf_stats_enable(int on);
 /* diagnostics: TFLOP/s of the batched FP64 GEMM on batch x (M x N x K), transposes ta/tb */
 double rsf_debug_gemm_bench(int M, int N, int K, int batch, int ta, int tb, int reps);
 void rsf_stats_get(double* out4);
+/* diagnostics: FP64 peak (TFLOP/s) of independent DMMA.8x8x4 (dmma=1) or DFMA (dmma=0) chains on the
+ * current device, best of `reps` timed launches -- the live roofline denominator of bench.py */
+double rsf_debug_fp64_peak(int dmma, int reps);
 void rsf_stats_reset(void);
 
 #ifdef __cplusplus

@@ -55,7 +55,7 @@ EXPORTS = ["rsf_opts_default", "rsf_ctx_create", "rsf_ctx_destroy", "rsf_factor"
            "rsf_fact_info", "rsf_logdet", "rsf_solve", "rsf_apply", "rsf_sample", "peel_trace",
            "gp_mle_eval", "rsf_last_error", "rsf_kernel_launches", "rsf_profile_dump",
            "rsf_profile_reset", "rsf_stats_enable", "rsf_stats_get", "rsf_stats_reset",
-           "rsf_debug_gemm_bench"]
+           "rsf_debug_gemm_bench", "rsf_debug_fp64_peak"]
 
 
 def load(path: str = LIB_PATH) -> C.CDLL:
@@ -96,9 +96,12 @@ def load(path: str = LIB_PATH) -> C.CDLL:
     lib.rsf_stats_reset.restype = None
     lib.rsf_debug_gemm_bench.argtypes = [C.c_int] * 7
     lib.rsf_debug_gemm_bench.restype = C.c_double
+    lib.rsf_debug_fp64_peak.argtypes = [C.c_int, C.c_int]
+    lib.rsf_debug_fp64_peak.restype = C.c_double
     for f in EXPORTS:
         if f not in ("rsf_ctx_destroy", "rsf_fact_destroy", "rsf_opts_default", "rsf_last_error",
                      "rsf_kernel_launches", "rsf_profile_dump", "rsf_profile_reset", "rsf_stats_enable",
-                     "rsf_stats_get", "rsf_stats_reset", "rsf_debug_gemm_bench"):
+                     "rsf_stats_get", "rsf_stats_reset", "rsf_debug_gemm_bench",
+                     "rsf_debug_fp64_peak"):
             getattr(lib, f).restype = C.c_int
     return lib

@@ -372,6 +372,70 @@ double rsf_debug_gemm_bench(int M, int N, int K, int batch, int ta, int tb, int 
   }
 }
 
+namespace {
+// FP64 peak probes (roofline denominator, measured live by bench.py): independent
+// DMMA.8x8x4 (mma.sync m8n8k4 f64) or DFMA chains, no memory traffic.
+__global__ void peak_dmma_kernel(double* out, int iters) {
+  double a = threadIdx.x * 1e-6, b = 1.0 - threadIdx.x * 1e-7;
+  double c[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(c[q][0]), "+d"(c[q][1]) : "d"(a), "d"(b));
+  }
+  double s = 0;
+  for (int q = 0; q < 4; ++q) s += c[q][0] + c[q][1];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+__global__ void peak_dfma_kernel(double* out, int iters) {
+  double a0 = threadIdx.x * 1e-9, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5, a6 = a0 + 6, a7 = a0 + 7;
+  const double b = 0.999999, c = 1e-9;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      a0 = fma(a0, b, c); a1 = fma(a1, b, c); a2 = fma(a2, b, c); a3 = fma(a3, b, c);
+      a4 = fma(a4, b, c); a5 = fma(a5, b, c); a6 = fma(a6, b, c); a7 = fma(a7, b, c);
+    }
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+}
+}  // namespace
+
+double rsf_debug_fp64_peak(int dmma, int reps) {
+  try {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int blocks = sms * 4, threads = 512, iters = 4000;
+    rsf::DBuf<double> out((size_t)blocks * threads, 0);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    double best = 0.0;
+    for (int r = 0; r < std::max(reps, 1) + 1; ++r) {
+      cudaEventRecord(e0, 0);
+      if (dmma) peak_dmma_kernel<<<blocks, threads>>>(out.p, iters);
+      else peak_dfma_kernel<<<blocks, threads>>>(out.p, iters);
+      cudaEventRecord(e1, 0);
+      cudaEventSynchronize(e1);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      const double fl = dmma ? 2.0 * 8 * 8 * 4 * 16 * (double)iters * blocks * (threads / 32)
+                             : 2.0 * 8 * 16 * (double)iters * blocks * threads;
+      if (r > 0) best = std::max(best, fl / (ms * 1e-3) / 1e12);   // first launch = warm-up
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaDeviceSynchronize();
+    return best;
+  } catch (...) {
+    return -1.0;
+  }
+}
+
 void rsf_stats_enable(int on) { rsf::KStats::on = on != 0; }
 void rsf_stats_get(double* out4) { rsf::KStats::collect(out4); }
 void rsf_stats_reset(void) { rsf::KStats::reset(); }

@@ -56,7 +56,8 @@ struct PanelDesc {
   int smem;        // panel staged in shared memory
 };
 
-__global__ void __launch_bounds__(NT) qr_panel_kernel(const PanelDesc* __restrict__ descs) {
+template <int NTH>
+__global__ void __launch_bounds__(NTH) qr_panel_kernel(const PanelDesc* __restrict__ descs) {
   extern __shared__ double sm[];
   const PanelDesc d = descs[blockIdx.x];
   double* red = sm;                 // 32
@@ -72,7 +73,7 @@ __global__ void __launch_bounds__(NT) qr_panel_kernel(const PanelDesc* __restric
   if (d.smem) {
     P = pan;
     ldp = rows;
-    for (long long e = tid; e < (long long)rows * ncol; e += NT) {
+    for (long long e = tid; e < (long long)rows * ncol; e += NTH) {
       int r = (int)(e % rows), c = (int)(e / rows);
       P[e] = d.A[c * d.lda + r];
     }
@@ -85,7 +86,7 @@ __global__ void __launch_bounds__(NT) qr_panel_kernel(const PanelDesc* __restric
     const int len = rows - jj;
     double* x = P + jj * ldp + jj;
     double s = 0.0;
-    for (int r = 1 + tid; r < len; r += NT) s += x[r] * x[r];
+    for (int r = 1 + tid; r < len; r += NTH) s += x[r] * x[r];
     s = block_sum(s, red);
     if (tid == 0) {
       double tau, beta, scale;
@@ -96,12 +97,12 @@ __global__ void __launch_bounds__(NT) qr_panel_kernel(const PanelDesc* __restric
     __syncthreads();
     const double tau = scal[0], scale = scal[2];
     if (tau != 0.0)
-      for (int r = 1 + tid; r < len; r += NT) x[r] *= scale;
+      for (int r = 1 + tid; r < len; r += NTH) x[r] *= scale;
     __syncthreads();
     if (tid == 0 && len > 0) x[0] = scal[1];
     // apply H to the remaining panel columns
     if (tau != 0.0) {
-      for (int col = jj + 1 + warp; col < ncol; col += NT / 32) {
+      for (int col = jj + 1 + warp; col < ncol; col += NTH / 32) {
         double* y = P + col * ldp + jj;
         double dot = 0.0;
         for (int r = 1 + lane; r < len; r += 32) dot += x[r] * y[r];
@@ -116,19 +117,19 @@ __global__ void __launch_bounds__(NT) qr_panel_kernel(const PanelDesc* __restric
     __syncthreads();
   }
   if (d.smem) {
-    for (long long e = tid; e < (long long)rows * ncol; e += NT) {
+    for (long long e = tid; e < (long long)rows * ncol; e += NTH) {
       int r = (int)(e % rows), c = (int)(e / rows);
       d.A[c * d.lda + r] = P[e];
     }
   }
   // explicit V
-  for (long long e = tid; e < (long long)rows * ncol; e += NT) {
+  for (long long e = tid; e < (long long)rows * ncol; e += NTH) {
     int r = (int)(e % rows), c = (int)(e / rows);
     d.V[e] = (r < c) ? 0.0 : (r == c ? 1.0 : P[c * ldp + r]);
   }
   // G(l, i) = v_l . v_i for l < i
   const int npair = ncol * (ncol - 1) / 2;
-  for (int pidx = warp; pidx < npair; pidx += NT / 32) {
+  for (int pidx = warp; pidx < npair; pidx += NTH / 32) {
     // decode pair (l, i), l < i
     int i = 1, acc = 0;
     while (acc + i <= pidx) { acc += i; ++i; }
@@ -156,12 +157,12 @@ __global__ void __launch_bounds__(NT) qr_panel_kernel(const PanelDesc* __restric
     }
   }
   __syncthreads();
-  for (int e = tid; e < QR_NB * QR_NB; e += NT) {
+  for (int e = tid; e < QR_NB * QR_NB; e += NTH) {
     int r = e % QR_NB, c = e / QR_NB;
     d.T[e] = (r < ncol && c < ncol) ? Ts[e] : 0.0;
   }
   if (d.tau)
-    for (int e = tid; e < ncol; e += NT) d.tau[e] = taus[e];
+    for (int e = tid; e < ncol; e += NTH) d.tau[e] = taus[e];
 }
 
 // explicit V for an already-factored panel (ormqr)
@@ -445,6 +446,26 @@ void launch_y(cudaStream_t s, const std::vector<D>& v, long long maxelems, K ker
   }
 }
 
+// panels in global memory (too tall for shared memory) are latency bound: give them
+// 1024 threads (one warp per remaining panel column, 4x the loads in flight)
+void launch_panels(cudaStream_t s, const std::vector<PanelDesc>& pd, const PanelDesc* d, size_t smem_need) {
+  static bool attr = false;
+  if (!attr) {
+    RSF_CUDA(cudaFuncSetAttribute(qr_panel_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_MAX));
+    RSF_CUDA(cudaFuncSetAttribute(qr_panel_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_MAX));
+    attr = true;
+  }
+  bool tall = false;
+  for (auto& p : pd) tall |= (p.smem == 0);
+  for (size_t o = 0; o < pd.size(); o += 65535) {
+    const unsigned nb = (unsigned)std::min<size_t>(65535, pd.size() - o);
+    if (tall) qr_panel_kernel<1024><<<nb, 1024, smem_need, s>>>(d + o);
+    else qr_panel_kernel<NT><<<nb, NT, smem_need, s>>>(d + o);
+    count_launch();
+    RSF_LAUNCH_CHECK();
+  }
+}
+
 }  // namespace
 
 void copy_batched(cudaStream_t s, const std::vector<CopyProb>& probs) {
@@ -459,8 +480,6 @@ void geqrf_batched(cudaStream_t s, const std::vector<QRProb>& probs, bool keep_q
   if (probs.empty()) return;
   static bool attr = false;
   if (!attr) {
-    RSF_CUDA(cudaFuncSetAttribute(qr_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)SMEM_MAX));
     attr = true;
   }
   const int P = (int)probs.size();
@@ -521,8 +540,7 @@ void geqrf_batched(cudaStream_t s, const std::vector<QRProb>& probs, bool keep_q
     }
     if (pd.empty()) continue;
     auto dd = upload_descs(pd, s);
-    qr_panel_kernel<<<(unsigned)pd.size(), NT, smem_need, s>>>(dd.p);
-    count_launch();
+    launch_panels(s, pd, dd.p, smem_need);
     RSF_LAUNCH_CHECK();
     g1.run(s);
     g2.run(s);
@@ -534,7 +552,6 @@ void panel_step_batched(cudaStream_t s, const std::vector<PanelStep>& v) {
   if (v.empty()) return;
   static bool attr = false;
   if (!attr) {
-    RSF_CUDA(cudaFuncSetAttribute(qr_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_MAX));
     attr = true;
   }
   const size_t base_smem = (40 + QR_NB + 2 * QR_NB * QR_NB) * sizeof(double);
@@ -564,12 +581,7 @@ void panel_step_batched(cudaStream_t s, const std::vector<PanelStep>& v) {
     }
   }
   auto dd = upload_descs(pd, s);
-  for (size_t o = 0; o < pd.size(); o += 65535) {
-    unsigned nb = (unsigned)std::min<size_t>(65535, pd.size() - o);
-    qr_panel_kernel<<<nb, NT, smem_need, s>>>(dd.p + o);
-    count_launch();
-    RSF_LAUNCH_CHECK();
-  }
+  launch_panels(s, pd, dd.p, smem_need);
   g1.run(s);
   g2.run(s);
   g3.run(s);

@@ -409,14 +409,18 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-constexpr int P_BM = 128, P_BN = 64, P_BK = 16, P_ST = 4, P_NT = 256;
-constexpr int P_LDA = P_BM + 8, P_LDB = P_BN + 8;
-constexpr size_t P_SMEM = (size_t)P_ST * P_BK * (P_LDA + P_LDB) * sizeof(double);
+constexpr int P_BM = 128, P_BK = 16, P_ST = 4, P_NT = 256;
+constexpr int P_LDA = P_BM + 4;   // row stride = 8 banks mod 32: conflict-free fragment loads
+template <int BN> constexpr int p_ldb() { return BN + 4; }
+template <int BN> constexpr size_t p_smem() { return (size_t)P_ST * P_BK * (P_LDA + p_ldb<BN>()) * sizeof(double); }
 
-template <bool TA, bool TB>
-__global__ void __launch_bounds__(P_NT, 2) gemm_pipe_kernel(const GemmDesc* __restrict__ descs,
+// CTA tile 128 x BN (BN = 32, 64, 128), 8 warps as 4 (M) x 2 (N), warp tile 32 x BN/2
+// (4 x BN/16 DMMA.8x8x4 tiles).
+template <bool TA, bool TB, int BN>
+__global__ void __launch_bounds__(P_NT, (BN >= 128 ? 1 : 2)) gemm_pipe_kernel(const GemmDesc* __restrict__ descs,
                                                             const int* __restrict__ prefix, int nprob,
                                                             double* X0, double* X1, int ldx, int Mglob) {
+  constexpr int LDB = p_ldb<BN>(), NI = BN / 16, WN = BN / 2;
   extern __shared__ __align__(16) double psm[];
   double* As = psm;                              // [ST][BK][LDA]
   double* Bs = psm + P_ST * P_BK * P_LDA;        // [ST][BK][LDB]
@@ -426,7 +430,7 @@ __global__ void __launch_bounds__(P_NT, 2) gemm_pipe_kernel(const GemmDesc* __re
   const int N = dd.N, K = dd.K;
   const int m0 = blockIdx.y * P_BM;
   if (m0 >= M) return;
-  const int n0 = (blockIdx.x - __ldg(prefix + p)) * P_BN;
+  const int n0 = (blockIdx.x - __ldg(prefix + p)) * BN;
   if (dd.lower && n0 >= m0 + P_BM) return;
   const double* A = dd.selA == 0 ? dd.A + dd.offA : (dd.selA == 1 ? X0 : X1) + dd.offA * (long long)ldx;
   const double* B = dd.selB == 0 ? dd.B + dd.offB : (dd.selB == 1 ? X0 : X1) + dd.offB * (long long)ldx;
@@ -443,7 +447,7 @@ __global__ void __launch_bounds__(P_NT, 2) gemm_pipe_kernel(const GemmDesc* __re
 
   auto load_stage = [&](int st, int k0) {
     double* as = As + st * P_BK * P_LDA;
-    double* bs = Bs + st * P_BK * P_LDB;
+    double* bs = Bs + st * P_BK * LDB;
 #pragma unroll
     for (int r = 0; r < (P_BM * P_BK) / P_NT; ++r) {
       const int e = tid + r * P_NT;
@@ -459,10 +463,10 @@ __global__ void __launch_bounds__(P_NT, 2) gemm_pipe_kernel(const GemmDesc* __re
       cp_async8(as + l * P_LDA + i, src, v);
     }
 #pragma unroll
-    for (int r = 0; r < (P_BK * P_BN) / P_NT; ++r) {
+    for (int r = 0; r < (P_BK * BN) / P_NT; ++r) {
       const int e = tid + r * P_NT;
       int l, j;
-      if (!TB) { l = e % P_BK; j = e / P_BK; } else { j = e % P_BN; l = e / P_BN; }
+      if (!TB) { l = e % P_BK; j = e / P_BK; } else { j = e % BN; l = e / BN; }
       const int gl = k0 + l, gj = n0 + j;
       const bool v = gl < K && gj < N;
       const double* src = B;
@@ -470,41 +474,44 @@ __global__ void __launch_bounds__(P_NT, 2) gemm_pipe_kernel(const GemmDesc* __re
         if (!TB) { const long long c = mapB ? __ldg(mapB + gj) : gj; src = B + c * ldb + gl; }
         else { const long long c = mapB ? __ldg(mapB + gl) : gl; src = B + c * ldb + gj; }
       }
-      cp_async8(bs + l * P_LDB + j, src, v);
+      cp_async8(bs + l * LDB + j, src, v);
     }
   };
 
-  double acc[4][4][2];
+  double acc[4][NI][2];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) { acc[a][b][0] = 0.0; acc[a][b][1] = 0.0; }
+    for (int b = 0; b < NI; ++b) { acc[a][b][0] = 0.0; acc[a][b][1] = 0.0; }
 
-  const int nk = (K + P_BK - 1) / P_BK;
+  // K range of the nonzero rows of op(B) for this N tile (triangular B: TRMM-style skipping)
+  const int kbeg = dd.btri == 1 ? min(n0, K) : 0;
+  const int kend = dd.btri == 2 ? min(K, n0 + BN) : K;
+  const int nk = (kend - kbeg + P_BK - 1) / P_BK;
 #pragma unroll
   for (int st = 0; st < P_ST - 1; ++st) {
-    if (st < nk) load_stage(st, st * P_BK);
+    if (st < nk) load_stage(st, kbeg + st * P_BK);
     cp_async_commit();
   }
   for (int kt = 0; kt < nk; ++kt) {
     cp_async_wait<P_ST - 2>();
     __syncthreads();
     const int pf = kt + P_ST - 1;
-    if (pf < nk) load_stage(pf % P_ST, pf * P_BK);
+    if (pf < nk) load_stage(pf % P_ST, kbeg + pf * P_BK);
     cp_async_commit();
     const double* as = As + (kt % P_ST) * P_BK * P_LDA;
-    const double* bs = Bs + (kt % P_ST) * P_BK * P_LDB;
+    const double* bs = Bs + (kt % P_ST) * P_BK * LDB;
 #pragma unroll
     for (int kk = 0; kk < P_BK; kk += 4) {
-      double af[4], bf[4];
+      double af[4], bf[NI];
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi) af[mi] = as[(kk + tq) * P_LDA + wm * 32 + mi * 8 + g];
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) bf[ni] = bs[(kk + tq) * P_LDB + wn * 32 + ni * 8 + g];
+      for (int ni = 0; ni < NI; ++ni) bf[ni] = bs[(kk + tq) * LDB + wn * WN + ni * 8 + g];
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni)
+        for (int ni = 0; ni < NI; ++ni)
           asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                        : "+d"(acc[mi][ni][0]), "+d"(acc[mi][ni][1])
                        : "d"(af[mi]), "d"(bf[ni]));
@@ -513,10 +520,10 @@ __global__ void __launch_bounds__(P_NT, 2) gemm_pipe_kernel(const GemmDesc* __re
   cp_async_wait<0>();
   const double alpha = dd.alpha, beta = dd.beta;
 #pragma unroll
-  for (int ni = 0; ni < 4; ++ni) {
+  for (int ni = 0; ni < NI; ++ni) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int gj = n0 + wn * 32 + ni * 8 + 2 * tq + h;
+      const int gj = n0 + wn * WN + ni * 8 + 2 * tq + h;
       if (gj >= N) continue;
       const long long cc = mapC ? __ldg(mapC + gj) : gj;
       double* Cc = C + cc * ldc;
@@ -532,20 +539,22 @@ __global__ void __launch_bounds__(P_NT, 2) gemm_pipe_kernel(const GemmDesc* __re
   }
 }
 
+template <int BN>
 void launch_pipe(bool ta, bool tb, dim3 grid, cudaStream_t s, const GemmDesc* d, const int* pre, int np,
                  double* X0, double* X1, int ldx, int Mg) {
   static bool attr = false;
+  constexpr size_t SM = p_smem<BN>();
   if (!attr) {
-    cudaFuncSetAttribute(gemm_pipe_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P_SMEM);
-    cudaFuncSetAttribute(gemm_pipe_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P_SMEM);
-    cudaFuncSetAttribute(gemm_pipe_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P_SMEM);
-    cudaFuncSetAttribute(gemm_pipe_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P_SMEM);
+    cudaFuncSetAttribute(gemm_pipe_kernel<false, false, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
+    cudaFuncSetAttribute(gemm_pipe_kernel<true, false, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
+    cudaFuncSetAttribute(gemm_pipe_kernel<false, true, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
+    cudaFuncSetAttribute(gemm_pipe_kernel<true, true, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
     attr = true;
   }
-  if (!ta && !tb) gemm_pipe_kernel<false, false><<<grid, P_NT, P_SMEM, s>>>(d, pre, np, X0, X1, ldx, Mg);
-  else if (ta && !tb) gemm_pipe_kernel<true, false><<<grid, P_NT, P_SMEM, s>>>(d, pre, np, X0, X1, ldx, Mg);
-  else if (!ta && tb) gemm_pipe_kernel<false, true><<<grid, P_NT, P_SMEM, s>>>(d, pre, np, X0, X1, ldx, Mg);
-  else gemm_pipe_kernel<true, true><<<grid, P_NT, P_SMEM, s>>>(d, pre, np, X0, X1, ldx, Mg);
+  if (!ta && !tb) gemm_pipe_kernel<false, false, BN><<<grid, P_NT, SM, s>>>(d, pre, np, X0, X1, ldx, Mg);
+  else if (ta && !tb) gemm_pipe_kernel<true, false, BN><<<grid, P_NT, SM, s>>>(d, pre, np, X0, X1, ldx, Mg);
+  else if (!ta && tb) gemm_pipe_kernel<false, true, BN><<<grid, P_NT, SM, s>>>(d, pre, np, X0, X1, ldx, Mg);
+  else gemm_pipe_kernel<true, true, BN><<<grid, P_NT, SM, s>>>(d, pre, np, X0, X1, ldx, Mg);
 }
 
 int gemm_mode() {
@@ -567,17 +576,25 @@ bool use_dmma() {
 }  // namespace
 
 void GemmBatch::finalize(cudaStream_t s) const {
-  std::vector<int> pre(h_.size() + 1, 0);
+  const size_t P = h_.size();
+  std::vector<int> pre(3 * (P + 1), 0);   // tile prefix sums for BN = 64, 32, 128
   maxM_ = 0;
+  maxN_ = 0;
   glob_ = false;
-  for (size_t i = 0; i < h_.size(); ++i) {
+  const int bns[3] = {64, 32, 128};
+  for (size_t i = 0; i < P; ++i) {
     const GemmDesc& d = h_[i];
-    int tn = (d.N > 0 && d.M != 0) ? ceil_div(d.N, BN) : 0;
-    pre[i + 1] = pre[i] + tn;
+    for (int v = 0; v < 3; ++v) {
+      const int tn = (d.N > 0 && d.M != 0) ? ceil_div(d.N, bns[v]) : 0;
+      pre[v * (P + 1) + i + 1] = pre[v * (P + 1) + i] + tn;
+    }
     if (d.M < 0) glob_ = true; else maxM_ = std::max(maxM_, d.M);
+    maxN_ = std::max(maxN_, d.N);
   }
-  totalN_ = pre.back();
-  d_.alloc(h_.size(), s);
+  totalN_ = pre[P];
+  totalN32_ = pre[(P + 1) + P];
+  totalN128_ = pre[2 * (P + 1) + P];
+  d_.alloc(P, s);
   d_.upload(h_);
   prefix_.alloc(pre.size(), s);
   prefix_.upload(pre);
@@ -596,9 +613,19 @@ void GemmBatch::run(cudaStream_t s, double* X0, double* X1, int ldx, int Mglob) 
     dim3 grid(totalN_, ceil_div(M, 16));
     launch_variant<16, 1>(ta_, tb_, grid, s, d_.p, prefix_.p, (int)h_.size(), X0, X1, ldx, Mglob);
   } else if (gemm_mode() == 2) {
-    // tiles are 64 wide in N for every variant (prefix computed with BN = 64)
-    dim3 grid(totalN_, ceil_div(M, P_BM));
-    launch_pipe(ta_, tb_, grid, s, d_.p, prefix_.p, (int)h_.size(), X0, X1, ldx, Mglob);
+    // N-tile width by the widest problem of the batch (prefix sums for each width)
+    const size_t P = h_.size();
+    static const bool wide = getenv("RSF_GEMM_BN128") && getenv("RSF_GEMM_BN128")[0] == '1';
+    if (maxN_ <= 32) {
+      dim3 grid(totalN32_, ceil_div(M, P_BM));
+      launch_pipe<32>(ta_, tb_, grid, s, d_.p, prefix_.p + (P + 1), (int)P, X0, X1, ldx, Mglob);
+    } else if (wide && maxN_ >= 512) {
+      dim3 grid(totalN128_, ceil_div(M, P_BM));
+      launch_pipe<128>(ta_, tb_, grid, s, d_.p, prefix_.p + 2 * (P + 1), (int)P, X0, X1, ldx, Mglob);
+    } else {
+      dim3 grid(totalN_, ceil_div(M, P_BM));
+      launch_pipe<64>(ta_, tb_, grid, s, d_.p, prefix_.p, (int)P, X0, X1, ldx, Mglob);
+    }
   } else if (gemm_mode() == 1) {
     dim3 grid(totalN_, ceil_div(M, 64));
     launch_dmma(ta_, tb_, grid, s, d_.p, prefix_.p, (int)h_.size(), X0, X1, ldx, Mglob);
@@ -612,8 +639,8 @@ void GemmBatch::run(cudaStream_t s, double* X0, double* X1, int ldx, int Mglob) 
     double f = 0, b = 0;
     for (const auto& d : h_) {
       const double m = d.M < 0 ? Mglob : d.M;
-      f += 2.0 * m * d.N * d.K;
-      b += 8.0 * (m * d.K + (double)d.K * d.N + m * d.N * (d.beta != 0.0 ? 2.0 : 1.0));
+      f += (d.btri ? 1.0 : 2.0) * m * d.N * d.K;   // triangular op(B): TRMM flops
+      b += 8.0 * (m * d.K + (double)d.K * d.N * (d.btri ? 0.5 : 1.0) + m * d.N * (d.beta != 0.0 ? 2.0 : 1.0));
     }
     KStats::push(e0, e1, f, b);
   }

@@ -22,6 +22,8 @@ struct GemmDesc {
   double* C; long long offC; int ldc; const int* mapC;
   double alpha, beta;
   int lower;                   // 1: only tiles touching the lower triangle of C (SYRK-style)
+  int btri;                    // op(B) triangular (TRMM-style K range): 1 lower (op(B)(l,j) = 0 for l < j),
+                               // 2 upper (op(B)(l,j) = 0 for l > j); 0 general
 };
 
 inline GemmDesc gdesc(int M, int N, int K) {
@@ -51,7 +53,7 @@ class GemmBatch {
   std::vector<GemmDesc> h_;
   mutable DBuf<GemmDesc> d_;
   mutable DBuf<int> prefix_;
-  mutable int totalN_ = 0, maxM_ = 0;
+  mutable int totalN_ = 0, totalN32_ = 0, totalN128_ = 0, maxM_ = 0, maxN_ = 0;
   mutable bool glob_ = false;
 };
 

@@ -289,6 +289,19 @@ void launch_colmax(cudaStream_t s, const std::vector<ColMaxDesc>& v) {
   RSF_LAUNCH_CHECK();
 }
 
+// diagnostics: histogram of row norms of V_i (counts of rows with ||V(t,:)|| < 1e-12, 1e-10, 1e-8, 1e-6)
+__global__ void rownorm_hist_kernel(const double* __restrict__ V, int rows, int cols, unsigned long long* cnt) {
+  for (int t = blockIdx.x * NT + threadIdx.x; t < rows; t += gridDim.x * NT) {
+    double s = 0.0;
+    for (int j = 0; j < cols; ++j) { const double v = V[(long long)j * rows + t]; s += v * v; }
+    const double nr = sqrt(s);
+    if (nr < 1e-12) atomicAdd(cnt + 0, 1ull);
+    if (nr < 1e-10) atomicAdd(cnt + 1, 1ull);
+    if (nr < 1e-8) atomicAdd(cnt + 2, 1ull);
+    if (nr < 1e-6) atomicAdd(cnt + 3, 1ull);
+  }
+}
+
 template <class D, class K>
 void launch_descs(cudaStream_t s, const std::vector<D>& v, long long maxelems, K kern) {
   if (v.empty() || maxelems <= 0) return;
@@ -328,6 +341,7 @@ void cholqr2_batched(cudaStream_t s, const std::vector<CQProb>& v, int lev, doub
       pp.push_back(PotrfProb{G.p + go[x], p.k, p.k, Gi.p + go[x], p.k});
       GemmDesc e = gdesc(p.rows, p.k, p.k);        // U <- U L^-T
       e.A = src; e.lda = p.rows; e.B = Gi.p + go[x]; e.ldb = p.k; e.C = dst; e.ldc = p.rows;
+      e.btri = 2;
       gu.add(e);
       if (flops) *flops += 4.0 * p.rows * (double)p.k * p.k;
     }
@@ -379,6 +393,7 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
   int prev_rank = -1;
   const int kb = std::max(16, o.probe_block);
   const double budget = 16.0 * (1ull << 30);   // bytes of transient per-batch buffers
+  const double wcache_budget = 8.0 * (1ull << 30);   // W_i^T kept for a whole probe group
 
   auto residual = [&](const double* W, double* Y, int k, int upto) {
     G.apply(W, Y, k);
@@ -468,6 +483,21 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
         DBuf<double> P(pt, s), CC(std::max<long long>(cct, 1), s), ref(NA, s);
         ref.zero();
         CC.zero();
+        // W_i^T of every act box for the whole group when it fits (else regenerated per batch)
+        std::vector<long long> wco(NA);
+        long long wct = 0;
+        for (size_t x = 0; x < NA; ++x) { wco[x] = wct; wct += (long long)c * bx[act[x]].ni; }
+        DBuf<double> Wc;
+        if (8.0 * wct <= wcache_budget) {
+          Wc.alloc(wct, s);
+          for (size_t x = 0; x < NA; ++x) {
+            const PBox& b = bx[act[x]];
+            probes_kernel<<<gxx((long long)b.ni * c), NT, 0, s>>>(Wc.p + wco[x], c, b.ib, b.ib + b.ni, t.d_perm.p,
+                                                                nullptr, 0, 0, lev, trace_id, seed32, c);
+            count_launch();
+          }
+          RSF_LAUNCH_CHECK();
+        }
         // sketch Y'_g = ((G - sum_{m<l} G^(m)) W_g)^T in chunks of kb probe columns;
         // every chunk extends the bases V_i of the boxes that see it
         DBuf<double> W((size_t)n * std::min(kb, c), s), Y((size_t)n * std::min(kb, c), s);
@@ -496,21 +526,28 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
               c1o[x] = c1t; c1t += (long long)k * rb[i];
               pro[x] = prt; prt += (long long)c * k;
             }
-            DBuf<double> Wi(wt, s), C1(std::max<long long>(c1t, 1), s), Pr(prt, s);
+            DBuf<double> Wi(Wc.p ? 1 : wt, s), C1(std::max<long long>(c1t, 1), s), Pr(prt, s);
             DBuf<int> pivr((size_t)k * B, s);
             GemmBatch gp(false, true), gc(false, false), gr(false, true), gpr(false, true);
             std::vector<ColMaxDesc> cm;
+            std::vector<CopyProb> pcp;
+            std::vector<double*> Wp(B);
             for (size_t x = 0; x < B; ++x) {
               const size_t xa = x0 + x;
               const int i = act[xa];
               const PBox& b = bx[i];
-              // W_i^T (c x n_i): the same Philox entries as box i's rows of its own group's probes
-              probes_kernel<<<gxx((long long)b.ni * c), NT, 0, s>>>(Wi.p + wo[x], c, b.ib, b.ib + b.ni, t.d_perm.p,
-                                                                  nullptr, 0, 0, lev, trace_id, seed32, c);
-              count_launch();
+              if (Wc.p) {
+                Wp[x] = Wc.p + wco[xa];
+              } else {
+                // W_i^T (c x n_i): the same Philox entries as box i's rows of its own group's probes
+                Wp[x] = Wi.p + wo[x];
+                probes_kernel<<<gxx((long long)b.ni * c), NT, 0, s>>>(Wp[x], c, b.ib, b.ib + b.ni, t.d_perm.p,
+                                                                    nullptr, 0, 0, lev, trace_id, seed32, c);
+                count_launch();
+              }
               double* Yi = Y.p + (long long)b.ib * k;
               GemmDesc d = gdesc(c, k, b.ni);              // P_ij(:, chunk) = W_i^T Y_ij(:, chunk)
-              d.A = Wi.p + wo[x]; d.lda = c; d.B = Yi; d.ldb = k; d.C = P.p + po[xa] + (long long)c * c0; d.ldc = c;
+              d.A = Wp[x]; d.lda = c; d.B = Yi; d.ldb = k; d.C = P.p + po[xa] + (long long)c * c0; d.ldc = c;
               gp.add(d);
               cm.push_back(ColMaxDesc{P.p + po[xa] + (long long)c * c0, c, c, k, ref.p + xa});
               pd.flops += 2.0 * c * (double)k * b.ni;
@@ -523,14 +560,17 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
                 f.alpha = -1.0; f.beta = 1.0;
                 gr.add(f);
                 pd.flops += 4.0 * k * (double)rb[i] * b.ni;
+                GemmDesc h = gdesc(c, k, rb[i]);           // W_i^T Res = W_i^T Y - A_i C1^T
+                h.A = Ab[i].p; h.lda = c; h.B = C1.p + c1o[x]; h.ldb = k; h.C = Pr.p + pro[x]; h.ldc = c;
+                h.alpha = -1.0; h.beta = 1.0;
+                gpr.add(h);
               }
-              GemmDesc h = gdesc(c, k, b.ni);              // W_i^T Res
-              h.A = Wi.p + wo[x]; h.lda = c; h.B = Yi; h.ldb = k; h.C = Pr.p + pro[x]; h.ldc = c;
-              gpr.add(h);
+              pcp.push_back(CopyProb{P.p + po[xa] + (long long)c * c0, c, Pr.p + pro[x], c, c, k, 1.0});
             }
             RSF_LAUNCH_CHECK();
             gp.run(s);
             launch_colmax(s, cm);
+            copy_batched(s, pcp);
             gc.run(s); gr.run(s); gpr.run(s);
             std::vector<RRQRProb> rp;
             for (size_t x = 0; x < B; ++x) {
@@ -577,7 +617,6 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
             }
             g0.run(s);
             Q0.release();
-            cholqr2_batched(s, cq, lev, &pd.flops);
             {
               GemmBatch gh(true, false), gq(false, false);
               long long ht = 0;
@@ -595,10 +634,8 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
                 e.alpha = -1.0; e.beta = 1.0;
                 gq.add(e);
               }
-              if (!gh.empty()) {
-                gh.run(s); gq.run(s);
-                cholqr2_batched(s, cq, lev, &pd.flops);
-              }
+              if (!gh.empty()) { gh.run(s); gq.run(s); }
+              cholqr2_batched(s, cq, lev, &pd.flops);   // right factors keep Q orthogonal to V_i
             }
             // C_ij'(chunk, :) = Y_ij(:, chunk)^T [V_i, Q_i] = [C1, Res^T Q_i]; V_i <- [V_i, Q_i],
             // A_i <- [A_i, W_i^T Q_i] (per-box buffers, regrown)
@@ -633,7 +670,7 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
               }
               cpv.push_back(CopyProb{Qb.p + qo[x], ni, nV[x].p + ni * rb[i], ni, (int)ni, qq[x], 1.0});
               GemmDesc e = gdesc(c, qq[x], bx[i].ni);
-              e.A = Wi.p + wo[x]; e.lda = c; e.B = Qb.p + qo[x]; e.ldb = bx[i].ni;
+              e.A = Wp[x]; e.lda = c; e.B = Qb.p + qo[x]; e.ldb = bx[i].ni;
               e.C = nA[x].p + (long long)c * rb[i]; e.ldc = c;
               gan.add(e);
             }
@@ -892,8 +929,21 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
       int rmax = 0;
       for (int b = 0; b < nb; ++b) { rsum += rb[b]; rmax = std::max(rmax, rb[b]); }
       fprintf(stderr, "[peel tr%d] level %d boxes %d pairs %d cols %d rank_max %d basis sum %lld max %d V %.2f GB "
-                      "dev_used %.2f GB t %.2f s\n",
-              trace_id, lev, nb, npairs, c, mr, rsum, rmax, 1e-9 * vbytes, 1e-9 * (tot - fr), now_s() - t0);
+                      "Brow %.2f GB dev_used %.2f GB t %.2f s\n",
+              trace_id, lev, nb, npairs, c, mr, rsum, rmax, 1e-9 * vbytes, 8e-9 * PL.Brow.n, 1e-9 * (tot - fr), now_s() - t0);
+      if (verbose > 1) {
+        DBuf<unsigned long long> cnt(4, s);
+        RSF_CUDA(cudaMemsetAsync(cnt.p, 0, 4 * sizeof(unsigned long long), s));
+        long long rows = 0;
+        for (int b = 0; b < nb; ++b)
+          if (rb[b] > 0) {
+            rownorm_hist_kernel<<<gxx(bx[b].ni), NT, 0, s>>>(PL.V[b].p, bx[b].ni, rb[b], cnt.p);
+            rows += bx[b].ni;
+          }
+        auto h = cnt.to_host(4);
+        fprintf(stderr, "    V rows %lld: row norm < 1e-12: %llu, < 1e-10: %llu, < 1e-8: %llu, < 1e-6: %llu\n", rows,
+                h[0], h[1], h[2], h[3]);
+      }
     }
   }
 

@@ -1,8 +1,13 @@
 // Blocked randomized rank-revealing QR truncated at the eps-rank (see rrqr.cuh).
 #include <algorithm>
+#include <climits>
 #include <cmath>
 
+#include <cooperative_groups.h>
+
 #include "rrqr.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace rsf {
 
@@ -185,6 +190,148 @@ __global__ void __launch_bounds__(NT) sketch_cpqr_kernel(const RDesc* __restrict
   }
 }
 
+// Cluster version of the block pivot selection: the sketch columns Y(:, J:c) are
+// distributed over the CL CTAs of a thread-block cluster and held in shared memory
+// (SP x chunk each); every greedy step exchanges the CTAs' best candidates and the
+// Householder vector of the winner through distributed shared memory, so one step
+// costs two cluster barriers instead of a pass of one SM over the whole sketch in
+// global memory.  Produces the same swap list as sketch_cpqr_kernel.
+constexpr int SK_NT = 512, SK_NW = SK_NT / 32;
+constexpr int SK_MAXCOLS = 600;   // columns per CTA: SP * 600 * 8 B = 192 KB of shared memory
+
+template <int CL>
+__global__ void __launch_bounds__(SK_NT) sketch_cpqr_cl_kernel(const RDesc* __restrict__ d0) {
+  extern __shared__ double sk_sm[];
+  __shared__ double cand_v[CL];
+  __shared__ int cand_i[CL];
+  __shared__ double hv[SP];
+  __shared__ double htau;
+  __shared__ double redv[SK_NW];
+  __shared__ int redi[SK_NW];
+  __shared__ int chosen[QR_NB];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const RDesc d = d0[blockIdx.x / CL];
+  const int J = d.J, cr = d.c - J, nbp = d.nbp;
+  const int chunk = (cr + CL - 1) / CL;
+  const int j0 = rank * chunk, nc = max(0, min(cr, j0 + chunk) - j0);
+  double* Zs = sk_sm;               // SP x chunk, column-major
+  double* zn = Zs + SP * chunk;     // squared trailing norms (-1: retired)
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int e = tid; e < SP * nc; e += SK_NT) Zs[e] = d.Y[(long long)(J + j0) * SP + e];
+  __syncthreads();
+  for (int j = warp; j < nc; j += SK_NW) {
+    const double* z = Zs + j * SP;
+    double v = (lane < SP) ? z[lane] : 0.0;
+    double s2 = v * v;
+    if (lane + 32 < SP) { const double w = z[lane + 32]; s2 += w * w; }
+    s2 = wsum(s2);
+    if (lane == 0) zn[j] = s2;
+  }
+  __syncthreads();
+  for (int t = 0; t < nbp; ++t) {
+    // local candidate: largest trailing norm, ties -> lowest global index
+    double bv = -2.0;
+    int bi = INT_MAX;
+    for (int j = tid; j < nc; j += SK_NT) {
+      const double v = zn[j];
+      if (v > bv) { bv = v; bi = j0 + j; }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    if (lane == 0) { redv[warp] = bv; redi[warp] = bi; }
+    __syncthreads();
+    if (tid < CL) {
+      double v = redv[0];
+      int b = redi[0];
+      for (int w = 1; w < SK_NW; ++w)
+        if (redv[w] > v || (redv[w] == v && redi[w] < b)) { v = redv[w]; b = redi[w]; }
+      double* rv = cluster.map_shared_rank(cand_v, tid);
+      int* ri = cluster.map_shared_rank(cand_i, tid);
+      rv[rank] = v;
+      ri[rank] = b;
+    }
+    cluster.sync();
+    double pv = cand_v[0];
+    int p = cand_i[0];
+    for (int r = 1; r < CL; ++r)
+      if (cand_v[r] > pv || (cand_v[r] == pv && cand_i[r] < p)) { pv = cand_v[r]; p = cand_i[r]; }
+    if (p >= cr) p = t;   // degenerate (no active column): keep the order
+    const int owner = p / chunk;
+    if (rank == owner && warp == 0) {
+      // Householder reflector of Zs(t:SP, p): v = [1; x(t+1:)/(x_t - beta)], tau = (beta - x_t)/beta
+      double* x = Zs + (p - j0) * SP;
+      double s2 = 0.0;
+      for (int r = t + 1 + lane; r < SP; r += 32) s2 += x[r] * x[r];
+      s2 = wsum(s2);
+      const double alpha = x[t];
+      double tau = 0.0, beta = alpha, scale = 0.0;
+      if (s2 != 0.0) {
+        const double mu = sqrt(alpha * alpha + s2);
+        beta = (alpha >= 0.0) ? -mu : mu;
+        tau = (beta - alpha) / beta;
+        scale = 1.0 / (alpha - beta);
+      }
+      for (int r = lane; r < SP; r += 32) {
+        const double v = (r < t) ? 0.0 : (r == t ? 1.0 : x[r] * scale);
+        for (int q = 0; q < CL; ++q) cluster.map_shared_rank(hv, q)[r] = v;
+      }
+      if (lane < CL) *cluster.map_shared_rank(&htau, lane) = tau;
+      if (lane == 0) zn[p - j0] = -1.0;   // retired
+    }
+    if (rank == 0 && tid == 0) chosen[t] = p;
+    cluster.sync();
+    // apply (I - tau v v^T) to the active local columns, recompute their trailing norms
+    const double tau = htau;
+    for (int j = warp; j < nc; j += SK_NW) {
+      if (zn[j] < 0.0) continue;
+      double* z = Zs + j * SP;
+      const double a0 = (lane < SP && lane >= t) ? z[lane] : 0.0;
+      const double a1 = (lane + 32 < SP && lane + 32 >= t) ? z[lane + 32] : 0.0;
+      const double v0 = (lane < SP) ? hv[lane] : 0.0;
+      const double v1 = (lane + 32 < SP) ? hv[lane + 32] : 0.0;
+      const double w = tau * wsum(a0 * v0 + a1 * v1);
+      const double b0 = a0 - w * v0, b1 = a1 - w * v1;
+      if (lane < SP && lane >= t) z[lane] = b0;
+      if (lane + 32 < SP && lane + 32 >= t) z[lane + 32] = b1;
+      const double s2 = wsum((lane > t && lane < SP ? b0 * b0 : 0.0) + (lane + 32 > t && lane + 32 < SP ? b1 * b1 : 0.0));
+      if (lane == 0) zn[j] = s2;
+    }
+    __syncthreads();
+  }
+  // chosen original indices -> sequential swap list (swap positions t and sw[t], t = 0..nbp-1)
+  if (rank == 0 && tid == 0) {
+    int mv_orig[2 * QR_NB], mv_pos[2 * QR_NB], nm = 0;   // moved columns: original index -> position
+    auto pos_of = [&](int o) {
+      for (int q = 0; q < nm; ++q) if (mv_orig[q] == o) return mv_pos[q];
+      return o;
+    };
+    auto at_pos = [&](int ps) {   // original column currently at position ps
+      for (int q = 0; q < nm; ++q) if (mv_pos[q] == ps) return mv_orig[q];
+      for (int q = 0; q < nm; ++q) if (mv_orig[q] == ps) return -1;   // ps's original moved away
+      return ps;
+    };
+    auto set_pos = [&](int o, int ps) {
+      for (int q = 0; q < nm; ++q) if (mv_orig[q] == o) { mv_pos[q] = ps; return; }
+      mv_orig[nm] = o; mv_pos[nm] = ps; ++nm;
+    };
+    for (int t = 0; t < nbp; ++t) {
+      const int p = chosen[t];
+      const int q = pos_of(p);
+      int ot = at_pos(t);
+      if (ot < 0) {   // search: the original column sitting at position t
+        for (int k2 = 0; k2 < nm; ++k2) if (mv_pos[k2] == t) { ot = mv_orig[k2]; break; }
+      }
+      d.sw[t] = q;
+      if (q != t) { set_pos(p, t); set_pos(ot, q); }
+    }
+  }
+}
+
 // apply the swap list to A (m rows), Y (SP rows) and piv
 __global__ void apply_swaps_kernel(const RDesc* __restrict__ d0) {
   const RDesc d = d0[blockIdx.x];
@@ -320,6 +467,48 @@ __global__ void upper_inv64_kernel(const DInvDesc* __restrict__ d0) {
   }
 }
 
+template <int CL>
+void launch_cl(cudaStream_t s, const RDesc* dd, int na, int chunk) {
+  static bool attr = false;
+  if (!attr) {
+    RSF_CUDA(cudaFuncSetAttribute(sketch_cpqr_cl_kernel<CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    if (CL > 8) RSF_CUDA(cudaFuncSetAttribute(sketch_cpqr_cl_kernel<CL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(na * CL));
+  cfg.blockDim = dim3(SK_NT);
+  cfg.dynamicSmemBytes = (size_t)(SP + 1) * chunk * sizeof(double);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  RSF_CUDA(cudaLaunchKernelEx(&cfg, sketch_cpqr_cl_kernel<CL>, dd));
+  count_launch();
+}
+
+// cluster pivot selection when the widest trailing sketch fits in <= 16 CTAs' shared memory
+bool launch_sketch_cluster(cudaStream_t s, const RDesc* dd, int na, int crmax) {
+  static const bool on = !(getenv("RSF_SKETCH_CLUSTER") && getenv("RSF_SKETCH_CLUSTER")[0] == '0');
+  if (!on || crmax <= 0) return false;
+  int CL = 1;
+  while (CL < 16 && (crmax + CL - 1) / CL > SK_MAXCOLS) CL *= 2;
+  const int chunk = (crmax + CL - 1) / CL;
+  if (chunk > SK_MAXCOLS) return false;
+  switch (CL) {
+    case 1: launch_cl<1>(s, dd, na, chunk); break;
+    case 2: launch_cl<2>(s, dd, na, chunk); break;
+    case 4: launch_cl<4>(s, dd, na, chunk); break;
+    case 8: launch_cl<8>(s, dd, na, chunk); break;
+    default: launch_cl<16>(s, dd, na, chunk); break;
+  }
+  return true;
+}
+
 }  // namespace
 
 void trsm_upper_batched(cudaStream_t s, const std::vector<TrsmProb>& probs) {
@@ -451,9 +640,14 @@ RRQRResult rrqr_batched(cudaStream_t s, const std::vector<RRQRProb>& probs, doub
     }
     auto dd = upd(dv, s);
     const unsigned na = (unsigned)dv.size();
-    sketch_cpqr_kernel<<<na, NT, 0, s>>>(dd.p);
+    int crmax = 0;
+    for (auto& d : dv) crmax = std::max(crmax, d.c - d.J);
+    if (!launch_sketch_cluster(s, dd.p, (int)na, crmax)) {
+      sketch_cpqr_kernel<<<na, NT, 0, s>>>(dd.p);
+      count_launch();
+    }
     apply_swaps_kernel<<<na, NT, 0, s>>>(dd.p);
-    count_launch(2);
+    count_launch();
     RSF_LAUNCH_CHECK();
     std::vector<PanelStep> ps;
     for (size_t a = 0; a < dv.size(); ++a) {

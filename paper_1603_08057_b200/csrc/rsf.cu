@@ -35,6 +35,8 @@ double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
+inline GemmDesc tri(GemmDesc d, int t) { d.btri = t; return d; }   // triangular op(B)
+
 struct BRef {
   const double* Bp = nullptr;   // permuted self block of a processed node (B_SS at top-left)
   int ld = 0;
@@ -392,6 +394,7 @@ std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams
           if (!solve_only) lc.push_back(CopyProb{B + (long long)k * c + k, c, LV.L.p + LV.loff[b], r, r, r, 1.0});
           if (k == 0) continue;
           GemmDesc d4 = gdesc(k, r, r);      // E = X_SR L^-T
+          d4.btri = 2;
           d4.A = B + (long long)k * c; d4.lda = c; d4.B = LV.Linv.p + LV.loff[b]; d4.ldb = r;
           d4.C = LV.E.p + LV.eoff[b]; d4.ldc = k;
           e4.add(d4);
@@ -462,17 +465,17 @@ std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams
       if (sig) {
         const double* Lib = LV.Linv.p + LV.loff[b];
         if (k > 0) LV.fs1.add(mk(r, k, 1, Sb, 0, Tb, k, 1, Rb, 0, -1.0, 1.0));
-        LV.fs2.add(mk(r, r, 1, Rb, 0, Lib, r, 2, nullptr, tc[b], 1.0, 0.0));
+        LV.fs2.add(tri(mk(r, r, 1, Rb, 0, Lib, r, 2, nullptr, tc[b], 1.0, 0.0), 2));
         if (k > 0) LV.fs3.add(mk(k, r, 2, nullptr, tc[b], Eb, k, 1, Sb, 0, -1.0, 1.0));
         if (k > 0) LV.bs2.add(mk(r, k, 1, Sb, 0, Eb, k, 2, nullptr, tc[b], -1.0, 1.0));
-        LV.bs3.add(mk(r, r, 2, nullptr, tc[b], Lib, r, 1, Rb, 0, 1.0, 0.0));
+        LV.bs3.add(tri(mk(r, r, 2, nullptr, tc[b], Lib, r, 1, Rb, 0, 1.0, 0.0), 1));
         if (k > 0) LV.bs4.add(mk(k, r, 1, Rb, 0, Tb, k, 1, Sb, 0, -1.0, 1.0));
         if (solve_only) continue;
         if (k > 0) LV.up1.add(mk(k, r, 1, Rb, 0, Tb, k, 1, Sb, 0, 1.0, 1.0));
-        LV.up2.add(mk(r, r, 1, Rb, 0, Lb, r, 2, nullptr, tc[b], 1.0, 0.0));
+        LV.up2.add(tri(mk(r, r, 1, Rb, 0, Lb, r, 2, nullptr, tc[b], 1.0, 0.0), 1));
         if (k > 0) LV.up3.add(mk(r, k, 1, Sb, 0, Eb, k, 2, nullptr, tc[b], 1.0, 1.0));
         if (k > 0) LV.dn1.add(mk(k, r, 1, Rb, 0, Eb, k, 1, Sb, 0, 1.0, 1.0));
-        LV.dn2.add(mk(r, r, 1, Rb, 0, Lb, r, 2, nullptr, tc[b], 1.0, 0.0));
+        LV.dn2.add(tri(mk(r, r, 1, Rb, 0, Lb, r, 2, nullptr, tc[b], 1.0, 0.0), 2));
         if (k > 0) LV.dn4.add(mk(r, k, 1, Sb, 0, Tb, k, 1, Rb, 0, 1.0, 1.0));
       } else {
         // X0 = x (modified), X1 = y
@@ -486,6 +489,29 @@ std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams
     for (GemmBatch* g : {&LV.fs1, &LV.fs2, &LV.fs3, &LV.bs2, &LV.bs3, &LV.bs4, &LV.up1, &LV.up2, &LV.up3,
                          &LV.dn1, &LV.dn2, &LV.dn4, &LV.ao1, &LV.ao2a, &LV.ao2b, &LV.ao3, &LV.ao4})
       if (!g->empty()) g->finalize(s);
+    // fused small-box sweeps for the solve (Sigma) and the apply-only operator (Sigma_i)
+    {
+      static const bool fused_on = !(getenv("RSF_FUSED") && std::string(getenv("RSF_FUSED")) == "0");
+      LV.max_i = 0;
+      for (int b = 0; b < nb; ++b) LV.max_i = std::max(LV.max_i, cvec[b]);
+      LV.fused = fused_on && LV.max_i <= SWEEP_MAX_I;
+      if (LV.fused) {
+        std::vector<BoxOp> ops;
+        for (int b = 0; b < nb; ++b) {
+          if (LV.r[b] == 0) continue;
+          BoxOp op;
+          op.S = LV.S.p + LV.soff[b]; op.R = LV.R.p + LV.roff[b];
+          op.kb = kvec[b]; op.r = LV.r[b];
+          op.T = LV.T.p + LV.toff[b];
+          op.L = sig ? LV.Linv.p + LV.loff[b] : LV.L.p + LV.loff[b];
+          op.E = LV.E.p + LV.eoff[b];
+          ops.push_back(op);
+        }
+        LV.nops = (int)ops.size();
+        LV.ops.alloc(std::max<size_t>(ops.size(), 1), s);
+        LV.ops.upload(ops);
+      }
+    }
   }
 
   // ---- top (level 0, R-Y): B_0 and its dense Cholesky
@@ -550,12 +576,12 @@ std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams
     if (n0 > 0) {
       const int* m0 = F->I0.p;
       if (sig) {
-        F->top_s1.add(mk(n0, n0, 1, m0, F->Cinv.p, n0, 2, nullptr, 0.0));   // tmp = X(I0) Cinv^T
-        F->top_s2.add(mk(n0, n0, 2, nullptr, F->Cinv.p, n0, 1, m0, 0.0));   // X(I0) = tmp Cinv
+        F->top_s1.add(tri(mk(n0, n0, 1, m0, F->Cinv.p, n0, 2, nullptr, 0.0), 2));   // tmp = X(I0) Cinv^T
+        F->top_s2.add(tri(mk(n0, n0, 2, nullptr, F->Cinv.p, n0, 1, m0, 0.0), 1));   // X(I0) = tmp Cinv
         if (!solve_only) {
-          F->top_a1.add(mk(n0, n0, 1, m0, F->C.p, n0, 2, nullptr, 0.0));      // tmp = X(I0) C
-          F->top_a2.add(mk(n0, n0, 2, nullptr, F->C.p, n0, 1, m0, 0.0));      // X(I0) = tmp C^T
-          F->top_q1.add(mk(n0, n0, 1, m0, F->C.p, n0, 2, nullptr, 0.0));      // tmp = X(I0) C^T
+          F->top_a1.add(tri(mk(n0, n0, 1, m0, F->C.p, n0, 2, nullptr, 0.0), 1));      // tmp = X(I0) C
+          F->top_a2.add(tri(mk(n0, n0, 2, nullptr, F->C.p, n0, 1, m0, 0.0), 2));      // X(I0) = tmp C^T
+          F->top_q1.add(tri(mk(n0, n0, 1, m0, F->C.p, n0, 2, nullptr, 0.0), 2));      // tmp = X(I0) C^T
         } else {
           F->C.release();
         }
@@ -573,21 +599,40 @@ std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams
 }
 
 // ------------------------------------------------------------------ operators
+// per-level phase names for RSF_PROFILE=1 (diagnostics)
+static const char* lvname(const char* op, int lev) {
+  static std::vector<std::string> names;
+  if (!Prof::enabled()) return op;
+  const std::string key = std::string(op) + ".L" + std::to_string(lev);
+  for (size_t i = 0; i < names.size(); ++i) if (names[i] == key) return names[i].c_str();
+  if (names.empty()) names.reserve(4096);   // stable c_str() pointers
+  if (names.size() >= 4096) return op;
+  names.push_back(key);
+  return names.back().c_str();
+}
+
 void solve_internal(const Fact& F, double* X, int k, double* tmp) {
   RSF_REQUIRE(F.which == W_SIGMA, ST_EINVAL, "solve needs a Sigma factor");
   cudaStream_t s = F.ctx->stream;
   const int L = F.tree->L;
   for (int lev = L; lev >= 1; --lev) {
     const Level& LV = F.levels[lev];
+    RSF_PHASE(lvname("sv", lev), s);
+    if (LV.fused) { sweep_level(s, LV.ops.p, LV.nops, LV.max_i, SW_SOLVE_FWD, X, nullptr, k); continue; }
     LV.fs1.run(s, X, tmp, k, k);
     LV.fs2.run(s, X, tmp, k, k);
     LV.fs3.run(s, X, tmp, k, k);
     colcopy(s, X, tmp, k, k, LV.R.p, nullptr, LV.rtot);
   }
-  F.top_s1.run(s, X, tmp, k, k);
-  F.top_s2.run(s, X, tmp, k, k);
+  {
+    RSF_PHASE("sv.top", s);
+    F.top_s1.run(s, X, tmp, k, k);
+    F.top_s2.run(s, X, tmp, k, k);
+  }
   for (int lev = 1; lev <= L; ++lev) {
     const Level& LV = F.levels[lev];
+    RSF_PHASE(lvname("sv", lev), s);
+    if (LV.fused) { sweep_level(s, LV.ops.p, LV.nops, LV.max_i, SW_SOLVE_BWD, X, nullptr, k); continue; }
     colcopy(s, tmp, X, k, k, nullptr, LV.R.p, LV.rtot);
     LV.bs2.run(s, X, tmp, k, k);
     LV.bs3.run(s, X, tmp, k, k);
@@ -637,13 +682,20 @@ void apply_only_internal(const Fact& F, double* X, double* Y, int k) {
   const int L = F.tree->L;
   for (int lev = L; lev >= 1; --lev) {
     const Level& LV = F.levels[lev];
+    RSF_PHASE(lvname("ao", lev), s);
+    if (LV.fused) { sweep_level(s, LV.ops.p, LV.nops, LV.max_i, SW_AO_UP, X, Y, k); continue; }
     LV.ao1.run(s, X, Y, k, k);
     LV.ao2a.run(s, X, Y, k, k);
     LV.ao2b.run(s, X, Y, k, k);
   }
-  F.top_ao.run(s, X, Y, k, k);
+  {
+    RSF_PHASE("ao.top", s);
+    F.top_ao.run(s, X, Y, k, k);
+  }
   for (int lev = 1; lev <= L; ++lev) {
     const Level& LV = F.levels[lev];
+    RSF_PHASE(lvname("ao", lev), s);
+    if (LV.fused) { sweep_level(s, LV.ops.p, LV.nops, LV.max_i, SW_AO_DN, X, Y, k); continue; }
     LV.ao3.run(s, X, Y, k, k);
     LV.ao4.run(s, X, Y, k, k);
   }

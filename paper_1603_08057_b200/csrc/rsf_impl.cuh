@@ -7,6 +7,7 @@
 #include "common.cuh"
 #include "covariance.cuh"
 #include "gemm.cuh"
+#include "sweep.cuh"
 
 namespace rsf {
 
@@ -78,6 +79,10 @@ struct Level {
   GemmBatch up1, up2, up3;            // apply, up
   GemmBatch dn1, dn2, dn4;            // apply, down
   GemmBatch ao1, ao2a, ao2b, ao3, ao4;  // apply-only (Sigma_i)
+  // fused small-box sweeps (sweep.cuh): used when every box has |I_b| <= SWEEP_MAX_I
+  bool fused = false;
+  int max_i = 0, nops = 0;
+  DBuf<BoxOp> ops;
 };
 
 struct FactDiag {

@@ -294,3 +294,41 @@ def test_kernel_launches_are_counted(ctx):
     l0 = R.kernel_launches()
     R.gp_mle_eval(ctx, _d(xy), _d(z), rk, c.eps_fact, c.leaf)
     assert R.kernel_launches() - l0 > 100
+
+
+_FUSED_PROBE = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_1603_08057_b200 as R
+from workloads import config, points_for
+c = config(2)
+n = 4096
+xy = points_for(c, n)
+dev = torch.device("cuda:0")
+ctx = R.Context(0)
+K = R.Kernel(c.family, c.rho, c.sigma2, c.nugget, c.alpha, c.theta)
+F = R.Factor(ctx, torch.from_numpy(xy).to(dev), K, 1e-8, 32)
+Fi = R.Factor(ctx, torch.from_numpy(xy).to(dev), K, 1e-8, 32, which=0)
+B = torch.from_numpy(np.random.default_rng(11).standard_normal((n, 40))).to(dev)
+np.save(sys.argv[2], np.concatenate([F.solve(B.clone()).cpu().numpy(), Fi.apply(B.clone()).cpu().numpy()], axis=1))
+"""
+
+
+def test_fused_sweeps_match_batched_gemm_path(tmp_path):
+    """The fused small-box level sweeps (sweep.cu, every level of a leaf-32 tree) against the
+    batched-GEMM level steps (RSF_FUSED=0): F^-1 B and F_i B on 40 right-hand sides agree to
+    round-off (same factor, same operation order up to FMA contraction)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "probe.py"
+    script.write_text(_FUSED_PROBE)
+    out = {}
+    for flag in ("1", "0"):
+        f = tmp_path / f"out{flag}.npy"
+        env = dict(os.environ, RSF_FUSED=flag)
+        subprocess.run([sys.executable, str(script), root, str(f)], env=env, check=True, timeout=600)
+        out[flag] = np.load(f)
+    a, b = out["1"], out["0"]
+    assert np.linalg.norm(a - b) <= 1e-10 * np.linalg.norm(b)

@@ -5,4 +5,4 @@ shapes = [(512, 512, 512, 64), (512, 64, 64, 4096), (512, 32, 32, 8192), (4096, 
 for (M, N, K, b) in shapes:
     for ta, tb in [(0, 0), (0, 1)]:
         v = R.lib.rsf_debug_gemm_bench(M, N, K, b, ta, tb, 5)
-        print(f"{os.environ.get('RSF_GEMM','pipe')} M={M} N={N} K={K} batch={b} ta={ta} tb={tb}: {v:.2f} TFLOP/s")
+        print(f"{os.environ.get("RSF_GEMM","pipe")} bn128={os.environ.get("RSF_GEMM_BN128","0")} M={M} N={N} K={K} batch={b} ta={ta} tb={tb}: {v:.2f} TFLOP/s")
