@@ -101,6 +101,16 @@ struct PhaseTimer {
   PhaseTimer(const char* n, cudaStream_t st);
   ~PhaseTimer();
 };
+// consecutive named phases inside one scope: next(name) closes the previous phase
+struct PhaseSeq {
+  cudaStream_t s;
+  const char* name = nullptr;
+  double t0 = 0;
+  bool on;
+  explicit PhaseSeq(cudaStream_t st);
+  void next(const char* n);
+  ~PhaseSeq() { next(nullptr); }
+};
 #define RSF_CAT2(a, b) a##b
 #define RSF_CAT(a, b) RSF_CAT2(a, b)
 #define RSF_PHASE(name, stream) ::rsf::PhaseTimer RSF_CAT(_rsf_pt_, __LINE__)(name, stream)

@@ -81,6 +81,15 @@ void Prof::reset() { prof_table().clear(); }
 PhaseTimer::PhaseTimer(const char* n, cudaStream_t st) : name(n), s(st), on(Prof::enabled()) {
   if (on) { cudaStreamSynchronize(s); t0 = wall(); }
 }
+PhaseSeq::PhaseSeq(cudaStream_t st) : s(st), on(Prof::enabled()) {}
+void PhaseSeq::next(const char* n) {
+  if (!on) return;
+  cudaStreamSynchronize(s);
+  const double t = wall();
+  if (name) Prof::add(name, t - t0);
+  name = n;
+  t0 = t;
+}
 PhaseTimer::~PhaseTimer() {
   if (on) { cudaStreamSynchronize(s); Prof::add(name, wall() - t0); }
 }
@@ -405,6 +414,11 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool
   const int sz = valid ? 8 : 0;
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz));
 }
+// 16-byte variant (L2 only): `bytes` of the pair are copied, the rest zero-filled
+__device__ __forceinline__ void cp_async16(double* smem, const double* gmem, int bytes) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(bytes));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
@@ -445,9 +459,25 @@ __global__ void __launch_bounds__(P_NT, (BN >= 128 ? 1 : 2)) gemm_pipe_kernel(co
   const int g = lane >> 2, tq = lane & 3;
   const int wm = warp & 3, wn = warp >> 2;
 
+  // 16-byte copies where the contiguous dimension of global and shared memory agree
+  // (A not transposed, B transposed) and the operand is 16-byte aligned with an even ld
+  const bool vecA = !TA && ((reinterpret_cast<unsigned long long>(A) & 15ull) == 0) && ((lda & 1) == 0);
+  const bool vecB = TB && ((reinterpret_cast<unsigned long long>(B) & 15ull) == 0) && ((ldb & 1) == 0);
   auto load_stage = [&](int st, int k0) {
     double* as = As + st * P_BK * P_LDA;
     double* bs = Bs + st * P_BK * LDB;
+    if (vecA) {
+#pragma unroll
+      for (int r = 0; r < (P_BM * P_BK) / (2 * P_NT); ++r) {
+        const int e = tid + r * P_NT;
+        const int i = 2 * (e % (P_BM / 2)), l = e / (P_BM / 2);
+        const int gi = m0 + i, gl = k0 + l;
+        const int nv = (gl < K) ? max(0, min(2, M - gi)) : 0;
+        const double* src = A;
+        if (nv) { const long long c = mapA ? __ldg(mapA + gl) : gl; src = A + c * lda + gi; }
+        cp_async16(as + l * P_LDA + i, src, 8 * nv);
+      }
+    } else {
 #pragma unroll
     for (int r = 0; r < (P_BM * P_BK) / P_NT; ++r) {
       const int e = tid + r * P_NT;
@@ -461,6 +491,21 @@ __global__ void __launch_bounds__(P_NT, (BN >= 128 ? 1 : 2)) gemm_pipe_kernel(co
         else { const long long c = mapA ? __ldg(mapA + gi) : gi; src = A + c * lda + gl; }
       }
       cp_async8(as + l * P_LDA + i, src, v);
+    }
+    }
+    if (vecB) {
+#pragma unroll
+      for (int r = 0; r < (P_BK * BN + 2 * P_NT - 1) / (2 * P_NT); ++r) {
+        const int e = tid + r * P_NT;
+        if ((P_BK * BN) % (2 * P_NT) != 0 && e >= P_BK * BN / 2) break;
+        const int j = 2 * (e % (BN / 2)), l = e / (BN / 2);
+        const int gl = k0 + l, gj = n0 + j;
+        const int nv = (gl < K) ? max(0, min(2, N - gj)) : 0;
+        const double* src = B;
+        if (nv) { const long long c = mapB ? __ldg(mapB + gl) : gl; src = B + c * ldb + gj; }
+        cp_async16(bs + l * LDB + j, src, 8 * nv);
+      }
+      return;
     }
 #pragma unroll
     for (int r = 0; r < (P_BK * BN) / P_NT; ++r) {

@@ -209,6 +209,14 @@ struct GOp {
       solve_internal(F, Y, k, tmp.p);
       return;
     }
+    static const bool sym = getenv("RSF_GOP") && std::string(getenv("RSF_GOP")) == "sym";
+    if (sym) {   // G' = L^-1 F_i L^-T (same trace as F^-1 F_i, R-Z variant): 1 solve + 1 apply
+      RSF_CUDA(cudaMemcpyAsync(B.p, X, bytes, cudaMemcpyDeviceToDevice, s));
+      solve_half_bwd(F, B.p, k, tmp.p);
+      apply_only_internal(*Fi, B.p, Y, k);
+      solve_half_fwd(F, Y, k, tmp.p);
+      return;
+    }
     RSF_CUDA(cudaMemcpyAsync(A.p, X, bytes, cudaMemcpyDeviceToDevice, s));
     apply_only_internal(*Fi, A.p, B.p, k);          // B = F_i X
     solve_internal(F, B.p, k, tmp.p);               // B = F^-1 F_i X
@@ -500,9 +508,12 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
         }
         // sketch Y'_g = ((G - sum_{m<l} G^(m)) W_g)^T in chunks of kb probe columns;
         // every chunk extends the bases V_i of the boxes that see it
-        DBuf<double> W((size_t)n * std::min(kb, c), s), Y((size_t)n * std::min(kb, c), s);
-        for (int c0 = 0; c0 < c; c0 += kb) {
-          const int k = std::min(kb, c - c0);
+        // equal chunks of <= kb columns (multiple of 8) instead of kb-wide chunks plus a thin tail
+        const int nch = (c + kb - 1) / kb;
+        const int kc = std::min(kb, ((c + nch - 1) / nch + 7) / 8 * 8);
+        DBuf<double> W((size_t)n * kc, s), Y((size_t)n * kc, s);
+        for (int c0 = 0; c0 < c; c0 += kc) {
+          const int k = std::min(kc, c - c0);
           gen_probes(s, W.p, k, n, t.d_perm.p, qmap.p, g, c0, lev, trace_id, seed);
           residual(W.p, Y.p, k, lev);
           RSF_PHASE("p.basis", s);
@@ -568,10 +579,10 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
               pcp.push_back(CopyProb{P.p + po[xa] + (long long)c * c0, c, Pr.p + pro[x], c, c, k, 1.0});
             }
             RSF_LAUNCH_CHECK();
-            gp.run(s);
-            launch_colmax(s, cm);
-            copy_batched(s, pcp);
-            gc.run(s); gr.run(s); gpr.run(s);
+            { RSF_PHASE("b.sketchP", s); gp.run(s); launch_colmax(s, cm); copy_batched(s, pcp); }
+            { RSF_PHASE("b.project", s); gc.run(s); gr.run(s); gpr.run(s); }
+            PhaseSeq pseq(s);
+            pseq.next("b.rrqr");
             std::vector<RRQRProb> rp;
             for (size_t x = 0; x < B; ++x) {
               RRQRProb r{Pr.p + pro[x], c, c, k, pivr.p + (long long)x * k, nullptr, nullptr, 0};
@@ -580,6 +591,7 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
             }
             std::vector<int> qq = rrqr_batched(s, rp, o.eps_peel,
                                                seed ^ (0x9E3779B97F4A7C15ull * (unsigned long long)(lev + 64 * (trace_id + 3) + 4096 * c0))).k;
+            pseq.next("b.orth");
             // new orthonormal directions Q_i = orth(Res(:, pivr[0:q])), re-orthogonalized against V_i
             long long qt = 0, rt = 0;
             std::vector<long long> qo(B), ro(B);
@@ -656,6 +668,7 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
               nA[x].alloc((size_t)c * (rb[i] + qq[x]), s);
               pd.flops += 4.0 * c * (double)qq[x] * bx[i].ni;
             }
+            pseq.next("b.grow");
             copy_batched(s, cc1);
             gcq.run(s);
             GemmBatch gan(false, false);
@@ -745,6 +758,8 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
             tz.push_back(TrsmProb{Pc.p + po[xa], c, Ri2.p + go[x], k, k, k});
             mz = std::max(mz, (long long)rb[i] * k);
           }
+          PhaseSeq cseq(s);
+          cseq.next("c.z");
           launch_descs(s, gz, mz, gather_t_kernel);
           launch_descs(s, ez, mz, eye_kernel);
           trsm_upper_batched(s, tz);
@@ -787,6 +802,7 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
             gt3.add(h);
             pd.flops += 2.0 * c * (double)k * rb[i] + 4.0 * k * (double)c * c;
           }
+          cseq.next("c.xlm");
           gx.run(s);
           gg.run(s);
           {

@@ -640,6 +640,46 @@ void solve_internal(const Fact& F, double* X, int k, double* tmp) {
   }
 }
 
+// F = L L^T with L = M_L ... M_1 C: the two halves of the solve
+// x <- L^-1 x (forward sweeps, then C^-1) and x <- L^-T x (C^-T, then backward sweeps)
+void solve_half_fwd(const Fact& F, double* X, int k, double* tmp) {
+  RSF_REQUIRE(F.which == W_SIGMA, ST_EINVAL, "solve needs a Sigma factor");
+  cudaStream_t s = F.ctx->stream;
+  for (int lev = F.tree->L; lev >= 1; --lev) {
+    const Level& LV = F.levels[lev];
+    RSF_PHASE(lvname("sv", lev), s);
+    if (LV.fused) { sweep_level(s, LV.ops.p, LV.nops, LV.max_i, SW_SOLVE_FWD, X, nullptr, k); continue; }
+    LV.fs1.run(s, X, tmp, k, k);
+    LV.fs2.run(s, X, tmp, k, k);
+    LV.fs3.run(s, X, tmp, k, k);
+    colcopy(s, X, tmp, k, k, LV.R.p, nullptr, LV.rtot);
+  }
+  if (F.n0 > 0) {
+    RSF_PHASE("sv.top", s);
+    F.top_s1.run(s, X, tmp, k, k);                        // tmp = X(I0) C^-T
+    colcopy(s, X, tmp, k, k, F.I0.p, nullptr, F.n0);      // X(I0) = tmp
+  }
+}
+
+void solve_half_bwd(const Fact& F, double* X, int k, double* tmp) {
+  RSF_REQUIRE(F.which == W_SIGMA, ST_EINVAL, "solve needs a Sigma factor");
+  cudaStream_t s = F.ctx->stream;
+  if (F.n0 > 0) {
+    RSF_PHASE("sv.top", s);
+    colcopy(s, tmp, X, k, k, nullptr, F.I0.p, F.n0);      // tmp = X(I0)
+    F.top_s2.run(s, X, tmp, k, k);                        // X(I0) = tmp C^-1
+  }
+  for (int lev = 1; lev <= F.tree->L; ++lev) {
+    const Level& LV = F.levels[lev];
+    RSF_PHASE(lvname("sv", lev), s);
+    if (LV.fused) { sweep_level(s, LV.ops.p, LV.nops, LV.max_i, SW_SOLVE_BWD, X, nullptr, k); continue; }
+    colcopy(s, tmp, X, k, k, nullptr, LV.R.p, LV.rtot);
+    LV.bs2.run(s, X, tmp, k, k);
+    LV.bs3.run(s, X, tmp, k, k);
+    LV.bs4.run(s, X, tmp, k, k);
+  }
+}
+
 static void down_sweep(const Fact& F, double* X, int k, double* tmp) {
   cudaStream_t s = F.ctx->stream;
   for (int lev = 1; lev <= F.tree->L; ++lev) {

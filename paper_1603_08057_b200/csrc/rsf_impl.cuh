@@ -116,6 +116,9 @@ std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams
 
 // operations on X' (k x n column-major, tree order, ld = k): in place
 void solve_internal(const Fact& F, double* X, int k, double* tmp);
+// halves of the solve for F = L L^T: X <- L^-1 X (fwd) and X <- L^-T X (bwd)
+void solve_half_fwd(const Fact& F, double* X, int k, double* tmp);
+void solve_half_bwd(const Fact& F, double* X, int k, double* tmp);
 void apply_internal(const Fact& F, double* X, int k, double* tmp);
 void sqrt_internal(const Fact& F, double* X, int k, double* tmp);
 // apply-only Sigma_i: Y = F_i X (X is overwritten)

@@ -26,7 +26,7 @@ struct BoxOp {
 
 enum SweepKind { SW_SOLVE_FWD = 0, SW_SOLVE_BWD = 1, SW_AO_UP = 2, SW_AO_DN = 3 };
 
-constexpr int SWEEP_MAX_I = 256;   // largest |I_b| handled by the fused kernel
+constexpr int SWEEP_MAX_I = 128;   // largest |I_b| handled by the fused kernel (measured: slower than the GEMM path above)
 
 // X0: the operand updated in place (solve: X'; apply-only: x'), X1: apply-only output y'.
 // ldx = k (number of right-hand sides, X' is k x n column-major).

@@ -309,8 +309,8 @@ ctx = R.Context(0)
 K = R.Kernel(c.family, c.rho, c.sigma2, c.nugget, c.alpha, c.theta)
 F = R.Factor(ctx, torch.from_numpy(xy).to(dev), K, 1e-8, 32)
 Fi = R.Factor(ctx, torch.from_numpy(xy).to(dev), K, 1e-8, 32, which=0)
-B = torch.from_numpy(np.random.default_rng(11).standard_normal((n, 40))).to(dev)
-np.save(sys.argv[2], np.concatenate([F.solve(B.clone()).cpu().numpy(), Fi.apply(B.clone()).cpu().numpy()], axis=1))
+B = torch.from_numpy(np.random.default_rng(11).standard_normal((40, n))).to(dev)
+np.save(sys.argv[2], np.concatenate([F.solve(B.clone()).cpu().numpy(), Fi.apply(B.clone()).cpu().numpy()], axis=0))
 """
 
 
