@@ -158,6 +158,10 @@ int64_t rsf_kernel_launches(void);
 /* phase timings "name=seconds;..." collected when RSF_PROFILE=1 (stream-synchronising; diagnostics only) */
 const char* rsf_profile_dump(void);
 void rsf_profile_reset(void);
+/* launch trace "phase|file:line=seconds,launches;..." collected when RSF_KTRACE=1: an event after every
+ * launch on the evaluation stream, the time between consecutive events attributed to the launch site
+ * (diagnostics only; resets with rsf_profile_reset) */
+const char* rsf_trace_dump(void);
 /* batched-GEMM statistics for the roofline: CUDA events around every launch on its stream.
  * rsf_stats_get fills {launches, seconds, algorithmic flops, compulsory bytes}. */
 void rsf_stats_enable(int on);

@@ -55,7 +55,7 @@ EXPORTS = ["rsf_opts_default", "rsf_ctx_create", "rsf_ctx_destroy", "rsf_factor"
            "rsf_fact_info", "rsf_logdet", "rsf_solve", "rsf_apply", "rsf_sample", "peel_trace",
            "gp_mle_eval", "rsf_last_error", "rsf_kernel_launches", "rsf_profile_dump",
            "rsf_profile_reset", "rsf_stats_enable", "rsf_stats_get", "rsf_stats_reset",
-           "rsf_debug_gemm_bench", "rsf_debug_fp64_peak"]
+           "rsf_debug_gemm_bench", "rsf_debug_fp64_peak", "rsf_trace_dump"]
 
 
 def load(path: str = LIB_PATH) -> C.CDLL:
@@ -86,6 +86,8 @@ def load(path: str = LIB_PATH) -> C.CDLL:
     lib.rsf_kernel_launches.restype = C.c_int64
     lib.rsf_profile_dump.argtypes = []
     lib.rsf_profile_dump.restype = C.c_char_p
+    lib.rsf_trace_dump.argtypes = []
+    lib.rsf_trace_dump.restype = C.c_char_p
     lib.rsf_profile_reset.argtypes = []
     lib.rsf_profile_reset.restype = None
     lib.rsf_stats_enable.argtypes = [C.c_int]
@@ -102,6 +104,6 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         if f not in ("rsf_ctx_destroy", "rsf_fact_destroy", "rsf_opts_default", "rsf_last_error",
                      "rsf_kernel_launches", "rsf_profile_dump", "rsf_profile_reset", "rsf_stats_enable",
                      "rsf_stats_get", "rsf_stats_reset", "rsf_debug_gemm_bench",
-                     "rsf_debug_fp64_peak"):
+                     "rsf_debug_fp64_peak", "rsf_trace_dump"):
             getattr(lib, f).restype = C.c_int
     return lib

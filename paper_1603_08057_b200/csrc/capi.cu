@@ -175,6 +175,8 @@ rsf_status rsf_ctx_create(int device, void* cuda_stream, void* nccl_comm, rsf_ct
 void rsf_ctx_destroy(rsf_ctx ctx) {
   if (!ctx) return;
   cudaStreamSynchronize(ctx->ctx.stream);
+  rsf::dev_cache_trim(ctx->ctx.stream);
+  cudaStreamSynchronize(ctx->ctx.stream);
   if (ctx->ctx.own_stream) cudaStreamDestroy(ctx->ctx.stream);
   delete ctx;
 }
@@ -335,7 +337,13 @@ const char* rsf_profile_dump(void) {
   s = rsf::Prof::dump();
   return s.c_str();
 }
-void rsf_profile_reset(void) { rsf::Prof::reset(); }
+void rsf_profile_reset(void) { rsf::Prof::reset(); rsf::KTrace::reset(); }
+
+const char* rsf_trace_dump(void) {
+  static thread_local std::string s;
+  s = rsf::KTrace::dump();
+  return s.c_str();
+}
 
 double rsf_debug_gemm_bench(int M, int N, int K, int batch, int ta, int tb, int reps) {
   // diagnostics: TFLOP/s of the batched FP64 GEMM on `batch` independent M x N x K problems

@@ -35,6 +35,18 @@ struct Error : std::runtime_error {
     if (!(cond)) throw ::rsf::Error(code, msg); \
   } while (0)
 
+// host seconds spent inside allocation / free / upload calls (diagnostics, RSF_KTRACE=1)
+double host_clock();
+extern double g_host_alloc, g_host_free, g_host_upload;
+extern long long g_n_alloc;
+
+// Size-class cache over cudaMallocAsync for buffers <= 64 MB (per stream: a block freed on a
+// stream is reusable by later work on the same stream, exactly like the stream-ordered pool,
+// without a driver call).  Larger buffers go to cudaMallocAsync directly.
+void* dev_alloc(size_t bytes, cudaStream_t s);
+void dev_free(void* p, size_t bytes, cudaStream_t s);
+void dev_cache_trim(cudaStream_t s);   // release the cached blocks of a stream
+
 // Stream-ordered device buffer (cudaMallocAsync on the context stream; the
 // default memory pool keeps freed blocks cached for the next evaluation).
 template <class T>
@@ -56,17 +68,28 @@ struct DBuf {
     release();
     s = st;
     n = count;
-    if (count) RSF_CUDA(cudaMallocAsync((void**)&p, count * sizeof(T), st));
+    if (count) {
+      const double t0 = host_clock();
+      p = static_cast<T*>(dev_alloc(count * sizeof(T), st));
+      g_host_alloc += host_clock() - t0;
+      ++g_n_alloc;
+    }
   }
   void release() {
-    if (p) cudaFreeAsync(p, s);
+    if (p) {
+      const double t0 = host_clock();
+      dev_free(p, n * sizeof(T), s);
+      g_host_free += host_clock() - t0;
+    }
     p = nullptr;
     n = 0;
   }
   void zero() { if (n) RSF_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s)); }
   void upload(const T* h, size_t count) {
     if (count > n) alloc(count, s);
+    const double t0 = host_clock();
     if (count) RSF_CUDA(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+    g_host_upload += host_clock() - t0;
   }
   void upload(const std::vector<T>& v) { upload(v.data(), v.size()); }
   void download(T* h, size_t count) const {
@@ -80,10 +103,37 @@ struct DBuf {
   }
 };
 
+// Transient upload ring (per stream): small host arrays that live only until the kernels
+// reading them have run (launch descriptors).  Data goes host -> pinned staging ring ->
+// device ring with one truly asynchronous copy; when the ring wraps the stream is
+// synchronised first, so every earlier reader has finished.  Replaces a cudaMallocAsync
+// plus a pageable (host-blocking) copy per launch.
+void* ring_upload(cudaStream_t s, const void* h, size_t bytes);
+template <class T>
+struct RPtr { T* p; };
+template <class T>
+RPtr<T> ring_up(const std::vector<T>& v, cudaStream_t s) {
+  return RPtr<T>{static_cast<T*>(ring_upload(s, v.data(), v.size() * sizeof(T)))};
+}
+
 // kernel launch counter (diagnostics: the bench reports how many of our
 // kernels ran inside the timed region)
 extern thread_local long long g_launches;
-inline void count_launch(long long k = 1) { g_launches += k; }
+// Launch trace (diagnostics, RSF_KTRACE=1): an event after every launch on the traced
+// stream; the time between consecutive events is attributed to (current phase, launch site).
+struct KTrace {
+  static bool on();
+  static void mark(const char* file, int line);
+  static void set_stream(cudaStream_t s);
+  static std::string dump();   // "phase|file:line=seconds,count;..." (synchronises)
+  static void reset();
+  static const char*& phase();   // current phase label (set by PhaseTimer / PhaseSeq)
+};
+inline void count_launch_at(const char* file, int line, long long k = 1) {
+  g_launches += k;
+  if (KTrace::on()) KTrace::mark(file, line);
+}
+#define count_launch(...) ::rsf::count_launch_at(__FILE__, __LINE__ __VA_OPT__(, ) __VA_ARGS__)
 
 // Phase profiler (enabled by RSF_PROFILE=1): synchronises the stream at the
 // scope boundaries and accumulates wall time per named phase.
@@ -98,6 +148,7 @@ struct PhaseTimer {
   cudaStream_t s;
   double t0 = 0;
   bool on;
+  const char* prev_phase;
   PhaseTimer(const char* n, cudaStream_t st);
   ~PhaseTimer();
 };
@@ -107,6 +158,7 @@ struct PhaseSeq {
   const char* name = nullptr;
   double t0 = 0;
   bool on;
+  const char* prev_phase;
   explicit PhaseSeq(cudaStream_t st);
   void next(const char* n);
   ~PhaseSeq() { next(nullptr); }

@@ -421,10 +421,8 @@ __global__ void copy_kernel(const CopyProb* __restrict__ descs) {
 }
 
 template <class D>
-DBuf<D> upload_descs(const std::vector<D>& v, cudaStream_t s) {
-  DBuf<D> b(v.size(), s);
-  b.upload(v);
-  return b;
+RPtr<D> upload_descs(const std::vector<D>& v, cudaStream_t s) {
+  return ring_up(v, s);
 }
 
 int grid_x_for(long long maxelems) {

@@ -4,6 +4,9 @@
 // of the next K-slab overlaps the FMA loop.
 #include <ctime>
 #include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
 
 #include "gemm.cuh"
 
@@ -24,6 +27,82 @@ double wall() {
 }  // namespace
 
 bool KStats::on = false;
+
+// ---------------------------------------------------------------- device allocation cache
+namespace {
+constexpr size_t CACHE_MAX = size_t(64) << 20;
+struct FreeList { cudaStream_t s; int bin; std::vector<void*> blocks; };
+std::mutex& cache_mu() { static std::mutex m; return m; }
+std::vector<FreeList>& cache() { static std::vector<FreeList> v; return v; }
+int bin_of(size_t bytes) { int b = 8; while ((size_t(1) << b) < bytes) ++b; return b; }   // >= 256 B
+}  // namespace
+void* dev_alloc(size_t bytes, cudaStream_t s) {
+  void* p = nullptr;
+  if (bytes > CACHE_MAX) {
+    RSF_CUDA(cudaMallocAsync(&p, bytes, s));
+    return p;
+  }
+  const int b = bin_of(bytes);
+  {
+    std::lock_guard<std::mutex> lk(cache_mu());
+    for (auto& f : cache())
+      if (f.s == s && f.bin == b && !f.blocks.empty()) { p = f.blocks.back(); f.blocks.pop_back(); return p; }
+  }
+  RSF_CUDA(cudaMallocAsync(&p, size_t(1) << b, s));
+  return p;
+}
+void dev_cache_trim(cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(cache_mu());
+  for (auto& f : cache())
+    if (f.s == s) { for (void* p : f.blocks) cudaFreeAsync(p, s); f.blocks.clear(); }
+}
+void dev_free(void* p, size_t bytes, cudaStream_t s) {
+  if (!p) return;
+  if (bytes > CACHE_MAX) { cudaFreeAsync(p, s); return; }
+  const int b = bin_of(bytes);
+  std::lock_guard<std::mutex> lk(cache_mu());
+  for (auto& f : cache())
+    if (f.s == s && f.bin == b) { f.blocks.push_back(p); return; }
+  cache().push_back(FreeList{s, b, {p}});
+}
+
+// ---------------------------------------------------------------- upload ring
+namespace {
+struct Ring { char* dev = nullptr; char* host = nullptr; size_t cap = 0, off = 0; };
+std::mutex& ring_mu() { static std::mutex m; return m; }
+std::vector<std::pair<cudaStream_t, Ring>>& rings() { static std::vector<std::pair<cudaStream_t, Ring>> v; return v; }
+}  // namespace
+void* ring_upload(cudaStream_t s, const void* h, size_t bytes) {
+  std::lock_guard<std::mutex> lk(ring_mu());
+  Ring* r = nullptr;
+  for (auto& x : rings()) if (x.first == s) { r = &x.second; break; }
+  if (!r) { rings().emplace_back(s, Ring{}); r = &rings().back().second; }
+  const size_t need = (std::max<size_t>(bytes, 1) + 255) / 256 * 256;
+  if (need > r->cap / 2) {   // (re)size: previous contents may still be read -> synchronise first
+    RSF_CUDA(cudaStreamSynchronize(s));
+    if (r->dev) { cudaFree(r->dev); cudaFreeHost(r->host); }
+    r->cap = std::max<size_t>(size_t(64) << 20, 4 * need);
+    RSF_CUDA(cudaMalloc((void**)&r->dev, r->cap));
+    RSF_CUDA(cudaMallocHost((void**)&r->host, r->cap));
+    r->off = 0;
+  }
+  if (r->off + need > r->cap) {   // wrap: every earlier reader must have run
+    RSF_CUDA(cudaStreamSynchronize(s));
+    r->off = 0;
+  }
+  const double t0 = host_clock();
+  if (bytes) {
+    std::memcpy(r->host + r->off, h, bytes);
+    RSF_CUDA(cudaMemcpyAsync(r->dev + r->off, r->host + r->off, bytes, cudaMemcpyHostToDevice, s));
+  }
+  g_host_upload += host_clock() - t0;
+  void* out = r->dev + r->off;
+  r->off += need;
+  return out;
+}
+double g_host_alloc = 0, g_host_free = 0, g_host_upload = 0;
+long long g_n_alloc = 0;
+double host_clock() { return wall(); }
 namespace {
 struct KRec { cudaEvent_t a, b; double flops, bytes; };
 std::vector<KRec>& krecs() { static std::vector<KRec> v; return v; }
@@ -79,10 +158,13 @@ std::string Prof::dump() {
 }
 void Prof::reset() { prof_table().clear(); }
 PhaseTimer::PhaseTimer(const char* n, cudaStream_t st) : name(n), s(st), on(Prof::enabled()) {
+  prev_phase = KTrace::phase();
+  KTrace::phase() = n;
   if (on) { cudaStreamSynchronize(s); t0 = wall(); }
 }
-PhaseSeq::PhaseSeq(cudaStream_t st) : s(st), on(Prof::enabled()) {}
+PhaseSeq::PhaseSeq(cudaStream_t st) : s(st), on(Prof::enabled()) { prev_phase = KTrace::phase(); }
 void PhaseSeq::next(const char* n) {
+  KTrace::phase() = n ? n : prev_phase;
   if (!on) return;
   cudaStreamSynchronize(s);
   const double t = wall();
@@ -91,8 +173,68 @@ void PhaseSeq::next(const char* n) {
   t0 = t;
 }
 PhaseTimer::~PhaseTimer() {
+  KTrace::phase() = prev_phase;
   if (on) { cudaStreamSynchronize(s); Prof::add(name, wall() - t0); }
 }
+
+// ---------------------------------------------------------------- launch trace
+namespace {
+struct TRec { cudaEvent_t e; const char* phase; const char* file; int line; double host; };
+std::vector<TRec>& trecs() { static std::vector<TRec> v; return v; }
+std::vector<cudaEvent_t>& tpool() { static std::vector<cudaEvent_t> v; return v; }
+cudaStream_t& tstream() { static cudaStream_t s = 0; return s; }
+struct TAgg { double sec = 0, host = 0; long long cnt = 0; };
+double t_last_host = 0;
+std::vector<std::pair<std::string, TAgg>>& tagg() { static std::vector<std::pair<std::string, TAgg>> v; return v; }
+cudaEvent_t t_last = nullptr;
+void tdrain() {
+  auto& r = trecs();
+  if (r.empty()) return;
+  cudaEventSynchronize(r.back().e);
+  for (auto& x : r) {
+    float ms = 0.f;
+    if (t_last) cudaEventElapsedTime(&ms, t_last, x.e);
+    std::string key = std::string(x.phase ? x.phase : "-") + "|" + x.file + ":" + std::to_string(x.line);
+    auto& a = tagg();
+    size_t i = 0;
+    for (; i < a.size(); ++i) if (a[i].first == key) break;
+    if (i == a.size()) a.emplace_back(key, TAgg{});
+    a[i].second.sec += ms * 1e-3;
+    a[i].second.host += t_last_host > 0 ? x.host - t_last_host : 0.0;
+    a[i].second.cnt += 1;
+    t_last_host = x.host;
+    if (t_last) tpool().push_back(t_last);
+    t_last = x.e;
+  }
+  r.clear();
+}
+}  // namespace
+bool KTrace::on() {
+  static int e = -1;
+  if (e < 0) { const char* v = getenv("RSF_KTRACE"); e = (v && v[0] == '1') ? 1 : 0; }
+  return e == 1;
+}
+const char*& KTrace::phase() { static thread_local const char* p = nullptr; return p; }
+void KTrace::set_stream(cudaStream_t s) { tstream() = s; }
+void KTrace::mark(const char* file, int line) {
+  cudaEvent_t e;
+  if (!tpool().empty()) { e = tpool().back(); tpool().pop_back(); }
+  else cudaEventCreate(&e);
+  const char* f = strrchr(file, '/');
+  cudaEventRecord(e, tstream());
+  trecs().push_back(TRec{e, phase(), f ? f + 1 : file, line, wall()});
+  if (trecs().size() > 8192) tdrain();
+}
+std::string KTrace::dump() {
+  tdrain();
+  std::string r = "host-alloc|n=" + std::to_string(g_n_alloc) + "=" + std::to_string(g_host_alloc) + ",1,0;" +
+                  "host-free|=" + std::to_string(g_host_free) + ",1,0;host-upload|=" + std::to_string(g_host_upload) + ",1,0;";
+  for (auto& a : tagg())
+    r += a.first + "=" + std::to_string(a.second.sec) + "," + std::to_string(a.second.cnt) + "," +
+         std::to_string(a.second.host) + ";";
+  return r;
+}
+void KTrace::reset() { tdrain(); tagg().clear(); g_host_alloc = g_host_free = g_host_upload = 0; g_n_alloc = 0; }
 
 namespace {
 
@@ -433,7 +575,9 @@ template <int BN> constexpr size_t p_smem() { return (size_t)P_ST * P_BK * (P_LD
 template <bool TA, bool TB, int BN>
 __global__ void __launch_bounds__(P_NT, (BN >= 128 ? 1 : 2)) gemm_pipe_kernel(const GemmDesc* __restrict__ descs,
                                                             const int* __restrict__ prefix, int nprob,
-                                                            double* X0, double* X1, int ldx, int Mglob) {
+                                                            double* X0, double* X1, int ldx, int Mglob,
+                                                            double* ws, const long long* __restrict__ mnpre,
+                                                            int kchunk) {
   constexpr int LDB = p_ldb<BN>(), NI = BN / 16, WN = BN / 2;
   extern __shared__ __align__(16) double psm[];
   double* As = psm;                              // [ST][BK][LDA]
@@ -455,6 +599,7 @@ __global__ void __launch_bounds__(P_NT, (BN >= 128 ? 1 : 2)) gemm_pipe_kernel(co
   const int* mapA = dd.mapA;
   const int* mapB = dd.mapB;
   const int* mapC = dd.mapC;
+  const int* mapK = dd.mapK;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, tq = lane & 3;
   const int wm = warp & 3, wn = warp >> 2;
@@ -474,7 +619,11 @@ __global__ void __launch_bounds__(P_NT, (BN >= 128 ? 1 : 2)) gemm_pipe_kernel(co
         const int gi = m0 + i, gl = k0 + l;
         const int nv = (gl < K) ? max(0, min(2, M - gi)) : 0;
         const double* src = A;
-        if (nv) { const long long c = mapA ? __ldg(mapA + gl) : gl; src = A + c * lda + gi; }
+        if (nv) {
+          const int kx = mapK ? __ldg(mapK + gl) : gl;
+          const long long c = mapA ? __ldg(mapA + kx) : kx;
+          src = A + c * lda + gi;
+        }
         cp_async16(as + l * P_LDA + i, src, 8 * nv);
       }
     } else {
@@ -487,8 +636,9 @@ __global__ void __launch_bounds__(P_NT, (BN >= 128 ? 1 : 2)) gemm_pipe_kernel(co
       const bool v = gi < M && gl < K;
       const double* src = A;
       if (v) {
-        if (!TA) { const long long c = mapA ? __ldg(mapA + gl) : gl; src = A + c * lda + gi; }
-        else { const long long c = mapA ? __ldg(mapA + gi) : gi; src = A + c * lda + gl; }
+        const int kx = mapK ? __ldg(mapK + gl) : gl;
+        if (!TA) { const long long c = mapA ? __ldg(mapA + kx) : kx; src = A + c * lda + gi; }
+        else { const long long c = mapA ? __ldg(mapA + gi) : gi; src = A + c * lda + kx; }
       }
       cp_async8(as + l * P_LDA + i, src, v);
     }
@@ -502,7 +652,11 @@ __global__ void __launch_bounds__(P_NT, (BN >= 128 ? 1 : 2)) gemm_pipe_kernel(co
         const int gl = k0 + l, gj = n0 + j;
         const int nv = (gl < K) ? max(0, min(2, N - gj)) : 0;
         const double* src = B;
-        if (nv) { const long long c = mapB ? __ldg(mapB + gl) : gl; src = B + c * ldb + gj; }
+        if (nv) {
+          const int kx = mapK ? __ldg(mapK + gl) : gl;
+          const long long c = mapB ? __ldg(mapB + kx) : kx;
+          src = B + c * ldb + gj;
+        }
         cp_async16(bs + l * LDB + j, src, 8 * nv);
       }
       return;
@@ -516,8 +670,9 @@ __global__ void __launch_bounds__(P_NT, (BN >= 128 ? 1 : 2)) gemm_pipe_kernel(co
       const bool v = gl < K && gj < N;
       const double* src = B;
       if (v) {
-        if (!TB) { const long long c = mapB ? __ldg(mapB + gj) : gj; src = B + c * ldb + gl; }
-        else { const long long c = mapB ? __ldg(mapB + gl) : gl; src = B + c * ldb + gj; }
+        const int kx = mapK ? __ldg(mapK + gl) : gl;
+        if (!TB) { const long long c = mapB ? __ldg(mapB + gj) : gj; src = B + c * ldb + kx; }
+        else { const long long c = mapB ? __ldg(mapB + kx) : kx; src = B + c * ldb + gj; }
       }
       cp_async8(bs + l * LDB + j, src, v);
     }
@@ -530,9 +685,13 @@ __global__ void __launch_bounds__(P_NT, (BN >= 128 ? 1 : 2)) gemm_pipe_kernel(co
     for (int b = 0; b < NI; ++b) { acc[a][b][0] = 0.0; acc[a][b][1] = 0.0; }
 
   // K range of the nonzero rows of op(B) for this N tile (triangular B: TRMM-style skipping)
-  const int kbeg = dd.btri == 1 ? min(n0, K) : 0;
-  const int kend = dd.btri == 2 ? min(K, n0 + BN) : K;
-  const int nk = (kend - kbeg + P_BK - 1) / P_BK;
+  int kbeg = dd.btri == 1 ? min(n0, K) : 0;
+  int kend = dd.btri == 2 ? min(K, n0 + BN) : K;
+  if (ws) {   // split-K: this CTA's slice of K, partial product to the workspace
+    kbeg = max(kbeg, (int)blockIdx.z * kchunk);
+    kend = min(kend, ((int)blockIdx.z + 1) * kchunk);
+  }
+  const int nk = kend > kbeg ? (kend - kbeg + P_BK - 1) / P_BK : 0;
 #pragma unroll
   for (int st = 0; st < P_ST - 1; ++st) {
     if (st < nk) load_stage(st, kbeg + st * P_BK);
@@ -563,6 +722,22 @@ __global__ void __launch_bounds__(P_NT, (BN >= 128 ? 1 : 2)) gemm_pipe_kernel(co
     }
   }
   cp_async_wait<0>();
+  if (ws) {
+    double* W = ws + (long long)gridDim.z * mnpre[p] + (long long)blockIdx.z * M * N;
+#pragma unroll
+    for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int gj = n0 + wn * WN + ni * 8 + 2 * tq + h;
+        if (gj >= N) continue;
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) {
+          const int gi = m0 + wm * 32 + mi * 8 + g;
+          if (gi < M) W[(long long)gj * M + gi] = acc[mi][ni][h];
+        }
+      }
+    return;
+  }
   const double alpha = dd.alpha, beta = dd.beta;
 #pragma unroll
   for (int ni = 0; ni < NI; ++ni) {
@@ -586,7 +761,8 @@ __global__ void __launch_bounds__(P_NT, (BN >= 128 ? 1 : 2)) gemm_pipe_kernel(co
 
 template <int BN>
 void launch_pipe(bool ta, bool tb, dim3 grid, cudaStream_t s, const GemmDesc* d, const int* pre, int np,
-                 double* X0, double* X1, int ldx, int Mg) {
+                 double* X0, double* X1, int ldx, int Mg, double* ws = nullptr, const long long* mnpre = nullptr,
+                 int kchunk = 0) {
   static bool attr = false;
   constexpr size_t SM = p_smem<BN>();
   if (!attr) {
@@ -596,10 +772,31 @@ void launch_pipe(bool ta, bool tb, dim3 grid, cudaStream_t s, const GemmDesc* d,
     cudaFuncSetAttribute(gemm_pipe_kernel<true, true, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
     attr = true;
   }
-  if (!ta && !tb) gemm_pipe_kernel<false, false, BN><<<grid, P_NT, SM, s>>>(d, pre, np, X0, X1, ldx, Mg);
-  else if (ta && !tb) gemm_pipe_kernel<true, false, BN><<<grid, P_NT, SM, s>>>(d, pre, np, X0, X1, ldx, Mg);
-  else if (!ta && tb) gemm_pipe_kernel<false, true, BN><<<grid, P_NT, SM, s>>>(d, pre, np, X0, X1, ldx, Mg);
-  else gemm_pipe_kernel<true, true, BN><<<grid, P_NT, SM, s>>>(d, pre, np, X0, X1, ldx, Mg);
+  if (!ta && !tb) gemm_pipe_kernel<false, false, BN><<<grid, P_NT, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk);
+  else if (ta && !tb) gemm_pipe_kernel<true, false, BN><<<grid, P_NT, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk);
+  else if (!ta && tb) gemm_pipe_kernel<false, true, BN><<<grid, P_NT, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk);
+  else gemm_pipe_kernel<true, true, BN><<<grid, P_NT, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk);
+}
+
+// split-K reduction: C = alpha * sum_z W_z + beta * C (fixed summation order: deterministic)
+__global__ void splitk_reduce_kernel(const GemmDesc* __restrict__ descs, const double* __restrict__ ws,
+                                     const long long* __restrict__ mnpre, int S, int p0,
+                                     double* X0, double* X1, int ldx, int Mglob) {
+  const int p = p0 + blockIdx.y;
+  const GemmDesc& dd = descs[p];
+  const int M = dd.M < 0 ? Mglob : dd.M, N = dd.N;
+  const long long MN = (long long)M * N;
+  double* C = dd.selC == 0 ? dd.C + dd.offC : (dd.selC == 1 ? X0 : X1) + dd.offC * (long long)ldx;
+  const long long ldc = dd.selC ? ldx : dd.ldc;
+  const double* W = ws + (long long)S * mnpre[p];
+  for (long long e = blockIdx.x * (long long)P_NT + threadIdx.x; e < MN; e += (long long)gridDim.x * P_NT) {
+    double v = 0.0;
+    for (int z = 0; z < S; ++z) v += W[(long long)z * MN + e];
+    const int i = (int)(e % M), j = (int)(e / M);
+    const long long cc = dd.mapC ? __ldg(dd.mapC + j) : j;
+    double* c = C + cc * ldc + i;
+    *c = dd.beta != 0.0 ? fma(dd.beta, *c, dd.alpha * v) : dd.alpha * v;
+  }
 }
 
 int gemm_mode() {
@@ -621,10 +818,25 @@ bool use_dmma() {
 }  // namespace
 
 void GemmBatch::finalize(cudaStream_t s) const {
+  finalize_meta();
+  d_.alloc(h_.size(), s);
+  d_.upload(h_);
+  prefix_.alloc(pre_.size(), s);
+  prefix_.upload(pre_);
+  dp_ = d_.p;
+  pp_ = prefix_.p;
+  ready_ = true;
+}
+
+void GemmBatch::finalize_meta() const {
   const size_t P = h_.size();
-  std::vector<int> pre(3 * (P + 1), 0);   // tile prefix sums for BN = 64, 32, 128
+  std::vector<int>& pre = pre_;
+  pre.assign(3 * (P + 1), 0);             // tile prefix sums for BN = 64, 32, 128
   maxM_ = 0;
   maxN_ = 0;
+  maxK_ = 0;
+  has_lower_ = false;
+  has_mapk_ = false;
   glob_ = false;
   const int bns[3] = {64, 32, 128};
   for (size_t i = 0; i < P; ++i) {
@@ -635,48 +847,88 @@ void GemmBatch::finalize(cudaStream_t s) const {
     }
     if (d.M < 0) glob_ = true; else maxM_ = std::max(maxM_, d.M);
     maxN_ = std::max(maxN_, d.N);
+    maxK_ = std::max(maxK_, d.K);
+    has_lower_ = has_lower_ || d.lower;
+    has_mapk_ = has_mapk_ || d.mapK;
   }
   totalN_ = pre[P];
   totalN32_ = pre[(P + 1) + P];
   totalN128_ = pre[2 * (P + 1) + P];
-  d_.alloc(P, s);
-  d_.upload(h_);
-  prefix_.alloc(pre.size(), s);
-  prefix_.upload(pre);
-  ready_ = true;
 }
 
 void GemmBatch::run(cudaStream_t s, double* X0, double* X1, int ldx, int Mglob) const {
   if (h_.empty()) return;
-  if (!ready_) finalize(s);
+  if (!ready_) {   // transient batch: descriptors through the upload ring (no allocation)
+    finalize_meta();
+    dp_ = static_cast<const GemmDesc*>(ring_upload(s, h_.data(), h_.size() * sizeof(GemmDesc)));
+    pp_ = static_cast<const int*>(ring_upload(s, pre_.data(), pre_.size() * sizeof(int)));
+  }
   if (totalN_ == 0) return;
   int M = std::max(maxM_, glob_ ? Mglob : 0);
   if (M <= 0) return;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (KStats::on) KStats::record(s, &e0, nullptr);
-  if (M <= 16) {
+  if (M <= 16 && !has_mapk_) {   // (only the pipelined kernel implements mapK)
     dim3 grid(totalN_, ceil_div(M, 16));
-    launch_variant<16, 1>(ta_, tb_, grid, s, d_.p, prefix_.p, (int)h_.size(), X0, X1, ldx, Mglob);
-  } else if (gemm_mode() == 2) {
+    launch_variant<16, 1>(ta_, tb_, grid, s, dp_, pp_, (int)h_.size(), X0, X1, ldx, Mglob);
+  } else if (gemm_mode() == 2 || has_mapk_) {
     // N-tile width by the widest problem of the batch (prefix sums for each width)
     const size_t P = h_.size();
     static const bool wide = getenv("RSF_GEMM_BN128") && getenv("RSF_GEMM_BN128")[0] == '1';
     if (maxN_ <= 32) {
       dim3 grid(totalN32_, ceil_div(M, P_BM));
-      launch_pipe<32>(ta_, tb_, grid, s, d_.p, prefix_.p + (P + 1), (int)P, X0, X1, ldx, Mglob);
+      launch_pipe<32>(ta_, tb_, grid, s, dp_, pp_ + (P + 1), (int)P, X0, X1, ldx, Mglob);
     } else if (wide && maxN_ >= 512) {
       dim3 grid(totalN128_, ceil_div(M, P_BM));
-      launch_pipe<128>(ta_, tb_, grid, s, d_.p, prefix_.p + 2 * (P + 1), (int)P, X0, X1, ldx, Mglob);
+      launch_pipe<128>(ta_, tb_, grid, s, dp_, pp_ + 2 * (P + 1), (int)P, X0, X1, ldx, Mglob);
     } else {
-      dim3 grid(totalN_, ceil_div(M, P_BM));
-      launch_pipe<64>(ta_, tb_, grid, s, d_.p, prefix_.p, (int)P, X0, X1, ldx, Mglob);
+      // split-K when the output tiles cannot fill the GPU but K is long (tall-skinny products:
+      // Gram matrices, projections onto bases, sketches of whole boxes)
+      static const bool splitk_on = getenv("RSF_SPLITK") && getenv("RSF_SPLITK")[0] == '1';   // measured: no gain (off)
+      long long ctas = 0;
+      int S = 1;
+      if (splitk_on && maxK_ >= 1024 && !has_lower_) {
+        for (const auto& d : h_) {
+          const int m = d.M < 0 ? Mglob : d.M;
+          if (m > 0 && d.N > 0) ctas += (long long)ceil_div(m, P_BM) * ceil_div(d.N, 64);
+        }
+        if (ctas > 0 && ctas < 2 * 148) {
+          S = (int)std::min<long long>(std::max<long long>(2, (3 * 148 + ctas - 1) / ctas), 32);
+          S = std::min(S, std::max(1, maxK_ / 256));
+        }
+      }
+      if (S > 1) {
+        std::vector<long long> mn(P + 1, 0);
+        for (size_t i = 0; i < P; ++i) {
+          const GemmDesc& d = h_[i];
+          const long long m = d.M < 0 ? Mglob : d.M;
+          mn[i + 1] = mn[i] + ((m > 0 && d.N > 0) ? m * d.N : 0);
+        }
+        const int kc = ((maxK_ + S - 1) / S + P_BK - 1) / P_BK * P_BK;
+        DBuf<long long> dmn(P + 1, s);
+        dmn.upload(mn);
+        DBuf<double> ws((size_t)S * std::max<long long>(mn[P], 1), s);
+        dim3 grid(totalN_, ceil_div(M, P_BM), S);
+        launch_pipe<64>(ta_, tb_, grid, s, dp_, pp_, (int)P, X0, X1, ldx, Mglob, ws.p, dmn.p, kc);
+        long long mx = 0;
+        for (size_t i = 0; i < P; ++i) mx = std::max(mx, mn[i + 1] - mn[i]);
+        const int gx = (int)std::max<long long>(1, std::min<long long>((mx + P_NT - 1) / P_NT, 1024));
+        for (size_t o = 0; o < P; o += 65535) {
+          const unsigned ny = (unsigned)std::min<size_t>(65535, P - o);
+          splitk_reduce_kernel<<<dim3(gx, ny), P_NT, 0, s>>>(dp_, ws.p, dmn.p, S, (int)o, X0, X1, ldx, Mglob);
+          count_launch();
+        }
+      } else {
+        dim3 grid(totalN_, ceil_div(M, P_BM));
+        launch_pipe<64>(ta_, tb_, grid, s, dp_, pp_, (int)P, X0, X1, ldx, Mglob);
+      }
     }
   } else if (gemm_mode() == 1) {
     dim3 grid(totalN_, ceil_div(M, 64));
-    launch_dmma(ta_, tb_, grid, s, d_.p, prefix_.p, (int)h_.size(), X0, X1, ldx, Mglob);
+    launch_dmma(ta_, tb_, grid, s, dp_, pp_, (int)h_.size(), X0, X1, ldx, Mglob);
   } else {
     dim3 grid(totalN_, ceil_div(M, 64));
-    launch_variant<64, 4>(ta_, tb_, grid, s, d_.p, prefix_.p, (int)h_.size(), X0, X1, ldx, Mglob);
+    launch_variant<64, 4>(ta_, tb_, grid, s, dp_, pp_, (int)h_.size(), X0, X1, ldx, Mglob);
   }
   if (KStats::on) {
     KStats::record(s, nullptr, &e1);

@@ -22,6 +22,7 @@ struct GemmDesc {
   double* C; long long offC; int ldc; const int* mapC;
   double alpha, beta;
   int lower;                   // 1: only tiles touching the lower triangle of C (SYRK-style)
+  const int* mapK;             // optional K-index gather applied to both operands (sparse right-hand sides)
   int btri;                    // op(B) triangular (TRMM-style K range): 1 lower (op(B)(l,j) = 0 for l < j),
                                // 2 upper (op(B)(l,j) = 0 for l > j); 0 general
 };
@@ -39,6 +40,8 @@ class GemmBatch {
   GemmBatch(bool ta, bool tb) : ta_(ta), tb_(tb) {}
   void reset(bool ta, bool tb) { ta_ = ta; tb_ = tb; h_.clear(); ready_ = false; }
   void add(const GemmDesc& d) { h_.push_back(d); ready_ = false; }
+  // finalize(): descriptors in a persistent device buffer (batches run many times); a batch
+  // that is run without finalize() uploads its descriptors through the transient ring
   size_t size() const { return h_.size(); }
   bool empty() const { return h_.empty(); }
   void finalize(cudaStream_t s) const;
@@ -53,7 +56,12 @@ class GemmBatch {
   std::vector<GemmDesc> h_;
   mutable DBuf<GemmDesc> d_;
   mutable DBuf<int> prefix_;
-  mutable int totalN_ = 0, totalN32_ = 0, totalN128_ = 0, maxM_ = 0, maxN_ = 0;
+  mutable std::vector<int> pre_;
+  mutable const GemmDesc* dp_ = nullptr;
+  mutable const int* pp_ = nullptr;
+  void finalize_meta() const;
+  mutable int totalN_ = 0, totalN32_ = 0, totalN128_ = 0, maxM_ = 0, maxN_ = 0, maxK_ = 0;
+  mutable bool has_lower_ = false, has_mapk_ = false;
   mutable bool glob_ = false;
 };
 

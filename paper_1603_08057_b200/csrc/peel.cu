@@ -182,11 +182,31 @@ DBuf<D> up(const std::vector<D>& v, cudaStream_t s) {
 }
 
 // ----------------------------------------------------------------- G operator
+// Z' rows [r0, r0+k) of a (cap x n) X'-matrix -> dst (k x n)
+__global__ void rowblock_extract_kernel(double* dst, const double* src, long long lds, int r0, int k, int n) {
+  const long long tot = (long long)n * k;
+  for (long long e = blockIdx.x * (long long)NT + threadIdx.x; e < tot; e += (long long)gridDim.x * NT) {
+    const long long t = e / k;
+    const int j = (int)(e - t * k);
+    dst[e] = src[t * lds + r0 + j];
+  }
+}
+
+// Y = 1/2 (Z'(rows [k, 2k)) + D)   (Z' is 2k x n, Y and D are k x n)
+__global__ void half_sum_kernel(double* Y, const double* Z, const double* D, int k, int n) {
+  const long long tot = (long long)n * k;
+  for (long long e = blockIdx.x * (long long)NT + threadIdx.x; e < tot; e += (long long)gridDim.x * NT) {
+    const long long t = e / k;
+    const int j = (int)(e - t * k);
+    Y[e] = 0.5 * (Z[t * 2 * k + k + j] + D[e]);
+  }
+}
+
 struct GOp {
   const Fact& F;
   const Fact* Fi;
   cudaStream_t s;
-  DBuf<double> A, B, tmp;
+  DBuf<double> A, B, Z, tmp;
   int kcap = 0;
   double columns = 0;
   GOp(const Fact& f, const Fact* fi) : F(f), Fi(fi), s(f.ctx->stream) {}
@@ -195,14 +215,15 @@ struct GOp {
     kcap = k;
     const size_t n = F.n();
     A.alloc(n * k, s);
-    if (Fi) B.alloc(n * k, s);
-    tmp.alloc((size_t)std::max<long long>(F.tmp_cols, 1) * k, s);
+    if (Fi) { B.alloc(n * k, s); Z.alloc(2 * n * k, s); }
+    tmp.alloc((size_t)std::max<long long>(F.tmp_cols, 1) * (Fi ? 2 : 1) * k, s);
   }
   // Y = G X (X preserved), X and Y are k x n
   void apply(const double* X, double* Y, int k) {
     RSF_PHASE("p.G_apply", s);
     reserve(k);
     const size_t bytes = (size_t)F.n() * k * sizeof(double);
+    const int n = F.n();
     columns += k;
     if (!Fi) {
       RSF_CUDA(cudaMemcpyAsync(Y, X, bytes, cudaMemcpyDeviceToDevice, s));
@@ -217,14 +238,17 @@ struct GOp {
       solve_half_fwd(F, Y, k, tmp.p);
       return;
     }
+    // G X = 1/2 (F^-1 (F_i X) + F_i (F^-1 X)): both solves in one 2k-column solve
     RSF_CUDA(cudaMemcpyAsync(A.p, X, bytes, cudaMemcpyDeviceToDevice, s));
-    apply_only_internal(*Fi, A.p, B.p, k);          // B = F_i X
-    solve_internal(F, B.p, k, tmp.p);               // B = F^-1 F_i X
-    RSF_CUDA(cudaMemcpyAsync(A.p, X, bytes, cudaMemcpyDeviceToDevice, s));
-    solve_internal(F, A.p, k, tmp.p);               // A = F^-1 X
-    apply_only_internal(*Fi, A.p, Y, k);            // Y = F_i F^-1 X
-    const long long nn = (long long)F.n() * k;
-    axpby_kernel<<<gxx(nn), NT, 0, s>>>(Y, B.p, 0.5, 0.5, nn);
+    apply_only_internal(*Fi, A.p, B.p, k);                      // B = F_i X
+    rowblock_copy_kernel<<<gxx((long long)n * k), NT, 0, s>>>(Z.p, 2 * k, 0, X, k, n);
+    rowblock_copy_kernel<<<gxx((long long)n * k), NT, 0, s>>>(Z.p, 2 * k, k, B.p, k, n);
+    count_launch(2);
+    solve_internal(F, Z.p, 2 * k, tmp.p);                       // Z = F^-1 [X, F_i X]
+    rowblock_extract_kernel<<<gxx((long long)n * k), NT, 0, s>>>(A.p, Z.p, 2 * k, 0, k, n);
+    count_launch();
+    apply_only_internal(*Fi, A.p, B.p, k);                      // B = F_i F^-1 X
+    half_sum_kernel<<<gxx((long long)n * k), NT, 0, s>>>(Y, Z.p, B.p, k, n);
     count_launch();
     RSF_LAUNCH_CHECK();
   }
@@ -243,13 +267,20 @@ struct PeelLevel {
   DBuf<double> Brow;
   long long tcols = 0;   // tmp columns per probe column: sum r (T') + sum r (S')
   GemmBatch g1, g2, g3;
-  // Y' -= G^(m) X'   (X', Y' are k x n; tmp has k * tcols doubles)
-  void subtract(cudaStream_t s, const double* X, double* Y, int k, double* tmp) const {
+  std::vector<int> ib, ni, r, bidx;      // boxes with r > 0: range, basis size, level box index
+  std::vector<long long> toff;           // T' column offsets
+  // Y' -= G^(m) X'   (X', Y' are k x n; tmp has k * tcols doubles).  g1x (optional) replaces
+  // the first step by a K-gathered version for right-hand sides known to vanish outside a
+  // row subset (block-sparse probes)
+  void subtract(cudaStream_t s, const double* X, double* Y, int k, double* tmp, const GemmBatch* g1x = nullptr,
+                const GemmBatch* g3x = nullptr) const {
     if (g3.empty()) return;
-    g1.run(s, const_cast<double*>(X), tmp, k, k);   // T'_j = X'(:, I_j) V_j
+    (g1x ? *g1x : g1).run(s, const_cast<double*>(X), tmp, k, k);   // T'_j = X'(:, I_j) V_j
     g2.run(s, nullptr, tmp, k, k);                  // S'_i = [T'_f]_{f in family(i)} Brow_i^T
-    g3.run(s, Y, tmp, k, k);                        // Y'(:, I_i) -= S'_i V_i^T
+    if (g3x && g3x->empty()) return;                // no row of Y' is needed
+    (g3x ? *g3x : g3).run(s, Y, tmp, k, k);         // Y'(:, I_i) -= S'_i V_i^T
   }
+  std::vector<long long> soff;           // S' column offsets
 };
 
 // out (rows x q, ld rows) = transpose of rows piv[0:q] of src (c x rows, ld lds)
@@ -289,7 +320,7 @@ __global__ void colmax_kernel(const ColMaxDesc* __restrict__ descs) {
 
 void launch_colmax(cudaStream_t s, const std::vector<ColMaxDesc>& v) {
   if (v.empty()) return;
-  auto d = up(v, s);
+  auto d = ring_up(v, s);
   for (size_t o = 0; o < v.size(); o += 65535) {
     colmax_kernel<<<(unsigned)std::min<size_t>(65535, v.size() - o), NT, 0, s>>>(d.p + o);
     count_launch();
@@ -313,7 +344,7 @@ __global__ void rownorm_hist_kernel(const double* __restrict__ V, int rows, int 
 template <class D, class K>
 void launch_descs(cudaStream_t s, const std::vector<D>& v, long long maxelems, K kern) {
   if (v.empty() || maxelems <= 0) return;
-  auto d = up(v, s);
+  auto d = ring_up(v, s);
   for (size_t o = 0; o < v.size(); o += 65535) {
     const unsigned nz = (unsigned)std::min<size_t>(65535, v.size() - o);
     kern<<<dim3(gxx(maxelems), nz), NT, 0, s>>>(d.p + o);
@@ -403,11 +434,65 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
   const double budget = 16.0 * (1ull << 30);   // bytes of transient per-batch buffers
   const double wcache_budget = 8.0 * (1ull << 30);   // W_i^T kept for a whole probe group
 
-  auto residual = [&](const double* W, double* Y, int k, int upto) {
+  struct SparseSub { std::vector<GemmBatch> g1, g3; std::vector<char> has1, has3; };
+  auto residual = [&](const double* W, double* Y, int k, int upto, const SparseSub* sp) {
     G.apply(W, Y, k);
     DBuf<double> tmp((size_t)std::max<long long>(max_tcols, 1) * k, s);
     RSF_PHASE("p.subtract", s);
-    for (int m = 1; m < upto; ++m) peeled[m].subtract(s, W, Y, k, tmp.p);
+    for (int m = 1; m < upto; ++m)
+      peeled[m].subtract(s, W, Y, k, tmp.p, sp && sp->has1[m] ? &sp->g1[m] : nullptr,
+                         sp && sp->has3[m] ? &sp->g3[m] : nullptr);
+  };
+  // T'_j = X'(:, I_j) V_j restricted to the rows where the level-l group-g probes are nonzero
+  // ... and Y'(:, I_i) -= S'_i V_i^T only on the rows the level-l sketch uses (boxes of the
+  // other three quadrants), as contiguous row ranges
+  auto sparse_g1 = [&](const std::vector<int>& hq, int g, int upto, std::vector<DBuf<int>>& keep) {
+    SparseSub sp;
+    sp.g1.resize(upto);
+    sp.g3.resize(upto);
+    sp.has1.assign(upto, 0);
+    sp.has3.assign(upto, 0);
+    std::vector<GemmBatch>& out = sp.g1;
+    for (int m = 1; m < upto; ++m) {
+      const PeelLevel& P = peeled[m];
+      if (P.g3.empty()) continue;
+      std::vector<int> idx;
+      std::vector<long long> off(P.ib.size() + 1, 0);
+      for (size_t b = 0; b < P.ib.size(); ++b) {
+        for (int t = 0; t < P.ni[b]; ++t)
+          if (hq[P.ib[b] + t] == g) idx.push_back(t);
+        off[b + 1] = idx.size();
+      }
+      keep.emplace_back(up(idx, s));
+      const int* dk = keep.back().p;
+      out[m].reset(false, false);
+      for (size_t b = 0; b < P.ib.size(); ++b) {
+        GemmDesc a = gdesc(-1, P.r[b], (int)(off[b + 1] - off[b]));
+        a.selA = 1; a.offA = P.ib[b]; a.B = P.V[P.bidx[b]].p; a.ldb = P.ni[b]; a.selC = 2; a.offC = P.toff[b];
+        a.mapK = dk + off[b];
+        out[m].add(a);
+      }
+      out[m].finalize(s);
+      sp.has1[m] = 1;
+      sp.g3[m].reset(false, true);
+      for (size_t b = 0; b < P.ib.size(); ++b) {
+        int t = 0;
+        while (t < P.ni[b]) {
+          const int q = hq[P.ib[b] + t];
+          if (q < 0 || q == g) { ++t; continue; }
+          int e = t + 1;
+          while (e < P.ni[b] && hq[P.ib[b] + e] >= 0 && hq[P.ib[b] + e] != g) ++e;
+          GemmDesc d = gdesc(-1, e - t, P.r[b]);
+          d.selA = 2; d.offA = P.soff[b]; d.B = P.V[P.bidx[b]].p + t; d.ldb = P.ni[b];
+          d.selC = 1; d.offC = P.ib[b] + t; d.alpha = -1.0; d.beta = 1.0;
+          sp.g3[m].add(d);
+          t = e;
+        }
+      }
+      if (!sp.g3[m].empty()) sp.g3[m].finalize(s);
+      sp.has3[m] = 1;
+    }
+    return sp;
   };
 
   static const int verbose = getenv("RSF_VERBOSE") ? atoi(getenv("RSF_VERBOSE")) : 0;
@@ -508,6 +593,8 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
         }
         // sketch Y'_g = ((G - sum_{m<l} G^(m)) W_g)^T in chunks of kb probe columns;
         // every chunk extends the bases V_i of the boxes that see it
+        std::vector<DBuf<int>> g1keep;
+        const SparseSub g1sp = sparse_g1(hq, g, lev, g1keep);
         // equal chunks of <= kb columns (multiple of 8) instead of kb-wide chunks plus a thin tail
         const int nch = (c + kb - 1) / kb;
         const int kc = std::min(kb, ((c + nch - 1) / nch + 7) / 8 * 8);
@@ -515,7 +602,7 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
         for (int c0 = 0; c0 < c; c0 += kc) {
           const int k = std::min(kc, c - c0);
           gen_probes(s, W.p, k, n, t.d_perm.p, qmap.p, g, c0, lev, trace_id, seed);
-          residual(W.p, Y.p, k, lev);
+          residual(W.p, Y.p, k, lev, &g1sp);
           RSF_PHASE("p.basis", s);
           size_t x0 = 0;
           while (x0 < NA) {
@@ -925,6 +1012,8 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
       GemmDesc a = gdesc(-1, rb[b], bx[b].ni);            // T'_b = X'(:, I_b) V_b
       a.selA = 1; a.offA = bx[b].ib; a.B = PL.V[b].p; a.ldb = bx[b].ni; a.selC = 2; a.offC = toff[b];
       PL.g1.add(a);
+      PL.ib.push_back(bx[b].ib); PL.ni.push_back(bx[b].ni); PL.r.push_back(rb[b]); PL.bidx.push_back(b);
+      PL.toff.push_back(toff[b]); PL.soff.push_back(soff[b]);
       GemmDesc d = gdesc(-1, rb[b], (int)tot);            // S'_b = T'_fam Brow_b^T
       d.selA = 2; d.offA = toff[bx[b].fam0]; d.B = PL.Brow.p + bo[b]; d.ldb = rb[b]; d.selC = 2; d.offC = soff[b];
       PL.g2.add(d);
@@ -981,7 +1070,7 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
     extract_probe_kernel<<<gxx((long long)n * k), NT, 0, s>>>(E.p, k, n, dlb.p, e0);
     count_launch();
     RSF_LAUNCH_CHECK();
-    residual(E.p, H.p, k, L + 1);
+    residual(E.p, H.p, k, L + 1, nullptr);
     extract_diag_kernel<<<GB, NT, 0, s>>>(H.p, k, n, dlb.p, e0, part.p, parta.p);
     count_launch();
     RSF_LAUNCH_CHECK();
@@ -1017,6 +1106,7 @@ EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KP
   const long long l0 = g_launches;
   const double T0 = now_s();
   cudaStream_t s = ctx.stream;
+  KTrace::set_stream(s);
   auto is_dev = [](const void* ptr) {
     cudaPointerAttributes a;
     if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) { cudaGetLastError(); return false; }

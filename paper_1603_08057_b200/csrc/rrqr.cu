@@ -534,7 +534,7 @@ void trsm_upper_batched(cudaStream_t s, const std::vector<TrsmProb>& probs) {
     }
   }
   if (!dv.empty()) {
-    auto dd = upd(dv, s);
+    auto dd = ring_up(dv, s);
     for (size_t o = 0; o < dv.size(); o += 65535) {
       unsigned nb = (unsigned)std::min<size_t>(65535, dv.size() - o);
       upper_inv64_kernel<<<nb, 64, 0, s>>>(dd.p + o);
@@ -607,7 +607,7 @@ RRQRResult rrqr_batched(cudaStream_t s, const std::vector<RRQRProb>& probs, doub
   {
     DBuf<double> G(gt, s);
     for (int i = 0; i < P; ++i) base[i].G = G.p + goff[i];
-    auto db = upd(base, s);
+    auto db = ring_up(base, s);
     ref_kernel<<<P, NT, 0, s>>>(db.p);
     long long mx = 0;
     for (auto& p : probs) mx = std::max(mx, (long long)SP * p.m);
@@ -638,7 +638,7 @@ RRQRResult rrqr_batched(cudaStream_t s, const std::vector<RRQRProb>& probs, doub
       d.nbp = std::min(QR_NB, std::min(probs[i].m, probs[i].c) - J);
       dv.push_back(d);
     }
-    auto dd = upd(dv, s);
+    auto dd = ring_up(dv, s);
     const unsigned na = (unsigned)dv.size();
     int crmax = 0;
     for (auto& d : dv) crmax = std::max(crmax, d.c - d.J);
@@ -685,7 +685,7 @@ RRQRResult rrqr_batched(cudaStream_t s, const std::vector<RRQRProb>& probs, doub
       }
     }
     if (!cont.empty()) {   // sketch downdate: Y2 -= Y1 R11^-1 R12
-      auto dc = upd(cont, s);
+      auto dc = ring_up(cont, s);
       r11_inv_kernel<<<(unsigned)cont.size(), 64, 0, s>>>(dc.p);
       count_launch();
       RSF_LAUNCH_CHECK();

@@ -134,7 +134,7 @@ int gx(long long maxelems) {
 template <class D, class K, class... Args>
 void launch_y(cudaStream_t s, const std::vector<D>& v, long long maxelems, K kern, Args... args) {
   if (v.empty() || maxelems <= 0) return;
-  auto d = up(v, s);
+  auto d = ring_up(v, s);
   for (size_t o = 0; o < v.size(); o += 65535) {
     int ny = (int)std::min<size_t>(65535, v.size() - o);
     kern<<<dim3(gx(maxelems), ny), NT, 0, s>>>(d.p + o, args...);

@@ -26,6 +26,7 @@ z = F.sample(w)
 del F
 torch.cuda.synchronize()
 free, tot = torch.cuda.mem_get_info(); print('mem free/total GB', free / 1e9, tot / 1e9, flush=True)
+R.lib.rsf_profile_reset()
 for rep in range(reps):
     t = time.time()
     r = R.gp_mle_eval(ctx, xy, z, K, c.eps_fact, c.leaf, R.Opts(eps_peel=c.eps_peel, seed=c.seed))
@@ -40,3 +41,16 @@ prof = R.lib.rsf_profile_dump().decode()
 if prof:
     items = sorted([(float(v), k) for k, v in (x.split('=') for x in prof.strip(';').split(';'))], reverse=True)
     print('PROFILE', ' '.join(f'{k}={v:.3f}' for v, k in items))
+
+tr = R.lib.rsf_trace_dump().decode()
+if tr:
+    rows = []
+    for item in tr.strip(';').split(';'):
+        k, v = item.rsplit('=', 1)
+        sec, cnt, host = v.split(',')
+        rows.append((float(sec), int(cnt), k, float(host)))
+    rows.sort(reverse=True)
+    tot = sum(r[0] for r in rows)
+    print(f'KTRACE total {tot:.3f} s over {sum(r[1] for r in rows)} launches')
+    for sec, cnt, k, host in rows[:45]:
+        print(f'  {sec:8.3f} s {100*sec/tot:5.1f}% {cnt:7d}  host {host:8.3f} s  {k}')
