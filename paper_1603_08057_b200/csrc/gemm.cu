@@ -36,10 +36,49 @@ std::mutex& cache_mu() { static std::mutex m; return m; }
 std::vector<FreeList>& cache() { static std::vector<FreeList> v; return v; }
 int bin_of(size_t bytes) { int b = 8; while ((size_t(1) << b) < bytes) ++b; return b; }   // >= 256 B
 }  // namespace
+// large blocks: best fit among cached blocks of the same stream (at most 1.5x + 64 MB of
+// slack), bounded total; the stream-ordered pool grows by mapping new memory for every miss
+constexpr size_t LARGE_CACHE_MAX = size_t(48) << 30;
+double g_amiss_small = 0, g_amiss_large = 0, g_amax = 0;
+long long g_nmiss_small = 0, g_nmiss_large = 0;
+double g_amax_bytes = 0;
+struct Large { cudaStream_t s; void* p; size_t bytes; };
+std::vector<Large>& large() { static std::vector<Large> v; return v; }
+size_t& large_total() { static size_t t = 0; return t; }
 void* dev_alloc(size_t bytes, cudaStream_t s) {
   void* p = nullptr;
   if (bytes > CACHE_MAX) {
-    RSF_CUDA(cudaMallocAsync(&p, bytes, s));
+    {
+      std::lock_guard<std::mutex> lk(cache_mu());
+      auto& L = large();
+      size_t best = L.size();
+      for (size_t i = 0; i < L.size(); ++i)
+        if (L[i].s == s && L[i].bytes >= bytes && L[i].bytes <= 4 * bytes + CACHE_MAX &&
+            (best == L.size() || L[i].bytes < L[best].bytes))
+          best = i;
+      if (best < L.size()) {
+        p = L[best].p;
+        large_total() -= L[best].bytes;
+        L.erase(L.begin() + best);
+        return p;
+      }
+    }
+    const size_t rb = (bytes + (size_t(2) << 20) - 1) / (size_t(2) << 20) * (size_t(2) << 20);
+    const double t0 = wall();
+    cudaError_t e = cudaMallocAsync(&p, rb, s);
+    const double dt = wall() - t0;
+    g_amiss_large += dt; ++g_nmiss_large;
+    if (dt > g_amax) { g_amax = dt; g_amax_bytes = (double)rb; }
+    if (e == cudaErrorMemoryAllocation) {   // give the cached large blocks back and retry
+      cudaGetLastError();
+      std::lock_guard<std::mutex> lk(cache_mu());
+      for (auto& b : large()) cudaFreeAsync(b.p, b.s);
+      large().clear();
+      large_total() = 0;
+      cudaStreamSynchronize(s);
+      e = cudaMallocAsync(&p, rb, s);
+    }
+    RSF_CUDA(e);
     return p;
   }
   const int b = bin_of(bytes);
@@ -48,17 +87,38 @@ void* dev_alloc(size_t bytes, cudaStream_t s) {
     for (auto& f : cache())
       if (f.s == s && f.bin == b && !f.blocks.empty()) { p = f.blocks.back(); f.blocks.pop_back(); return p; }
   }
+  const double t0 = wall();
   RSF_CUDA(cudaMallocAsync(&p, size_t(1) << b, s));
+  const double dt = wall() - t0;
+  g_amiss_small += dt; ++g_nmiss_small;
+  if (dt > g_amax) { g_amax = dt; g_amax_bytes = (double)(size_t(1) << b); }
   return p;
 }
 void dev_cache_trim(cudaStream_t s) {
   std::lock_guard<std::mutex> lk(cache_mu());
   for (auto& f : cache())
     if (f.s == s) { for (void* p : f.blocks) cudaFreeAsync(p, s); f.blocks.clear(); }
+  auto& L = large();
+  for (size_t i = 0; i < L.size();) {
+    if (L[i].s == s) { cudaFreeAsync(L[i].p, s); large_total() -= L[i].bytes; L.erase(L.begin() + i); }
+    else ++i;
+  }
 }
 void dev_free(void* p, size_t bytes, cudaStream_t s) {
   if (!p) return;
-  if (bytes > CACHE_MAX) { cudaFreeAsync(p, s); return; }
+  if (bytes > CACHE_MAX) {
+    const size_t rb = (bytes + (size_t(2) << 20) - 1) / (size_t(2) << 20) * (size_t(2) << 20);
+    std::lock_guard<std::mutex> lk(cache_mu());
+    auto& L = large();
+    L.push_back(Large{s, p, rb});
+    large_total() += rb;
+    while (large_total() > LARGE_CACHE_MAX && !L.empty()) {   // drop the oldest
+      cudaFreeAsync(L.front().p, L.front().s);
+      large_total() -= L.front().bytes;
+      L.erase(L.begin());
+    }
+    return;
+  }
   const int b = bin_of(bytes);
   std::lock_guard<std::mutex> lk(cache_mu());
   for (auto& f : cache())
@@ -228,13 +288,23 @@ void KTrace::mark(const char* file, int line) {
 std::string KTrace::dump() {
   tdrain();
   std::string r = "host-alloc|n=" + std::to_string(g_n_alloc) + "=" + std::to_string(g_host_alloc) + ",1,0;" +
+                  "alloc-miss-small|n=" + std::to_string(g_nmiss_small) + "=" + std::to_string(g_amiss_small) + ",1,0;" +
+                  "alloc-miss-large|n=" + std::to_string(g_nmiss_large) + "=" + std::to_string(g_amiss_large) + ",1,0;" +
+                  "alloc-max|bytes=" + std::to_string(g_amax_bytes) + "=" + std::to_string(g_amax) + ",1,0;" +
                   "host-free|=" + std::to_string(g_host_free) + ",1,0;host-upload|=" + std::to_string(g_host_upload) + ",1,0;";
   for (auto& a : tagg())
     r += a.first + "=" + std::to_string(a.second.sec) + "," + std::to_string(a.second.cnt) + "," +
          std::to_string(a.second.host) + ";";
   return r;
 }
-void KTrace::reset() { tdrain(); tagg().clear(); g_host_alloc = g_host_free = g_host_upload = 0; g_n_alloc = 0; }
+void KTrace::reset() {
+  tdrain();
+  tagg().clear();
+  g_host_alloc = g_host_free = g_host_upload = 0;
+  g_n_alloc = 0;
+  g_amiss_small = g_amiss_large = g_amax = g_amax_bytes = 0;
+  g_nmiss_small = g_nmiss_large = 0;
+}
 
 namespace {
 

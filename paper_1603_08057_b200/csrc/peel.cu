@@ -64,6 +64,17 @@ __global__ void probes_kernel(double* X, int k, int t0, int t1, const int* __res
   }
 }
 
+// probe rows of a list of tree indices: X'(j, q) = normal(perm[rows[q]], col0 + j, level, trace)
+__global__ void probes_rows_kernel(double* X, int k, const int* __restrict__ rows, long long nrows,
+                                   const int* __restrict__ perm, int col0, int lev, int tr, unsigned seed) {
+  const long long tot = nrows * k;
+  for (long long e = blockIdx.x * (long long)NT + threadIdx.x; e < tot; e += (long long)gridDim.x * NT) {
+    const long long q = e / k;
+    const int j = (int)(e - q * k);
+    X[e] = probe_normal((unsigned)perm[rows[q]], (unsigned)(col0 + j), (unsigned)lev, (unsigned)tr, seed);
+  }
+}
+
 // dst rows [r0, r0+k) of a (cap x n) X'-matrix <- src (k x n)
 __global__ void rowblock_copy_kernel(double* dst, long long ldd, int r0, const double* src, int k, int n) {
   const long long tot = (long long)n * k;
@@ -539,6 +550,7 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
     // per-level state (reset when the width grows)
     std::vector<int> rb(nb, 0);                   // basis size r_i
     std::vector<DBuf<double>> Vb(nb), Ab(nb);     // V_i (n_i x r_i, ld n_i), A_i = W_i^T V_i (c x r_i, ld c)
+    std::vector<int> vcap(nb, 0);                 // allocated columns of V_i / A_i
     // per ordered pair (index: b * 4 + position of the sibling in the family)
     struct PairData { int k = 0, rz = 0; double *Z = nullptr, *X = nullptr, *Lm = nullptr, *Gi = nullptr; };
     std::vector<PairData> pdat((size_t)nb * 4);
@@ -548,6 +560,15 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
       std::fill(rb.begin(), rb.end(), 0);
       for (auto& v : Vb) v.release();
       for (auto& v : Ab) v.release();
+      // fixed capacity per box: every probe group adds at most c directions (no regrowth)
+      std::fill(vcap.begin(), vcap.end(), 0);
+      for (int b = 0; b < nb; ++b) {
+        const int ng = bx[b].fam1 - bx[b].fam0 - 1;
+        if (ng <= 0) continue;
+        vcap[b] = std::min(bx[b].ni, ng * c);
+        Vb[b].alloc((size_t)bx[b].ni * vcap[b], s);
+        Ab[b].alloc((size_t)c * vcap[b], s);
+      }
       arenas.clear();
       for (auto& q : pdat) q = PairData{};
       bool fail = false;
@@ -583,12 +604,16 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
         DBuf<double> Wc;
         if (8.0 * wct <= wcache_budget) {
           Wc.alloc(wct, s);
+          std::vector<int> rows;   // tree indices of the act boxes, in Wc order
+          rows.reserve(wct / c);
           for (size_t x = 0; x < NA; ++x) {
             const PBox& b = bx[act[x]];
-            probes_kernel<<<gxx((long long)b.ni * c), NT, 0, s>>>(Wc.p + wco[x], c, b.ib, b.ib + b.ni, t.d_perm.p,
-                                                                nullptr, 0, 0, lev, trace_id, seed32, c);
-            count_launch();
+            for (int q = 0; q < b.ni; ++q) rows.push_back(b.ib + q);
           }
+          DBuf<int> drows = up(rows, s);
+          probes_rows_kernel<<<gxx((long long)rows.size() * c), NT, 0, s>>>(Wc.p, c, drows.p, (long long)rows.size(),
+                                                                          t.d_perm.p, 0, lev, trace_id, seed32);
+          count_launch();
           RSF_LAUNCH_CHECK();
         }
         // sketch Y'_g = ((G - sum_{m<l} G^(m)) W_g)^T in chunks of kb probe columns;
@@ -684,11 +709,17 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
             std::vector<long long> qo(B), ro(B);
             for (size_t x = 0; x < B; ++x) {
               const int i = act[x0 + x];
-              qq[x] = std::min<int>(qq[x], (int)(cccap[x0 + x] - rb[i]));
+              qq[x] = std::min<int>(qq[x], std::min<int>((int)(cccap[x0 + x] - rb[i]), vcap[i] - rb[i]));
               qo[x] = qt; qt += (long long)bx[i].ni * qq[x];
               ro[x] = rt; rt += (long long)qq[x] * qq[x];
             }
-            DBuf<double> Qb(std::max<long long>(qt, 1), s), Q0(std::max<long long>(qt, 1), s), Ri(std::max<long long>(rt, 1), s);
+            DBuf<double> Q0(std::max<long long>(qt, 1), s), Ri(std::max<long long>(rt, 1), s);
+            // the new directions are formed in place in the free columns of V_i
+            std::vector<double*> Qp(B, nullptr);
+            for (size_t x = 0; x < B; ++x) {
+              const int i = act[x0 + x];
+              if (qq[x] > 0) Qp[x] = Vb[i].p + (long long)bx[i].ni * rb[i];
+            }
             std::vector<GatherTDesc> gd;
             std::vector<EyeDesc> ed;
             std::vector<TrsmProb> tp;
@@ -710,9 +741,9 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
               const int i = act[x0 + x];
               if (qq[x] == 0) continue;
               GemmDesc d = gdesc(bx[i].ni, qq[x], qq[x]);   // Q0 R11^-1 (well conditioned)
-              d.A = Q0.p + qo[x]; d.lda = bx[i].ni; d.B = Ri.p + ro[x]; d.ldb = qq[x]; d.C = Qb.p + qo[x]; d.ldc = bx[i].ni;
+              d.A = Q0.p + qo[x]; d.lda = bx[i].ni; d.B = Ri.p + ro[x]; d.ldb = qq[x]; d.C = Qp[x]; d.ldc = bx[i].ni;
               g0.add(d);
-              cq.push_back(CQProb{Qb.p + qo[x], bx[i].ni, qq[x]});
+              cq.push_back(CQProb{Qp[x], bx[i].ni, qq[x]});
             }
             g0.run(s);
             Q0.release();
@@ -726,63 +757,40 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
                 const int i = act[x0 + x];
                 if (qq[x] == 0 || rb[i] == 0) continue;
                 GemmDesc d = gdesc(rb[i], qq[x], bx[i].ni);  // H = V^T Q
-                d.A = Vb[i].p; d.lda = bx[i].ni; d.B = Qb.p + qo[x]; d.ldb = bx[i].ni; d.C = H.p + hoff[x]; d.ldc = rb[i];
+                d.A = Vb[i].p; d.lda = bx[i].ni; d.B = Qp[x]; d.ldb = bx[i].ni; d.C = H.p + hoff[x]; d.ldc = rb[i];
                 gh.add(d);
                 GemmDesc e = gdesc(bx[i].ni, qq[x], rb[i]);  // Q -= V H
-                e.A = Vb[i].p; e.lda = bx[i].ni; e.B = H.p + hoff[x]; e.ldb = rb[i]; e.C = Qb.p + qo[x]; e.ldc = bx[i].ni;
+                e.A = Vb[i].p; e.lda = bx[i].ni; e.B = H.p + hoff[x]; e.ldb = rb[i]; e.C = Qp[x]; e.ldc = bx[i].ni;
                 e.alpha = -1.0; e.beta = 1.0;
                 gq.add(e);
               }
               if (!gh.empty()) { gh.run(s); gq.run(s); }
               cholqr2_batched(s, cq, lev, &pd.flops);   // right factors keep Q orthogonal to V_i
             }
-            // C_ij'(chunk, :) = Y_ij(:, chunk)^T [V_i, Q_i] = [C1, Res^T Q_i]; V_i <- [V_i, Q_i],
-            // A_i <- [A_i, W_i^T Q_i] (per-box buffers, regrown)
-            GemmBatch gcq(false, false);
+            // C_ij'(chunk, :) = Y_ij(:, chunk)^T [V_i, Q_i] = [C1, Res^T Q_i]; A_i <- [A_i, W_i^T Q_i]
+            // (V_i <- [V_i, Q_i] happened in place)
+            pseq.next("b.grow");
+            GemmBatch gcq(false, false), gan(false, false);
             std::vector<CopyProb> cc1;
-            std::vector<DBuf<double>> nV(B), nA(B);
             for (size_t x = 0; x < B; ++x) {
               const size_t xa = x0 + x;
               const int i = act[xa];
-              const long long ni = bx[i].ni;
               if (rb[i] > 0) cc1.push_back(CopyProb{C1.p + c1o[x], k, CC.p + cco[xa] + c0, c, k, rb[i], 1.0});
               if (qq[x] == 0) continue;
               GemmDesc d = gdesc(k, qq[x], bx[i].ni);
-              d.A = Y.p + (long long)bx[i].ib * k; d.lda = k; d.B = Qb.p + qo[x]; d.ldb = bx[i].ni;
+              d.A = Y.p + (long long)bx[i].ib * k; d.lda = k; d.B = Qp[x]; d.ldb = bx[i].ni;
               d.C = CC.p + cco[xa] + c0 + (long long)c * rb[i]; d.ldc = c;
               gcq.add(d);
-              nV[x].alloc((size_t)ni * (rb[i] + qq[x]), s);
-              nA[x].alloc((size_t)c * (rb[i] + qq[x]), s);
+              GemmDesc e = gdesc(c, qq[x], bx[i].ni);
+              e.A = Wp[x]; e.lda = c; e.B = Qp[x]; e.ldb = bx[i].ni;
+              e.C = Ab[i].p + (long long)c * rb[i]; e.ldc = c;
+              gan.add(e);
               pd.flops += 4.0 * c * (double)qq[x] * bx[i].ni;
             }
-            pseq.next("b.grow");
             copy_batched(s, cc1);
             gcq.run(s);
-            GemmBatch gan(false, false);
-            std::vector<CopyProb> cpv;
-            for (size_t x = 0; x < B; ++x) {
-              const int i = act[x0 + x];
-              const long long ni = bx[i].ni;
-              if (qq[x] == 0) continue;
-              if (rb[i] > 0) {
-                cpv.push_back(CopyProb{Vb[i].p, ni, nV[x].p, ni, (int)ni, rb[i], 1.0});
-                cpv.push_back(CopyProb{Ab[i].p, c, nA[x].p, c, c, rb[i], 1.0});
-              }
-              cpv.push_back(CopyProb{Qb.p + qo[x], ni, nV[x].p + ni * rb[i], ni, (int)ni, qq[x], 1.0});
-              GemmDesc e = gdesc(c, qq[x], bx[i].ni);
-              e.A = Wp[x]; e.lda = c; e.B = Qb.p + qo[x]; e.ldb = bx[i].ni;
-              e.C = nA[x].p + (long long)c * rb[i]; e.ldc = c;
-              gan.add(e);
-            }
-            copy_batched(s, cpv);
             gan.run(s);
-            for (size_t x = 0; x < B; ++x) {
-              const int i = act[x0 + x];
-              if (qq[x] == 0) continue;
-              Vb[i] = std::move(nV[x]);
-              Ab[i] = std::move(nA[x]);
-              rb[i] += qq[x];
-            }
+            for (size_t x = 0; x < B; ++x) rb[act[x0 + x]] += qq[x];
             x0 = x1;
           }
         }
@@ -995,7 +1003,18 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
     for (auto& q : pdat) q = PairData{};
 
     // ---- subtraction batches of G^(lev)
-    PL.V = std::move(Vb);
+    PL.V.clear();
+    PL.V.resize(nb);
+    {
+      std::vector<CopyProb> cpv;
+      for (int b = 0; b < nb; ++b) {
+        if (rb[b] == 0) continue;
+        PL.V[b].alloc((size_t)bx[b].ni * rb[b], s);
+        cpv.push_back(CopyProb{Vb[b].p, bx[b].ni, PL.V[b].p, bx[b].ni, bx[b].ni, rb[b], 1.0});
+      }
+      copy_batched(s, cpv);
+      for (auto& v : Vb) v.release();
+    }
     double vbytes = 0;
     for (auto& v : PL.V) vbytes += 8.0 * v.n;
     PL.g1.reset(false, false);

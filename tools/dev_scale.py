@@ -26,10 +26,10 @@ z = F.sample(w)
 del F
 torch.cuda.synchronize()
 free, tot = torch.cuda.mem_get_info(); print('mem free/total GB', free / 1e9, tot / 1e9, flush=True)
-R.lib.rsf_profile_reset()
 for rep in range(reps):
+    R.lib.rsf_profile_reset()
     t = time.time()
-    r = R.gp_mle_eval(ctx, xy, z, K, c.eps_fact, c.leaf, R.Opts(eps_peel=c.eps_peel, seed=c.seed))
+    r = R.gp_mle_eval(ctx, xy, z, K, c.eps_fact, c.leaf, R.Opts(eps_peel=c.eps_peel, seed=c.seed, probe_block=int(__import__('os').environ.get('PROBE_BLOCK', '512'))))
     el = time.time() - t
     d = r.diag
     print(f'eval {el:.3f}s ell={r.ell:.10e} grad={r.grad} tree {d.t_tree:.3f} factor {d.t_factor:.3f} compress {d.t_compress:.3f} solve {d.t_solve:.3f} peel {d.t_peel:.3f} launches {d.kernel_launches:.0f}', flush=True)

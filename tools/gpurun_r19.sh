@@ -1,0 +1,3 @@
+cd $GRAFT_REPO_ROOT
+RSF_KTRACE=1 timeout 600 python tools/dev_scale.py 3 262144 2 > gpurun_out/r19_trace3.log 2>&1; echo "exit $?" >> gpurun_out/r19_trace3.log
+timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/r19_pytest.log 2>&1; echo "pytest exit $?" >> gpurun_out/r19_pytest.log
