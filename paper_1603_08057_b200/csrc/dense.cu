@@ -1,9 +1,13 @@
 // Batched dense FP64 factorizations (see dense.cuh).
 #include <algorithm>
 
+#include <cooperative_groups.h>
+
 #include "dense.cuh"
 
 namespace rsf {
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -444,6 +448,176 @@ void launch_y(cudaStream_t s, const std::vector<D>& v, long long maxelems, K ker
   }
 }
 
+// Cluster panel factorization for tall panels: the rows are distributed over the CL CTAs
+// of a thread-block cluster and held in shared memory.  Every Householder step needs the
+// column norm below the diagonal and the dot products with the remaining columns; each CTA
+// computes its partial sums over its rows and writes them to every CTA's exchange buffer
+// (DSMEM, double-buffered by step parity), one cluster barrier per column.  The sums over
+// ranks are taken in rank order, so the result is deterministic.
+constexpr int PC_NT = 512, PC_NW = PC_NT / 32;
+constexpr int PC_MAXROWS = 480;            // rows per CTA: QR_NB * 480 * 8 B = 120 KB
+constexpr int PC_NPAIR = QR_NB * (QR_NB - 1) / 2;
+constexpr int PC_XW = 2 * QR_NB + 2;       // exchange width per rank
+
+template <int CL>
+__global__ void __launch_bounds__(PC_NT) qr_panel_cl_kernel(const PanelDesc* __restrict__ descs) {
+  extern __shared__ double pcm[];
+  __shared__ double xch[2][CL][PC_XW];
+  __shared__ double scal[4];
+  __shared__ double wv[QR_NB];
+  __shared__ double taus[QR_NB];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const PanelDesc d = descs[blockIdx.x / CL];
+  const int rows = d.rows, ncol = d.ncol;
+  const int chunk = max((rows + CL - 1) / CL, QR_NB);   // rows < QR_NB (R, pivots) live in rank 0
+  const int r0 = rank * chunk, nr = max(0, min(rows, r0 + chunk) - r0);
+  double* P = pcm;                          // local rows: P[c * chunk + lr]
+  double* gbuf = pcm + QR_NB * chunk;       // rank 0: partial Gram [CL][PC_NPAIR]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int e = tid; e < ncol * nr; e += PC_NT) {
+    const int c = e / nr, lr = e % nr;
+    P[c * chunk + lr] = d.A[(long long)c * d.lda + r0 + lr];
+  }
+  __syncthreads();
+  for (int j = 0; j < ncol; ++j) {
+    const int buf = j & 1;
+    // partial sums over the local rows below the diagonal: sigma (column j) and x . y_c (c > j)
+    for (int c = j + warp; c < ncol; c += PC_NW) {
+      double acc = 0.0;
+      const double* x = P + j * chunk;
+      const double* y = P + c * chunk;
+      for (int lr = lane; lr < nr; lr += 32)
+        if (r0 + lr > j) acc += x[lr] * y[lr];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) wv[c - j] = acc;      // wv[0] = sigma, wv[c - j] = dot_c
+    }
+    __syncthreads();
+    // publish (rank 0 adds alpha = x_j and y_c[j], its own rows)
+    if (tid < CL) {
+      double* dst = &cluster.map_shared_rank(&xch[0][0][0], tid)[(buf * CL + rank) * PC_XW];
+      for (int q = 0; q < ncol - j; ++q) dst[q] = wv[q];
+      if (rank == 0) {
+        dst[QR_NB] = P[j * chunk + j];
+        for (int c = j + 1; c < ncol; ++c) dst[QR_NB + 1 + (c - j - 1)] = P[c * chunk + j];
+      }
+    }
+    cluster.sync();
+    if (tid == 0) {
+      double sigma = 0.0;
+      for (int r = 0; r < CL; ++r) sigma += xch[buf][r][0];
+      const double alpha = xch[buf][0][QR_NB];
+      double tau = 0.0, beta = alpha, scale = 0.0;
+      if (sigma != 0.0) {
+        const double mu = sqrt(alpha * alpha + sigma);
+        beta = (alpha >= 0.0) ? -mu : mu;
+        tau = (beta - alpha) / beta;
+        scale = 1.0 / (alpha - beta);
+      }
+      scal[0] = tau; scal[1] = beta; scal[2] = scale;
+      taus[j] = tau;
+      for (int c = j + 1; c < ncol; ++c) {
+        double dot = 0.0;
+        for (int r = 0; r < CL; ++r) dot += xch[buf][r][c - j];
+        wv[c - j] = tau * (xch[buf][0][QR_NB + 1 + (c - j - 1)] + scale * dot);
+      }
+    }
+    __syncthreads();
+    const double scale = scal[2];
+    // v = x(j+1:)/scale-normalised; y_c -= w_c v
+    for (int lr = tid; lr < nr; lr += PC_NT) {
+      const int g = r0 + lr;
+      if (g <= j) continue;
+      const double v = P[j * chunk + lr] * scale;
+      P[j * chunk + lr] = v;
+      for (int c = j + 1; c < ncol; ++c) P[c * chunk + lr] -= wv[c - j] * v;
+    }
+    if (rank == 0 && tid == 0) {
+      for (int c = j + 1; c < ncol; ++c) P[c * chunk + j] -= wv[c - j];
+      P[j * chunk + j] = scal[1];
+    }
+    __syncthreads();
+  }
+  // write back R (rank 0's top rows) and the reflectors, explicit unit-lower V
+  for (int e = tid; e < ncol * nr; e += PC_NT) {
+    const int c = e / nr, lr = e % nr, g = r0 + lr;
+    const double v = P[c * chunk + lr];
+    d.A[(long long)c * d.lda + g] = v;
+    d.V[(long long)c * rows + g] = (g < c) ? 0.0 : (g == c ? 1.0 : v);
+  }
+  // partial Gram G(l, i) = sum_{rows > i} v_l v_i (l < i) -> rank 0
+  for (int pidx = warp; pidx < ncol * (ncol - 1) / 2; pidx += PC_NW) {
+    int i = 1, acc0 = 0;
+    while (acc0 + i <= pidx) { acc0 += i; ++i; }
+    const int l = pidx - acc0;
+    double acc = 0.0;
+    for (int lr = lane; lr < nr; lr += 32)
+      if (r0 + lr > i) acc += P[l * chunk + lr] * P[i * chunk + lr];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) cluster.map_shared_rank(gbuf, 0)[rank * PC_NPAIR + pidx] = acc;
+  }
+  cluster.sync();
+  if (rank != 0) return;
+  // rank 0: G(l, i) = v_l(i) + sum over ranks; T (forward, columnwise) as qr_panel_kernel
+  double* G = gbuf + CL * PC_NPAIR;       // QR_NB x QR_NB
+  double* Ts = G + QR_NB * QR_NB;
+  for (int pidx = tid; pidx < ncol * (ncol - 1) / 2; pidx += PC_NT) {
+    int i = 1, acc0 = 0;
+    while (acc0 + i <= pidx) { acc0 += i; ++i; }
+    const int l = pidx - acc0;
+    double v = P[l * chunk + i];   // v_l(i) (row i < QR_NB lives in rank 0)
+    for (int r = 0; r < CL; ++r) v += gbuf[r * PC_NPAIR + pidx];
+    G[l * QR_NB + i] = v;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    for (int i = 0; i < ncol; ++i) {
+      double v = 0.0;
+      if (lane < i)
+        for (int l2 = lane; l2 < i; ++l2) v += Ts[lane + l2 * QR_NB] * G[l2 * QR_NB + i];
+      __syncwarp();
+      if (lane < i) Ts[lane + i * QR_NB] = -taus[i] * v;
+      for (int r = i + 1 + lane; r < QR_NB; r += 32) Ts[r + i * QR_NB] = 0.0;
+      if (lane == 0) Ts[i + i * QR_NB] = taus[i];
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < QR_NB * QR_NB; e += PC_NT) {
+    const int r = e % QR_NB, c = e / QR_NB;
+    d.T[e] = (r < ncol && c < ncol) ? Ts[e] : 0.0;
+  }
+  if (d.tau)
+    for (int e = tid; e < ncol; e += PC_NT) d.tau[e] = taus[e];
+}
+
+template <int CL>
+void launch_panel_cl(cudaStream_t s, const PanelDesc* d, int np, int chunk) {
+  static bool attr = false;
+  const size_t smem = ((size_t)QR_NB * chunk + (size_t)CL * PC_NPAIR + 2 * QR_NB * QR_NB) * sizeof(double);
+  if (!attr) {
+    RSF_CUDA(cudaFuncSetAttribute(qr_panel_cl_kernel<CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_MAX));
+    if (CL > 8) RSF_CUDA(cudaFuncSetAttribute(qr_panel_cl_kernel<CL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(np * CL));
+  cfg.blockDim = dim3(PC_NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  RSF_CUDA(cudaLaunchKernelEx(&cfg, qr_panel_cl_kernel<CL>, d));
+  count_launch();
+}
+
 // panels in global memory (too tall for shared memory) are latency bound: give them
 // 1024 threads (one warp per remaining panel column, 4x the loads in flight)
 void launch_panels(cudaStream_t s, const std::vector<PanelDesc>& pd, const PanelDesc* d, size_t smem_need) {
@@ -454,7 +628,22 @@ void launch_panels(cudaStream_t s, const std::vector<PanelDesc>& pd, const Panel
     attr = true;
   }
   bool tall = false;
-  for (auto& p : pd) tall |= (p.smem == 0);
+  int maxrows = 0;
+  for (auto& p : pd) { tall |= (p.smem == 0); maxrows = std::max(maxrows, p.rows); }
+  static const bool cl_on = !(getenv("RSF_PANEL_CLUSTER") && getenv("RSF_PANEL_CLUSTER")[0] == '0');
+  if (tall && cl_on && maxrows <= 16 * PC_MAXROWS && pd.size() <= 65535) {
+    int CL = 2;
+    while ((maxrows + CL - 1) / CL > PC_MAXROWS) CL *= 2;
+    const int chunk = std::max((maxrows + CL - 1) / CL, QR_NB);
+    switch (CL) {
+      case 2: launch_panel_cl<2>(s, d, (int)pd.size(), chunk); break;
+      case 4: launch_panel_cl<4>(s, d, (int)pd.size(), chunk); break;
+      case 8: launch_panel_cl<8>(s, d, (int)pd.size(), chunk); break;
+      default: launch_panel_cl<16>(s, d, (int)pd.size(), chunk); break;
+    }
+    RSF_LAUNCH_CHECK();
+    return;
+  }
   for (size_t o = 0; o < pd.size(); o += 65535) {
     const unsigned nb = (unsigned)std::min<size_t>(65535, pd.size() - o);
     if (tall) qr_panel_kernel<1024><<<nb, 1024, smem_need, s>>>(d + o);

@@ -647,18 +647,20 @@ __global__ void __launch_bounds__(P_NT, (BN >= 128 ? 1 : 2)) gemm_pipe_kernel(co
                                                             const int* __restrict__ prefix, int nprob,
                                                             double* X0, double* X1, int ldx, int Mglob,
                                                             double* ws, const long long* __restrict__ mnpre,
-                                                            int kchunk) {
+                                                            int kchunk, int mtiles) {
   constexpr int LDB = p_ldb<BN>(), NI = BN / 16, WN = BN / 2;
   extern __shared__ __align__(16) double psm[];
   double* As = psm;                              // [ST][BK][LDA]
   double* Bs = psm + P_ST * P_BK * P_LDA;        // [ST][BK][LDB]
-  const int p = find_prob(prefix, nprob, blockIdx.x);
+  // 1-D grid, M-tiles fastest: the CTAs sharing an N-tile (and its B tile) run together
+  const int bid_n = (int)(blockIdx.x / mtiles), bid_m = (int)(blockIdx.x % mtiles);
+  const int p = find_prob(prefix, nprob, bid_n);
   const GemmDesc& dd = descs[p];
   const int M = dd.M < 0 ? Mglob : dd.M;
   const int N = dd.N, K = dd.K;
-  const int m0 = blockIdx.y * P_BM;
+  const int m0 = bid_m * P_BM;
   if (m0 >= M) return;
-  const int n0 = (blockIdx.x - __ldg(prefix + p)) * BN;
+  const int n0 = (bid_n - __ldg(prefix + p)) * BN;
   if (dd.lower && n0 >= m0 + P_BM) return;
   const double* A = dd.selA == 0 ? dd.A + dd.offA : (dd.selA == 1 ? X0 : X1) + dd.offA * (long long)ldx;
   const double* B = dd.selB == 0 ? dd.B + dd.offB : (dd.selB == 1 ? X0 : X1) + dd.offB * (long long)ldx;
@@ -842,10 +844,12 @@ void launch_pipe(bool ta, bool tb, dim3 grid, cudaStream_t s, const GemmDesc* d,
     cudaFuncSetAttribute(gemm_pipe_kernel<true, true, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
     attr = true;
   }
-  if (!ta && !tb) gemm_pipe_kernel<false, false, BN><<<grid, P_NT, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk);
-  else if (ta && !tb) gemm_pipe_kernel<true, false, BN><<<grid, P_NT, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk);
-  else if (!ta && tb) gemm_pipe_kernel<false, true, BN><<<grid, P_NT, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk);
-  else gemm_pipe_kernel<true, true, BN><<<grid, P_NT, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk);
+  const int mt = (int)grid.y;
+  const dim3 g1((unsigned)((long long)grid.x * grid.y), 1, grid.z);   // 1-D over (N-tile, M-tile)
+  if (!ta && !tb) gemm_pipe_kernel<false, false, BN><<<g1, P_NT, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk, mt);
+  else if (ta && !tb) gemm_pipe_kernel<true, false, BN><<<g1, P_NT, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk, mt);
+  else if (!ta && tb) gemm_pipe_kernel<false, true, BN><<<g1, P_NT, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk, mt);
+  else gemm_pipe_kernel<true, true, BN><<<g1, P_NT, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk, mt);
 }
 
 // split-K reduction: C = alpha * sum_z W_z + beta * C (fixed summation order: deterministic)
