@@ -598,7 +598,10 @@ void launch_panel_cl(cudaStream_t s, const PanelDesc* d, int np, int chunk) {
   static bool attr = false;
   const size_t smem = ((size_t)QR_NB * chunk + (size_t)CL * PC_NPAIR + 2 * QR_NB * QR_NB) * sizeof(double);
   if (!attr) {
-    RSF_CUDA(cudaFuncSetAttribute(qr_panel_cl_kernel<CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_MAX));
+    cudaFuncAttributes fa;
+    RSF_CUDA(cudaFuncGetAttributes(&fa, qr_panel_cl_kernel<CL>));
+    RSF_CUDA(cudaFuncSetAttribute(qr_panel_cl_kernel<CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(SMEM_MAX - fa.sharedSizeBytes)));
     if (CL > 8) RSF_CUDA(cudaFuncSetAttribute(qr_panel_cl_kernel<CL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     attr = true;
   }

@@ -364,9 +364,21 @@ void launch_descs(cudaStream_t s, const std::vector<D>& v, long long maxelems, K
   RSF_LAUNCH_CHECK();
 }
 
+// failure flags of batched factorizations, checked once per level instead of a host
+// synchronisation per call
+__global__ void info_or_kernel(const int* __restrict__ info, int n, int* flag) {
+  for (int i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT)
+    if (info[i]) atomicOr(flag, 1);
+}
+void flag_infos(cudaStream_t s, const int* info, int n, int* dflag) {
+  if (n <= 0) return;
+  info_or_kernel<<<std::max(1, std::min(64, (n + NT - 1) / NT)), NT, 0, s>>>(info, n, dflag);
+  count_launch();
+}
+
 // U <- orth(U) by two passes of U <- U chol(U^T U)^-T (CholeskyQR2), in place.
 struct CQProb { double* U; int rows, k; };
-void cholqr2_batched(cudaStream_t s, const std::vector<CQProb>& v, int lev, double* flops) {
+void cholqr2_batched(cudaStream_t s, const std::vector<CQProb>& v, int lev, double* flops, int* dflag) {
   std::vector<CQProb> w;
   for (auto& p : v) if (p.k > 0 && p.rows > 0) w.push_back(p);
   if (w.empty()) return;
@@ -397,8 +409,7 @@ void cholqr2_batched(cudaStream_t s, const std::vector<CQProb>& v, int lev, doub
     }
     gg.run(s);
     potrf_batched(s, pp, ls.p, inf.p);
-    for (int v2 : inf.to_host(w.size()))
-      if (v2) throw Error(ST_ENUMERIC, "peeling: CholeskyQR of a sketch basis failed at level " + std::to_string(lev));
+    flag_infos(s, inf.p, (int)w.size(), dflag);
     gu.run(s);
   }
 }
@@ -438,6 +449,8 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
   std::vector<PeelLevel> peeled(L + 1);
   long long max_tcols = 0;
   PeelDiag pd;
+  DBuf<int> dfail(1, s);   // set by any failed Cholesky of the level (CholeskyQR, core Gram matrices)
+  dfail.zero();
   pd.cols.assign(L + 1, 0);
   pd.rank_max.assign(L + 1, 0);
   int prev_rank = -1;
@@ -765,7 +778,7 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
                 gq.add(e);
               }
               if (!gh.empty()) { gh.run(s); gq.run(s); }
-              cholqr2_batched(s, cq, lev, &pd.flops);   // right factors keep Q orthogonal to V_i
+              cholqr2_batched(s, cq, lev, &pd.flops, dfail.p);   // right factors keep Q orthogonal to V_i
             }
             // C_ij'(chunk, :) = Y_ij(:, chunk)^T [V_i, Q_i] = [C1, Res^T Q_i]; A_i <- [A_i, W_i^T Q_i]
             // (V_i <- [V_i, Q_i] happened in place)
@@ -871,7 +884,7 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
             cz.push_back(CQProb{arena.p + zo[x], rb[i], k});
           }
           gz1.run(s);
-          cholqr2_batched(s, cz, lev, &pd.flops);
+          cholqr2_batched(s, cz, lev, &pd.flops, dfail.p);
           GemmBatch gx(false, false), gg(true, false), gt1(true, false), gt2(false, false), gt3(true, false);
           std::vector<PotrfProb> pp;
           for (size_t x = 0; x < B; ++x) {
@@ -904,8 +917,7 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
             DBuf<double> ls(std::max<size_t>(pp.size(), 1), s);
             DBuf<int> inf(std::max<size_t>(pp.size(), 1), s);
             potrf_batched(s, pp, ls.p, inf.p);
-            for (int v2 : inf.to_host(pp.size()))
-              if (v2) throw Error(ST_ENUMERIC, "peeling: rank-deficient sketch product at level " + std::to_string(lev));
+            flag_infos(s, inf.p, (int)pp.size(), dfail.p);
           }
           gt1.run(s); gt2.run(s); gt3.run(s);
           for (size_t x = 0; x < B; ++x) {
@@ -997,7 +1009,9 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
         pd.flops += 2.0 * k1 * (double)k2 * c + 2.0 * a.rz * (double)b2.rz * (k1 + k2);
       }
       m1.run(s); m2.run(s); m3.run(s); m4.run(s); m5.run(s); m6.run(s); m7.run(s);
-      RSF_CUDA(cudaStreamSynchronize(s));
+      if (dfail.to_host(1)[0])
+        throw Error(ST_ENUMERIC, "peeling: Cholesky of a sketch basis or core Gram matrix failed at level " +
+                                     std::to_string(lev));
     }
     arenas.clear();
     for (auto& q : pdat) q = PairData{};
