@@ -687,7 +687,7 @@ void geqrf_batched(cudaStream_t s, const std::vector<QRProb>& probs, bool keep_q
   const size_t base_smem = (40 + QR_NB + 2 * QR_NB * QR_NB) * sizeof(double);
   for (int j0 = 0; j0 < maxk; j0 += QR_NB) {
     std::vector<PanelDesc> pd;
-    GemmBatch g1(true, false), g2(true, false), g3(false, false);
+    GemmBatch g1(true, false), g2(false, false), g3(false, true);
     size_t smem_need = base_smem;
     for (int i = 0; i < P; ++i) {
       const QRProb& q = probs[i];
@@ -710,19 +710,20 @@ void geqrf_batched(cudaStream_t s, const std::vector<QRProb>& probs, bool keep_q
       const int j1 = j0 + nbp;
       const int c2 = q.c - j1;
       if (c2 > 0) {
-        GemmDesc a = gdesc(nbp, c2, rows);          // W = V^T A2
-        a.A = d.V; a.lda = rows;
-        a.B = q.A + (long long)j1 * q.lda + j0; a.ldb = (int)q.lda;
-        a.C = W.p + woff[i]; a.ldc = QR_NB;
+        // compact-WY update with the skinny dimension as N (the 128-row tiles stay full):
+        GemmDesc a = gdesc(c2, nbp, rows);          // W^T = A2^T V
+        a.A = q.A + (long long)j1 * q.lda + j0; a.lda = (int)q.lda;
+        a.B = d.V; a.ldb = rows;
+        a.C = W.p + woff[i]; a.ldc = c2;
         g1.add(a);
-        GemmDesc b = gdesc(nbp, c2, nbp);           // W2 = T^T W
-        b.A = d.T; b.lda = QR_NB;
-        b.B = W.p + woff[i]; b.ldb = QR_NB;
-        b.C = W2.p + woff[i]; b.ldc = QR_NB;
+        GemmDesc b = gdesc(c2, nbp, nbp);           // W2^T = W^T T
+        b.A = W.p + woff[i]; b.lda = c2;
+        b.B = d.T; b.ldb = QR_NB;
+        b.C = W2.p + woff[i]; b.ldc = c2;
         g2.add(b);
         GemmDesc c = gdesc(rows, c2, nbp);          // A2 -= V W2
         c.A = d.V; c.lda = rows;
-        c.B = W2.p + woff[i]; c.ldb = QR_NB;
+        c.B = W2.p + woff[i]; c.ldb = c2;
         c.C = q.A + (long long)j1 * q.lda + j0; c.ldc = (int)q.lda;
         c.alpha = -1.0; c.beta = 1.0;
         g3.add(c);
@@ -747,7 +748,7 @@ void panel_step_batched(cudaStream_t s, const std::vector<PanelStep>& v) {
   const size_t base_smem = (40 + QR_NB + 2 * QR_NB * QR_NB) * sizeof(double);
   size_t smem_need = base_smem;
   std::vector<PanelDesc> pd;
-  GemmBatch g1(true, false), g2(true, false), g3(false, false);
+  GemmBatch g1(true, false), g2(false, false), g3(false, true);
   for (const PanelStep& q : v) {
     PanelDesc d;
     d.A = q.A; d.lda = q.lda; d.rows = q.rows; d.ncol = q.ncol;
@@ -758,14 +759,14 @@ void panel_step_batched(cudaStream_t s, const std::vector<PanelStep>& v) {
     pd.push_back(d);
     if (q.c2 > 0) {
       double* A2 = q.A + (long long)q.ncol * q.lda;
-      GemmDesc a = gdesc(q.ncol, q.c2, q.rows);
-      a.A = q.V; a.lda = q.rows; a.B = A2; a.ldb = (int)q.lda; a.C = q.W; a.ldc = QR_NB;
+      GemmDesc a = gdesc(q.c2, q.ncol, q.rows);     // W^T = A2^T V
+      a.A = A2; a.lda = (int)q.lda; a.B = q.V; a.ldb = q.rows; a.C = q.W; a.ldc = q.c2;
       g1.add(a);
-      GemmDesc b = gdesc(q.ncol, q.c2, q.ncol);
-      b.A = q.T; b.lda = QR_NB; b.B = q.W; b.ldb = QR_NB; b.C = q.W2; b.ldc = QR_NB;
+      GemmDesc b = gdesc(q.c2, q.ncol, q.ncol);     // W2^T = W^T T
+      b.A = q.W; b.lda = q.c2; b.B = q.T; b.ldb = QR_NB; b.C = q.W2; b.ldc = q.c2;
       g2.add(b);
-      GemmDesc c = gdesc(q.rows, q.c2, q.ncol);
-      c.A = q.V; c.lda = q.rows; c.B = q.W2; c.ldb = QR_NB; c.C = A2; c.ldc = (int)q.lda;
+      GemmDesc c = gdesc(q.rows, q.c2, q.ncol);     // A2 -= V W2
+      c.A = q.V; c.lda = q.rows; c.B = q.W2; c.ldb = q.c2; c.C = A2; c.ldc = (int)q.lda;
       c.alpha = -1.0; c.beta = 1.0;
       g3.add(c);
     }
