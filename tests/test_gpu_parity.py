@@ -332,3 +332,50 @@ def test_fused_sweeps_match_batched_gemm_path(tmp_path):
         out[flag] = np.load(f)
     a, b = out["1"], out["0"]
     assert np.linalg.norm(a - b) <= 1e-10 * np.linalg.norm(b)
+
+
+@pytest.fixture(scope="module")
+def cfg2_4096(ctx):
+    """Config 2's recipe (Matern 3/2, theta = (rho, sigma2)) at n = 4096: dense oracle O1."""
+    c, xy, ok, rk, z = _case(2, 4096)
+    d = dense_eval(ok, xy, z)
+    return c, xy, ok, rk, z, d
+
+
+def test_cfg2_sigma_rho_compression_and_traces(ctx, cfg2_4096):
+    """Sigma_rho compression (apply-only, R-F) against the dense derivative matrix on 24 random
+    vectors; peeled Tr(F^-1 F_rho) and Tr(F^-1) (G = F^-1, R-G) against the dense traces."""
+    c, xy, ok, rk, z, d = cfg2_4096
+    n = len(xy)
+    F = R.Factor(ctx, _d(xy), rk, c.eps_fact, c.leaf)
+    Fi = R.Factor(ctx, _d(xy), rk, c.eps_fact, c.leaf, which=0)
+    V = np.random.default_rng(21).standard_normal((24, n))
+    Si = ok.dsigma_block("rho", xy, np.arange(n), np.arange(n))
+    got = Fi.apply(_d(V)).cpu().numpy()
+    want = V @ Si
+    assert np.linalg.norm(got - want) <= 1e-6 * np.linalg.norm(want)
+    tr, pd = R.peel_trace(F, Fi, c.eps_peel)
+    assert abs(tr - d["trace"][0]) <= 1e-5 * abs(d["trace"][0])
+    tinv, _ = R.peel_trace(F, None, c.eps_peel)
+    assert abs(tinv - d["trace_inv"]) <= 1e-5 * d["trace_inv"]
+
+
+def test_abi_strided_and_host_blocks(ctx, cfg2_4096):
+    """rsf_solve on a strided (ld > n) host block equals the device result; nrhs = 0 is a no-op;
+    ld < n is rejected (RSF_EINVAL)."""
+    import ctypes as C
+    from paper_1603_08057_b200 import _lib
+    c, xy, ok, rk, z, d = cfg2_4096
+    n = len(xy)
+    F = R.Factor(ctx, _d(xy), rk, c.eps_fact, c.leaf)
+    B = np.random.default_rng(22).standard_normal((3, n))
+    ref = F.solve(_d(B)).cpu().numpy()
+    ld = n + 5
+    H = np.zeros((3, ld))
+    H[:, :n] = B
+    out = np.zeros_like(H)
+    st = R.lib.rsf_solve(F.h, H.ctypes.data, out.ctypes.data, 3, ld)
+    assert st == 0
+    assert np.array_equal(out[:, :n], ref)
+    assert R.lib.rsf_solve(F.h, H.ctypes.data, out.ctypes.data, 0, ld) == 0
+    assert R.lib.rsf_solve(F.h, H.ctypes.data, out.ctypes.data, 3, n - 1) == _lib.RSF_EINVAL
