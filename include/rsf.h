@@ -144,6 +144,12 @@ rsf_status rsf_sample(rsf_fact f, const double* w, double* z, int64_t nrhs, int6
 rsf_status peel_trace(rsf_fact F, rsf_fact Fi, double eps_peel, const rsf_opts* opts, int32_t trace_id,
                       double* trace, rsf_peel_diag* diag);
 
+/* Hutchinson estimate (Eq. hutch; the baseline the paper compares peeling with):
+ * trace = (1/q) sum_p u_p^T F^-1 F_i u_p over q = nprobe Rademacher probes (Philox4x32-10, key (seed, 4),
+ * counter (original point index, probe, 0, 0), sign from bit 0), std_err = sample standard deviation / sqrt(q).
+ * Fi == NULL estimates Tr(F^-1).  One solve and one apply per probe.  trace, std_err: host. */
+rsf_status hutch_trace(rsf_fact F, rsf_fact Fi, int64_t nprobe, uint64_t seed, double* trace, double* std_err);
+
 /* Alg. 1: l-hat and g-hat at theta = kernel values.  eps is the ID tolerance of every
  * factorization (eps_fact), opts->eps_peel the peeling tolerance.  ell: host scalar; grad: host
  * array of p doubles.  xy, z device or host.  diag nullable. */

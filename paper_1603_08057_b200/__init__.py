@@ -178,6 +178,14 @@ def peel_trace(F: Factor, Fi: Factor | None, eps_peel: float = 1e-6, opts: Opts 
     return v.value, d
 
 
+def hutch_trace(F: Factor, Fi: Factor | None, nprobe: int = 64, seed: int = 1603080570):
+    """Hutchinson estimate of Tr(F^-1 F_i) (Fi None: Tr(F^-1)) -> (trace, standard error)."""
+    t = C.c_double()
+    se = C.c_double()
+    _check(lib.hutch_trace(F.h, Fi.h if Fi is not None else None, nprobe, seed, C.byref(t), C.byref(se)))
+    return t.value, se.value
+
+
 @dataclass
 class EvalResult:
     ell: float

@@ -292,6 +292,18 @@ rsf_status rsf_sample(rsf_fact f, const double* w, double* z, int64_t nrhs, int6
   });
 }
 
+rsf_status hutch_trace(rsf_fact F, rsf_fact Fi, int64_t nprobe, uint64_t seed, double* trace, double* std_err) {
+  return guard([&] {
+    RSF_REQUIRE(F && trace && std_err, rsf::ST_EINVAL, "null argument");
+    RSF_REQUIRE(F->F->which == rsf::W_SIGMA, rsf::ST_EINVAL, "F must be a Sigma factor");
+    RSF_REQUIRE(!Fi || Fi->F->which != rsf::W_SIGMA, rsf::ST_EINVAL, "Fi must be a Sigma_i compression");
+    RSF_REQUIRE(!Fi || Fi->F->n() == F->F->n(), rsf::ST_EINVAL, "dimension mismatch");
+    RSF_REQUIRE(nprobe >= 1, rsf::ST_EINVAL, "nprobe must be >= 1");
+    RSF_CUDA(cudaSetDevice(F->owner->ctx.device));
+    rsf::hutch(*F->F, Fi ? Fi->F.get() : nullptr, nprobe, seed, trace, std_err);
+  });
+}
+
 rsf_status peel_trace(rsf_fact F, rsf_fact Fi, double eps_peel, const rsf_opts* opts, int32_t trace_id,
                       double* trace, rsf_peel_diag* diag) {
   return guard([&] {

@@ -64,6 +64,29 @@ __global__ void probes_kernel(double* X, int k, int t0, int t1, const int* __res
   }
 }
 
+// Hutchinson probes (R-W stream 4): X'(j, t) = +-1 from bit 0 of the first Philox
+// word of counter (perm[t], col0 + j, 0, 0) under key (seed, 4)
+__global__ void rademacher_kernel(double* X, int k, int n, const int* __restrict__ perm, int col0, unsigned seed) {
+  const long long tot = (long long)n * k;
+  for (long long e = blockIdx.x * (long long)NT + threadIdx.x; e < tot; e += (long long)gridDim.x * NT) {
+    const int t = (int)(e / k), j = (int)(e % k);
+    const uint4 x = philox4x32_10(make_uint4((unsigned)perm[t], (unsigned)(col0 + j), 0u, 0u), make_uint2(seed, 4u));
+    X[e] = (x.x & 1u) ? -1.0 : 1.0;
+  }
+}
+
+// per-row dot products of two k x n X'-blocks: part[b * k + j] = sum_{t in block b} A'(j,t) B'(j,t)
+__global__ void rowdot_kernel(const double* __restrict__ A, const double* __restrict__ B, int k, int n,
+                              double* part) {
+  const int per = (n + gridDim.x - 1) / gridDim.x;
+  const int t0 = blockIdx.x * per, t1 = min(n, t0 + per);
+  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    double acc = 0.0;
+    for (int t = t0; t < t1; ++t) acc += A[(long long)t * k + j] * B[(long long)t * k + j];
+    part[(long long)blockIdx.x * k + j] = acc;
+  }
+}
+
 // probe rows of a list of tree indices: X'(j, q) = normal(perm[rows[q]], col0 + j, level, trace)
 __global__ void probes_rows_kernel(double* X, int k, const int* __restrict__ rows, long long nrows,
                                    const int* __restrict__ perm, int col0, int lev, int tr, unsigned seed) {
@@ -1117,6 +1140,51 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
   pd.seconds = now_s() - t0;
   if (diag) *diag = pd;
   return tr;
+}
+
+// Hutchinson estimate of Tr(F^-1 F_i) (Fi != null) or Tr(F^-1): (1/q) sum_p u_p^T F^-1 F_i u_p
+// with Rademacher u_p; u^T F^-1 F_i u = (F^-1 u)^T (F_i u), one solve + one apply
+// per probe.  Deterministic (fixed-order reductions).
+void hutch(const Fact& F, const Fact* Fi, long long q, unsigned long long seed, double* mean, double* se) {
+  RSF_REQUIRE(q >= 1, ST_EINVAL, "hutch: nprobe < 1");
+  cudaStream_t s = F.ctx->stream;
+  const Tree& t = *F.tree;
+  const int n = t.n, kb = 512, GB = 256;
+  DBuf<double> U((size_t)n * kb, s), A((size_t)n * kb, s), B, C, tmp((size_t)std::max<long long>(F.tmp_cols, 1) * kb, s);
+  if (Fi) { B.alloc((size_t)n * kb, s); C.alloc((size_t)n * kb, s); }
+  DBuf<double> part((size_t)GB * kb, s);
+  std::vector<double> vals;
+  vals.reserve(q);
+  for (long long p0 = 0; p0 < q; p0 += kb) {
+    const int k = (int)std::min<long long>(kb, q - p0);
+    const long long nn = (long long)n * k;
+    rademacher_kernel<<<gxx(nn), NT, 0, s>>>(U.p, k, n, t.d_perm.p, (int)p0, (unsigned)(seed & 0xffffffffull));
+    count_launch();
+    RSF_CUDA(cudaMemcpyAsync(A.p, U.p, nn * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    solve_internal(F, A.p, k, tmp.p);                                   // A = F^-1 U
+    const double* other = U.p;
+    if (Fi) {
+      RSF_CUDA(cudaMemcpyAsync(B.p, U.p, nn * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      apply_only_internal(*Fi, B.p, C.p, k);                            // C = F_i U
+      other = C.p;
+    }
+    rowdot_kernel<<<GB, 256, 0, s>>>(A.p, other, k, n, part.p);
+    count_launch();
+    RSF_LAUNCH_CHECK();
+    const std::vector<double> h = part.to_host((size_t)GB * k);
+    for (int j = 0; j < k; ++j) {
+      double v = 0.0;
+      for (int b = 0; b < GB; ++b) v += h[(size_t)b * k + j];
+      vals.push_back(v);
+    }
+  }
+  double m = 0.0;
+  for (double v : vals) m += v;
+  m /= (double)vals.size();
+  double var = 0.0;
+  for (double v : vals) var += (v - m) * (v - m);
+  *mean = m;
+  *se = vals.size() > 1 ? std::sqrt(var / (double)(vals.size() - 1) / (double)vals.size()) : INFINITY;
 }
 
 void fill_peel_diag(const PeelDiag& d, rsf_peel_diag* out) {

@@ -18,6 +18,9 @@ struct PeelDiag {
 double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag* diag);
 void fill_peel_diag(const PeelDiag& d, rsf_peel_diag* out);
 
+// Hutchinson estimate of Tr(F^-1 F_i) or Tr(F^-1): mean and standard error over q probes
+void hutch(const Fact& F, const Fact* Fi, long long q, unsigned long long seed, double* mean, double* se);
+
 struct EvalResult {
   double ell = 0, logdet = 0, quad = 0;
   double grad[4] = {0, 0, 0, 0}, q[4] = {0, 0, 0, 0}, trace[4] = {0, 0, 0, 0};

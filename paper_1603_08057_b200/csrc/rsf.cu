@@ -45,6 +45,18 @@ struct BRef {
 
 }  // namespace
 
+// per-level phase names for RSF_PROFILE=1 (diagnostics)
+static const char* lvname(const char* op, int lev) {
+  static std::vector<std::string> names;
+  if (!Prof::enabled()) return op;
+  const std::string key = std::string(op) + ".L" + std::to_string(lev);
+  for (size_t i = 0; i < names.size(); ++i) if (names[i] == key) return names[i].c_str();
+  if (names.empty()) names.reserve(4096);   // stable c_str() pointers
+  if (names.size() >= 4096) return op;
+  names.push_back(key);
+  return names.back().c_str();
+}
+
 std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams& kp, int which,
                              double eps, const Opts& opts, bool solve_only) {
   RSF_REQUIRE(eps > 0.0, ST_EINVAL, "eps must be > 0");
@@ -70,6 +82,7 @@ std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams
   double logdet = 0.0;
 
   for (int lev = L; lev >= 1; --lev) {
+    RSF_PHASE(lvname(sig ? "fS" : "fI", lev), s);
     Level& LV = F->levels[lev];
     LV.lev = lev;
     const std::vector<int>& nodes = t.levels[lev];
@@ -599,18 +612,6 @@ std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams
 }
 
 // ------------------------------------------------------------------ operators
-// per-level phase names for RSF_PROFILE=1 (diagnostics)
-static const char* lvname(const char* op, int lev) {
-  static std::vector<std::string> names;
-  if (!Prof::enabled()) return op;
-  const std::string key = std::string(op) + ".L" + std::to_string(lev);
-  for (size_t i = 0; i < names.size(); ++i) if (names[i] == key) return names[i].c_str();
-  if (names.empty()) names.reserve(4096);   // stable c_str() pointers
-  if (names.size() >= 4096) return op;
-  names.push_back(key);
-  return names.back().c_str();
-}
-
 void solve_internal(const Fact& F, double* X, int k, double* tmp) {
   RSF_REQUIRE(F.which == W_SIGMA, ST_EINVAL, "solve needs a Sigma factor");
   cudaStream_t s = F.ctx->stream;

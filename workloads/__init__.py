@@ -22,7 +22,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 __all__ = [
-    "philox4x32", "philox_uniform_pair", "philox_normal_pair", "philox_normal",
+    "philox4x32", "philox_uniform_pair", "philox_normal_pair", "philox_normal", "philox_rademacher",
     "CONFIGS", "Config", "points_for", "w_for", "config",
 ]
 
@@ -33,7 +33,7 @@ _W1 = np.uint64(0xBB67AE85)
 _MASK = np.uint64(0xFFFFFFFF)
 
 SEED_BASE = 1603080570  # R-W: seed_k = SEED_BASE + k
-STREAM_POINTS, STREAM_MIXTURE, STREAM_W, STREAM_PROBES = 0, 1, 2, 3
+STREAM_POINTS, STREAM_MIXTURE, STREAM_W, STREAM_PROBES, STREAM_HUTCH = 0, 1, 2, 3, 4
 
 
 def philox4x32(c0, c1, c2, c3, k0: int, k1: int):
@@ -87,6 +87,14 @@ def philox_normal(seed: int, stream: int, c0, c1, c2, c3):
     """
     n0, _ = philox_normal_pair(c0, c1, c2, c3, seed, stream)
     return n0
+
+
+def philox_rademacher(seed: int, c0, c1):
+    """Rademacher (+-1) entries for the Hutchinson estimator (stream 4, R-W): entry
+    (point j, probe p) is +1 if bit 0 of the first Philox4x32-10 output word of counter
+    (j, p, 0, 0) under key (seed, 4) is 0, else -1."""
+    x0, _, _, _ = philox4x32(c0, c1, 0, 0, seed, STREAM_HUTCH)
+    return 1.0 - 2.0 * (x0 & np.uint64(1)).astype(np.float64)
 
 
 # --------------------------------------------------------------------------
