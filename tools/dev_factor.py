@@ -22,5 +22,5 @@ for rep in range(reps):
     print(f'rep {rep}: factor {tf:.3f}s ({fl/1e12:.2f} TF algorithmic -> {fl/tf/1e12:.2f} TF/s), compressions {tc:.3f}s')
     del F, Fi
 prof = R.lib.rsf_profile_dump().decode()
-items = sorted([(float(v), k) for k, v in (x.split('=') for x in prof.strip(';').split(';'))], reverse=True)
+items = sorted([(float(v), k) for k, v in (x.split("=") for x in prof.strip(";").split(";") if "=" in x)], reverse=True) if prof else []
 print('PROFILE', ' '.join(f'{k}={v:.3f}' for v, k in items))
