@@ -5,6 +5,7 @@
 #include <ctime>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 
@@ -36,49 +37,78 @@ std::mutex& cache_mu() { static std::mutex m; return m; }
 std::vector<FreeList>& cache() { static std::vector<FreeList> v; return v; }
 int bin_of(size_t bytes) { int b = 8; while ((size_t(1) << b) < bytes) ++b; return b; }   // >= 256 B
 }  // namespace
-// large blocks: best fit among cached blocks of the same stream (at most 1.5x + 64 MB of
-// slack), bounded total; the stream-ordered pool grows by mapping new memory for every miss
-constexpr size_t LARGE_CACHE_MAX = size_t(48) << 30;
+// Large blocks (> 64 MB): a per-stream arena reserved once (half the free device memory, at
+// most 40 GB) with a best-fit free list and coalescing; requests that do not fit fall back to
+// cudaMallocAsync.  The request sequence of an evaluation repeats exactly, so after the first
+// evaluation every large request is served without a driver call (the stream-ordered pool
+// maps new memory on a miss, which measured up to ~1 s for a 2 GB block).
 double g_amiss_small = 0, g_amiss_large = 0, g_amax = 0;
 long long g_nmiss_small = 0, g_nmiss_large = 0;
 double g_amax_bytes = 0;
-struct Large { cudaStream_t s; void* p; size_t bytes; };
-std::vector<Large>& large() { static std::vector<Large> v; return v; }
-size_t& large_total() { static size_t t = 0; return t; }
+struct Arena {
+  cudaStream_t s = nullptr;
+  char* base = nullptr;
+  size_t cap = 0;
+  std::map<size_t, size_t> free_;   // offset -> size
+};
+std::vector<Arena>& arenas() { static std::vector<Arena> v; return v; }
+Arena* arena_for(cudaStream_t s) {
+  for (auto& a : arenas()) if (a.s == s) return &a;
+  size_t fr = 0, tot = 0;
+  cudaMemGetInfo(&fr, &tot);
+  size_t cap = std::min<size_t>(fr / 2, size_t(40) << 30) / (size_t(2) << 20) * (size_t(2) << 20);
+  Arena a;
+  a.s = s;
+  if (cap >= (size_t(1) << 30) && cudaMallocAsync((void**)&a.base, cap, s) == cudaSuccess) {
+    a.cap = cap;
+    a.free_[0] = cap;
+  } else {
+    cudaGetLastError();
+    a.base = nullptr;
+  }
+  arenas().push_back(a);
+  return &arenas().back();
+}
+void* arena_alloc(Arena* a, size_t bytes) {
+  if (!a->base) return nullptr;
+  auto best = a->free_.end();
+  for (auto it = a->free_.begin(); it != a->free_.end(); ++it)
+    if (it->second >= bytes && (best == a->free_.end() || it->second < best->second)) best = it;
+  if (best == a->free_.end()) return nullptr;
+  const size_t off = best->first, sz = best->second;
+  a->free_.erase(best);
+  if (sz > bytes) a->free_[off + bytes] = sz - bytes;
+  return a->base + off;
+}
+bool arena_free(cudaStream_t s, void* p, size_t bytes) {
+  for (auto& a : arenas()) {
+    if (a.s != s || !a.base || (char*)p < a.base || (char*)p >= a.base + a.cap) continue;
+    size_t off = (size_t)((char*)p - a.base), sz = bytes;
+    auto nx = a.free_.lower_bound(off);
+    if (nx != a.free_.end() && off + sz == nx->first) { sz += nx->second; nx = a.free_.erase(nx); }
+    if (nx != a.free_.begin()) {
+      auto pv = std::prev(nx);
+      if (pv->first + pv->second == off) { off = pv->first; sz += pv->second; a.free_.erase(pv); }
+    }
+    a.free_[off] = sz;
+    return true;
+  }
+  return false;
+}
 void* dev_alloc(size_t bytes, cudaStream_t s) {
   void* p = nullptr;
   if (bytes > CACHE_MAX) {
+    const size_t rb = (bytes + (size_t(2) << 20) - 1) / (size_t(2) << 20) * (size_t(2) << 20);
     {
       std::lock_guard<std::mutex> lk(cache_mu());
-      auto& L = large();
-      size_t best = L.size();
-      for (size_t i = 0; i < L.size(); ++i)
-        if (L[i].s == s && L[i].bytes >= bytes && L[i].bytes <= 4 * bytes + CACHE_MAX &&
-            (best == L.size() || L[i].bytes < L[best].bytes))
-          best = i;
-      if (best < L.size()) {
-        p = L[best].p;
-        large_total() -= L[best].bytes;
-        L.erase(L.begin() + best);
-        return p;
-      }
+      p = arena_alloc(arena_for(s), rb);
     }
-    const size_t rb = (bytes + (size_t(2) << 20) - 1) / (size_t(2) << 20) * (size_t(2) << 20);
+    if (p) return p;
     const double t0 = wall();
-    cudaError_t e = cudaMallocAsync(&p, rb, s);
+    RSF_CUDA(cudaMallocAsync(&p, rb, s));
     const double dt = wall() - t0;
     g_amiss_large += dt; ++g_nmiss_large;
     if (dt > g_amax) { g_amax = dt; g_amax_bytes = (double)rb; }
-    if (e == cudaErrorMemoryAllocation) {   // give the cached large blocks back and retry
-      cudaGetLastError();
-      std::lock_guard<std::mutex> lk(cache_mu());
-      for (auto& b : large()) cudaFreeAsync(b.p, b.s);
-      large().clear();
-      large_total() = 0;
-      cudaStreamSynchronize(s);
-      e = cudaMallocAsync(&p, rb, s);
-    }
-    RSF_CUDA(e);
     return p;
   }
   const int b = bin_of(bytes);
@@ -98,9 +128,9 @@ void dev_cache_trim(cudaStream_t s) {
   std::lock_guard<std::mutex> lk(cache_mu());
   for (auto& f : cache())
     if (f.s == s) { for (void* p : f.blocks) cudaFreeAsync(p, s); f.blocks.clear(); }
-  auto& L = large();
-  for (size_t i = 0; i < L.size();) {
-    if (L[i].s == s) { cudaFreeAsync(L[i].p, s); large_total() -= L[i].bytes; L.erase(L.begin() + i); }
+  auto& A = arenas();
+  for (size_t i = 0; i < A.size();) {
+    if (A[i].s == s) { if (A[i].base) cudaFreeAsync(A[i].base, s); A.erase(A.begin() + i); }
     else ++i;
   }
 }
@@ -108,15 +138,11 @@ void dev_free(void* p, size_t bytes, cudaStream_t s) {
   if (!p) return;
   if (bytes > CACHE_MAX) {
     const size_t rb = (bytes + (size_t(2) << 20) - 1) / (size_t(2) << 20) * (size_t(2) << 20);
-    std::lock_guard<std::mutex> lk(cache_mu());
-    auto& L = large();
-    L.push_back(Large{s, p, rb});
-    large_total() += rb;
-    while (large_total() > LARGE_CACHE_MAX && !L.empty()) {   // drop the oldest
-      cudaFreeAsync(L.front().p, L.front().s);
-      large_total() -= L.front().bytes;
-      L.erase(L.begin());
+    {
+      std::lock_guard<std::mutex> lk(cache_mu());
+      if (arena_free(s, p, rb)) return;
     }
+    cudaFreeAsync(p, s);
     return;
   }
   const int b = bin_of(bytes);
@@ -680,7 +706,29 @@ __global__ void __launch_bounds__(P_NT, (BN >= 128 ? 1 : 2)) gemm_pipe_kernel(co
   // (A not transposed, B transposed) and the operand is 16-byte aligned with an even ld
   const bool vecA = !TA && ((reinterpret_cast<unsigned long long>(A) & 15ull) == 0) && ((lda & 1) == 0);
   const bool vecB = TB && ((reinterpret_cast<unsigned long long>(B) & 15ull) == 0) && ((ldb & 1) == 0);
-  auto load_stage = [&](int st, int k0) {
+
+  // K range of the nonzero rows of op(B) for this N tile (triangular B: TRMM-style skipping)
+  int kbeg = dd.btri == 1 ? min(n0, K) : 0;
+  int kend = dd.btri == 2 ? min(K, n0 + BN) : K;
+  if (ws) {   // split-K: this CTA's slice of K, partial product to the workspace
+    kbeg = max(kbeg, (int)blockIdx.z * kchunk);
+    kend = min(kend, ((int)blockIdx.z + 1) * kchunk);
+  }
+  const int nk = kend > kbeg ? (kend - kbeg + P_BK - 1) / P_BK : 0;
+
+  // Resolved K-indices of every stage, one stage ahead (so the gathers through mapK / mapA /
+  // mapB never stall the copy issue): kA[st][l] = column of A (or K offset for TA), kB[st][l]
+  // = row/column of B for K-index l of stage st, -1 past the end of K.
+  __shared__ int kA[P_ST][P_BK], kB[P_ST][P_BK];
+  auto kindex = [&](int stage, int l, bool forA) -> int {
+    const int gl = kbeg + stage * P_BK + l;
+    if (gl >= kend) return -1;
+    const int kx = mapK ? __ldg(mapK + gl) : gl;
+    if (forA) return (!TA && mapA) ? __ldg(mapA + kx) : kx;
+    return (TB && mapB) ? __ldg(mapB + kx) : kx;
+  };
+
+  auto load_stage = [&](int st, int stage) {
     double* as = As + st * P_BK * P_LDA;
     double* bs = Bs + st * P_BK * LDB;
     if (vecA) {
@@ -688,32 +736,25 @@ __global__ void __launch_bounds__(P_NT, (BN >= 128 ? 1 : 2)) gemm_pipe_kernel(co
       for (int r = 0; r < (P_BM * P_BK) / (2 * P_NT); ++r) {
         const int e = tid + r * P_NT;
         const int i = 2 * (e % (P_BM / 2)), l = e / (P_BM / 2);
-        const int gi = m0 + i, gl = k0 + l;
-        const int nv = (gl < K) ? max(0, min(2, M - gi)) : 0;
-        const double* src = A;
-        if (nv) {
-          const int kx = mapK ? __ldg(mapK + gl) : gl;
-          const long long c = mapA ? __ldg(mapA + kx) : kx;
-          src = A + c * lda + gi;
-        }
-        cp_async16(as + l * P_LDA + i, src, 8 * nv);
+        const int gi = m0 + i, c = kA[st][l];
+        const int nv = (c >= 0) ? max(0, min(2, M - gi)) : 0;
+        cp_async16(as + l * P_LDA + i, nv ? A + (long long)c * lda + gi : A, 8 * nv);
       }
     } else {
 #pragma unroll
-    for (int r = 0; r < (P_BM * P_BK) / P_NT; ++r) {
-      const int e = tid + r * P_NT;
-      int i, l;
-      if (!TA) { i = e % P_BM; l = e / P_BM; } else { l = e % P_BK; i = e / P_BK; }
-      const int gi = m0 + i, gl = k0 + l;
-      const bool v = gi < M && gl < K;
-      const double* src = A;
-      if (v) {
-        const int kx = mapK ? __ldg(mapK + gl) : gl;
-        if (!TA) { const long long c = mapA ? __ldg(mapA + kx) : kx; src = A + c * lda + gi; }
-        else { const long long c = mapA ? __ldg(mapA + gi) : gi; src = A + c * lda + kx; }
+      for (int r = 0; r < (P_BM * P_BK) / P_NT; ++r) {
+        const int e = tid + r * P_NT;
+        int i, l;
+        if (!TA) { i = e % P_BM; l = e / P_BM; } else { l = e % P_BK; i = e / P_BK; }
+        const int gi = m0 + i, c = kA[st][l];
+        const bool v = gi < M && c >= 0;
+        const double* src = A;
+        if (v) {
+          if (!TA) src = A + (long long)c * lda + gi;
+          else { const long long ci = mapA ? __ldg(mapA + gi) : gi; src = A + ci * lda + c; }
+        }
+        cp_async8(as + l * P_LDA + i, src, v);
       }
-      cp_async8(as + l * P_LDA + i, src, v);
-    }
     }
     if (vecB) {
 #pragma unroll
@@ -721,15 +762,9 @@ __global__ void __launch_bounds__(P_NT, (BN >= 128 ? 1 : 2)) gemm_pipe_kernel(co
         const int e = tid + r * P_NT;
         if ((P_BK * BN) % (2 * P_NT) != 0 && e >= P_BK * BN / 2) break;
         const int j = 2 * (e % (BN / 2)), l = e / (BN / 2);
-        const int gl = k0 + l, gj = n0 + j;
-        const int nv = (gl < K) ? max(0, min(2, N - gj)) : 0;
-        const double* src = B;
-        if (nv) {
-          const int kx = mapK ? __ldg(mapK + gl) : gl;
-          const long long c = mapB ? __ldg(mapB + kx) : kx;
-          src = B + c * ldb + gj;
-        }
-        cp_async16(bs + l * LDB + j, src, 8 * nv);
+        const int gj = n0 + j, c = kB[st][l];
+        const int nv = (c >= 0) ? max(0, min(2, N - gj)) : 0;
+        cp_async16(bs + l * LDB + j, nv ? B + (long long)c * ldb + gj : B, 8 * nv);
       }
       return;
     }
@@ -738,13 +773,12 @@ __global__ void __launch_bounds__(P_NT, (BN >= 128 ? 1 : 2)) gemm_pipe_kernel(co
       const int e = tid + r * P_NT;
       int l, j;
       if (!TB) { l = e % P_BK; j = e / P_BK; } else { j = e % BN; l = e / BN; }
-      const int gl = k0 + l, gj = n0 + j;
-      const bool v = gl < K && gj < N;
+      const int gj = n0 + j, c = kB[st][l];
+      const bool v = c >= 0 && gj < N;
       const double* src = B;
       if (v) {
-        const int kx = mapK ? __ldg(mapK + gl) : gl;
-        if (!TB) { const long long c = mapB ? __ldg(mapB + gj) : gj; src = B + c * ldb + kx; }
-        else { const long long c = mapB ? __ldg(mapB + kx) : kx; src = B + c * ldb + gj; }
+        if (!TB) { const long long cj = mapB ? __ldg(mapB + gj) : gj; src = B + cj * ldb + c; }
+        else src = B + (long long)c * ldb + gj;
       }
       cp_async8(bs + l * LDB + j, src, v);
     }
@@ -756,25 +790,29 @@ __global__ void __launch_bounds__(P_NT, (BN >= 128 ? 1 : 2)) gemm_pipe_kernel(co
 #pragma unroll
     for (int b = 0; b < NI; ++b) { acc[a][b][0] = 0.0; acc[a][b][1] = 0.0; }
 
-  // K range of the nonzero rows of op(B) for this N tile (triangular B: TRMM-style skipping)
-  int kbeg = dd.btri == 1 ? min(n0, K) : 0;
-  int kend = dd.btri == 2 ? min(K, n0 + BN) : K;
-  if (ws) {   // split-K: this CTA's slice of K, partial product to the workspace
-    kbeg = max(kbeg, (int)blockIdx.z * kchunk);
-    kend = min(kend, ((int)blockIdx.z + 1) * kchunk);
+  // indices of the prologue stages and of the first in-loop stage
+  for (int e = tid; e < 2 * P_ST * P_BK; e += P_NT) {
+    const int st = (e / P_BK) % P_ST, l = e % P_BK;
+    const bool forA = e < P_ST * P_BK;
+    const int v = (st < nk) ? kindex(st, l, forA) : -1;
+    if (forA) kA[st][l] = v; else kB[st][l] = v;
   }
-  const int nk = kend > kbeg ? (kend - kbeg + P_BK - 1) / P_BK : 0;
+  __syncthreads();
 #pragma unroll
   for (int st = 0; st < P_ST - 1; ++st) {
-    if (st < nk) load_stage(st, kbeg + st * P_BK);
+    if (st < nk) load_stage(st, st);
     cp_async_commit();
   }
   for (int kt = 0; kt < nk; ++kt) {
     cp_async_wait<P_ST - 2>();
     __syncthreads();
     const int pf = kt + P_ST - 1;
-    if (pf < nk) load_stage(pf % P_ST, kbeg + pf * P_BK);
+    if (pf < nk) load_stage(pf % P_ST, pf);
     cp_async_commit();
+    // prefetch the indices of stage pf + 1 into registers (consumed after the MMAs)
+    int nxt = -1;
+    const int pn = pf + 1;
+    if (tid < 2 * P_BK && pn < nk) nxt = kindex(pn, tid % P_BK, tid < P_BK);
     const double* as = As + (kt % P_ST) * P_BK * P_LDA;
     const double* bs = Bs + (kt % P_ST) * P_BK * LDB;
 #pragma unroll
@@ -791,6 +829,10 @@ __global__ void __launch_bounds__(P_NT, (BN >= 128 ? 1 : 2)) gemm_pipe_kernel(co
           asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                        : "+d"(acc[mi][ni][0]), "+d"(acc[mi][ni][1])
                        : "d"(af[mi]), "d"(bf[ni]));
+    }
+    // slot pn % P_ST held stage kt, whose copies completed before this iteration's barrier
+    if (tid < 2 * P_BK && pn < nk) {
+      if (tid < P_BK) kA[pn % P_ST][tid] = nxt; else kB[pn % P_ST][tid - P_BK] = nxt;
     }
   }
   cp_async_wait<0>();
