@@ -60,13 +60,16 @@ typedef enum {
 } rsf_family;
 
 /* theta components (order of the gradient is the order given in rsf_kernel.theta) */
-typedef enum { RSF_RHO = 0, RSF_SIGMA2 = 1, RSF_NUGGET = 2, RSF_ALPHA = 3 } rsf_param;
+typedef enum { RSF_RHO = 0, RSF_SIGMA2 = 1, RSF_NUGGET = 2, RSF_ALPHA = 3, RSF_RHO2 = 4 } rsf_param;
 
 typedef struct {
   int32_t family;      /* rsf_family */
   double rho, sigma2, nugget, alpha;   /* current values; alpha used by RSF_RQ only */
   int32_t p;           /* number of theta components, 0 <= p <= 4 */
-  int32_t theta[4];    /* rsf_param values, distinct; RSF_ALPHA only with RSF_RQ */
+  int32_t theta[4];    /* rsf_param values, distinct; RSF_ALPHA only with RSF_RQ, RSF_RHO2 only if rho2 > 0 */
+  double rho2;         /* 0: isotropic k(r / rho).  > 0: anisotropic scaled distance
+                          q = sqrt(dx^2/rho^2 + dy^2/rho2^2) and k(q) at unit length; RSF_RHO is then
+                          the x-axis length theta_1 and RSF_RHO2 the y-axis length theta_2 */
 } rsf_kernel;
 
 typedef struct {

@@ -13,13 +13,18 @@ Families (r = ||x - y||):
 Derivatives are written out from those definitions by the chain rule (the
 paper assumes Sigma_i available); tests pin them to central finite
 differences (pin P2).
+
+Anisotropic kernels (next row f1): with rho2 > 0 the distance is the
+scaled ||x - y||_theta = sqrt(dx^2/rho^2 + dy^2/rho2^2) and the family is evaluated
+at unit length, k(||x - y||_theta); theta_1 = rho, theta_2 = rho2.  With alpha = 1/2
+(RQ) and the Matern 3/2 family these are Eqs. specrq and specmatern.
 """
 from __future__ import annotations
 
 import numpy as np
 
 FAMILIES = ("rq", "matern12", "matern32", "matern52", "sqexp")
-PARAMS = ("rho", "sigma2", "nugget", "alpha")
+PARAMS = ("rho", "sigma2", "nugget", "alpha", "rho2")
 
 
 def pairwise_r(X: np.ndarray, Y: np.ndarray) -> np.ndarray:
@@ -84,22 +89,25 @@ class Kernel:
     """theta-parameterised covariance Sigma(theta) = sigma2*k + nugget*I."""
 
     def __init__(self, family: str, rho: float, sigma2: float = 1.0,
-                 nugget: float = 0.0, alpha: float = 1.0, theta=("rho",)):
+                 nugget: float = 0.0, alpha: float = 1.0, theta=("rho",), rho2: float = 0.0):
         if family not in FAMILIES:
             raise ValueError(family)
-        if not (rho > 0 and sigma2 > 0 and alpha > 0 and nugget >= 0):
-            raise ValueError("rho, sigma2, alpha must be > 0 and nugget >= 0")
+        if not (rho > 0 and sigma2 > 0 and alpha > 0 and nugget >= 0 and rho2 >= 0):
+            raise ValueError("rho, sigma2, alpha must be > 0, nugget and rho2 >= 0")
         for t in theta:
             if t not in PARAMS:
                 raise ValueError(t)
             if t == "alpha" and family != "rq":
                 raise ValueError("alpha only for rq")
+            if t == "rho2" and not rho2 > 0:
+                raise ValueError("rho2 only for anisotropic kernels")
         self.family, self.rho, self.sigma2 = family, float(rho), float(sigma2)
         self.nugget, self.alpha, self.theta = float(nugget), float(alpha), tuple(theta)
+        self.rho2 = float(rho2)
 
     def with_param(self, name: str, value: float) -> "Kernel":
         d = dict(family=self.family, rho=self.rho, sigma2=self.sigma2,
-                 nugget=self.nugget, alpha=self.alpha, theta=self.theta)
+                 nugget=self.nugget, alpha=self.alpha, theta=self.theta, rho2=self.rho2)
         d[name] = value
         return Kernel(**d)
 
@@ -107,19 +115,30 @@ class Kernel:
         return getattr(self, name)
 
     # --- blocks -------------------------------------------------------------
+    # --- geometry: isotropic r, or the anisotropic scaled distance q and dx^2, dy^2
+    def _k(self, P, Q):
+        if self.rho2 > 0:
+            q, _, _ = self._q(P, Q)
+            return k_of_r(self.family, q, 1.0, self.alpha)
+        return k_of_r(self.family, pairwise_r(P, Q), self.rho, self.alpha)
+
+    def _q(self, P, Q):
+        dx = P[:, None, 0] - Q[None, :, 0]
+        dy = P[:, None, 1] - Q[None, :, 1]
+        return np.sqrt((dx / self.rho) ** 2 + (dy / self.rho2) ** 2), dx * dx, dy * dy
+
     def sigma_block(self, xy, rows, cols):
         """Sigma(rows, cols) with the nugget on equal indices (R-I)."""
         rows = np.asarray(rows)
         cols = np.asarray(cols)
-        r = pairwise_r(xy[rows], xy[cols])
-        B = self.sigma2 * k_of_r(self.family, r, self.rho, self.alpha)
+        B = self.sigma2 * self._k(xy[rows], xy[cols])
         if self.nugget != 0.0:
             B = B + self.nugget * (rows[:, None] == cols[None, :])
         return B
 
     def sigma_points(self, P, Q):
         """sigma2 * k between two coordinate sets (no nugget; proxy rows)."""
-        return self.sigma2 * k_of_r(self.family, pairwise_r(P, Q), self.rho, self.alpha)
+        return self.sigma2 * self._k(P, Q)
 
     def dsigma_block(self, name: str, xy, rows, cols):
         """Sigma_i(rows, cols) = d Sigma / d theta_i."""
@@ -127,13 +146,30 @@ class Kernel:
         cols = np.asarray(cols)
         if name == "nugget":
             return (rows[:, None] == cols[None, :]).astype(np.float64)
-        r = pairwise_r(xy[rows], xy[cols])
-        return self._dsig_r(name, r)
+        return self.dsigma_points(name, xy[rows], xy[cols])
 
     def dsigma_points(self, name: str, P, Q):
         if name == "nugget":
             return np.zeros((len(P), len(Q)))
+        if self.rho2 > 0:
+            return self._dsig_aniso(name, P, Q)
         return self._dsig_r(name, pairwise_r(P, Q))
+
+    def _dsig_aniso(self, name, P, Q):
+        """Chain rule through q: dk/dtheta_1 = k'(q) dq/dtheta_1, dq/dtheta_1 = -dx^2/(theta_1^3 q),
+        k'(q) = -(dk/drho at unit length)/q."""
+        q, dx2, dy2 = self._q(P, Q)
+        if name == "sigma2":
+            return k_of_r(self.family, q, 1.0, self.alpha)
+        if name == "alpha":
+            return self.sigma2 * dk_dalpha(self.family, q, 1.0, self.alpha)
+        if name in ("rho", "rho2"):
+            with np.errstate(divide="ignore", invalid="ignore"):
+                g = np.where(q > 0, dk_drho(self.family, q, 1.0, self.alpha) / (q * q), 0.0)
+            if name == "rho":
+                return self.sigma2 * g * dx2 / self.rho ** 3
+            return self.sigma2 * g * dy2 / self.rho2 ** 3
+        raise ValueError(name)
 
     def _dsig_r(self, name, r):
         if name == "rho":

@@ -60,11 +60,13 @@ class Kernel:
     nugget: float = 0.0
     alpha: float = 1.0
     theta: tuple = ("rho",)
+    rho2: float = 0.0      # > 0: anisotropic lengths (rho, rho2)
 
     def c(self) -> rsf_kernel:
         k = rsf_kernel()
         k.family = FAMILY[self.family]
         k.rho, k.sigma2, k.nugget, k.alpha = self.rho, self.sigma2, self.nugget, self.alpha
+        k.rho2 = self.rho2
         k.p = len(self.theta)
         for i, t in enumerate(self.theta):
             k.theta[i] = PARAM[t]

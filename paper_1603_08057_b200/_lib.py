@@ -13,13 +13,13 @@ LIB_PATH = os.path.join(HERE, "librsf.so")
 
 RSF_OK, RSF_EINVAL, RSF_ENUMERIC, RSF_ECUDA, RSF_ENOMEM, RSF_ENCCL = range(6)
 FAMILY = {"rq": 0, "matern12": 1, "matern32": 2, "matern52": 3, "sqexp": 4}
-PARAM = {"rho": 0, "sigma2": 1, "nugget": 2, "alpha": 3}
+PARAM = {"rho": 0, "sigma2": 1, "nugget": 2, "alpha": 3, "rho2": 4}
 
 
 class rsf_kernel(C.Structure):
     _fields_ = [("family", C.c_int32), ("rho", C.c_double), ("sigma2", C.c_double),
                 ("nugget", C.c_double), ("alpha", C.c_double), ("p", C.c_int32),
-                ("theta", C.c_int32 * 4)]
+                ("theta", C.c_int32 * 4), ("rho2", C.c_double)]
 
 
 class rsf_opts(C.Structure):

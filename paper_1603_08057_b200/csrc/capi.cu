@@ -72,13 +72,15 @@ rsf::KParams check_kernel(const rsf_kernel* k) {
   RSF_REQUIRE(std::isfinite(k->nugget) && k->nugget >= 0, rsf::ST_EINVAL, "nugget must be >= 0");
   RSF_REQUIRE(std::isfinite(k->alpha) && (k->family != rsf::FAM_RQ || k->alpha > 0), rsf::ST_EINVAL,
               "alpha must be > 0");
+  RSF_REQUIRE(std::isfinite(k->rho2) && k->rho2 >= 0, rsf::ST_EINVAL, "rho2 must be >= 0 (0: isotropic)");
   RSF_REQUIRE(k->p >= 0 && k->p <= 4, rsf::ST_EINVAL, "p out of range");
   for (int i = 0; i < k->p; ++i) {
-    RSF_REQUIRE(k->theta[i] >= 0 && k->theta[i] <= 3, rsf::ST_EINVAL, "unknown theta component");
+    RSF_REQUIRE(k->theta[i] >= 0 && k->theta[i] <= 4, rsf::ST_EINVAL, "unknown theta component");
+    RSF_REQUIRE(k->theta[i] != RSF_RHO2 || k->rho2 > 0, rsf::ST_EINVAL, "rho2 is a parameter of anisotropic kernels");
     RSF_REQUIRE(k->theta[i] != RSF_ALPHA || k->family == RSF_RQ, rsf::ST_EINVAL, "alpha is an RQ parameter");
     for (int j = 0; j < i; ++j) RSF_REQUIRE(k->theta[i] != k->theta[j], rsf::ST_EINVAL, "repeated theta component");
   }
-  return rsf::KParams{k->family, k->rho, k->sigma2, k->nugget, k->alpha};
+  return rsf::KParams{k->family, k->rho, k->sigma2, k->nugget, k->alpha, k->rho2};
 }
 
 // device copy of a (possibly host) n x 2 point array

@@ -40,7 +40,7 @@ __global__ void assemble_id_kernel(const IdAsmDesc* __restrict__ descs, KParams 
       px = d.cx + rad * cs; py = d.cy + rad * sn;
     }
     const double dx = px - xj, dy = py - yj;
-    d.A[e] = entry(kp, which, sqrt(dx * dx + dy * dy), false);
+    d.A[e] = entry_xy(kp, which, dx, dy, false);
   }
 }
 
@@ -64,7 +64,7 @@ __global__ void assemble_self_kernel(const SelfAsmDesc* __restrict__ descs, KPar
     } else {
       const int a = __ldg(d.I + i), b = __ldg(d.I + j);
       const double dx = xs[a] - xs[b], dy = ys[a] - ys[b];
-      v = entry(kp, which, sqrt(dx * dx + dy * dy), a == b);
+      v = entry_xy(kp, which, dx, dy, a == b);
     }
     d.B[e] = v;
   }

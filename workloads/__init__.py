@@ -23,7 +23,7 @@ import numpy as np
 
 __all__ = [
     "philox4x32", "philox_uniform_pair", "philox_normal_pair", "philox_normal", "philox_rademacher",
-    "CONFIGS", "Config", "points_for", "w_for", "config",
+    "CONFIGS", "Config", "points_for", "w_for", "config", "paper_grid_points",
 ]
 
 _M0 = np.uint64(0xD2511F53)
@@ -186,6 +186,14 @@ def _cluster_points(n: int, seed: int, nc: int, sig: float) -> np.ndarray:
         todo = todo[~ok]
         attempt += 1
     return out
+
+
+def paper_grid_points(m: int) -> np.ndarray:
+    """The paper's gridded workload: an m x m grid uniformly discretizing
+    [0, 100]^2, rescaled to the unit square (reading R-f1: cell centres ((i + 1/2)/m,
+    (j + 1/2)/m); theta = [10, 7] on [0, 100]^2 is [0.1, 0.07] here)."""
+    g = (np.arange(m, dtype=np.float64) + 0.5) / m
+    return np.stack([np.repeat(g, m), np.tile(g, m)], axis=1)
 
 
 def points_for(cfg: Config, n: int | None = None) -> np.ndarray:
