@@ -160,6 +160,22 @@ rsf_status gp_mle_eval(rsf_ctx ctx, const double* xy, const double* z, int64_t n
                        double eps, int32_t leaf, const rsf_opts* opts, double* ell, double* grad,
                        rsf_eval_diag* diag);
 
+/* Log profile likelihood (next row f3; Eq. prof and its gradient): z ~ N(mu 1, s2 Sigma(theta))
+ * with mu and s2 profiled out,
+ *   l~ = -1/2 log|Sigma| - n/2 log Q + n/2 (log n - 1 - log 2pi),  Q = z^T (Sigma + 1 1^T)^-1 z,
+ *   g~_i = -1/2 Tr(Sigma^-1 Sigma_i) + n/2 v^T Sigma_i v / Q,        v = (Sigma + 1 1^T)^-1 z
+ * (Sherman-Morrison through F^-1 z and F^-1 1; reading R-Prof: the printed constant's "2 pi" is log 2 pi).
+ * Arguments as gp_mle_eval; theta may not contain RSF_SIGMA2 (profiled out); n >= 2.  diag->quad = Q. */
+rsf_status gp_profile_eval(rsf_ctx ctx, const double* xy, const double* z, int64_t n, const rsf_kernel* kernel,
+                           double eps, int32_t leaf, const rsf_opts* opts, double* ell, double* grad,
+                           rsf_eval_diag* diag);
+
+/* Conditional (kriging) mean at m new locations (Remark conditional):
+ * out = Sigma_12 F^-1 z with (Sigma_12)_aj = sigma2 k(x'_a, x_j) (no nugget between distinct observations).
+ * F: Sigma factor of the n data locations; z: n values in original order; xy_new: m x 2 row-major;
+ * out: m.  Device or host buffers.  Direct O(m n) cross product (FP64). */
+rsf_status gp_cond_mean(rsf_fact F, const double* z, const double* xy_new, int64_t m, double* out);
+
 /* message of the last failing call on this thread ("" if none) */
 const char* rsf_last_error(void);
 /* number of CUDA kernels launched by this thread so far (diagnostics) */

@@ -180,6 +180,36 @@ def peel_trace(F: Factor, Fi: Factor | None, eps_peel: float = 1e-6, opts: Opts 
     return v.value, d
 
 
+def gp_profile_eval(ctx: Context, xy, z, kernel: Kernel, eps: float, leaf: int = 64,
+                    opts: Opts | None = None) -> "EvalResult":
+    """Log profile likelihood (Eq. prof) and gradient; diag.quad = z^T (Sigma + 1 1^T)^-1 z."""
+    px, kx = _ptr(xy)
+    pz, kz = _ptr(z)
+    n = xy.shape[0]
+    kc = kernel.c()
+    oc = (opts or Opts()).c()
+    ell = C.c_double()
+    grad = (C.c_double * 4)()
+    d = rsf_eval_diag()
+    _check(lib.gp_profile_eval(ctx.h, px, pz, n, C.byref(kc), eps, leaf, C.byref(oc), C.byref(ell), grad,
+                               C.byref(d)))
+    return EvalResult(ell.value, [grad[i] for i in range(len(kernel.theta))], d)
+
+
+def gp_cond_mean(F: Factor, z, xy_new, out=None):
+    """Kriging mean Sigma_12 F^-1 z at the rows of xy_new (m x 2)."""
+    import torch
+    m = xy_new.shape[0]
+    if out is None:
+        out = torch.empty(m, dtype=torch.float64, device=xy_new.device) if hasattr(xy_new, "device") else \
+            __import__("numpy").empty(m)
+    pz, kz = _ptr(z)
+    px, kx = _ptr(xy_new)
+    po, ko = _ptr(out)
+    _check(lib.gp_cond_mean(F.h, pz, px, m, po))
+    return out
+
+
 def hutch_trace(F: Factor, Fi: Factor | None, nprobe: int = 64, seed: int = 1603080570):
     """Hutchinson estimate of Tr(F^-1 F_i) (Fi None: Tr(F^-1)) -> (trace, standard error)."""
     t = C.c_double()

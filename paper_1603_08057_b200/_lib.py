@@ -52,7 +52,7 @@ class rsf_eval_diag(C.Structure):
 
 
 EXPORTS = ["rsf_opts_default", "rsf_ctx_create", "rsf_ctx_destroy", "rsf_factor", "rsf_fact_destroy",
-           "rsf_fact_info", "rsf_logdet", "rsf_solve", "rsf_apply", "rsf_sample", "peel_trace", "hutch_trace",
+           "rsf_fact_info", "rsf_logdet", "rsf_solve", "rsf_apply", "rsf_sample", "peel_trace", "hutch_trace", "gp_profile_eval", "gp_cond_mean",
            "gp_mle_eval", "rsf_last_error", "rsf_kernel_launches", "rsf_profile_dump",
            "rsf_profile_reset", "rsf_stats_enable", "rsf_stats_get", "rsf_stats_reset",
            "rsf_debug_gemm_bench", "rsf_debug_fp64_peak", "rsf_trace_dump"]
@@ -79,6 +79,9 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         getattr(lib, f).argtypes = [vp, vp, vp, i64, i64]
     lib.peel_trace.argtypes = [vp, vp, C.c_double, C.POINTER(rsf_opts), i32, dp, C.POINTER(rsf_peel_diag)]
     lib.hutch_trace.argtypes = [vp, vp, i64, C.c_uint64, dp, dp]
+    lib.gp_profile_eval.argtypes = [vp, vp, vp, i64, C.POINTER(rsf_kernel), C.c_double, i32,
+                                    C.POINTER(rsf_opts), dp, dp, C.POINTER(rsf_eval_diag)]
+    lib.gp_cond_mean.argtypes = [vp, vp, vp, i64, vp]
     lib.gp_mle_eval.argtypes = [vp, vp, vp, i64, C.POINTER(rsf_kernel), C.c_double, i32,
                                 C.POINTER(rsf_opts), dp, dp, C.POINTER(rsf_eval_diag)]
     lib.rsf_last_error.argtypes = []

@@ -342,6 +342,50 @@ rsf_status gp_mle_eval(rsf_ctx ctx, const double* xy, const double* z, int64_t n
   });
 }
 
+rsf_status gp_profile_eval(rsf_ctx ctx, const double* xy, const double* z, int64_t n, const rsf_kernel* kernel,
+                           double eps, int32_t leaf, const rsf_opts* opts, double* ell, double* grad,
+                           rsf_eval_diag* diag) {
+  return guard([&] {
+    RSF_REQUIRE(ctx && xy && z && ell, rsf::ST_EINVAL, "null argument");
+    RSF_REQUIRE(n >= 2 && n < (1ll << 31), rsf::ST_EINVAL, "n out of range");
+    RSF_REQUIRE(eps > 0 && std::isfinite(eps), rsf::ST_EINVAL, "eps must be > 0");
+    RSF_REQUIRE(leaf >= 1, rsf::ST_EINVAL, "leaf must be >= 1");
+    rsf::KParams kp = check_kernel(kernel);
+    RSF_REQUIRE(kernel->p == 0 || grad != nullptr, rsf::ST_EINVAL, "grad is NULL");
+    for (int i = 0; i < kernel->p; ++i)
+      RSF_REQUIRE(kernel->theta[i] != RSF_SIGMA2, rsf::ST_EINVAL, "sigma2 is profiled out (not a theta component)");
+    RSF_CUDA(cudaSetDevice(ctx->ctx.device));
+    rsf::Opts o = make_opts(opts);
+    rsf::EvalResult r = rsf::mle_eval(ctx->ctx, xy, z, (int)n, kp, kernel->p, kernel->theta, eps, leaf, o, true);
+    *ell = r.ell;
+    for (int i = 0; i < kernel->p; ++i) grad[i] = r.grad[i];
+    if (diag) rsf::fill_eval_diag(r, diag);
+  });
+}
+
+rsf_status gp_cond_mean(rsf_fact F, const double* z, const double* xy_new, int64_t m, double* out) {
+  return guard([&] {
+    RSF_REQUIRE(F && z && (m == 0 || (xy_new && out)), rsf::ST_EINVAL, "null argument");
+    RSF_REQUIRE(F->F->which == rsf::W_SIGMA, rsf::ST_EINVAL, "F must be a Sigma factor");
+    RSF_REQUIRE(m >= 0, rsf::ST_EINVAL, "m < 0");
+    RSF_CUDA(cudaSetDevice(F->owner->ctx.device));
+    const rsf::Fact& f = *F->F;
+    cudaStream_t s = f.ctx->stream;
+    const int n = f.n();
+    rsf::DBuf<double> zd, xd, od;
+    const double* dz = z;
+    const double* dx = xy_new;
+    double* dout = out;
+    if (!is_device_ptr(z)) { zd.alloc(n, s); zd.upload(z, n); dz = zd.p; }
+    if (m > 0 && !is_device_ptr(xy_new)) { xd.alloc(2 * (size_t)m, s); xd.upload(xy_new, 2 * (size_t)m); dx = xd.p; }
+    const bool host_out = m > 0 && !is_device_ptr(out);
+    if (host_out) { od.alloc((size_t)m, s); dout = od.p; }
+    rsf::cond_mean(f, dz, dx, m, dout);
+    if (host_out) RSF_CUDA(cudaMemcpyAsync(out, od.p, (size_t)m * sizeof(double), cudaMemcpyDeviceToHost, s));
+    RSF_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
 const char* rsf_last_error(void) { return g_err.c_str(); }
 
 int64_t rsf_kernel_launches(void) { return rsf::g_launches; }

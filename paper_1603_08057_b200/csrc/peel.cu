@@ -199,6 +199,35 @@ __global__ void dot_kernel(const double* a, const double* b, long long n, double
   if (threadIdx.x == 0) part[blockIdx.x] = s[0];
 }
 
+__global__ void fill_kernel(double* y, double v, long long n) {
+  for (long long i = blockIdx.x * (long long)NT + threadIdx.x; i < n; i += (long long)gridDim.x * NT) y[i] = v;
+}
+
+// out_a = sum_j sigma2 k(x'_a - x_j) u_j  (conditional mean, Remark conditional P:680-690): data
+// coordinates and u staged in shared memory tiles, one new point per thread
+__global__ void __launch_bounds__(NT) cross_matvec_kernel(const double* __restrict__ xs, const double* __restrict__ ys,
+                                                          const double* __restrict__ u, int n,
+                                                          const double* __restrict__ xyn, long long m, KParams kp,
+                                                          double* out) {
+  __shared__ double sx[NT], sy[NT], su[NT];
+  for (long long a0 = (long long)blockIdx.x * NT; a0 < m; a0 += (long long)gridDim.x * NT) {
+    const long long a = a0 + threadIdx.x;
+    const double px = a < m ? xyn[2 * a] : 0.0, py = a < m ? xyn[2 * a + 1] : 0.0;
+    double acc = 0.0;
+    for (int j0 = 0; j0 < n; j0 += NT) {
+      __syncthreads();
+      const int j = j0 + threadIdx.x;
+      sx[threadIdx.x] = j < n ? xs[j] : 0.0;
+      sy[threadIdx.x] = j < n ? ys[j] : 0.0;
+      su[threadIdx.x] = j < n ? u[j] : 0.0;
+      __syncthreads();
+      const int cnt = min(NT, n - j0);
+      for (int q = 0; q < cnt; ++q) acc += entry_xy(kp, W_SIGMA, px - sx[q], py - sy[q], false) * su[q];
+    }
+    if (a < m) out[a] = acc;
+  }
+}
+
 __global__ void axpby_kernel(double* y, const double* x, double a, double b, long long n) {
   for (long long i = blockIdx.x * (long long)NT + threadIdx.x; i < n; i += (long long)gridDim.x * NT)
     y[i] = a * x[i] + b * y[i];
@@ -1187,6 +1216,24 @@ void hutch(const Fact& F, const Fact* Fi, long long q, unsigned long long seed, 
   *se = vals.size() > 1 ? std::sqrt(var / (double)(vals.size() - 1) / (double)vals.size()) : INFINITY;
 }
 
+// conditional mean E[z' | z] = Sigma_12 Sigma_22^-1 z at m new points (Remark conditional,
+// P:680-690): u = F^-1 z through the factor, then the cross-covariance product on the fly
+void cond_mean(const Fact& F, const double* z, const double* xyn, long long m, double* out) {
+  RSF_REQUIRE(F.which == W_SIGMA, ST_EINVAL, "conditional mean needs a Sigma factor");
+  cudaStream_t s = F.ctx->stream;
+  const Tree& t = *F.tree;
+  const int n = t.n;
+  DBuf<double> u(n, s), tmp((size_t)std::max<long long>(F.tmp_cols, 1), s);
+  to_internal(s, t, z, n, 1, u.p);
+  solve_internal(F, u.p, 1, tmp.p);
+  if (m > 0) {
+    const int grid = (int)std::min<long long>((m + NT - 1) / NT, 148 * 8);
+    cross_matvec_kernel<<<grid, NT, 0, s>>>(t.xs.p, t.ys.p, u.p, n, xyn, m, F.kp, out);
+    count_launch();
+    RSF_LAUNCH_CHECK();
+  }
+}
+
 void fill_peel_diag(const PeelDiag& d, rsf_peel_diag* out) {
   std::memset(out, 0, sizeof(*out));
   out->levels = (int)d.cols.size() - 1;
@@ -1202,7 +1249,7 @@ void fill_peel_diag(const PeelDiag& d, rsf_peel_diag* out) {
 
 // ----------------------------------------------------------------- Alg. 1
 EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KParams& kp, int p,
-                    const int* theta, double eps, int leaf, const Opts& o) {
+                    const int* theta, double eps, int leaf, const Opts& o, bool profile) {
   EvalResult R;
   const long long l0 = g_launches;
   const double T0 = now_s();
@@ -1237,11 +1284,31 @@ EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KP
   solve_internal(*F, u.p, 1, tmp.p);
   R.quad = ddot(s, zt.p, u.p, n);
   R.ell = -0.5 * R.quad - 0.5 * R.logdet - 0.5 * n * std::log(2.0 * M_PI);
+  double Qp = 0.0;
+  if (profile) {
+    // profile likelihood (Eq. prof): z ~ N(mu 1, s2 Sigma) with mu, s2 profiled out,
+    //   Q = z^T (Sigma + 1 1^T)^-1 z = z^T u - (1^T u)^2 / (1 + 1^T w),  w = F^-1 1 (Sherman-Morrison)
+    //   l~ = -1/2 log|Sigma| - n/2 log Q + n/2 (log n - 1 - log 2 pi)          (reading R-Prof)
+    //   v = (Sigma + 1 1^T)^-1 z = u - w (1^T u) / (1 + 1^T w)   (held in u from here on)
+    DBuf<double> one(n, s), wv(n, s);
+    fill_kernel<<<gxx(n), NT, 0, s>>>(one.p, 1.0, n);
+    count_launch();
+    RSF_CUDA(cudaMemcpyAsync(wv.p, one.p, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    solve_internal(*F, wv.p, 1, tmp.p);
+    const double a = ddot(s, one.p, wv.p, n), b = ddot(s, one.p, u.p, n);
+    Qp = R.quad - b * b / (1.0 + a);
+    R.ell = -0.5 * R.logdet - 0.5 * n * std::log(Qp) + 0.5 * n * (std::log((double)n) - 1.0 - std::log(2.0 * M_PI));
+    axpby_kernel<<<gxx(n), NT, 0, s>>>(u.p, wv.p, -b / (1.0 + a), 1.0, n);   // u <- u - w b/(1+a)
+    count_launch();
+    RSF_LAUNCH_CHECK();
+    R.quad = Qp;
+  }
   R.t_solve = now_s() - t;
   double trinv = NAN, utu = NAN;
   for (int i = 0; i < p; ++i) {
     const int w = theta[i];
     double q, tr;
+    RSF_REQUIRE(!(profile && w == W_SIGMA2), ST_EINVAL, "profile likelihood: sigma2 is profiled out, not a theta component");
     if (w == W_SIGMA2 || w == W_NUGGET) {   // reading R-G
       if (std::isnan(trinv)) {
         t = now_s();
@@ -1270,7 +1337,7 @@ EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KP
     }
     R.q[i] = q;
     R.trace[i] = tr;
-    R.grad[i] = 0.5 * q - 0.5 * tr;
+    R.grad[i] = profile ? 0.5 * n * q / Qp - 0.5 * tr : 0.5 * q - 0.5 * tr;
   }
   RSF_CUDA(cudaStreamSynchronize(s));
   R.t_total = now_s() - T0;

@@ -32,8 +32,12 @@ struct EvalResult {
   PeelDiag pd[4];
 };
 
+// profile = true: the log profile likelihood of Eq. prof and its gradient; quad holds
+// Q = z^T (Sigma + 1 1^T)^-1 z, q_i = v^T Sigma_i v with v = (Sigma + 1 1^T)^-1 z
 EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KParams& kp, int p,
-                    const int* theta, double eps, int leaf, const Opts& o);
+                    const int* theta, double eps, int leaf, const Opts& o, bool profile = false);
+// conditional mean Sigma_12 F^-1 z at m new points (xyn, m x 2 device; out device)
+void cond_mean(const Fact& F, const double* z, const double* xyn, long long m, double* out);
 void fill_eval_diag(const EvalResult& r, rsf_eval_diag* out);
 
 // deterministic dot product of two device vectors (n doubles)

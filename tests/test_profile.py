@@ -1,0 +1,92 @@
+"""Profile likelihood and kriging mean (next row f3): oracle pins
+(CPU) and the CUDA path against the dense oracle (GPU)."""
+import numpy as np
+import pytest
+
+from oracle.kernels import Kernel
+from oracle.profile import dense_cond_mean, dense_profile_eval
+from workloads import config, points_for, w_for
+
+
+def _case(n=200, seed=0):
+    xy = np.random.default_rng(seed).random((n, 2))
+    k = Kernel("matern32", 0.12, 1.0, 1e-2, 1.0, ("rho", "nugget"))
+    z = 0.7 + 1.9 * np.random.default_rng(seed + 1).standard_normal(n)
+    return xy, k, z
+
+
+def test_profile_gradient_vs_finite_differences():
+    xy, k, z = _case()
+    d = dense_profile_eval(k, xy, z)
+    for i, name in enumerate(k.theta):
+        v = k.value(name)
+        h = 1e-5 * v
+        lp = dense_profile_eval(k.with_param(name, v + h), xy, z)["ell"]
+        lm = dense_profile_eval(k.with_param(name, v - h), xy, z)["ell"]
+        assert d["grad"][i] == pytest.approx((lp - lm) / (2 * h), rel=1e-6)
+
+
+def test_profile_scaling_identity():
+    """Q(s z) = s^2 Q(z)  =>  l~(s z) = l~(z) - n log s  (the profiled variance absorbs the scale)."""
+    xy, k, z = _case(150, 3)
+    a = dense_profile_eval(k, xy, z)["ell"]
+    b = dense_profile_eval(k, xy, 3.7 * z)["ell"]
+    assert b == pytest.approx(a - len(z) * np.log(3.7), rel=1e-12)
+
+
+def test_profile_is_maximum_over_scale():
+    """With Sigma + 1 1^T as the covariance model of z, maximizing the Gaussian log-likelihood of
+    z ~ N(0, s2 (Sigma + 1 1^T)) over s2 gives l~ + 1/2 log(1 + 1^T Sigma^-1 1) (matrix determinant lemma)."""
+    xy, k, z = _case(120, 5)
+    n = len(z)
+    d = dense_profile_eval(k, xy, z)
+    S = np.array(k.sigma_block(xy, np.arange(n), np.arange(n))) + np.ones((n, n))
+    s2 = d["Q"] / n
+    sign, ld = np.linalg.slogdet(s2 * S)
+    full = -0.5 * n - 0.5 * ld - 0.5 * n * np.log(2 * np.pi)
+    Sig = np.array(k.sigma_block(xy, np.arange(n), np.arange(n)))
+    corr = 0.5 * np.log(1.0 + np.ones(n) @ np.linalg.solve(Sig, np.ones(n)))
+    assert full == pytest.approx(d["ell"] - corr, rel=1e-12)
+
+
+def test_cond_mean_interpolates_without_nugget():
+    """nugget = 0: Sigma_12 = Sigma_22 rows at the data locations, so the mean reproduces z."""
+    xy = np.random.default_rng(7).random((80, 2))
+    k = Kernel("matern12", 0.1, 1.3, 0.0, 1.0, ("rho",))
+    z = np.random.default_rng(8).standard_normal(80)
+    m = dense_cond_mean(k, xy, z, xy[:10])
+    assert np.allclose(m, z[:10], rtol=1e-9, atol=1e-9)
+
+
+@pytest.mark.gpu
+def test_gpu_profile_and_cond_mean_vs_dense():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_1603_08057_b200 as R
+    c = config(2)
+    n = 4096
+    xy = points_for(c, n)
+    ok = Kernel("matern32", c.rho, 1.0, c.nugget, 1.0, ("rho", "nugget"))
+    rk = R.Kernel("matern32", c.rho, 1.0, c.nugget, 1.0, ("rho", "nugget"))
+    z = 0.5 + 2.0 * w_for(c, n)
+    d = dense_profile_eval(ok, xy, z)
+    dev = torch.device("cuda:0")
+    ctx = R.Context(0)
+    r = R.gp_profile_eval(ctx, torch.from_numpy(xy).to(dev), torch.from_numpy(z).to(dev), rk, c.eps_fact, c.leaf,
+                          R.Opts(eps_peel=c.eps_peel))
+    assert abs(r.ell - d["ell"]) <= 1e-5 * abs(d["ell"])
+    assert abs(r.diag.quad - d["Q"]) <= 10 * c.eps * d["Q"]
+    g = np.array(r.grad)
+    assert np.all(np.abs(g - d["grad"]) <= 1e-3 * np.abs(d["grad"])), (g, d["grad"])
+    with pytest.raises(R.RsfError):
+        R.gp_profile_eval(ctx, torch.from_numpy(xy).to(dev), torch.from_numpy(z).to(dev),
+                          R.Kernel("matern32", c.rho, 1.0, c.nugget, 1.0, ("sigma2",)), c.eps_fact, c.leaf)
+    # kriging mean at 300 new locations
+    F = R.Factor(ctx, torch.from_numpy(xy).to(dev), rk, c.eps_fact, c.leaf)
+    xn = np.random.default_rng(9).random((300, 2))
+    want = dense_cond_mean(ok, xy, z, xn)
+    got = R.gp_cond_mean(F, torch.from_numpy(z).to(dev), torch.from_numpy(xn).to(dev)).cpu().numpy()
+    assert np.linalg.norm(got - want) <= 1e-6 * np.linalg.norm(want)
+    got_h = R.gp_cond_mean(F, np.ascontiguousarray(z), np.ascontiguousarray(xn), np.empty(300))
+    assert np.array_equal(got_h, got)
