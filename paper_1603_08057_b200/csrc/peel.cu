@@ -108,28 +108,6 @@ __global__ void rowblock_copy_kernel(double* dst, long long ldd, int r0, const d
   }
 }
 
-// transpose: Q (ni x c, ld ni) <- Y' block (c x ni, ld ldy)
-struct TrDesc { const double* Y; long long ldy; double* Q; int ni, c; };
-__global__ void transpose_kernel(const TrDesc* __restrict__ descs) {
-  __shared__ double tile[32][33];
-  const TrDesc d = descs[blockIdx.z];
-  const int tilesN = (d.ni + 31) / 32, tilesC = (d.c + 31) / 32;
-  for (int tb = blockIdx.x; tb < tilesN * tilesC; tb += gridDim.x) {
-    const int tn = tb % tilesN, tc = tb / tilesN;
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
-    for (int yy = ty; yy < 32; yy += 8) {
-      const int t = tn * 32 + yy, j = tc * 32 + tx;
-      tile[yy][tx] = (t < d.ni && j < d.c) ? d.Y[(long long)t * d.ldy + j] : 0.0;
-    }
-    __syncthreads();
-    for (int yy = ty; yy < 32; yy += 8) {
-      const int j = tc * 32 + yy, t = tn * 32 + tx;
-      if (t < d.ni && j < d.c) d.Q[(long long)j * d.ni + t] = tile[tx][yy];
-    }
-    __syncthreads();
-  }
-}
-
 // U (ni x k, ld ni) <- [I_k; 0]
 struct EyeDesc { double* U; int ni, k; };
 __global__ void eye_kernel(const EyeDesc* __restrict__ descs) {
@@ -137,20 +115,6 @@ __global__ void eye_kernel(const EyeDesc* __restrict__ descs) {
   for (long long e = blockIdx.x * (long long)NT + threadIdx.x; e < (long long)d.ni * d.k; e += (long long)gridDim.x * NT) {
     const int r = (int)(e % d.ni), c = (int)(e / d.ni);
     d.U[e] = (r == c) ? 1.0 : 0.0;
-  }
-}
-
-// Y_k (n_i x k, ld n_i) <- probe columns piv[0:k] of the sketch rows of box i,
-// read from the column chunks of Y_g (chunk c holds probe columns [c*kb, ...), X' layout)
-struct GatherDesc { double* Yk; const int* piv; int ib, ni, k; };
-__global__ void gather_cols_kernel(const GatherDesc* __restrict__ descs, double* const* __restrict__ chunks,
-                                   const int* __restrict__ chw, int kb) {
-  const GatherDesc d = descs[blockIdx.y];
-  const long long tot = (long long)d.ni * d.k;
-  for (long long e = blockIdx.x * (long long)NT + threadIdx.x; e < tot; e += (long long)gridDim.x * NT) {
-    const int t = (int)(e % d.ni), j = (int)(e / d.ni);
-    const int col = __ldg(d.piv + j), ch = col / kb, w = __ldg(chw + ch);
-    d.Yk[e] = chunks[ch][(long long)(d.ib + t) * w + (col - ch * kb)];
   }
 }
 
