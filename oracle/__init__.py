@@ -16,6 +16,7 @@ Parts (each function cites the PAPER.md passage it follows; "P:n" is
   peel.py     O2: weak-admissibility matrix peeling
   mle.py      O2: Alg. 1 (l-hat and g-hat)
   hutch.py    Hutchinson estimator (next row f2)
+  profile.py  profile likelihood, kriging mean (f3)
 
 Pins (tests/test_oracle_pins.py) tie these to closed forms, brute force and
 special cases; see DESIGN.md §3 for the list and for the one part that is
