@@ -572,7 +572,10 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
     int hint = o.peel_start;
     if (prev_rank < 0 && F.levels.size() > 1)
       for (int kk : F.levels[1].k) hint = std::max(hint, kk);
-    int c = (prev_rank < 0) ? (int)std::ceil(0.6 * hint) : prev_rank + o.oversample;
+    // (0.75: a short first guess costs a whole probe group of the level on restart, a long one only
+    // its extra columns)
+    int c = (prev_rank < 0) ? (int)std::ceil(0.75 * hint) : prev_rank + o.oversample;
+    int restarts = 0;
     c = std::min(std::max(c, o.oversample + 8), cmax);
     c = (c + 7) / 8 * 8;
 
@@ -948,6 +951,7 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
         }
       }
       if (!fail) break;
+      ++restarts;
       int nc = (mr >= c - 1) ? (int)std::ceil(1.4 * c) : std::max(c + 8, (int)std::ceil(1.1 * mr) + o.oversample);
       c = std::max(std::min((nc + 7) / 8 * 8, cmax), c + 8);
     }
@@ -1082,9 +1086,10 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
       long long rsum = 0;
       int rmax = 0;
       for (int b = 0; b < nb; ++b) { rsum += rb[b]; rmax = std::max(rmax, rb[b]); }
-      fprintf(stderr, "[peel tr%d] level %d boxes %d pairs %d cols %d rank_max %d basis sum %lld max %d V %.2f GB "
-                      "Brow %.2f GB dev_used %.2f GB t %.2f s\n",
-              trace_id, lev, nb, npairs, c, mr, rsum, rmax, 1e-9 * vbytes, 8e-9 * PL.Brow.n, 1e-9 * (tot - fr), now_s() - t0);
+      fprintf(stderr, "[peel tr%d] level %d boxes %d pairs %d cols %d rank_max %d restarts %d basis sum %lld max %d "
+                      "V %.2f GB Brow %.2f GB dev_used %.2f GB t %.2f s\n",
+              trace_id, lev, nb, npairs, c, mr, restarts, rsum, rmax, 1e-9 * vbytes, 8e-9 * PL.Brow.n,
+              1e-9 * (tot - fr), now_s() - t0);
       if (verbose > 1) {
         DBuf<unsigned long long> cnt(4, s);
         RSF_CUDA(cudaMemsetAsync(cnt.p, 0, 4 * sizeof(unsigned long long), s));

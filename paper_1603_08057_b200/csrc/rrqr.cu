@@ -76,6 +76,7 @@ __global__ void ref_kernel(const RDesc* __restrict__ d0) {
     // nothing to factor: an all-zero matrix, or every column already below the absolute threshold
     d.flag[0] = (v > 0.0 && rf > 0.0 && sqrt(v) > d.eps * rf) ? 0 : 1;
     d.flag[1] = 0;
+    d.flag[2] = 0;
   }
 }
 
@@ -367,6 +368,7 @@ __global__ void trail_norm_kernel(const RDesc* __restrict__ d0) {
 // smallest k' in [J, j1] with max trailing column norm <= eps * ref (exact, from R and nrm2)
 __global__ void __launch_bounds__(NT) rank_kernel(const RDesc* __restrict__ d0) {
   const RDesc d = d0[blockIdx.x];
+  if (d.flag[0]) return;   // finished at an earlier block (checks are deferred, see rrqr_batched)
   const int J = d.J, nbp = d.nbp, j1 = J + nbp;
   __shared__ double red[QR_NB + 1][NT / 32];
   double mx[QR_NB + 1];
@@ -409,7 +411,7 @@ __global__ void __launch_bounds__(NT) rank_kernel(const RDesc* __restrict__ d0) 
       if (sqrt(v) <= thr) { k = J + q; break; }
     }
     if (k < 0 && j1 >= min(d.m, d.c)) k = j1;
-    if (k >= 0) { d.flag[0] = 1; d.flag[1] = k; }
+    if (k >= 0) { d.flag[0] = 1; d.flag[1] = k; d.flag[2] = j1; }
   }
 }
 
@@ -591,14 +593,14 @@ RRQRResult rrqr_batched(cudaStream_t s, const std::vector<RRQRProb>& probs, doub
   }
   DBuf<double> Y(yt, s), Z(yt, s), zn(ct, s), nrm2(ct, s), V(vt, s), W(wt, s), W2(wt, s), Wt(wt, s);
   DBuf<double> Tsc((size_t)P * QR_NB * QR_NB, s), R11i((size_t)P * QR_NB * QR_NB, s), ref(P, s);
-  DBuf<int> sw((size_t)P * QR_NB, s), flag((size_t)2 * P, s);
+  DBuf<int> sw((size_t)P * QR_NB, s), flag((size_t)3 * P, s);
   std::vector<RDesc> base(P);
   for (int i = 0; i < P; ++i) {
     const auto& p = probs[i];
     RDesc d{};
     d.A = p.A; d.lda = p.lda; d.m = p.m; d.c = p.c;
     d.Y = Y.p + yoff[i]; d.Z = Z.p + yoff[i]; d.zn = zn.p + coff[i]; d.nrm2 = nrm2.p + coff[i];
-    d.piv = p.piv; d.sw = sw.p + (long long)i * QR_NB; d.ref = ref.p + i; d.flag = flag.p + 2 * i;
+    d.piv = p.piv; d.sw = sw.p + (long long)i * QR_NB; d.ref = ref.p + i; d.flag = flag.p + 3 * i;
     d.R11i = R11i.p + (long long)i * QR_NB * QR_NB;
     d.id = i; d.eps = eps;
     d.ref_in = p.ref_in; d.ref_out = p.ref_out;
@@ -624,13 +626,28 @@ RRQRResult rrqr_batched(cudaStream_t s, const std::vector<RRQRProb>& probs, doub
     gy.run(s);
     for (int i = 0; i < P; ++i) base[i].G = nullptr;
   }
-  std::vector<int> hflag = flag.to_host(2 * P);
+  std::vector<int> hflag = flag.to_host(3 * P);
   std::vector<int> active;
   for (int i = 0; i < P; ++i) {
-    if (hflag[2 * i]) { res.k[i] = 0; res.done[i] = 0; }
+    if (hflag[3 * i]) { res.k[i] = 0; res.done[i] = 0; }
     else active.push_back(i);
   }
+  // The rank test of a block is read back only every `every` blocks (and at a problem's last
+  // block): finished problems run a few more (harmless) blocks -- the later panels touch rows and
+  // columns past the rank only, rank_kernel ignores them -- in exchange for 1/every host syncs.
+  static const int every = getenv("RSF_RRQR_CHECK") ? std::max(1, atoi(getenv("RSF_RRQR_CHECK"))) : 4;
   for (int J = 0; !active.empty(); J += QR_NB) {
+    {
+      std::vector<int> keep;   // problems whose columns are exhausted were finished at the previous block
+      for (int i : active) if (J < std::min(probs[i].m, probs[i].c)) keep.push_back(i);
+      if (keep.size() != active.size()) {
+        hflag = flag.to_host(3 * P);
+        for (int i : active)
+          if (J >= std::min(probs[i].m, probs[i].c)) { res.k[i] = hflag[3 * i + 1]; res.done[i] = hflag[3 * i + 2]; }
+        active.swap(keep);
+        if (active.empty()) break;
+      }
+    }
     std::vector<RDesc> dv;
     for (int i : active) {
       RDesc d = base[i];
@@ -671,18 +688,26 @@ RRQRResult rrqr_batched(cudaStream_t s, const std::vector<RRQRProb>& probs, doub
     rank_kernel<<<na, NT, 0, s>>>(dd.p);
     count_launch();
     RSF_LAUNCH_CHECK();
-    hflag = flag.to_host(2 * P);
+    bool last = false;
+    for (size_t a = 0; a < dv.size(); ++a) last |= (J + dv[a].nbp >= std::min(dv[a].m, dv[a].c));
+    const bool check = last || ((J / QR_NB) % every == every - 1);
     std::vector<int> next;
     std::vector<RDesc> cont;
-    for (size_t a = 0; a < dv.size(); ++a) {
-      const int i = active[a];
-      if (hflag[2 * i]) {
-        res.k[i] = hflag[2 * i + 1];
-        res.done[i] = J + dv[a].nbp;
-      } else {
-        next.push_back(i);
-        cont.push_back(dv[a]);
+    if (check) {
+      hflag = flag.to_host(3 * P);
+      for (size_t a = 0; a < dv.size(); ++a) {
+        const int i = active[a];
+        if (hflag[3 * i]) {
+          res.k[i] = hflag[3 * i + 1];
+          res.done[i] = hflag[3 * i + 2];
+        } else {
+          next.push_back(i);
+          cont.push_back(dv[a]);
+        }
       }
+    } else {
+      next = active;
+      cont = dv;
     }
     if (!cont.empty()) {   // sketch downdate: Y2 -= Y1 R11^-1 R12
       auto dc = ring_up(cont, s);
