@@ -187,6 +187,10 @@ void rsf_profile_reset(void);
  * launch on the evaluation stream, the time between consecutive events attributed to the launch site
  * (diagnostics only; resets with rsf_profile_reset) */
 const char* rsf_trace_dump(void);
+/* batched-GEMM log "phase|file:line|TATB=seconds,flops,launches,ctas_min,ctas_max,kmin,kmax;..." collected
+ * when RSF_GEMMLOG=1: events around every batched GEMM, aggregated by phase and call site
+ * (diagnostics only; resets with rsf_profile_reset) */
+const char* rsf_debug_gemm_log(void);
 /* batched-GEMM statistics for the roofline: CUDA events around every launch on its stream.
  * rsf_stats_get fills {launches, seconds, algorithmic flops, compulsory bytes}. */
 void rsf_stats_enable(int on);

@@ -395,11 +395,17 @@ const char* rsf_profile_dump(void) {
   s = rsf::Prof::dump();
   return s.c_str();
 }
-void rsf_profile_reset(void) { rsf::Prof::reset(); rsf::KTrace::reset(); }
+void rsf_profile_reset(void) { rsf::Prof::reset(); rsf::KTrace::reset(); rsf::GemmLog::reset(); }
 
 const char* rsf_trace_dump(void) {
   static thread_local std::string s;
   s = rsf::KTrace::dump();
+  return s.c_str();
+}
+
+const char* rsf_debug_gemm_log(void) {
+  static thread_local std::string s;
+  s = rsf::GemmLog::dump();
   return s.c_str();
 }
 

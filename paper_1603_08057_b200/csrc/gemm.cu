@@ -333,6 +333,55 @@ void KTrace::reset() {
 }
 
 namespace {
+struct GRec { cudaEvent_t a, b; const char* phase; const char* file; int line; bool ta, tb; double flops;
+              long long ctas; int maxK, nprob; };
+struct GAgg { double sec = 0, flops = 0; long long cnt = 0, ctas_min = 1LL << 60, ctas_max = 0; int kmin = 1 << 30, kmax = 0; };
+std::vector<GRec>& grecs() { static std::vector<GRec> v; return v; }
+std::vector<std::pair<std::string, GAgg>>& gagg() { static std::vector<std::pair<std::string, GAgg>> v; return v; }
+void gdrain() {
+  for (auto& r : grecs()) {
+    cudaEventSynchronize(r.b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    const char* f = strrchr(r.file, '/');
+    std::string key = std::string(r.phase ? r.phase : "-") + "|" + (f ? f + 1 : r.file) + ":" + std::to_string(r.line) +
+                      "|" + (r.ta ? "T" : "N") + (r.tb ? "T" : "N");
+    auto& a = gagg();
+    size_t i = 0;
+    for (; i < a.size(); ++i) if (a[i].first == key) break;
+    if (i == a.size()) a.emplace_back(key, GAgg{});
+    GAgg& g = a[i].second;
+    g.sec += ms * 1e-3; g.flops += r.flops; g.cnt += 1;
+    g.ctas_min = std::min(g.ctas_min, r.ctas); g.ctas_max = std::max(g.ctas_max, r.ctas);
+    g.kmin = std::min(g.kmin, r.maxK); g.kmax = std::max(g.kmax, r.maxK);
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  grecs().clear();
+}
+}  // namespace
+bool GemmLog::on() {
+  static int e = -1;
+  if (e < 0) { const char* v = getenv("RSF_GEMMLOG"); e = (v && v[0] == '1') ? 1 : 0; }
+  return e == 1;
+}
+void GemmLog::push(cudaEvent_t e0, cudaEvent_t e1, const char* file, int line, bool ta, bool tb, double flops,
+                   long long ctas, int maxK, int nprob) {
+  grecs().push_back(GRec{e0, e1, KTrace::phase(), file, line, ta, tb, flops, ctas, maxK, nprob});
+  if (grecs().size() > 4096) gdrain();
+}
+std::string GemmLog::dump() {
+  gdrain();
+  std::string r;
+  for (auto& a : gagg())
+    r += a.first + "=" + std::to_string(a.second.sec) + "," + std::to_string(a.second.flops) + "," +
+         std::to_string(a.second.cnt) + "," + std::to_string(a.second.ctas_min) + "," +
+         std::to_string(a.second.ctas_max) + "," + std::to_string(a.second.kmin) + "," + std::to_string(a.second.kmax) + ";";
+  return r;
+}
+void GemmLog::reset() { gdrain(); gagg().clear(); }
+
+namespace {
 
 constexpr int BN = 64;
 constexpr int BK = 16;
@@ -972,7 +1021,7 @@ void GemmBatch::finalize_meta() const {
   totalN128_ = pre[2 * (P + 1) + P];
 }
 
-void GemmBatch::run(cudaStream_t s, double* X0, double* X1, int ldx, int Mglob) const {
+void GemmBatch::run(cudaStream_t s, double* X0, double* X1, int ldx, int Mglob, const char* file, int line) const {
   if (h_.empty()) return;
   if (!ready_) {   // transient batch: descriptors through the upload ring (no allocation)
     finalize_meta();
@@ -982,8 +1031,10 @@ void GemmBatch::run(cudaStream_t s, double* X0, double* X1, int ldx, int Mglob) 
   if (totalN_ == 0) return;
   int M = std::max(maxM_, glob_ ? Mglob : 0);
   if (M <= 0) return;
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr, g0 = nullptr, g1 = nullptr;
   if (KStats::on) KStats::record(s, &e0, nullptr);
+  const bool glog = GemmLog::on();
+  if (glog) KStats::record(s, &g0, nullptr);
   if (M <= 16 && !has_mapk_) {   // (only the pipelined kernel implements mapK)
     dim3 grid(totalN_, ceil_div(M, 16));
     launch_variant<16, 1>(ta_, tb_, grid, s, dp_, pp_, (int)h_.size(), X0, X1, ldx, Mglob);
@@ -1045,6 +1096,15 @@ void GemmBatch::run(cudaStream_t s, double* X0, double* X1, int ldx, int Mglob) 
   } else {
     dim3 grid(totalN_, ceil_div(M, 64));
     launch_variant<64, 4>(ta_, tb_, grid, s, dp_, pp_, (int)h_.size(), X0, X1, ldx, Mglob);
+  }
+  if (glog) {
+    KStats::record(s, nullptr, &g1);
+    long long ctas = 0;
+    for (const auto& d : h_) {
+      const int m = d.M < 0 ? Mglob : d.M;
+      if (m > 0 && d.N > 0) ctas += (long long)ceil_div(m, P_BM) * ceil_div(d.N, maxN_ <= 32 ? 32 : 64);
+    }
+    GemmLog::push(g0, g1, file, line, ta_, tb_, flops(Mglob), ctas, maxK_, (int)h_.size());
   }
   if (KStats::on) {
     KStats::record(s, nullptr, &e1);

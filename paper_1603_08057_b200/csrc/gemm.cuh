@@ -34,6 +34,17 @@ inline GemmDesc gdesc(int M, int N, int K) {
   return d;
 }
 
+// Per-launch GEMM log (diagnostics, RSF_GEMMLOG=1): events around every batched launch,
+// aggregated by (phase, call site, transposes); dump() lists the sites by time with their
+// achieved FP64 rate, CTA count and K range.
+struct GemmLog {
+  static bool on();
+  static void push(cudaEvent_t e0, cudaEvent_t e1, const char* file, int line, bool ta, bool tb, double flops,
+                   long long ctas, int maxK, int nprob);
+  static std::string dump();
+  static void reset();
+};
+
 class GemmBatch {
  public:
   GemmBatch() = default;
@@ -46,7 +57,9 @@ class GemmBatch {
   bool empty() const { return h_.empty(); }
   void finalize(cudaStream_t s) const;
   // Launch; X0/X1/ldx/Mglob resolve the per-call operands.
-  void run(cudaStream_t s, double* X0 = nullptr, double* X1 = nullptr, int ldx = 0, int Mglob = 0) const;
+  // (file/line: the call site, for the RSF_GEMMLOG diagnostics)
+  void run(cudaStream_t s, double* X0 = nullptr, double* X1 = nullptr, int ldx = 0, int Mglob = 0,
+           const char* file = __builtin_FILE(), int line = __builtin_LINE()) const;
   // flops of one run (2*M*N*K summed), for diagnostics
   double flops(int Mglob = 0) const;
 

@@ -37,6 +37,12 @@ double now_s() {
 
 inline GemmDesc tri(GemmDesc d, int t) { d.btri = t; return d; }   // triangular op(B)
 
+}  // namespace
+
+cudaStream_t& stream_override() { static thread_local cudaStream_t s = nullptr; return s; }
+
+namespace {
+
 struct BRef {
   const double* Bp = nullptr;   // permuted self block of a processed node (B_SS at top-left)
   int ld = 0;
@@ -614,7 +620,7 @@ std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams
 // ------------------------------------------------------------------ operators
 void solve_internal(const Fact& F, double* X, int k, double* tmp) {
   RSF_REQUIRE(F.which == W_SIGMA, ST_EINVAL, "solve needs a Sigma factor");
-  cudaStream_t s = F.ctx->stream;
+  cudaStream_t s = op_stream(F);
   const int L = F.tree->L;
   for (int lev = L; lev >= 1; --lev) {
     const Level& LV = F.levels[lev];
@@ -645,7 +651,7 @@ void solve_internal(const Fact& F, double* X, int k, double* tmp) {
 // x <- L^-1 x (forward sweeps, then C^-1) and x <- L^-T x (C^-T, then backward sweeps)
 void solve_half_fwd(const Fact& F, double* X, int k, double* tmp) {
   RSF_REQUIRE(F.which == W_SIGMA, ST_EINVAL, "solve needs a Sigma factor");
-  cudaStream_t s = F.ctx->stream;
+  cudaStream_t s = op_stream(F);
   for (int lev = F.tree->L; lev >= 1; --lev) {
     const Level& LV = F.levels[lev];
     RSF_PHASE(lvname("sv", lev), s);
@@ -664,7 +670,7 @@ void solve_half_fwd(const Fact& F, double* X, int k, double* tmp) {
 
 void solve_half_bwd(const Fact& F, double* X, int k, double* tmp) {
   RSF_REQUIRE(F.which == W_SIGMA, ST_EINVAL, "solve needs a Sigma factor");
-  cudaStream_t s = F.ctx->stream;
+  cudaStream_t s = op_stream(F);
   if (F.n0 > 0) {
     RSF_PHASE("sv.top", s);
     colcopy(s, tmp, X, k, k, nullptr, F.I0.p, F.n0);      // tmp = X(I0)
@@ -682,7 +688,7 @@ void solve_half_bwd(const Fact& F, double* X, int k, double* tmp) {
 }
 
 static void down_sweep(const Fact& F, double* X, int k, double* tmp) {
-  cudaStream_t s = F.ctx->stream;
+  cudaStream_t s = op_stream(F);
   for (int lev = 1; lev <= F.tree->L; ++lev) {
     const Level& LV = F.levels[lev];
     LV.dn1.run(s, X, tmp, k, k);
@@ -694,7 +700,7 @@ static void down_sweep(const Fact& F, double* X, int k, double* tmp) {
 
 void apply_internal(const Fact& F, double* X, int k, double* tmp) {
   RSF_REQUIRE(F.which == W_SIGMA && !F.solve_only, ST_EINVAL, "apply_internal needs a full Sigma factor");
-  cudaStream_t s = F.ctx->stream;
+  cudaStream_t s = op_stream(F);
   for (int lev = F.tree->L; lev >= 1; --lev) {
     const Level& LV = F.levels[lev];
     LV.up1.run(s, X, tmp, k, k);
@@ -709,7 +715,7 @@ void apply_internal(const Fact& F, double* X, int k, double* tmp) {
 
 void sqrt_internal(const Fact& F, double* X, int k, double* tmp) {
   RSF_REQUIRE(F.which == W_SIGMA && !F.solve_only, ST_EINVAL, "sample needs a full Sigma factor");
-  cudaStream_t s = F.ctx->stream;
+  cudaStream_t s = op_stream(F);
   if (F.n0 > 0) {
     F.top_q1.run(s, X, tmp, k, k);
     colcopy(s, X, tmp, k, k, F.I0.p, nullptr, F.n0);
@@ -719,7 +725,7 @@ void sqrt_internal(const Fact& F, double* X, int k, double* tmp) {
 
 void apply_only_internal(const Fact& F, double* X, double* Y, int k) {
   RSF_REQUIRE(F.which != W_SIGMA, ST_EINVAL, "apply_only needs a Sigma_i compression");
-  cudaStream_t s = F.ctx->stream;
+  cudaStream_t s = op_stream(F);
   const int L = F.tree->L;
   for (int lev = L; lev >= 1; --lev) {
     const Level& LV = F.levels[lev];

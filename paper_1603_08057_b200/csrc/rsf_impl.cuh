@@ -114,6 +114,16 @@ struct Fact {
 std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams& kp, int which,
                              double eps, const Opts& opts, bool solve_only = false);
 
+// Stream of the operators below: the factor's context stream unless a StreamScope on this
+// thread redirects them (the peeling runs its G applies on a second stream).
+cudaStream_t& stream_override();
+inline cudaStream_t op_stream(const Fact& F) { return stream_override() ? stream_override() : F.ctx->stream; }
+struct StreamScope {
+  cudaStream_t prev;
+  explicit StreamScope(cudaStream_t s) : prev(stream_override()) { stream_override() = s; }
+  ~StreamScope() { stream_override() = prev; }
+};
+
 // operations on X' (k x n column-major, tree order, ld = k): in place
 void solve_internal(const Fact& F, double* X, int k, double* tmp);
 // halves of the solve for F = L L^T: X <- L^-1 X (fwd) and X <- L^-T X (bwd)
