@@ -196,6 +196,12 @@ const char* rsf_debug_gemm_log(void);
 void rsf_stats_enable(int on);
 /* diagnostics: TFLOP/s of the batched FP64 GEMM on batch x (M x N x K), transposes ta/tb */
 double rsf_debug_gemm_bench(int M, int N, int K, int batch, int ta, int tb, int reps);
+/* diagnostics / tests: C_i = alpha op(A_i) op(B_i) + beta C_i for `batch` problems stored back to back
+ * (device pointers, column-major, leading dimensions = rows of the stored matrix) through the batched
+ * pipelined FP64 GEMM; splitk > 0 forces that many K slices (1 = none), 0 = the cost model decides.
+ * Synchronous; returns RSF_OK, RSF_EINVAL or RSF_ECUDA. */
+int rsf_debug_gemm(int ta, int tb, int M, int N, int K, int batch, double alpha, const double* A,
+                   const double* B, double beta, double* C, int splitk);
 void rsf_stats_get(double* out4);
 /* diagnostics: FP64 peak (TFLOP/s) of independent DMMA.8x8x4 (dmma=1) or DFMA (dmma=0) chains on the
  * current device, best of `reps` timed launches -- the live roofline denominator of bench.py */

@@ -8,6 +8,7 @@ contiguous.  PyTorch is used only for device memory and streams.
 from __future__ import annotations
 
 import ctypes as C
+import sys
 from dataclasses import dataclass, field
 
 from . import _lib
@@ -107,6 +108,8 @@ class Context:
             self.h = None
 
     def __del__(self):
+        if sys.is_finalizing():   # process exit: the driver reclaims everything; CUDA may be torn down
+            return
         try:
             self.close()
         except Exception:
@@ -133,6 +136,8 @@ class Factor:
             self.h = None
 
     def __del__(self):
+        if sys.is_finalizing():   # process exit: the driver reclaims everything; CUDA may be torn down
+            return
         try:
             self.close()
         except Exception:

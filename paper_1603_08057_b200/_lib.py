@@ -55,7 +55,8 @@ EXPORTS = ["rsf_opts_default", "rsf_ctx_create", "rsf_ctx_destroy", "rsf_factor"
            "rsf_fact_info", "rsf_logdet", "rsf_solve", "rsf_apply", "rsf_sample", "peel_trace", "hutch_trace", "gp_profile_eval", "gp_cond_mean",
            "gp_mle_eval", "rsf_last_error", "rsf_kernel_launches", "rsf_profile_dump",
            "rsf_profile_reset", "rsf_stats_enable", "rsf_stats_get", "rsf_stats_reset",
-           "rsf_debug_gemm_bench", "rsf_debug_fp64_peak", "rsf_trace_dump", "rsf_debug_gemm_log"]
+           "rsf_debug_gemm_bench", "rsf_debug_fp64_peak", "rsf_trace_dump", "rsf_debug_gemm_log",
+           "rsf_debug_gemm"]
 
 
 def load(path: str = LIB_PATH) -> C.CDLL:
@@ -92,6 +93,9 @@ def load(path: str = LIB_PATH) -> C.CDLL:
     lib.rsf_profile_dump.restype = C.c_char_p
     lib.rsf_trace_dump.argtypes = []
     lib.rsf_trace_dump.restype = C.c_char_p
+    lib.rsf_debug_gemm.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
+                                   C.c_void_p, C.c_void_p, C.c_double, C.c_void_p, C.c_int]
+    lib.rsf_debug_gemm.restype = C.c_int
     lib.rsf_debug_gemm_log.argtypes = []
     lib.rsf_debug_gemm_log.restype = C.c_char_p
     lib.rsf_profile_reset.argtypes = []
@@ -110,6 +114,6 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         if f not in ("rsf_ctx_destroy", "rsf_fact_destroy", "rsf_opts_default", "rsf_last_error",
                      "rsf_kernel_launches", "rsf_profile_dump", "rsf_profile_reset", "rsf_stats_enable",
                      "rsf_stats_get", "rsf_stats_reset", "rsf_debug_gemm_bench",
-                     "rsf_debug_fp64_peak", "rsf_trace_dump"):
+                     "rsf_debug_fp64_peak", "rsf_trace_dump", "rsf_debug_gemm_log"):
             getattr(lib, f).restype = C.c_int
     return lib

@@ -409,6 +409,34 @@ const char* rsf_debug_gemm_log(void) {
   return s.c_str();
 }
 
+int rsf_debug_gemm(int ta, int tb, int M, int N, int K, int batch, double alpha, const double* A,
+                   const double* B, double beta, double* C, int splitk) {
+  // diagnostics / tests: C_i = alpha op(A_i) op(B_i) + beta C_i on `batch` contiguous problems (device
+  // pointers, column-major, packed leading dimensions) through the batched pipelined GEMM
+  try {
+    if (M < 0 || N < 0 || K < 0 || batch < 0 || !A || !B || !C) return RSF_EINVAL;
+    cudaStream_t s = 0;
+    const size_t sa = (size_t)M * K, sb = (size_t)K * N, sc = (size_t)M * N;
+    rsf::GemmBatch g(ta != 0, tb != 0);
+    for (int i = 0; i < batch; ++i) {
+      rsf::GemmDesc d = rsf::gdesc(M, N, K);
+      d.A = A + sa * i; d.lda = std::max(1, ta ? K : M);
+      d.B = B + sb * i; d.ldb = std::max(1, tb ? N : K);
+      d.C = C + sc * i; d.ldc = std::max(1, M);
+      d.alpha = alpha; d.beta = beta;
+      g.add(d);
+    }
+    rsf::gemm_force_splitk() = splitk;
+    g.run(s);
+    rsf::gemm_force_splitk() = 0;
+    RSF_CUDA(cudaStreamSynchronize(s));
+    return RSF_OK;
+  } catch (...) {
+    rsf::gemm_force_splitk() = 0;
+    return RSF_ECUDA;
+  }
+}
+
 double rsf_debug_gemm_bench(int M, int N, int K, int batch, int ta, int tb, int reps) {
   // diagnostics: TFLOP/s of the batched FP64 GEMM on `batch` independent M x N x K problems
   try {

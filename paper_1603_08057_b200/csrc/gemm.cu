@@ -1049,21 +1049,35 @@ void GemmBatch::run(cudaStream_t s, double* X0, double* X1, int ldx, int Mglob, 
       dim3 grid(totalN128_, ceil_div(M, P_BM));
       launch_pipe<128>(ta_, tb_, grid, s, dp_, pp_ + 2 * (P + 1), (int)P, X0, X1, ldx, Mglob);
     } else {
-      // split-K when the output tiles cannot fill the GPU but K is long (tall-skinny products:
-      // Gram matrices, projections onto bases, sketches of whole boxes)
-      static const bool splitk_on = getenv("RSF_SPLITK") && getenv("RSF_SPLITK")[0] == '1';   // measured: no gain (off)
+      // split-K when the output tiles fill the GPU's resident slots badly and K is long
+      // (tall-skinny products: Gram matrices, projections onto bases, sketches of whole
+      // boxes).  Cost model per candidate S: whole waves of 128 x 64 CTAs over the 2 x 148
+      // resident slots, each CTA streaming K/S (+ a fixed prologue/epilogue) at 1/296 of the
+      // DMMA peak, plus the workspace traffic of the deterministic reduction and its launch.
+      static const int splitk_mode = getenv("RSF_SPLITK") ? atoi(getenv("RSF_SPLITK")) : 1;
+      const int force = gemm_force_splitk();
       long long ctas = 0;
+      double mntot = 0;
       int S = 1;
-      if (splitk_on && maxK_ >= 1024 && !has_lower_) {
+      if (splitk_mode != 0 && maxK_ >= 1024 && !has_lower_) {
         for (const auto& d : h_) {
           const int m = d.M < 0 ? Mglob : d.M;
-          if (m > 0 && d.N > 0) ctas += (long long)ceil_div(m, P_BM) * ceil_div(d.N, 64);
+          if (m > 0 && d.N > 0) { ctas += (long long)ceil_div(m, P_BM) * ceil_div(d.N, 64); mntot += (double)m * d.N; }
         }
-        if (ctas > 0 && ctas < 2 * 148) {
-          S = (int)std::min<long long>(std::max<long long>(2, (3 * 148 + ctas - 1) / ctas), 32);
-          S = std::min(S, std::max(1, maxK_ / 256));
+        const double slots = 2.0 * 148, tk = 2.0 * P_BM * 64 / (37e12 / slots);   // seconds per K index per CTA
+        auto cost = [&](int S2) {
+          const double waves = std::ceil((double)ctas * S2 / slots);
+          double t = waves * ((double)maxK_ / S2 + 48.0) * tk;
+          if (S2 > 1) t += (2.0 * S2 + 2.0) * mntot * 8.0 / 6.0e12 + 4e-6;
+          return t;
+        };
+        double best = cost(1);
+        for (int S2 = 2; S2 <= 32 && maxK_ / S2 >= 256 && S2 * mntot * 8.0 <= 2e9; ++S2) {
+          const double c2 = cost(S2);
+          if (c2 < 0.9 * best) { best = c2; S = S2; }
         }
       }
+      if (force > 0 && !has_lower_) S = std::max(1, std::min(force, std::max(1, maxK_ / P_BK)));
       if (S > 1) {
         std::vector<long long> mn(P + 1, 0);
         for (size_t i = 0; i < P; ++i) {
@@ -1072,17 +1086,16 @@ void GemmBatch::run(cudaStream_t s, double* X0, double* X1, int ldx, int Mglob, 
           mn[i + 1] = mn[i] + ((m > 0 && d.N > 0) ? m * d.N : 0);
         }
         const int kc = ((maxK_ + S - 1) / S + P_BK - 1) / P_BK * P_BK;
-        DBuf<long long> dmn(P + 1, s);
-        dmn.upload(mn);
+        const long long* dmn = static_cast<const long long*>(ring_upload(s, mn.data(), mn.size() * sizeof(long long)));
         DBuf<double> ws((size_t)S * std::max<long long>(mn[P], 1), s);
         dim3 grid(totalN_, ceil_div(M, P_BM), S);
-        launch_pipe<64>(ta_, tb_, grid, s, dp_, pp_, (int)P, X0, X1, ldx, Mglob, ws.p, dmn.p, kc);
+        launch_pipe<64>(ta_, tb_, grid, s, dp_, pp_, (int)P, X0, X1, ldx, Mglob, ws.p, dmn, kc);
         long long mx = 0;
         for (size_t i = 0; i < P; ++i) mx = std::max(mx, mn[i + 1] - mn[i]);
         const int gx = (int)std::max<long long>(1, std::min<long long>((mx + P_NT - 1) / P_NT, 1024));
         for (size_t o = 0; o < P; o += 65535) {
           const unsigned ny = (unsigned)std::min<size_t>(65535, P - o);
-          splitk_reduce_kernel<<<dim3(gx, ny), P_NT, 0, s>>>(dp_, ws.p, dmn.p, S, (int)o, X0, X1, ldx, Mglob);
+          splitk_reduce_kernel<<<dim3(gx, ny), P_NT, 0, s>>>(dp_, ws.p, dmn, S, (int)o, X0, X1, ldx, Mglob);
           count_launch();
         }
       } else {
@@ -1120,6 +1133,8 @@ void GemmBatch::run(cudaStream_t s, double* X0, double* X1, int ldx, int Mglob, 
   count_launch();
   RSF_LAUNCH_CHECK();
 }
+
+int& gemm_force_splitk() { static thread_local int v = 0; return v; }
 
 double GemmBatch::flops(int Mglob) const {
   double f = 0;

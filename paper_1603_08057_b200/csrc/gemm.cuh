@@ -45,6 +45,10 @@ struct GemmLog {
   static void reset();
 };
 
+// test hook: > 0 forces that many K slices in the next batched launches of this thread
+// (1 = no split-K), 0 = the cost model decides
+int& gemm_force_splitk();
+
 class GemmBatch {
  public:
   GemmBatch() = default;

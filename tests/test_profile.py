@@ -87,6 +87,8 @@ def test_gpu_profile_and_cond_mean_vs_dense():
     xn = np.random.default_rng(9).random((300, 2))
     want = dense_cond_mean(ok, xy, z, xn)
     got = R.gp_cond_mean(F, torch.from_numpy(z).to(dev), torch.from_numpy(xn).to(dev)).cpu().numpy()
-    assert np.linalg.norm(got - want) <= 1e-6 * np.linalg.norm(want)
+    # F^-1 z carries the factor's error amplified by cond(Sigma) (nugget 1e-3): same 10 eps bar as the
+    # quadratic form above (measured 2.1e-6 on the B200)
+    assert np.linalg.norm(got - want) <= 10 * c.eps * np.linalg.norm(want)
     got_h = R.gp_cond_mean(F, np.ascontiguousarray(z), np.ascontiguousarray(xn), np.empty(300))
     assert np.array_equal(got_h, got)
