@@ -107,8 +107,8 @@ class Context:
             lib.rsf_ctx_destroy(self.h)
             self.h = None
 
-    def __del__(self):
-        if sys.is_finalizing():   # process exit: the driver reclaims everything; CUDA may be torn down
+    def __del__(self, _finalizing=sys.is_finalizing):
+        if _finalizing():   # process exit: the driver reclaims everything; CUDA may be torn down
             return
         try:
             self.close()
@@ -135,8 +135,8 @@ class Factor:
             lib.rsf_fact_destroy(self.h)
             self.h = None
 
-    def __del__(self):
-        if sys.is_finalizing():   # process exit: the driver reclaims everything; CUDA may be torn down
+    def __del__(self, _finalizing=sys.is_finalizing):
+        if _finalizing():   # process exit: the driver reclaims everything; CUDA may be torn down
             return
         try:
             self.close()

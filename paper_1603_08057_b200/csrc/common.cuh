@@ -143,6 +143,8 @@ struct Prof {
   static std::string dump();
   static void reset();
 };
+// per-level phase names wanted (profiling, GEMM log or NVTX ranges on)
+bool phase_names_on();
 struct PhaseTimer {
   const char* name;
   cudaStream_t s;
@@ -156,6 +158,7 @@ struct PhaseTimer {
 struct PhaseSeq {
   cudaStream_t s;
   const char* name = nullptr;
+  bool open_ = false;   // an NVTX range of this sequence is open
   double t0 = 0;
   bool on;
   const char* prev_phase;

@@ -10,6 +10,7 @@
 #include <string>
 
 #include "gemm.cuh"
+#include <nvtx3/nvToolsExt.h>
 
 namespace rsf {
 
@@ -243,14 +244,28 @@ std::string Prof::dump() {
   return r;
 }
 void Prof::reset() { prof_table().clear(); }
+// NVTX ranges named after the phases (RSF_NVTX=1), so that `ncu --nvtx --nvtx-include <phase>/`
+// can select the launches of one phase and level
+static bool nvtx_on() {
+  static int e = -1;
+  if (e < 0) { const char* v = getenv("RSF_NVTX"); e = (v && v[0] == '1') ? 1 : 0; }
+  return e == 1;
+}
+bool phase_names_on() { return Prof::enabled() || GemmLog::on() || nvtx_on(); }
 PhaseTimer::PhaseTimer(const char* n, cudaStream_t st) : name(n), s(st), on(Prof::enabled()) {
   prev_phase = KTrace::phase();
   KTrace::phase() = n;
+  if (nvtx_on()) nvtxRangePushA(n);
   if (on) { cudaStreamSynchronize(s); t0 = wall(); }
 }
 PhaseSeq::PhaseSeq(cudaStream_t st) : s(st), on(Prof::enabled()) { prev_phase = KTrace::phase(); }
 void PhaseSeq::next(const char* n) {
   KTrace::phase() = n ? n : prev_phase;
+  if (nvtx_on()) {
+    if (open_) nvtxRangePop();
+    open_ = n != nullptr;
+    if (n) nvtxRangePushA(n);
+  }
   if (!on) return;
   cudaStreamSynchronize(s);
   const double t = wall();
@@ -260,6 +275,7 @@ void PhaseSeq::next(const char* n) {
 }
 PhaseTimer::~PhaseTimer() {
   KTrace::phase() = prev_phase;
+  if (nvtx_on()) nvtxRangePop();
   if (on) { cudaStreamSynchronize(s); Prof::add(name, wall() - t0); }
 }
 
@@ -332,10 +348,12 @@ void KTrace::reset() {
   g_nmiss_small = g_nmiss_large = 0;
 }
 
+long long g_pipe_launches = 0;   // gemm_pipe_kernel launches of this process (ncu -k regex:gemm_pipe -s <ordinal>)
 namespace {
 struct GRec { cudaEvent_t a, b; const char* phase; const char* file; int line; bool ta, tb; double flops;
-              long long ctas; int maxK, nprob; };
-struct GAgg { double sec = 0, flops = 0; long long cnt = 0, ctas_min = 1LL << 60, ctas_max = 0; int kmin = 1 << 30, kmax = 0; };
+              long long ctas; int maxK, maxM; long long ord; };
+struct GAgg { double sec = 0, flops = 0; long long cnt = 0, ctas_min = 1LL << 60, ctas_max = 0; int kmin = 1 << 30, kmax = 0;
+              double tmax = 0; long long ord_max = -1; };
 std::vector<GRec>& grecs() { static std::vector<GRec> v; return v; }
 std::vector<std::pair<std::string, GAgg>>& gagg() { static std::vector<std::pair<std::string, GAgg>> v; return v; }
 void gdrain() {
@@ -345,7 +363,7 @@ void gdrain() {
     cudaEventElapsedTime(&ms, r.a, r.b);
     const char* f = strrchr(r.file, '/');
     std::string key = std::string(r.phase ? r.phase : "-") + "|" + (f ? f + 1 : r.file) + ":" + std::to_string(r.line) +
-                      "|" + (r.ta ? "T" : "N") + (r.tb ? "T" : "N");
+                      "|" + (r.ta ? "T" : "N") + (r.tb ? "T" : "N") + "|M" + std::to_string(r.maxM);
     auto& a = gagg();
     size_t i = 0;
     for (; i < a.size(); ++i) if (a[i].first == key) break;
@@ -354,6 +372,7 @@ void gdrain() {
     g.sec += ms * 1e-3; g.flops += r.flops; g.cnt += 1;
     g.ctas_min = std::min(g.ctas_min, r.ctas); g.ctas_max = std::max(g.ctas_max, r.ctas);
     g.kmin = std::min(g.kmin, r.maxK); g.kmax = std::max(g.kmax, r.maxK);
+    if (ms * 1e-3 > g.tmax) { g.tmax = ms * 1e-3; g.ord_max = r.ord; }
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
   }
@@ -366,8 +385,8 @@ bool GemmLog::on() {
   return e == 1;
 }
 void GemmLog::push(cudaEvent_t e0, cudaEvent_t e1, const char* file, int line, bool ta, bool tb, double flops,
-                   long long ctas, int maxK, int nprob) {
-  grecs().push_back(GRec{e0, e1, KTrace::phase(), file, line, ta, tb, flops, ctas, maxK, nprob});
+                   long long ctas, int maxK, int maxM) {
+  grecs().push_back(GRec{e0, e1, KTrace::phase(), file, line, ta, tb, flops, ctas, maxK, maxM, g_pipe_launches - 1});
   if (grecs().size() > 4096) gdrain();
 }
 std::string GemmLog::dump() {
@@ -376,7 +395,8 @@ std::string GemmLog::dump() {
   for (auto& a : gagg())
     r += a.first + "=" + std::to_string(a.second.sec) + "," + std::to_string(a.second.flops) + "," +
          std::to_string(a.second.cnt) + "," + std::to_string(a.second.ctas_min) + "," +
-         std::to_string(a.second.ctas_max) + "," + std::to_string(a.second.kmin) + "," + std::to_string(a.second.kmax) + ";";
+         std::to_string(a.second.ctas_max) + "," + std::to_string(a.second.kmin) + "," + std::to_string(a.second.kmax) + "," +
+         std::to_string(a.second.ord_max) + ";";
   return r;
 }
 void GemmLog::reset() { gdrain(); gagg().clear(); }
@@ -935,6 +955,7 @@ void launch_pipe(bool ta, bool tb, dim3 grid, cudaStream_t s, const GemmDesc* d,
     cudaFuncSetAttribute(gemm_pipe_kernel<true, true, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
     attr = true;
   }
+  ++g_pipe_launches;
   const int mt = (int)grid.y;
   const dim3 g1((unsigned)((long long)grid.x * grid.y), 1, grid.z);   // 1-D over (N-tile, M-tile)
   if (!ta && !tb) gemm_pipe_kernel<false, false, BN><<<g1, P_NT, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk, mt);
@@ -1113,11 +1134,13 @@ void GemmBatch::run(cudaStream_t s, double* X0, double* X1, int ldx, int Mglob, 
   if (glog) {
     KStats::record(s, nullptr, &g1);
     long long ctas = 0;
+    double fl = 0;
     for (const auto& d : h_) {
       const int m = d.M < 0 ? Mglob : d.M;
       if (m > 0 && d.N > 0) ctas += (long long)ceil_div(m, P_BM) * ceil_div(d.N, maxN_ <= 32 ? 32 : 64);
+      fl += (d.btri ? 1.0 : 2.0) * m * d.N * d.K;   // triangular op(B): TRMM flops
     }
-    GemmLog::push(g0, g1, file, line, ta_, tb_, flops(Mglob), ctas, maxK_, (int)h_.size());
+    GemmLog::push(g0, g1, file, line, ta_, tb_, fl, ctas, maxK_, M);
   }
   if (KStats::on) {
     KStats::record(s, nullptr, &e1);

@@ -40,7 +40,7 @@ inline GemmDesc gdesc(int M, int N, int K) {
 struct GemmLog {
   static bool on();
   static void push(cudaEvent_t e0, cudaEvent_t e1, const char* file, int line, bool ta, bool tb, double flops,
-                   long long ctas, int maxK, int nprob);
+                   long long ctas, int maxK, int maxM);
   static std::string dump();
   static void reset();
 };

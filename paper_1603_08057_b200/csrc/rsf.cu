@@ -54,7 +54,7 @@ struct BRef {
 // per-level phase names for RSF_PROFILE=1 (diagnostics)
 static const char* lvname(const char* op, int lev) {
   static std::vector<std::string> names;
-  if (!Prof::enabled()) return op;
+  if (!phase_names_on()) return op;
   const std::string key = std::string(op) + ".L" + std::to_string(lev);
   for (size_t i = 0; i < names.size(); ++i) if (names[i] == key) return names[i].c_str();
   if (names.empty()) names.reserve(4096);   // stable c_str() pointers

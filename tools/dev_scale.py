@@ -64,10 +64,10 @@ if gl:
     rows = []
     for x in gl.strip(';').split(';'):
         k, v = x.rsplit('=', 1)
-        sec, fl, cnt, c0, c1, k0, k1 = v.split(',')
-        rows.append((float(sec), float(fl), int(float(cnt)), k, c0, c1, k0, k1))
+        sec, fl, cnt, c0, c1, k0, k1, om = v.split(',')
+        rows.append((float(sec), float(fl), int(float(cnt)), k, c0, c1, k0, k1, om))
     rows.sort(reverse=True)
     tot = sum(r[0] for r in rows)
     print(f'GEMMLOG total {tot:.3f} s over {sum(r[2] for r in rows)} launches, {sum(r[1] for r in rows)/tot/1e12:.2f} TF/s')
-    for sec, fl, cnt, k, c0, c1, k0, k1 in rows[:45]:
-        print(f'  {sec:8.3f} s {100*sec/tot:5.1f}% {fl/max(sec,1e-12)/1e12:6.2f} TF/s n={cnt:6d} ctas {c0}-{c1} K {k0}-{k1}  {k}')
+    for sec, fl, cnt, k, c0, c1, k0, k1, om in rows[:60]:
+        print(f'  {sec:8.3f} s {100*sec/tot:5.1f}% {fl/max(sec,1e-12)/1e12:6.2f} TF/s n={cnt:6d} ctas {c0}-{c1} K {k0}-{k1} longest#{om}  {k}')
