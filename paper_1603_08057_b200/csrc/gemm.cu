@@ -742,8 +742,9 @@ __global__ void __launch_bounds__(P_NT, (BN >= 128 ? 1 : 2)) gemm_pipe_kernel(co
                                                             const int* __restrict__ prefix, int nprob,
                                                             double* X0, double* X1, int ldx, int Mglob,
                                                             double* ws, const long long* __restrict__ mnpre,
-                                                            int kchunk, int mtiles) {
+                                                            int kchunk, int mtiles, int smem_epi) {
   constexpr int LDB = p_ldb<BN>(), NI = BN / 16, WN = BN / 2;
+  static_assert(BN * P_LDA <= P_ST * P_BK * (P_LDA + p_ldb<BN>()), "C tile must fit in the pipeline buffers");
   extern __shared__ __align__(16) double psm[];
   double* As = psm;                              // [ST][BK][LDA]
   double* Bs = psm + P_ST * P_BK * P_LDA;        // [ST][BK][LDB]
@@ -922,6 +923,48 @@ __global__ void __launch_bounds__(P_NT, (BN >= 128 ? 1 : 2)) gemm_pipe_kernel(co
     return;
   }
   const double alpha = dd.alpha, beta = dd.beta;
+  if (smem_epi) {
+    // Epilogue through shared memory (the pipeline buffers are free now): the C tile is
+    // fetched with one burst of cp.async when beta != 0 (instead of 32 dependent global loads
+    // per thread) and written back column by column with coalesced stores.
+    constexpr int LDC = P_LDA;                    // 2 wavefronts per 32-lane fragment access
+    double* Cs = psm;                             // [BN][LDC], column j of the tile at Cs + j * LDC
+    const int mrows = min(P_BM, M - m0), ncols = min(BN, N - n0);
+    __syncthreads();                              // every warp is done with the last stage
+    if (beta != 0.0) {
+      for (int e = tid; e < P_BM * BN; e += P_NT) {
+        const int i = e % P_BM, j = e / P_BM;
+        if (i < mrows && j < ncols) {
+          const long long cc = mapC ? __ldg(mapC + n0 + j) : n0 + j;
+          cp_async8(Cs + j * LDC + i, C + cc * ldc + m0 + i, true);
+        }
+      }
+      cp_async_commit();
+      cp_async_wait<0>();
+      __syncthreads();
+    }
+#pragma unroll
+    for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = wn * WN + ni * 8 + 2 * tq + h;
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) {
+          const int i = wm * 32 + mi * 8 + g;
+          double* c = Cs + j * LDC + i;
+          *c = (beta != 0.0) ? fma(beta, *c, alpha * acc[mi][ni][h]) : alpha * acc[mi][ni][h];
+        }
+      }
+    __syncthreads();
+    for (int e = tid; e < P_BM * BN; e += P_NT) {
+      const int i = e % P_BM, j = e / P_BM;
+      if (i < mrows && j < ncols) {
+        const long long cc = mapC ? __ldg(mapC + n0 + j) : n0 + j;
+        C[cc * ldc + m0 + i] = Cs[j * LDC + i];
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int ni = 0; ni < NI; ++ni) {
 #pragma unroll
@@ -956,12 +999,13 @@ void launch_pipe(bool ta, bool tb, dim3 grid, cudaStream_t s, const GemmDesc* d,
     attr = true;
   }
   ++g_pipe_launches;
+  static const int epi = getenv("RSF_GEMM_EPI") ? atoi(getenv("RSF_GEMM_EPI")) : 1;
   const int mt = (int)grid.y;
   const dim3 g1((unsigned)((long long)grid.x * grid.y), 1, grid.z);   // 1-D over (N-tile, M-tile)
-  if (!ta && !tb) gemm_pipe_kernel<false, false, BN><<<g1, P_NT, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk, mt);
-  else if (ta && !tb) gemm_pipe_kernel<true, false, BN><<<g1, P_NT, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk, mt);
-  else if (!ta && tb) gemm_pipe_kernel<false, true, BN><<<g1, P_NT, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk, mt);
-  else gemm_pipe_kernel<true, true, BN><<<g1, P_NT, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk, mt);
+  if (!ta && !tb) gemm_pipe_kernel<false, false, BN><<<g1, P_NT, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk, mt, epi);
+  else if (ta && !tb) gemm_pipe_kernel<true, false, BN><<<g1, P_NT, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk, mt, epi);
+  else if (!ta && tb) gemm_pipe_kernel<false, true, BN><<<g1, P_NT, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk, mt, epi);
+  else gemm_pipe_kernel<true, true, BN><<<g1, P_NT, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk, mt, epi);
 }
 
 // split-K reduction: C = alpha * sum_z W_z + beta * C (fixed summation order: deterministic)

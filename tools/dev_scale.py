@@ -69,5 +69,5 @@ if gl:
     rows.sort(reverse=True)
     tot = sum(r[0] for r in rows)
     print(f'GEMMLOG total {tot:.3f} s over {sum(r[2] for r in rows)} launches, {sum(r[1] for r in rows)/tot/1e12:.2f} TF/s')
-    for sec, fl, cnt, k, c0, c1, k0, k1, om in rows[:60]:
+    for sec, fl, cnt, k, c0, c1, k0, k1, om in rows[:400]:
         print(f'  {sec:8.3f} s {100*sec/tot:5.1f}% {fl/max(sec,1e-12)/1e12:6.2f} TF/s n={cnt:6d} ctas {c0}-{c1} K {k0}-{k1} longest#{om}  {k}')
