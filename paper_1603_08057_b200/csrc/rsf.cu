@@ -300,6 +300,24 @@ std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams
     LV.S.upload(hS);
     LV.R.alloc(std::max<size_t>(hR.size(), 1), s);
     LV.R.upload(hR);
+    {
+      static const bool fused_on0 = !(getenv("RSF_FUSED") && std::string(getenv("RSF_FUSED")) == "0");
+      static const bool stack_on = !(getenv("RSF_STACKED") && std::string(getenv("RSF_STACKED")) == "0");
+      int mi = 0;
+      for (int b = 0; b < nb; ++b) mi = std::max(mi, cvec[b]);
+      LV.stacked = !sig && stack_on && !(fused_on0 && mi <= SWEEP_MAX_I);
+      if (LV.stacked) {
+        std::vector<int> hSR;
+        LV.sroff.resize(nb);
+        for (int b = 0; b < nb; ++b) {
+          LV.sroff[b] = hSR.size();
+          hSR.insert(hSR.end(), hS.begin() + LV.soff[b], hS.begin() + LV.soff[b] + kvec[b]);
+          hSR.insert(hSR.end(), hR.begin() + LV.roff[b], hR.begin() + LV.roff[b] + (cvec[b] - kvec[b]));
+        }
+        LV.SR.alloc(std::max<size_t>(hSR.size(), 1), s);
+        LV.SR.upload(hSR);
+      }
+    }
 
     // ---- self blocks and permutation
     std::vector<int> hIall;
@@ -352,9 +370,16 @@ std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams
       LV.loff[b] = ltot; ltot += r * r;
     }
     LV.T.alloc(std::max<long long>(ttot, 1), s);
-    LV.E.alloc(std::max<long long>(ttot, 1), s);
+    if (LV.stacked) {
+      long long et = 0;
+      LV.eloff.resize(nb);
+      for (int b = 0; b < nb; ++b) { LV.eloff[b] = et; et += (long long)cvec[b] * LV.r[b]; }
+      LV.EL.alloc(std::max<long long>(et, 1), s);
+    } else {
+      LV.E.alloc(std::max<long long>(ttot, 1), s);
+    }
     // L is needed by apply / sample only; a solve-only factor (Alg. 1) keeps L^-1
-    if (!(sig && solve_only)) LV.L.alloc(std::max<long long>(ltot, 1), s);
+    if (!(sig && solve_only) && !LV.stacked) LV.L.alloc(std::max<long long>(ltot, 1), s);
     if (sig) LV.Linv.alloc(std::max<long long>(ltot, 1), s);
     {
       GemmBatch e1(false, false), e2(false, false), e3(true, false);
@@ -434,6 +459,10 @@ std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams
           if (r == 0) continue;
           double* B = Bp.p + bsz[b];
           sy.push_back(SymDesc{B + (long long)k * c + k, c, r});
+          if (LV.stacked) {   // [X_SR; X_RR] = the columns R of the pivoted block, as they are
+            lc.push_back(CopyProb{B + (long long)k * c, c, LV.EL.p + LV.eloff[b], c, c, r, 1.0});
+            continue;
+          }
           lc.push_back(CopyProb{B + (long long)k * c + k, c, LV.L.p + LV.loff[b], r, r, r, 1.0});
           if (k > 0) lc.push_back(CopyProb{B + (long long)k * c, c, LV.E.p + LV.eoff[b], k, k, r, 1.0});
         }
@@ -470,8 +499,8 @@ std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams
       const int* Sb = LV.S.p + LV.soff[b];
       const int* Rb = LV.R.p + LV.roff[b];
       const double* Tb = LV.T.p + LV.toff[b];
-      const double* Lb = LV.L.p + LV.loff[b];
-      const double* Eb = LV.E.p + LV.eoff[b];
+      const double* Lb = LV.L.p ? LV.L.p + LV.loff[b] : nullptr;
+      const double* Eb = LV.E.p ? LV.E.p + LV.eoff[b] : nullptr;
       auto mk = [&](int N, int K, int selA, const int* mapA, long long offA, const double* Bm, int ldb,
                     int selC, const int* mapC, long long offC, double alpha, double beta) {
         GemmDesc d = gdesc(-1, N, K);
@@ -496,6 +525,15 @@ std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams
         if (k > 0) LV.dn1.add(mk(k, r, 1, Rb, 0, Eb, k, 1, Sb, 0, 1.0, 1.0));
         LV.dn2.add(tri(mk(r, r, 1, Rb, 0, Lb, r, 2, nullptr, tc[b], 1.0, 0.0), 2));
         if (k > 0) LV.dn4.add(mk(r, k, 1, Sb, 0, Tb, k, 1, Rb, 0, 1.0, 1.0));
+      } else if (LV.stacked) {
+        // X0 = x (modified), X1 = y;  y_R = [X_SR; X_RR]^T [x_S; x_R] in one GEMM (K = |I_b|)
+        const int* SRb = LV.SR.p + LV.sroff[b];
+        const double* ELb = LV.EL.p + LV.eloff[b];
+        const int c = k + r;
+        if (k > 0) LV.ao1.add(mk(k, r, 1, Rb, 0, Tb, k, 1, Sb, 0, 1.0, 1.0));
+        LV.ao2a.add(mk(r, c, 1, SRb, 0, ELb, c, 2, Rb, 0, 1.0, 0.0));
+        if (k > 0) LV.ao3.add(mk(k, r, 1, Rb, 0, ELb, c, 2, Sb, 0, 1.0, 1.0));
+        if (k > 0) LV.ao4.add(mk(r, k, 2, Sb, 0, Tb, k, 2, Rb, 0, 1.0, 1.0));
       } else {
         // X0 = x (modified), X1 = y
         if (k > 0) LV.ao1.add(mk(k, r, 1, Rb, 0, Tb, k, 1, Sb, 0, 1.0, 1.0));

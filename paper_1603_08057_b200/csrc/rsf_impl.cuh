@@ -72,13 +72,20 @@ struct Level {
   DBuf<double> T;      // k x r (ld k)
   DBuf<double> L, Linv;  // r x r (Sigma) | XRR r x r (Sigma_i, in L)
   DBuf<double> E;      // k x r (Sigma: E; Sigma_i: X_SR)
+  // Sigma_i levels swept by batched GEMMs: [X_SR; X_RR] stacked per box (c x r, ld c, the
+  // columns R of the pivoted block), so that y_R = X_SR^T x_S + X_RR x_R is one GEMM over the
+  // box's indices in [S; R] order (SR)
+  bool stacked = false;
+  DBuf<double> EL;
+  std::vector<long long> eloff, sroff;
+  DBuf<int> SR;
   long long rtot = 0;  // sum r (tmp columns)
   // sweep GEMM batches (M = number of RHS, per call)
   GemmBatch fs1, fs2, fs3;            // forward solve
   GemmBatch bs2, bs3, bs4;            // backward solve
   GemmBatch up1, up2, up3;            // apply, up
   GemmBatch dn1, dn2, dn4;            // apply, down
-  GemmBatch ao1, ao2a, ao2b, ao3, ao4;  // apply-only (Sigma_i)
+  GemmBatch ao1, ao2a, ao2b, ao3, ao4;  // apply-only (Sigma_i); ao2a alone when stacked
   // fused small-box sweeps (sweep.cuh): used when every box has |I_b| <= SWEEP_MAX_I
   bool fused = false;
   int max_i = 0, nops = 0;

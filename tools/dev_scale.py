@@ -35,7 +35,8 @@ for rep in range(reps):
     if __import__('os').environ.get('RSF_KTRACE') == '1':
         trr = R.lib.rsf_trace_dump().decode()
         print('   alloc:', ' '.join(x for x in trr.split(';') if x.startswith('alloc') or x.startswith('host-')))
-        R.lib.rsf_profile_reset()
+        if rep < reps - 1:
+            R.lib.rsf_profile_reset()
     print(f'eval {el:.3f}s ell={r.ell:.10e} grad={r.grad} tree {d.t_tree:.3f} factor {d.t_factor:.3f} compress {d.t_compress:.3f} solve {d.t_solve:.3f} peel {d.t_peel:.3f} launches {d.kernel_launches:.0f}', flush=True)
     for i in range(len(c.theta)):
         p = d.peel[i]
