@@ -196,6 +196,14 @@ def cpu_baseline_sample(args, c):
                       f"n^1.6 (P:830)", "sample_seconds": t_s}
 
 
+# ncu --set full of the longest launch of the dominant kernel (profiles/r01_gemm_pipe_ncu_v3.txt)
+TRAFFIC_BYTES = 4.119e9 + 0.692e9
+TRAFFIC_NOTE = ("dram__bytes_read.sum + dram__bytes_write.sum of gemm_pipe_kernel launch #14677 (the longest "
+                "peeling-subtraction launch, 14.05 ms, 12288 CTAs, DMMA pipe 83 % busy); its compulsory "
+                "bytes are ~5.6e9 (V_i of three level-1 boxes 4.2 GB + the Y' block read and written), "
+                "so operands are not re-read from DRAM")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -324,7 +332,12 @@ def main():
                                 f"{fp64_peak:.2f} TFLOP/s, DFMA {fp64_peak_dfma:.2f}; no FP64 figure in "
                                 "MEASURED_PEAKS.json; nominal 148 SM x 64 FMA/clk x 2 x 1.965 GHz = "
                                 f"{FP64_PEAK_TFLOPS:.1f}"),
-                "traffic": None, "launches": int(gl), "kernel_seconds": gsec,
+                # DRAM bytes of one representative dominant launch (ncu --set full, see the note)
+                "traffic": TRAFFIC_BYTES, "traffic_note": TRAFFIC_NOTE,
+                "launches": int(gl), "kernel_seconds": gsec,
+                "timing": "CUDA events around every launch on its stream; kernel_seconds = length of the "
+                          "union of the launch intervals (the trace jobs run on concurrent streams, so "
+                          "summed durations would double-count overlap)",
                 "share_of_step": gsec / (t_local) if t_local > 0 else None,
                 "algorithmic_flops_per_launch": gfl / gl if gl else None}
     fl_factor = d.flops_factor

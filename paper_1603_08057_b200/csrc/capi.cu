@@ -176,6 +176,12 @@ rsf_status rsf_ctx_create(int device, void* cuda_stream, void* nccl_comm, rsf_ct
 
 void rsf_ctx_destroy(rsf_ctx ctx) {
   if (!ctx) return;
+  for (cudaStream_t a : ctx->ctx.aux) {
+    cudaStreamSynchronize(a);
+    rsf::dev_cache_trim(a);
+    cudaStreamSynchronize(a);
+    cudaStreamDestroy(a);
+  }
   cudaStreamSynchronize(ctx->ctx.stream);
   rsf::dev_cache_trim(ctx->ctx.stream);
   cudaStreamSynchronize(ctx->ctx.stream);

@@ -2,6 +2,8 @@
 // 256 threads, CTA tile BM x 64, BK = 16, each thread TM x 4 outputs with an
 // interleaved (bank-conflict-free) column pattern; global->register prefetch
 // of the next K-slab overlaps the FMA loop.
+#include <algorithm>
+#include <atomic>
 #include <ctime>
 #include <cstdlib>
 #include <cstring>
@@ -195,6 +197,9 @@ struct KRec { cudaEvent_t a, b; double flops, bytes; };
 std::vector<KRec>& krecs() { static std::vector<KRec> v; return v; }
 std::vector<cudaEvent_t>& kpool() { static std::vector<cudaEvent_t> v; return v; }
 double k_launch = 0, k_sec = 0, k_flops = 0, k_bytes = 0;
+cudaEvent_t k_ref = nullptr;                       // time origin of the launch intervals
+std::vector<std::pair<double, double>> k_iv;       // [start, end) of every launch (ms after k_ref)
+std::mutex& k_mu() { static std::mutex m; return m; }
 cudaEvent_t get_ev() {
   auto& p = kpool();
   if (!p.empty()) { cudaEvent_t e = p.back(); p.pop_back(); return e; }
@@ -205,28 +210,55 @@ cudaEvent_t get_ev() {
 void drain() {
   for (auto& r : krecs()) {
     cudaEventSynchronize(r.b);
-    float ms = 0.f;
+    float ms = 0.f, t0 = 0.f, t1 = 0.f;
     cudaEventElapsedTime(&ms, r.a, r.b);
+    cudaEventElapsedTime(&t0, k_ref, r.a);
+    cudaEventElapsedTime(&t1, k_ref, r.b);
+    k_iv.emplace_back(t0, t1);
     k_launch += 1; k_sec += ms * 1e-3; k_flops += r.flops; k_bytes += r.bytes;
     kpool().push_back(r.a);
     kpool().push_back(r.b);
   }
   krecs().clear();
 }
+// length of the union of the launch intervals: the time at least one launch was running
+// (equals the sum of the durations when launches are serial; smaller when streams overlap)
+double busy_seconds() {
+  std::vector<std::pair<double, double>> v = k_iv;
+  std::sort(v.begin(), v.end());
+  double tot = 0, a = 0, b = 0;
+  bool open = false;
+  for (auto& x : v) {
+    if (!open || x.first > b) { if (open) tot += b - a; a = x.first; b = x.second; open = true; }
+    else b = std::max(b, x.second);
+  }
+  if (open) tot += b - a;
+  return tot * 1e-3;
+}
 }  // namespace
 void KStats::record(cudaStream_t s, cudaEvent_t* e0, cudaEvent_t* e1) {
+  std::lock_guard<std::mutex> lk(k_mu());
+  if (!k_ref) { cudaEventCreate(&k_ref); cudaEventRecord(k_ref, s); }
   if (e0) { *e0 = get_ev(); cudaEventRecord(*e0, s); }
   if (e1) { *e1 = get_ev(); cudaEventRecord(*e1, s); }
 }
 void KStats::push(cudaEvent_t e0, cudaEvent_t e1, double flops, double bytes) {
+  std::lock_guard<std::mutex> lk(k_mu());
   krecs().push_back(KRec{e0, e1, flops, bytes});
   if (krecs().size() > 4096) drain();
 }
 void KStats::collect(double out[4]) {
+  std::lock_guard<std::mutex> lk(k_mu());
   drain();
-  out[0] = k_launch; out[1] = k_sec; out[2] = k_flops; out[3] = k_bytes;
+  out[0] = k_launch; out[1] = busy_seconds(); out[2] = k_flops; out[3] = k_bytes;
 }
-void KStats::reset() { drain(); k_launch = k_sec = k_flops = k_bytes = 0; }
+void KStats::reset() {
+  std::lock_guard<std::mutex> lk(k_mu());
+  drain();
+  k_launch = k_sec = k_flops = k_bytes = 0;
+  k_iv.clear();
+  if (k_ref) { cudaEventDestroy(k_ref); k_ref = nullptr; }
+}
 
 bool Prof::enabled() {
   static int e = -1;
@@ -348,7 +380,8 @@ void KTrace::reset() {
   g_nmiss_small = g_nmiss_large = 0;
 }
 
-long long g_pipe_launches = 0;   // gemm_pipe_kernel launches of this process (ncu -k regex:gemm_pipe -s <ordinal>)
+std::atomic<long long> g_pipe_launches{0};   // gemm_pipe_kernel launches of this process (ncu -k regex:gemm_pipe -s <ordinal>)
+std::mutex& g_mu() { static std::mutex m; return m; }
 namespace {
 struct GRec { cudaEvent_t a, b; const char* phase; const char* file; int line; bool ta, tb; double flops;
               long long ctas; int maxK, maxM; long long ord; };
@@ -386,10 +419,12 @@ bool GemmLog::on() {
 }
 void GemmLog::push(cudaEvent_t e0, cudaEvent_t e1, const char* file, int line, bool ta, bool tb, double flops,
                    long long ctas, int maxK, int maxM) {
-  grecs().push_back(GRec{e0, e1, KTrace::phase(), file, line, ta, tb, flops, ctas, maxK, maxM, g_pipe_launches - 1});
+  std::lock_guard<std::mutex> lk(g_mu());
+  grecs().push_back(GRec{e0, e1, KTrace::phase(), file, line, ta, tb, flops, ctas, maxK, maxM, g_pipe_launches.load() - 1});
   if (grecs().size() > 4096) gdrain();
 }
 std::string GemmLog::dump() {
+  std::lock_guard<std::mutex> lk(g_mu());
   gdrain();
   std::string r;
   for (auto& a : gagg())
@@ -399,7 +434,11 @@ std::string GemmLog::dump() {
          std::to_string(a.second.ord_max) + ";";
   return r;
 }
-void GemmLog::reset() { gdrain(); gagg().clear(); }
+void GemmLog::reset() {
+  std::lock_guard<std::mutex> lk(g_mu());
+  gdrain();
+  gagg().clear();
+}
 
 namespace {
 

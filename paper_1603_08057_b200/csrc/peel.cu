@@ -17,6 +17,9 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <exception>
+#include <thread>
+#include <functional>
 
 #include "dense.cuh"
 #include "peel.cuh"
@@ -236,7 +239,7 @@ struct GOp {
   DBuf<double> A, B, Z, tmp;
   int kcap = 0;
   double columns = 0;
-  GOp(const Fact& f, const Fact* fi) : F(f), Fi(fi), s(f.ctx->stream) {}
+  GOp(const Fact& f, const Fact* fi) : F(f), Fi(fi), s(op_stream(f)) {}
   void reserve(int k) {
     if (k <= kcap) return;
     kcap = k;
@@ -456,7 +459,7 @@ double ddot(cudaStream_t s, const double* a, const double* b, long long n) {
 
 double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag* diag) {
   const double t0 = now_s();
-  cudaStream_t s = F.ctx->stream;
+  cudaStream_t s = op_stream(F);
   const Tree& t = *F.tree;
   const int n = t.n, L = t.L;
   const unsigned long long seed = o.seed;
@@ -1146,7 +1149,7 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
 // per probe.  Deterministic (fixed-order reductions).
 void hutch(const Fact& F, const Fact* Fi, long long q, unsigned long long seed, double* mean, double* se) {
   RSF_REQUIRE(q >= 1, ST_EINVAL, "hutch: nprobe < 1");
-  cudaStream_t s = F.ctx->stream;
+  cudaStream_t s = op_stream(F);
   const Tree& t = *F.tree;
   const int n = t.n, kb = 512, GB = 256;
   DBuf<double> U((size_t)n * kb, s), A((size_t)n * kb, s), B, C, tmp((size_t)std::max<long long>(F.tmp_cols, 1) * kb, s);
@@ -1190,7 +1193,7 @@ void hutch(const Fact& F, const Fact* Fi, long long q, unsigned long long seed, 
 // P:680-690): u = F^-1 z through the factor, then the cross-covariance product on the fly
 void cond_mean(const Fact& F, const double* z, const double* xyn, long long m, double* out) {
   RSF_REQUIRE(F.which == W_SIGMA, ST_EINVAL, "conditional mean needs a Sigma factor");
-  cudaStream_t s = F.ctx->stream;
+  cudaStream_t s = op_stream(F);
   const Tree& t = *F.tree;
   const int n = t.n;
   DBuf<double> u(n, s), tmp((size_t)std::max<long long>(F.tmp_cols, 1), s);
@@ -1274,36 +1277,100 @@ EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KP
     R.quad = Qp;
   }
   R.t_solve = now_s() - t;
+  // The traces Tr(F^-1 F_i) are independent given F and u: one job per general component
+  // (compression of Sigma_i, q_i = u^T F_i u, peeling) plus one job for Tr(F^-1) when sigma^2 or
+  // the nugget is in theta (reading R-G).  With p > 1 the jobs run concurrently, each on its
+  // own stream from its own host thread: a job's latency-bound phases (rank-revealing QR,
+  // panels, small batches) overlap the other job's GEMMs.  Results do not depend on it.
+  for (int i = 0; i < p; ++i)
+    RSF_REQUIRE(!(profile && theta[i] == W_SIGMA2), ST_EINVAL,
+                "profile likelihood: sigma2 is profiled out, not a theta component");
   double trinv = NAN, utu = NAN;
+  PeelDiag pd_trinv;
+  double t_trinv = 0;
+  std::vector<double> qv(p, NAN), trv(p, NAN), tcomp(p, 0.0), tsol(p, 0.0), tpl(p, 0.0), ffl(p, 0.0);
+  std::vector<std::function<void()>> jobs;
+  bool need_trinv = false;
+  for (int i = 0; i < p; ++i) {
+    const int w = theta[i];
+    if (w == W_SIGMA2 || w == W_NUGGET) { need_trinv = true; continue; }
+    jobs.push_back([&, i, w]() {
+      double t1 = now_s();
+      auto Fi = factor(ctx, tree, kp, w, eps, o);
+      tcomp[i] = now_s() - t1;
+      ffl[i] = Fi->diag.flops_id + Fi->diag.flops_elim;
+      cudaStream_t s2 = ctx_stream(ctx);
+      t1 = now_s();
+      DBuf<double> x(n, s2), y(n, s2);
+      RSF_CUDA(cudaMemcpyAsync(x.p, u.p, n * sizeof(double), cudaMemcpyDeviceToDevice, s2));
+      apply_only_internal(*Fi, x.p, y.p, 1);
+      qv[i] = ddot(s2, u.p, y.p, n);
+      tsol[i] = now_s() - t1;
+      t1 = now_s();
+      trv[i] = peel(*F, Fi.get(), o, i, &R.pd[i]);
+      tpl[i] = now_s() - t1;
+    });
+  }
+  if (need_trinv)
+    jobs.push_back([&]() {
+      const double t1 = now_s();
+      trinv = peel(*F, nullptr, o, 100, &pd_trinv);
+      utu = ddot(ctx_stream(ctx), u.p, u.p, n);
+      t_trinv = now_s() - t1;
+    });
+  static const bool par_on = !(getenv("RSF_PAR_TRACES") && getenv("RSF_PAR_TRACES")[0] == '0');
+  // (the profiler and the launch trace synchronise one stream at a time: serial then)
+  if (!par_on || jobs.size() < 2 || Prof::enabled() || KTrace::on()) {
+    for (auto& j : jobs) j();
+  } else {
+    while (ctx.aux.size() < jobs.size()) {
+      cudaStream_t a;
+      RSF_CUDA(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
+      ctx.aux.push_back(a);
+    }
+    cudaEvent_t ready;
+    RSF_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    RSF_CUDA(cudaEventRecord(ready, s));   // F, u and the tree are complete on the main stream
+    int dev = 0;
+    RSF_CUDA(cudaGetDevice(&dev));
+    std::vector<std::exception_ptr> err(jobs.size());
+    std::vector<long long> nl(jobs.size(), 0);
+    std::vector<std::thread> th;
+    for (size_t j = 0; j < jobs.size(); ++j)
+      th.emplace_back([&, j]() {
+        const long long l0j = g_launches;
+        try {
+          RSF_CUDA(cudaSetDevice(dev));
+          StreamScope scope(ctx.aux[j]);
+          RSF_CUDA(cudaStreamWaitEvent(ctx.aux[j], ready, 0));
+          jobs[j]();
+          RSF_CUDA(cudaStreamSynchronize(ctx.aux[j]));
+        } catch (...) {
+          err[j] = std::current_exception();
+        }
+        nl[j] = g_launches - l0j;
+      });
+    for (auto& x : th) x.join();
+    cudaEventDestroy(ready);
+    for (long long v : nl) g_launches += v;
+    for (auto& e : err)
+      if (e) std::rethrow_exception(e);
+  }
+  R.t_peel += t_trinv;
   for (int i = 0; i < p; ++i) {
     const int w = theta[i];
     double q, tr;
-    RSF_REQUIRE(!(profile && w == W_SIGMA2), ST_EINVAL, "profile likelihood: sigma2 is profiled out, not a theta component");
-    if (w == W_SIGMA2 || w == W_NUGGET) {   // reading R-G
-      if (std::isnan(trinv)) {
-        t = now_s();
-        trinv = peel(*F, nullptr, o, 100, &R.pd[i]);
-        R.t_peel += now_s() - t;
-        utu = ddot(s, u.p, u.p, n);
-      } else {
-        R.pd[i] = R.pd[0];
-      }
+    if (w == W_SIGMA2 || w == W_NUGGET) {
+      R.pd[i] = pd_trinv;
       if (w == W_NUGGET) { q = utu; tr = trinv; }
       else { q = (R.quad - kp.nugget * utu) / kp.sigma2; tr = (n - kp.nugget * trinv) / kp.sigma2; }
     } else {
-      t = now_s();
-      auto Fi = factor(ctx, tree, kp, w, eps, o);
-      R.t_compress += now_s() - t;
-      R.flops_factor += Fi->diag.flops_id + Fi->diag.flops_elim;
-      t = now_s();
-      DBuf<double> x(n, s), y(n, s);
-      RSF_CUDA(cudaMemcpyAsync(x.p, u.p, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-      apply_only_internal(*Fi, x.p, y.p, 1);
-      q = ddot(s, u.p, y.p, n);
-      R.t_solve += now_s() - t;
-      t = now_s();
-      tr = peel(*F, Fi.get(), o, i, &R.pd[i]);
-      R.t_peel += now_s() - t;
+      q = qv[i];
+      tr = trv[i];
+      R.t_compress += tcomp[i];
+      R.t_solve += tsol[i];
+      R.t_peel += tpl[i];
+      R.flops_factor += ffl[i];
     }
     R.q[i] = q;
     R.trace[i] = tr;

@@ -287,20 +287,47 @@ __global__ void __launch_bounds__(SK_NT) sketch_cpqr_cl_kernel(const RDesc* __re
     if (rank == 0 && tid == 0) chosen[t] = p;
     cluster.sync();
     // apply (I - tau v v^T) to the active local columns, recompute their trailing norms
+    // (U columns per warp at a time: their warp reductions interleave instead of running back
+    // to back)
     const double tau = htau;
-    for (int j = warp; j < nc; j += SK_NW) {
-      if (zn[j] < 0.0) continue;
-      double* z = Zs + j * SP;
-      const double a0 = (lane < SP && lane >= t) ? z[lane] : 0.0;
-      const double a1 = (lane + 32 < SP && lane + 32 >= t) ? z[lane + 32] : 0.0;
-      const double v0 = (lane < SP) ? hv[lane] : 0.0;
-      const double v1 = (lane + 32 < SP) ? hv[lane + 32] : 0.0;
-      const double w = tau * wsum(a0 * v0 + a1 * v1);
-      const double b0 = a0 - w * v0, b1 = a1 - w * v1;
-      if (lane < SP && lane >= t) z[lane] = b0;
-      if (lane + 32 < SP && lane + 32 >= t) z[lane + 32] = b1;
-      const double s2 = wsum((lane > t && lane < SP ? b0 * b0 : 0.0) + (lane + 32 > t && lane + 32 < SP ? b1 * b1 : 0.0));
-      if (lane == 0) zn[j] = s2;
+    const double v0 = (lane < SP) ? hv[lane] : 0.0;
+    const double v1 = (lane + 32 < SP) ? hv[lane + 32] : 0.0;
+    constexpr int U = 4;
+    for (int jb = warp; jb < nc; jb += U * SK_NW) {
+      double a0[U], a1[U], w[U];
+      bool on[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int j = jb + u * SK_NW;
+        on[u] = j < nc && zn[j] >= 0.0;
+        const double* z = Zs + j * SP;
+        a0[u] = (on[u] && lane < SP && lane >= t) ? z[lane] : 0.0;
+        a1[u] = (on[u] && lane + 32 < SP && lane + 32 >= t) ? z[lane + 32] : 0.0;
+        w[u] = a0[u] * v0 + a1[u] * v1;
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1)
+#pragma unroll
+        for (int u = 0; u < U; ++u) w[u] += __shfl_xor_sync(0xffffffffu, w[u], o);
+      double s2[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int j = jb + u * SK_NW;
+        const double ww = tau * w[u];
+        const double b0 = a0[u] - ww * v0, b1 = a1[u] - ww * v1;
+        double* z = Zs + j * SP;
+        if (on[u] && lane < SP && lane >= t) z[lane] = b0;
+        if (on[u] && lane + 32 < SP && lane + 32 >= t) z[lane + 32] = b1;
+        s2[u] = (lane > t && lane < SP ? b0 * b0 : 0.0) + (lane + 32 > t && lane + 32 < SP ? b1 * b1 : 0.0);
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1)
+#pragma unroll
+        for (int u = 0; u < U; ++u) s2[u] += __shfl_xor_sync(0xffffffffu, s2[u], o);
+      if (lane == 0)
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (on[u]) zn[jb + u * SK_NW] = s2[u];
     }
     __syncthreads();
   }
@@ -334,21 +361,38 @@ __global__ void __launch_bounds__(SK_NT) sketch_cpqr_cl_kernel(const RDesc* __re
 }
 
 // apply the swap list to A (m rows), Y (SP rows) and piv
+// The block's column swaps (positions J + t and J + sw[t], t = 0..nbp-1, in order).  Rows are
+// independent: every thread applies the whole swap sequence to its rows of A, so the CTAs of
+// one problem split its rows (grid.x) with no barrier; CTA 0 also swaps Y's rows and piv.
 __global__ void apply_swaps_kernel(const RDesc* __restrict__ d0) {
-  const RDesc d = d0[blockIdx.x];
-  for (int t = 0; t < d.nbp; ++t) {
-    const int a = d.J + t, b = d.J + d.sw[t];
-    if (a != b) {
-      double* ca = d.A + (long long)a * d.lda;
-      double* cb = d.A + (long long)b * d.lda;
-      for (int r = threadIdx.x; r < d.m; r += NT) { double v = ca[r]; ca[r] = cb[r]; cb[r] = v; }
-      double* ya = d.Y + (long long)a * SP;
-      double* yb = d.Y + (long long)b * SP;
-      for (int r = threadIdx.x; r < SP; r += NT) { double v = ya[r]; ya[r] = yb[r]; yb[r] = v; }
-      if (threadIdx.x == 0) { int v = d.piv[a]; d.piv[a] = d.piv[b]; d.piv[b] = v; }
+  const RDesc d = d0[blockIdx.y];
+  __shared__ int sw[QR_NB];
+  if (threadIdx.x < d.nbp) sw[threadIdx.x] = d.J + d.sw[threadIdx.x];
+  __syncthreads();
+  for (long long r = blockIdx.x * (long long)NT + threadIdx.x; r < d.m; r += (long long)gridDim.x * NT)
+    for (int t = 0; t < d.nbp; ++t) {
+      const int a = d.J + t, b = sw[t];
+      if (a != b) {
+        double* ca = d.A + (long long)a * d.lda + r;
+        double* cb = d.A + (long long)b * d.lda + r;
+        const double v = *ca; *ca = *cb; *cb = v;
+      }
     }
-    __syncthreads();
-  }
+  if (blockIdx.x != 0) return;
+  for (int r = threadIdx.x; r < SP; r += NT)
+    for (int t = 0; t < d.nbp; ++t) {
+      const int a = d.J + t, b = sw[t];
+      if (a != b) {
+        double* ya = d.Y + (long long)a * SP + r;
+        double* yb = d.Y + (long long)b * SP + r;
+        const double v = *ya; *ya = *yb; *yb = v;
+      }
+    }
+  if (threadIdx.x == 0)
+    for (int t = 0; t < d.nbp; ++t) {
+      const int a = d.J + t, b = sw[t];
+      if (a != b) { const int v = d.piv[a]; d.piv[a] = d.piv[b]; d.piv[b] = v; }
+    }
 }
 
 // squared norms of the trailing columns A(j1:m, j) for j >= j1 (warp per column, many CTAs)
@@ -663,8 +707,12 @@ RRQRResult rrqr_batched(cudaStream_t s, const std::vector<RRQRProb>& probs, doub
       sketch_cpqr_kernel<<<na, NT, 0, s>>>(dd.p);
       count_launch();
     }
-    apply_swaps_kernel<<<na, NT, 0, s>>>(dd.p);
-    count_launch();
+    {
+      int mmax = 0;
+      for (auto& d : dv) mmax = std::max(mmax, d.m);
+      apply_swaps_kernel<<<dim3((unsigned)std::max(1, std::min(64, (mmax + NT - 1) / NT)), na), NT, 0, s>>>(dd.p);
+      count_launch();
+    }
     RSF_LAUNCH_CHECK();
     std::vector<PanelStep> ps;
     for (size_t a = 0; a < dv.size(); ++a) {

@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <mutex>
 #include <numeric>
 #include <unordered_set>
 
@@ -54,7 +55,9 @@ struct BRef {
 // per-level phase names for RSF_PROFILE=1 (diagnostics)
 static const char* lvname(const char* op, int lev) {
   static std::vector<std::string> names;
+  static std::mutex mu;
   if (!phase_names_on()) return op;
+  std::lock_guard<std::mutex> lk(mu);
   const std::string key = std::string(op) + ".L" + std::to_string(lev);
   for (size_t i = 0; i < names.size(); ++i) if (names[i] == key) return names[i].c_str();
   if (names.empty()) names.reserve(4096);   // stable c_str() pointers
@@ -67,7 +70,7 @@ std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams
                              double eps, const Opts& opts, bool solve_only) {
   RSF_REQUIRE(eps > 0.0, ST_EINVAL, "eps must be > 0");
   const double t0 = now_s();
-  cudaStream_t s = ctx.stream;
+  cudaStream_t s = ctx_stream(ctx);
   auto F = std::make_unique<Fact>();
   F->ctx = &ctx;
   F->which = which;

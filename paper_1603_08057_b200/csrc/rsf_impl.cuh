@@ -24,6 +24,7 @@ struct Opts {
 struct Ctx {
   int device = 0;
   cudaStream_t stream = 0;
+  std::vector<cudaStream_t> aux;   // streams of the concurrent trace jobs of gp_mle_eval (created lazily)
   bool own_stream = false;
   void* nccl = nullptr;
   std::string last_error;
@@ -124,7 +125,8 @@ std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams
 // Stream of the operators below: the factor's context stream unless a StreamScope on this
 // thread redirects them (the peeling runs its G applies on a second stream).
 cudaStream_t& stream_override();
-inline cudaStream_t op_stream(const Fact& F) { return stream_override() ? stream_override() : F.ctx->stream; }
+inline cudaStream_t ctx_stream(const Ctx& c) { return stream_override() ? stream_override() : c.stream; }
+inline cudaStream_t op_stream(const Fact& F) { return ctx_stream(*F.ctx); }
 struct StreamScope {
   cudaStream_t prev;
   explicit StreamScope(cudaStream_t s) : prev(stream_override()) { stream_override() = s; }
