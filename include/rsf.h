@@ -155,7 +155,10 @@ rsf_status hutch_trace(rsf_fact F, rsf_fact Fi, int64_t nprobe, uint64_t seed, d
 
 /* Alg. 1: l-hat and g-hat at theta = kernel values.  eps is the ID tolerance of every
  * factorization (eps_fact), opts->eps_peel the peeling tolerance.  ell: host scalar; grad: host
- * array of p doubles.  xy, z device or host.  diag nullable. */
+ * array of p doubles.  xy, z device or host.  diag nullable.  The independent trace jobs (one per
+ * theta component) run concurrently on streams the context creates on first use and
+ * releases in rsf_ctx_destroy; the call returns after all of them (and the context stream) are
+ * complete.  Results equal the serial order (RSF_PAR_TRACES=0).  diag times are summed over jobs. */
 rsf_status gp_mle_eval(rsf_ctx ctx, const double* xy, const double* z, int64_t n, const rsf_kernel* kernel,
                        double eps, int32_t leaf, const rsf_opts* opts, double* ell, double* grad,
                        rsf_eval_diag* diag);
@@ -192,7 +195,9 @@ const char* rsf_trace_dump(void);
  * (diagnostics only; resets with rsf_profile_reset) */
 const char* rsf_debug_gemm_log(void);
 /* batched-GEMM statistics for the roofline: CUDA events around every launch on its stream.
- * rsf_stats_get fills {launches, seconds, algorithmic flops, compulsory bytes}. */
+ * rsf_stats_get fills {launches, busy seconds (length of the union of the launch intervals, so that
+ * launches overlapping on concurrent streams are not double-counted), algorithmic flops,
+ * compulsory bytes}. */
 void rsf_stats_enable(int on);
 /* diagnostics: TFLOP/s of the batched FP64 GEMM on batch x (M x N x K), transposes ta/tb */
 double rsf_debug_gemm_bench(int M, int N, int K, int batch, int ta, int tb, int reps);

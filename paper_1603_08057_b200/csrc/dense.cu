@@ -1,5 +1,6 @@
 // Batched dense FP64 factorizations (see dense.cuh).
 #include <algorithm>
+#include <mutex>
 
 #include <cooperative_groups.h>
 
@@ -595,16 +596,15 @@ __global__ void __launch_bounds__(PC_NT) qr_panel_cl_kernel(const PanelDesc* __r
 
 template <int CL>
 void launch_panel_cl(cudaStream_t s, const PanelDesc* d, int np, int chunk) {
-  static bool attr = false;
+  static std::once_flag attr_once;
   const size_t smem = ((size_t)QR_NB * chunk + (size_t)CL * PC_NPAIR + 2 * QR_NB * QR_NB) * sizeof(double);
-  if (!attr) {
+  std::call_once(attr_once, [&] {
     cudaFuncAttributes fa;
     RSF_CUDA(cudaFuncGetAttributes(&fa, qr_panel_cl_kernel<CL>));
     RSF_CUDA(cudaFuncSetAttribute(qr_panel_cl_kernel<CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(SMEM_MAX - fa.sharedSizeBytes)));
     if (CL > 8) RSF_CUDA(cudaFuncSetAttribute(qr_panel_cl_kernel<CL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    attr = true;
-  }
+  });
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(np * CL));
   cfg.blockDim = dim3(PC_NT);
@@ -624,12 +624,11 @@ void launch_panel_cl(cudaStream_t s, const PanelDesc* d, int np, int chunk) {
 // panels in global memory (too tall for shared memory) are latency bound: give them
 // 1024 threads (one warp per remaining panel column, 4x the loads in flight)
 void launch_panels(cudaStream_t s, const std::vector<PanelDesc>& pd, const PanelDesc* d, size_t smem_need) {
-  static bool attr = false;
-  if (!attr) {
+  static std::once_flag attr_once;
+  std::call_once(attr_once, [&] {
     RSF_CUDA(cudaFuncSetAttribute(qr_panel_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_MAX));
     RSF_CUDA(cudaFuncSetAttribute(qr_panel_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_MAX));
-    attr = true;
-  }
+  });
   bool tall = false;
   int maxrows = 0;
   for (auto& p : pd) { tall |= (p.smem == 0); maxrows = std::max(maxrows, p.rows); }
@@ -668,10 +667,9 @@ void copy_batched(cudaStream_t s, const std::vector<CopyProb>& probs) {
 // ------------------------------------------------------------------ geqrf
 void geqrf_batched(cudaStream_t s, const std::vector<QRProb>& probs, bool keep_q) {
   if (probs.empty()) return;
-  static bool attr = false;
-  if (!attr) {
-    attr = true;
-  }
+  static std::once_flag attr_once;
+  std::call_once(attr_once, [&] {
+  });
   const int P = (int)probs.size();
   // workspace: V (m x QR_NB), T (QR_NB^2), W and W2 (QR_NB x c)
   std::vector<long long> voff(P), woff(P), toff(P);
@@ -741,10 +739,9 @@ void geqrf_batched(cudaStream_t s, const std::vector<QRProb>& probs, bool keep_q
 
 void panel_step_batched(cudaStream_t s, const std::vector<PanelStep>& v) {
   if (v.empty()) return;
-  static bool attr = false;
-  if (!attr) {
-    attr = true;
-  }
+  static std::once_flag attr_once;
+  std::call_once(attr_once, [&] {
+  });
   const size_t base_smem = (40 + QR_NB + 2 * QR_NB * QR_NB) * sizeof(double);
   size_t smem_need = base_smem;
   std::vector<PanelDesc> pd;
@@ -836,12 +833,11 @@ void ormqr_batched(cudaStream_t s, const std::vector<QApplyProb>& probs, bool tr
 void cpqr_id_batched(cudaStream_t s, const std::vector<CPQRProb>& probs, double eps, int* d_k,
                      bool want_T) {
   if (probs.empty()) return;
-  static bool attr = false;
-  if (!attr) {
+  static std::once_flag attr_once;
+  std::call_once(attr_once, [&] {
     RSF_CUDA(cudaFuncSetAttribute(cpqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(SMEM_BUDGET + 24 * 1024)));
-    attr = true;
-  }
+  });
   std::vector<CPQRDesc> dv;
   size_t smem_need = 0;
   for (size_t i = 0; i < probs.size(); ++i) {
@@ -876,12 +872,11 @@ void cpqr_id_batched(cudaStream_t s, const std::vector<CPQRProb>& probs, double 
 // ------------------------------------------------------------------ potrf (+ inverse)
 void potrf_batched(cudaStream_t s, const std::vector<PotrfProb>& probs, double* d_logsum, int* d_info) {
   if (probs.empty()) return;
-  static bool attr = false;
-  if (!attr) {
+  static std::once_flag attr_once;
+  std::call_once(attr_once, [&] {
     RSF_CUDA(cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(2 * CH_NB * CH_NB * sizeof(double))));
-    attr = true;
-  }
+  });
   const int P = (int)probs.size();
   RSF_CUDA(cudaMemsetAsync(d_logsum, 0, P * sizeof(double), s));
   RSF_CUDA(cudaMemsetAsync(d_info, 0, P * sizeof(int), s));

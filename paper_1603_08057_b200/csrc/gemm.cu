@@ -1028,15 +1028,14 @@ template <int BN>
 void launch_pipe(bool ta, bool tb, dim3 grid, cudaStream_t s, const GemmDesc* d, const int* pre, int np,
                  double* X0, double* X1, int ldx, int Mg, double* ws = nullptr, const long long* mnpre = nullptr,
                  int kchunk = 0) {
-  static bool attr = false;
+  static std::once_flag attr_once;
   constexpr size_t SM = p_smem<BN>();
-  if (!attr) {
+  std::call_once(attr_once, [&] {
     cudaFuncSetAttribute(gemm_pipe_kernel<false, false, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
     cudaFuncSetAttribute(gemm_pipe_kernel<true, false, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
     cudaFuncSetAttribute(gemm_pipe_kernel<false, true, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
     cudaFuncSetAttribute(gemm_pipe_kernel<true, true, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
-    attr = true;
-  }
+  });
   ++g_pipe_launches;
   static const int epi = getenv("RSF_GEMM_EPI") ? atoi(getenv("RSF_GEMM_EPI")) : 1;
   const int mt = (int)grid.y;

@@ -20,6 +20,7 @@
 #include <exception>
 #include <thread>
 #include <functional>
+#include <future>
 
 #include "dense.cuh"
 #include "peel.cuh"
@@ -1241,54 +1242,29 @@ EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KP
   double t = now_s();
   auto tree = build_tree(ctx, dxy, n, leaf, o.max_depth);
   R.t_tree = now_s() - t;
-  t = now_s();
-  auto F = factor(ctx, tree, kp, W_SIGMA, eps, o, /*solve_only=*/true);
-  R.t_factor = now_s() - t;
-  R.fdiag = F->diag;
-  R.L = tree->L;
-  R.n0 = F->n0;
-  R.flops_factor = F->diag.flops_id + F->diag.flops_elim + F->diag.flops_top;
-  R.logdet = F->logdet;
-  // u = F^-1 z (k = 1), q0 = z^T u
-  t = now_s();
-  DBuf<double> zt(n, s), u(n, s), tmp((size_t)std::max<long long>(F->tmp_cols, 1), s);
-  to_internal(s, *tree, dz, n, 1, zt.p);
-  RSF_CUDA(cudaMemcpyAsync(u.p, zt.p, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  solve_internal(*F, u.p, 1, tmp.p);
-  R.quad = ddot(s, zt.p, u.p, n);
-  R.ell = -0.5 * R.quad - 0.5 * R.logdet - 0.5 * n * std::log(2.0 * M_PI);
-  double Qp = 0.0;
-  if (profile) {
-    // profile likelihood (Eq. prof): z ~ N(mu 1, s2 Sigma) with mu, s2 profiled out,
-    //   Q = z^T (Sigma + 1 1^T)^-1 z = z^T u - (1^T u)^2 / (1 + 1^T w),  w = F^-1 1 (Sherman-Morrison)
-    //   l~ = -1/2 log|Sigma| - n/2 log Q + n/2 (log n - 1 - log 2 pi)          (reading R-Prof)
-    //   v = (Sigma + 1 1^T)^-1 z = u - w (1^T u) / (1 + 1^T w)   (held in u from here on)
-    DBuf<double> one(n, s), wv(n, s);
-    fill_kernel<<<gxx(n), NT, 0, s>>>(one.p, 1.0, n);
-    count_launch();
-    RSF_CUDA(cudaMemcpyAsync(wv.p, one.p, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    solve_internal(*F, wv.p, 1, tmp.p);
-    const double a = ddot(s, one.p, wv.p, n), b = ddot(s, one.p, u.p, n);
-    Qp = R.quad - b * b / (1.0 + a);
-    R.ell = -0.5 * R.logdet - 0.5 * n * std::log(Qp) + 0.5 * n * (std::log((double)n) - 1.0 - std::log(2.0 * M_PI));
-    axpby_kernel<<<gxx(n), NT, 0, s>>>(u.p, wv.p, -b / (1.0 + a), 1.0, n);   // u <- u - w b/(1+a)
-    count_launch();
-    RSF_LAUNCH_CHECK();
-    R.quad = Qp;
-  }
-  R.t_solve = now_s() - t;
-  // The traces Tr(F^-1 F_i) are independent given F and u: one job per general component
-  // (compression of Sigma_i, q_i = u^T F_i u, peeling) plus one job for Tr(F^-1) when sigma^2 or
-  // the nugget is in theta (reading R-G).  With p > 1 the jobs run concurrently, each on its
-  // own stream from its own host thread: a job's latency-bound phases (rank-revealing QR,
-  // panels, small batches) overlap the other job's GEMMs.  Results do not depend on it.
   for (int i = 0; i < p; ++i)
     RSF_REQUIRE(!(profile && theta[i] == W_SIGMA2), ST_EINVAL,
                 "profile likelihood: sigma2 is profiled out, not a theta component");
-  double trinv = NAN, utu = NAN;
+
+  // Jobs (Alg. 1): the traces Tr(F^-1 F_i) are independent given F and u: one job
+  // per general component (compression of Sigma_i, which needs only the tree; then
+  // q_i = u^T F_i u and the peeling, which need F and u) plus one job for Tr(F^-1) when sigma^2
+  // or the nugget is in theta (reading R-G).  With more than one job they run concurrently,
+  // each on its own stream from its own host thread, the compressions alongside the Sigma
+  // factor: the latency-bound phases of one job (rank-revealing QR, panels, small batches)
+  // overlap the GEMMs of another.  Results do not depend on it.
+  std::shared_ptr<Fact> F;
+  DBuf<double> u;
+  double trinv = NAN, utu = NAN, t_trinv = 0;
   PeelDiag pd_trinv;
-  double t_trinv = 0;
   std::vector<double> qv(p, NAN), trv(p, NAN), tcomp(p, 0.0), tsol(p, 0.0), tpl(p, 0.0), ffl(p, 0.0);
+  std::promise<void> f_promise;
+  std::shared_future<void> f_ready = f_promise.get_future().share();
+  cudaEvent_t f_event = nullptr;   // recorded on the main stream once F and u are complete
+  std::function<void()> wait_f = [&]() {
+    f_ready.get();
+    if (f_event && ctx_stream(ctx) != s) RSF_CUDA(cudaStreamWaitEvent(ctx_stream(ctx), f_event, 0));
+  };
   std::vector<std::function<void()>> jobs;
   bool need_trinv = false;
   for (int i = 0; i < p; ++i) {
@@ -1299,6 +1275,7 @@ EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KP
       auto Fi = factor(ctx, tree, kp, w, eps, o);
       tcomp[i] = now_s() - t1;
       ffl[i] = Fi->diag.flops_id + Fi->diag.flops_elim;
+      wait_f();
       cudaStream_t s2 = ctx_stream(ctx);
       t1 = now_s();
       DBuf<double> x(n, s2), y(n, s2);
@@ -1313,24 +1290,69 @@ EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KP
   }
   if (need_trinv)
     jobs.push_back([&]() {
+      wait_f();
       const double t1 = now_s();
       trinv = peel(*F, nullptr, o, 100, &pd_trinv);
       utu = ddot(ctx_stream(ctx), u.p, u.p, n);
       t_trinv = now_s() - t1;
     });
+
+  // F ~ Sigma (solve-only), u = F^-1 z (k = 1), q0 = z^T u; profile terms (Eq. prof)
+  double Qp = 0.0;
+  auto main_part = [&]() {
+    double t1 = now_s();
+    F = factor(ctx, tree, kp, W_SIGMA, eps, o, /*solve_only=*/true);
+    R.t_factor = now_s() - t1;
+    R.fdiag = F->diag;
+    R.L = tree->L;
+    R.n0 = F->n0;
+    R.flops_factor += F->diag.flops_id + F->diag.flops_elim + F->diag.flops_top;
+    R.logdet = F->logdet;
+    t1 = now_s();
+    DBuf<double> zt(n, s), tmp((size_t)std::max<long long>(F->tmp_cols, 1), s);
+    u.alloc(n, s);
+    to_internal(s, *tree, dz, n, 1, zt.p);
+    RSF_CUDA(cudaMemcpyAsync(u.p, zt.p, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    solve_internal(*F, u.p, 1, tmp.p);
+    R.quad = ddot(s, zt.p, u.p, n);
+    R.ell = -0.5 * R.quad - 0.5 * R.logdet - 0.5 * n * std::log(2.0 * M_PI);
+    if (profile) {
+      // profile likelihood (Eq. prof): z ~ N(mu 1, s2 Sigma) with mu, s2 profiled out,
+      //   Q = z^T (Sigma + 1 1^T)^-1 z = z^T u - (1^T u)^2 / (1 + 1^T w),  w = F^-1 1 (Sherman-Morrison)
+      //   l~ = -1/2 log|Sigma| - n/2 log Q + n/2 (log n - 1 - log 2 pi)          (reading R-Prof)
+      //   v = (Sigma + 1 1^T)^-1 z = u - w (1^T u) / (1 + 1^T w)   (held in u from here on)
+      DBuf<double> one(n, s), wv(n, s);
+      fill_kernel<<<gxx(n), NT, 0, s>>>(one.p, 1.0, n);
+      count_launch();
+      RSF_CUDA(cudaMemcpyAsync(wv.p, one.p, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      solve_internal(*F, wv.p, 1, tmp.p);
+      const double a = ddot(s, one.p, wv.p, n), b = ddot(s, one.p, u.p, n);
+      Qp = R.quad - b * b / (1.0 + a);
+      R.ell = -0.5 * R.logdet - 0.5 * n * std::log(Qp) + 0.5 * n * (std::log((double)n) - 1.0 - std::log(2.0 * M_PI));
+      axpby_kernel<<<gxx(n), NT, 0, s>>>(u.p, wv.p, -b / (1.0 + a), 1.0, n);   // u <- u - w b/(1+a)
+      count_launch();
+      RSF_LAUNCH_CHECK();
+      R.quad = Qp;
+    }
+    R.t_solve = now_s() - t1;
+  };
+
   static const bool par_on = !(getenv("RSF_PAR_TRACES") && getenv("RSF_PAR_TRACES")[0] == '0');
   // (the profiler and the launch trace synchronise one stream at a time: serial then)
   if (!par_on || jobs.size() < 2 || Prof::enabled() || KTrace::on()) {
+    main_part();
+    f_promise.set_value();
     for (auto& j : jobs) j();
   } else {
     while (ctx.aux.size() < jobs.size()) {
-      cudaStream_t a;
-      RSF_CUDA(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
-      ctx.aux.push_back(a);
+      cudaStream_t a2;
+      RSF_CUDA(cudaStreamCreateWithFlags(&a2, cudaStreamNonBlocking));
+      ctx.aux.push_back(a2);
     }
-    cudaEvent_t ready;
-    RSF_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-    RSF_CUDA(cudaEventRecord(ready, s));   // F, u and the tree are complete on the main stream
+    cudaEvent_t t_event;
+    RSF_CUDA(cudaEventCreateWithFlags(&t_event, cudaEventDisableTiming));
+    RSF_CUDA(cudaEventCreateWithFlags(&f_event, cudaEventDisableTiming));
+    RSF_CUDA(cudaEventRecord(t_event, s));   // the tree is complete on the main stream
     int dev = 0;
     RSF_CUDA(cudaGetDevice(&dev));
     std::vector<std::exception_ptr> err(jobs.size());
@@ -1342,7 +1364,7 @@ EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KP
         try {
           RSF_CUDA(cudaSetDevice(dev));
           StreamScope scope(ctx.aux[j]);
-          RSF_CUDA(cudaStreamWaitEvent(ctx.aux[j], ready, 0));
+          RSF_CUDA(cudaStreamWaitEvent(ctx.aux[j], t_event, 0));
           jobs[j]();
           RSF_CUDA(cudaStreamSynchronize(ctx.aux[j]));
         } catch (...) {
@@ -1350,9 +1372,20 @@ EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KP
         }
         nl[j] = g_launches - l0j;
       });
+    std::exception_ptr main_err;
+    try {
+      main_part();
+      RSF_CUDA(cudaEventRecord(f_event, s));
+      f_promise.set_value();
+    } catch (...) {
+      main_err = std::current_exception();
+      f_promise.set_exception(main_err);   // releases the jobs waiting for F
+    }
     for (auto& x : th) x.join();
-    cudaEventDestroy(ready);
+    cudaEventDestroy(t_event);
+    cudaEventDestroy(f_event);
     for (long long v : nl) g_launches += v;
+    if (main_err) std::rethrow_exception(main_err);
     for (auto& e : err)
       if (e) std::rethrow_exception(e);
   }

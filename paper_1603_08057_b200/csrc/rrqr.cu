@@ -1,5 +1,6 @@
 // Blocked randomized rank-revealing QR truncated at the eps-rank (see rrqr.cuh).
 #include <algorithm>
+#include <mutex>
 #include <climits>
 #include <cmath>
 
@@ -515,12 +516,11 @@ __global__ void upper_inv64_kernel(const DInvDesc* __restrict__ d0) {
 
 template <int CL>
 void launch_cl(cudaStream_t s, const RDesc* dd, int na, int chunk) {
-  static bool attr = false;
-  if (!attr) {
+  static std::once_flag attr_once;
+  std::call_once(attr_once, [&] {
     RSF_CUDA(cudaFuncSetAttribute(sketch_cpqr_cl_kernel<CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     if (CL > 8) RSF_CUDA(cudaFuncSetAttribute(sketch_cpqr_cl_kernel<CL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    attr = true;
-  }
+  });
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(na * CL));
   cfg.blockDim = dim3(SK_NT);

@@ -1,5 +1,6 @@
 // Fused small-box level sweeps (see sweep.cuh).
 #include "sweep.cuh"
+#include <mutex>
 
 namespace rsf {
 
@@ -118,12 +119,11 @@ void sweep_level(cudaStream_t s, const BoxOp* d_ops, int nops, int max_i, SweepK
                  int k) {
   if (nops == 0 || k <= 0) return;
   RSF_REQUIRE(max_i <= SWEEP_MAX_I, ST_EINVAL, "sweep_level: box too large for the fused kernel");
-  static bool attr = false;
-  if (!attr) {
+  static std::once_flag attr_once;
+  std::call_once(attr_once, [&] {
     RSF_CUDA(cudaFuncSetAttribute(sweep_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     RSF_CUDA(cudaFuncSetAttribute(sweep_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
+  });
   // shared memory: (kb + 2 r) * KC doubles <= 2 |I| * KC
   const int KC = (max_i <= 128) ? 32 : 16;
   const size_t smem = (size_t)2 * max_i * KC * sizeof(double);
