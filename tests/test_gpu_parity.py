@@ -379,3 +379,40 @@ def test_abi_strided_and_host_blocks(ctx, cfg2_4096):
     assert np.array_equal(out[:, :n], ref)
     assert R.lib.rsf_solve(F.h, H.ctypes.data, out.ctypes.data, 0, ld) == 0
     assert R.lib.rsf_solve(F.h, H.ctypes.data, out.ctypes.data, 3, n - 1) == _lib.RSF_EINVAL
+
+
+_PAR_PROBE = r"""
+import sys, json, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_1603_08057_b200 as R
+from workloads import config, points_for, w_for
+c = config(3)
+n = 4096
+xy = torch.from_numpy(points_for(c, n)).cuda()
+z = torch.from_numpy(w_for(c, n)).cuda()
+ctx = R.Context(0)
+K = R.Kernel(c.family, c.rho, c.sigma2, c.nugget, c.alpha, ("rho", "alpha", "nugget"))
+r = R.gp_mle_eval(ctx, xy, z, K, 1e-9, c.leaf, R.Opts(eps_peel=c.eps_peel, seed=c.seed))
+json.dump({"ell": r.ell, "grad": list(r.grad), "trace": list(r.diag.trace)[:3]}, open(sys.argv[2], "w"))
+"""
+
+
+def test_concurrent_trace_jobs_equal_serial_order(tmp_path):
+    """gp_mle_eval with theta = (rho, alpha, nugget): three trace jobs (two compressions + peelings
+    and the Tr(F^-1) peeling) run concurrently on their own streams; the result must be
+    bit-identical to the serial order (RSF_PAR_TRACES=0)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "par.py"
+    script.write_text(_PAR_PROBE)
+    out = {}
+    for flag in ("1", "0"):
+        f = tmp_path / f"par{flag}.json"
+        env = dict(os.environ, RSF_PAR_TRACES=flag)
+        subprocess.run([sys.executable, str(script), root, str(f)], env=env, check=True, timeout=600)
+        out[flag] = json.load(open(f))
+    assert out["1"] == out["0"]
+    assert all(np.isfinite(out["1"]["grad"]))
