@@ -772,17 +772,21 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 constexpr int P_BM = 128, P_BK = 16, P_ST = 4, P_NT = 256;
 constexpr int P_LDA = P_BM + 4;   // row stride = 8 banks mod 32: conflict-free fragment loads
 template <int BN> constexpr int p_ldb() { return BN + 4; }
-template <int BN> constexpr size_t p_smem() { return (size_t)P_ST * P_BK * (P_LDA + p_ldb<BN>()) * sizeof(double); }
+template <int BN, int BM = P_BM, int ST = P_ST>
+constexpr size_t p_smem() { return (size_t)ST * P_BK * (BM + 4 + p_ldb<BN>()) * sizeof(double); }
 
-// CTA tile 128 x BN (BN = 32, 64, 128), 8 warps as 4 (M) x 2 (N), warp tile 32 x BN/2
+// CTA tile BM x BN (BM = 128: BN = 32, 64, 128, 8 warps as 4 (M) x 2 (N), 4 stages; BM = 64:
+// BN = 64, 4 warps as 2 x 2, 3 stages, 4 CTAs per SM -- for short K, where the prologue and the
+// epilogue of a CTA dominate and more resident CTAs overlap them), warp tile 32 x BN/2
 // (4 x BN/16 DMMA.8x8x4 tiles).
-template <bool TA, bool TB, int BN>
-__global__ void __launch_bounds__(P_NT, (BN >= 128 ? 1 : 2)) gemm_pipe_kernel(const GemmDesc* __restrict__ descs,
+template <bool TA, bool TB, int BN, int BM, int ST>
+__global__ void __launch_bounds__(2 * BM, (BN >= 128 ? 1 : (BM == 64 ? 4 : 2))) gemm_pipe_kernel(const GemmDesc* __restrict__ descs,
                                                             const int* __restrict__ prefix, int nprob,
                                                             double* X0, double* X1, int ldx, int Mglob,
                                                             double* ws, const long long* __restrict__ mnpre,
                                                             int kchunk, int mtiles, int smem_epi) {
   constexpr int LDB = p_ldb<BN>(), NI = BN / 16, WN = BN / 2;
+  constexpr int P_BM = BM, P_NT = 2 * BM, P_LDA = BM + 4, P_ST = ST, WMN = BM / 32;   // warps: WMN (M) x 2 (N)
   static_assert(BN * P_LDA <= P_ST * P_BK * (P_LDA + p_ldb<BN>()), "C tile must fit in the pipeline buffers");
   extern __shared__ __align__(16) double psm[];
   double* As = psm;                              // [ST][BK][LDA]
@@ -809,7 +813,7 @@ __global__ void __launch_bounds__(P_NT, (BN >= 128 ? 1 : 2)) gemm_pipe_kernel(co
   const int* mapK = dd.mapK;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, tq = lane & 3;
-  const int wm = warp & 3, wn = warp >> 2;
+  const int wm = warp % WMN, wn = warp / WMN;
 
   // 16-byte copies where the contiguous dimension of global and shared memory agree
   // (A not transposed, B transposed) and the operand is 16-byte aligned with an even ld
@@ -1024,26 +1028,27 @@ __global__ void __launch_bounds__(P_NT, (BN >= 128 ? 1 : 2)) gemm_pipe_kernel(co
   }
 }
 
-template <int BN>
+template <int BN, int BM = P_BM, int ST = P_ST>
 void launch_pipe(bool ta, bool tb, dim3 grid, cudaStream_t s, const GemmDesc* d, const int* pre, int np,
                  double* X0, double* X1, int ldx, int Mg, double* ws = nullptr, const long long* mnpre = nullptr,
                  int kchunk = 0) {
   static std::once_flag attr_once;
-  constexpr size_t SM = p_smem<BN>();
+  constexpr size_t SM = p_smem<BN, BM, ST>();
   std::call_once(attr_once, [&] {
-    cudaFuncSetAttribute(gemm_pipe_kernel<false, false, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
-    cudaFuncSetAttribute(gemm_pipe_kernel<true, false, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
-    cudaFuncSetAttribute(gemm_pipe_kernel<false, true, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
-    cudaFuncSetAttribute(gemm_pipe_kernel<true, true, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
+    cudaFuncSetAttribute(gemm_pipe_kernel<false, false, BN, BM, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
+    cudaFuncSetAttribute(gemm_pipe_kernel<true, false, BN, BM, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
+    cudaFuncSetAttribute(gemm_pipe_kernel<false, true, BN, BM, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
+    cudaFuncSetAttribute(gemm_pipe_kernel<true, true, BN, BM, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
   });
   ++g_pipe_launches;
   static const int epi = getenv("RSF_GEMM_EPI") ? atoi(getenv("RSF_GEMM_EPI")) : 1;
   const int mt = (int)grid.y;
   const dim3 g1((unsigned)((long long)grid.x * grid.y), 1, grid.z);   // 1-D over (N-tile, M-tile)
-  if (!ta && !tb) gemm_pipe_kernel<false, false, BN><<<g1, P_NT, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk, mt, epi);
-  else if (ta && !tb) gemm_pipe_kernel<true, false, BN><<<g1, P_NT, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk, mt, epi);
-  else if (!ta && tb) gemm_pipe_kernel<false, true, BN><<<g1, P_NT, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk, mt, epi);
-  else gemm_pipe_kernel<true, true, BN><<<g1, P_NT, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk, mt, epi);
+  constexpr int NTH = 2 * BM;
+  if (!ta && !tb) gemm_pipe_kernel<false, false, BN, BM, ST><<<g1, NTH, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk, mt, epi);
+  else if (ta && !tb) gemm_pipe_kernel<true, false, BN, BM, ST><<<g1, NTH, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk, mt, epi);
+  else if (!ta && tb) gemm_pipe_kernel<false, true, BN, BM, ST><<<g1, NTH, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk, mt, epi);
+  else gemm_pipe_kernel<true, true, BN, BM, ST><<<g1, NTH, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk, mt, epi);
 }
 
 // split-K reduction: C = alpha * sum_z W_z + beta * C (fixed summation order: deterministic)
@@ -1158,6 +1163,7 @@ void GemmBatch::run(cudaStream_t s, double* X0, double* X1, int ldx, int Mglob, 
       // resident slots, each CTA streaming K/S (+ a fixed prologue/epilogue) at 1/296 of the
       // DMMA peak, plus the workspace traffic of the deterministic reduction and its launch.
       static const int splitk_mode = getenv("RSF_SPLITK") ? atoi(getenv("RSF_SPLITK")) : 1;
+      static const int small_k = getenv("RSF_GEMM_SMALLK") ? atoi(getenv("RSF_GEMM_SMALLK")) : 256;
       const int force = gemm_force_splitk();
       long long ctas = 0;
       double mntot = 0;
@@ -1201,6 +1207,10 @@ void GemmBatch::run(cudaStream_t s, double* X0, double* X1, int ldx, int Mglob, 
           splitk_reduce_kernel<<<dim3(gx, ny), P_NT, 0, s>>>(dp_, ws.p, dmn, S, (int)o, X0, X1, ldx, Mglob);
           count_launch();
         }
+      } else if (maxK_ <= small_k) {
+        // short K: 64 x 64 tiles, 4 resident CTAs per SM (their prologues/epilogues overlap)
+        dim3 grid(totalN_, ceil_div(M, 64));
+        launch_pipe<64, 64, 3>(ta_, tb_, grid, s, dp_, pp_, (int)P, X0, X1, ldx, Mglob);
       } else {
         dim3 grid(totalN_, ceil_div(M, P_BM));
         launch_pipe<64>(ta_, tb_, grid, s, dp_, pp_, (int)P, X0, X1, ldx, Mglob);
