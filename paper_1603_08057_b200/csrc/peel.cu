@@ -316,13 +316,42 @@ struct PeelLevel {
 
 // out (rows x q, ld rows) = transpose of rows piv[0:q] of src (c x rows, ld lds)
 struct GatherTDesc { const double* src; long long lds; const int* piv; double* out; int rows, q; };
-__global__ void gather_t_kernel(const GatherTDesc* __restrict__ descs) {
-  const GatherTDesc d = descs[blockIdx.y];
-  const long long tot = (long long)d.rows * d.q;
-  for (long long e = blockIdx.x * (long long)NT + threadIdx.x; e < tot; e += (long long)gridDim.x * NT) {
-    const int t = (int)(e % d.rows), j = (int)(e / d.rows);
-    d.out[e] = d.src[(long long)t * d.lds + __ldg(d.piv + j)];
+// 32 x 32 tiles through shared memory: the gathered rows piv[j0:j0+32] of one source column
+// are read together (one 8*c-byte column, L1/L2 resident), the output columns are written
+// coalesced (a direct element-per-thread transpose reads with stride lds).
+constexpr int GT_TILE = 32, GT_ROWS = 8;
+__global__ void __launch_bounds__(GT_TILE * GT_ROWS) gather_t_kernel(const GatherTDesc* __restrict__ descs) {
+  __shared__ double tile[GT_TILE][GT_TILE + 1];
+  const GatherTDesc d = descs[blockIdx.z];
+  const int tilesT = (d.rows + GT_TILE - 1) / GT_TILE, tilesJ = (d.q + GT_TILE - 1) / GT_TILE;
+  const int tx = threadIdx.x, ty0 = threadIdx.y;
+  for (int ti = blockIdx.x; ti < tilesT * tilesJ; ti += gridDim.x) {
+    const int t0 = (ti % tilesT) * GT_TILE, j0 = (ti / tilesT) * GT_TILE;
+    const int jl = j0 + tx;
+    const long long pj = jl < d.q ? __ldg(d.piv + jl) : 0;
+    for (int ty = ty0; ty < GT_TILE; ty += GT_ROWS) {
+      const int t = t0 + ty;
+      if (t < d.rows && jl < d.q) tile[ty][tx] = d.src[(long long)t * d.lds + pj];
+    }
+    __syncthreads();
+    for (int ty = ty0; ty < GT_TILE; ty += GT_ROWS) {
+      const int j = j0 + ty, t = t0 + tx;
+      if (t < d.rows && j < d.q) d.out[(long long)j * d.rows + t] = tile[tx][ty];
+    }
+    __syncthreads();
   }
+}
+void launch_gather_t(cudaStream_t s, const std::vector<GatherTDesc>& v) {
+  if (v.empty()) return;
+  long long mt = 1;
+  for (auto& d : v) mt = std::max<long long>(mt, (long long)((d.rows + GT_TILE - 1) / GT_TILE) * ((d.q + GT_TILE - 1) / GT_TILE));
+  auto dd = ring_up(v, s);
+  for (size_t o = 0; o < v.size(); o += 65535) {
+    const unsigned nz = (unsigned)std::min<size_t>(65535, v.size() - o);
+    gather_t_kernel<<<dim3((unsigned)std::min<long long>(mt, 2048), 1, nz), dim3(GT_TILE, GT_ROWS), 0, s>>>(dd.p + o);
+    count_launch();
+  }
+  RSF_LAUNCH_CHECK();
 }
 
 // out = max(out, max_j ||A(:, j)||)   (one CTA per problem)
@@ -769,7 +798,7 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
               tp.push_back(TrsmProb{Pr.p + pro[x], c, Ri.p + ro[x], qq[x], qq[x], qq[x]});
               mx = std::max(mx, (long long)bx[i].ni * qq[x]);
             }
-            launch_descs(s, gd, mx, gather_t_kernel);
+            launch_gather_t(s, gd);
             launch_descs(s, ed, mx, eye_kernel);
             trsm_upper_batched(s, tp);                    // R11^-1 of the residual sketch
             GemmBatch g0(false, false);
@@ -892,7 +921,7 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
           }
           PhaseSeq cseq(s);
           cseq.next("c.z");
-          launch_descs(s, gz, mz, gather_t_kernel);
+          launch_gather_t(s, gz);
           launch_descs(s, ez, mz, eye_kernel);
           trsm_upper_batched(s, tz);
           GemmBatch gz1(false, false);
