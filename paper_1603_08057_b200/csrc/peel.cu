@@ -1394,6 +1394,9 @@ EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KP
           RSF_CUDA(cudaSetDevice(dev));
           StreamScope scope(ctx.aux[j]);
           RSF_CUDA(cudaStreamWaitEvent(ctx.aux[j], t_event, 0));
+          // test hook: the last job reports out-of-memory (exercises the serial fallback)
+          static const bool test_oom = getenv("RSF_TEST_PAR_OOM") && getenv("RSF_TEST_PAR_OOM")[0] == '1';
+          if (test_oom && j + 1 == jobs.size()) throw Error(ST_ENOMEM, "RSF_TEST_PAR_OOM");
           jobs[j]();
           RSF_CUDA(cudaStreamSynchronize(ctx.aux[j]));
         } catch (...) {
@@ -1413,10 +1416,34 @@ EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KP
     for (auto& x : th) x.join();
     cudaEventDestroy(t_event);
     cudaEventDestroy(f_event);
+    f_event = nullptr;
     for (long long v : nl) g_launches += v;
-    if (main_err) std::rethrow_exception(main_err);
-    for (auto& e : err)
-      if (e) std::rethrow_exception(e);
+    // Out of memory with the jobs side by side: release what the jobs' streams cached and
+    // run everything again in the serial order (peak memory of one job at a time)
+    auto is_oom = [](const std::exception_ptr& e) {
+      if (!e) return false;
+      try { std::rethrow_exception(e); } catch (const Error& x) { return x.code == ST_ENOMEM; } catch (...) {}
+      return false;
+    };
+    bool oom = is_oom(main_err);
+    for (auto& e : err) oom = oom || is_oom(e);
+    if (oom) {
+      for (size_t j = 0; j < jobs.size(); ++j) {
+        cudaStreamSynchronize(ctx.aux[j]);
+        dev_cache_trim(ctx.aux[j]);
+      }
+      cudaGetLastError();
+      F.reset();
+      u.release();
+      wait_f = []() {};
+      R.flops_factor = 0;
+      main_part();
+      for (auto& j : jobs) j();
+    } else {
+      if (main_err) std::rethrow_exception(main_err);
+      for (auto& e : err)
+        if (e) std::rethrow_exception(e);
+    }
   }
   R.t_peel += t_trinv;
   for (int i = 0; i < p; ++i) {

@@ -400,7 +400,8 @@ json.dump({"ell": r.ell, "grad": list(r.grad), "trace": list(r.diag.trace)[:3]},
 def test_concurrent_trace_jobs_equal_serial_order(tmp_path):
     """gp_mle_eval with theta = (rho, alpha, nugget): three trace jobs (two compressions + peelings
     and the Tr(F^-1) peeling) run concurrently on their own streams; the result must be
-    bit-identical to the serial order (RSF_PAR_TRACES=0)."""
+    bit-identical to the serial order (RSF_PAR_TRACES=0), also when a concurrent job runs out of
+    memory and the evaluation falls back to the serial order (RSF_TEST_PAR_OOM=1)."""
     import json
     import os
     import subprocess
@@ -409,10 +410,12 @@ def test_concurrent_trace_jobs_equal_serial_order(tmp_path):
     script = tmp_path / "par.py"
     script.write_text(_PAR_PROBE)
     out = {}
-    for flag in ("1", "0"):
-        f = tmp_path / f"par{flag}.json"
-        env = dict(os.environ, RSF_PAR_TRACES=flag)
+    for flag, oom in (("1", "0"), ("0", "0"), ("1", "1")):
+        f = tmp_path / f"par{flag}{oom}.json"
+        env = dict(os.environ, RSF_PAR_TRACES=flag, RSF_TEST_PAR_OOM=oom)
         subprocess.run([sys.executable, str(script), root, str(f)], env=env, check=True, timeout=600)
-        out[flag] = json.load(open(f))
-    assert out["1"] == out["0"]
-    assert all(np.isfinite(out["1"]["grad"]))
+        out[flag + oom] = json.load(open(f))
+    assert out["10"] == out["00"]
+    # out of memory in a concurrent job: everything is redone in the serial order
+    assert out["11"] == out["00"]
+    assert all(np.isfinite(out["10"]["grad"]))
