@@ -308,7 +308,7 @@ std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams
       static const bool stack_on = !(getenv("RSF_STACKED") && std::string(getenv("RSF_STACKED")) == "0");
       int mi = 0;
       for (int b = 0; b < nb; ++b) mi = std::max(mi, cvec[b]);
-      LV.stacked = !sig && stack_on && !(fused_on0 && mi <= SWEEP_MAX_I);
+      LV.stacked = !sig && stack_on && !(fused_on0 && mi <= sweep_max_i());
       if (LV.stacked) {
         std::vector<int> hSR;
         LV.sroff.resize(nb);
@@ -554,7 +554,7 @@ std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams
       static const bool fused_on = !(getenv("RSF_FUSED") && std::string(getenv("RSF_FUSED")) == "0");
       LV.max_i = 0;
       for (int b = 0; b < nb; ++b) LV.max_i = std::max(LV.max_i, cvec[b]);
-      LV.fused = fused_on && LV.max_i <= SWEEP_MAX_I;
+      LV.fused = fused_on && LV.max_i <= sweep_max_i();
       if (LV.fused) {
         std::vector<BoxOp> ops;
         for (int b = 0; b < nb; ++b) {

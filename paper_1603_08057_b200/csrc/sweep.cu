@@ -113,25 +113,149 @@ __global__ void __launch_bounds__(NT) sweep_kernel(const BoxOp* __restrict__ ops
   }
 }
 
+// DMMA.8x8x4 version of slab_mm: C (rho x j) = A (rho x kk) B (kk x j) with A(rho, kk) =
+// in[kk][rho] (shared memory) and B(kk, j) = M(kk, j) (global, read-only path).  Warp w owns
+// the N-tiles w, w + 8, ... (8 columns each) for all KC/8 row tiles, two N-tiles at a time; the
+// element (rho, j) of out is always written by the same thread (lane layout of the DMMA
+// accumulator), so consecutive calls on the same out need no barrier.
+template <int KC, bool TR>
+__device__ __forceinline__ void slab_mm_mma(double* __restrict__ out, const double* __restrict__ in, int K, int N,
+                                            const double* __restrict__ Mat, int ldm, double alpha, double beta) {
+  constexpr int MT = KC / 8, NW = NT / 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+  const int ntiles = (N + 7) / 8;
+  for (int nt0 = warp; nt0 < ntiles; nt0 += 2 * NW) {
+    const int nt1 = nt0 + NW;
+    const bool has1 = nt1 < ntiles;
+    double acc[2][MT][2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int m = 0; m < MT; ++m) { acc[u][m][0] = 0.0; acc[u][m][1] = 0.0; }
+    const int jb0 = nt0 * 8 + g, jb1 = nt1 * 8 + g;
+    for (int k0 = 0; k0 < K; k0 += 4) {
+      const int kk = k0 + tq;
+      const bool kv = kk < K;
+      double a[MT];
+#pragma unroll
+      for (int m = 0; m < MT; ++m) a[m] = kv ? in[kk * KC + m * 8 + g] : 0.0;
+      double b0 = 0.0, b1 = 0.0;
+      if (kv && jb0 < N) b0 = TR ? __ldg(Mat + jb0 + (long long)kk * ldm) : __ldg(Mat + kk + (long long)jb0 * ldm);
+      if (kv && has1 && jb1 < N) b1 = TR ? __ldg(Mat + jb1 + (long long)kk * ldm) : __ldg(Mat + kk + (long long)jb1 * ldm);
+#pragma unroll
+      for (int m = 0; m < MT; ++m) {
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(acc[0][m][0]), "+d"(acc[0][m][1]) : "d"(a[m]), "d"(b0));
+        if (has1)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                       : "+d"(acc[1][m][0]), "+d"(acc[1][m][1]) : "d"(a[m]), "d"(b1));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      if (u == 1 && !has1) break;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = (u ? nt1 : nt0) * 8 + 2 * tq + h;
+        if (j >= N) continue;
+#pragma unroll
+        for (int m = 0; m < MT; ++m) {
+          double* o = out + j * KC + m * 8 + g;
+          *o = (beta == 0.0) ? alpha * acc[u][m][h] : fma(beta, *o, alpha * acc[u][m][h]);
+        }
+      }
+    }
+  }
+}
+
+template <int KC>
+__global__ void __launch_bounds__(NT) sweep_mma_kernel(const BoxOp* __restrict__ ops, int kind, double* X0, double* X1,
+                                                       int k) {
+  extern __shared__ double sm[];
+  const BoxOp op = ops[blockIdx.x];
+  const int kb = op.kb, r = op.r, r0 = blockIdx.y * KC;
+  double* xs = sm;
+  double* xr = sm + kb * KC;
+  double* yr = xr + r * KC;
+  if (kind == SW_SOLVE_FWD || kind == SW_SOLVE_BWD) {
+    load_cols<KC>(xs, X0, op.S, kb, k, r0, k);
+    load_cols<KC>(xr, X0, op.R, r, k, r0, k);
+    __syncthreads();
+    if (kind == SW_SOLVE_FWD) {
+      if (kb) slab_mm_mma<KC, false>(xr, xs, kb, r, op.T, kb, -1.0, 1.0);
+      __syncthreads();
+      slab_mm_mma<KC, true>(yr, xr, r, r, op.L, r, 1.0, 0.0);
+      __syncthreads();
+      if (kb) slab_mm_mma<KC, true>(xs, yr, r, kb, op.E, kb, -1.0, 1.0);
+    } else {
+      if (kb) slab_mm_mma<KC, false>(xr, xs, kb, r, op.E, kb, -1.0, 1.0);
+      __syncthreads();
+      slab_mm_mma<KC, false>(yr, xr, r, r, op.L, r, 1.0, 0.0);
+      __syncthreads();
+      if (kb) slab_mm_mma<KC, true>(xs, yr, r, kb, op.T, kb, -1.0, 1.0);
+    }
+    __syncthreads();
+    store_cols<KC>(xs, X0, op.S, kb, k, r0, k);
+    store_cols<KC>(yr, X0, op.R, r, k, r0, k);
+  } else if (kind == SW_AO_UP) {
+    load_cols<KC>(xs, X0, op.S, kb, k, r0, k);
+    load_cols<KC>(xr, X0, op.R, r, k, r0, k);
+    __syncthreads();
+    if (kb) slab_mm_mma<KC, true>(xs, xr, r, kb, op.T, kb, 1.0, 1.0);
+    __syncthreads();
+    if (kb) slab_mm_mma<KC, false>(yr, xs, kb, r, op.E, kb, 1.0, 0.0);
+    slab_mm_mma<KC, false>(yr, xr, r, r, op.L, r, 1.0, kb ? 1.0 : 0.0);
+    __syncthreads();
+    store_cols<KC>(xs, X0, op.S, kb, k, r0, k);
+    store_cols<KC>(yr, X1, op.R, r, k, r0, k);
+  } else {
+    load_cols<KC>(xs, X1, op.S, kb, k, r0, k);
+    load_cols<KC>(xr, X0, op.R, r, k, r0, k);
+    load_cols<KC>(yr, X1, op.R, r, k, r0, k);
+    __syncthreads();
+    if (kb) slab_mm_mma<KC, true>(xs, xr, r, kb, op.E, kb, 1.0, 1.0);
+    __syncthreads();
+    if (kb) slab_mm_mma<KC, false>(yr, xs, kb, r, op.T, kb, 1.0, 1.0);
+    __syncthreads();
+    store_cols<KC>(xs, X1, op.S, kb, k, r0, k);
+    store_cols<KC>(yr, X1, op.R, r, k, r0, k);
+  }
+}
+
+bool sweep_mma_on() {
+  static const bool on = getenv("RSF_SWEEP_MMA") && getenv("RSF_SWEEP_MMA")[0] == '1';
+  return on;
+}
+
 }  // namespace
+
+int sweep_max_i() { return sweep_mma_on() ? SWEEP_MAX_I_MMA : SWEEP_MAX_I; }
 
 void sweep_level(cudaStream_t s, const BoxOp* d_ops, int nops, int max_i, SweepKind kind, double* X0, double* X1,
                  int k) {
   if (nops == 0 || k <= 0) return;
-  RSF_REQUIRE(max_i <= SWEEP_MAX_I, ST_EINVAL, "sweep_level: box too large for the fused kernel");
+  RSF_REQUIRE(max_i <= sweep_max_i(), ST_EINVAL, "sweep_level: box too large for the fused kernel");
   static std::once_flag attr_once;
   std::call_once(attr_once, [&] {
     RSF_CUDA(cudaFuncSetAttribute(sweep_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     RSF_CUDA(cudaFuncSetAttribute(sweep_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    RSF_CUDA(cudaFuncSetAttribute(sweep_mma_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    RSF_CUDA(cudaFuncSetAttribute(sweep_mma_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   });
   // shared memory: (kb + 2 r) * KC doubles <= 2 |I| * KC
   const int KC = (max_i <= 128) ? 32 : 16;
   const size_t smem = (size_t)2 * max_i * KC * sizeof(double);
   const unsigned gy = (unsigned)((k + KC - 1) / KC);
+  const bool mma = sweep_mma_on();
   for (int o = 0; o < nops; o += 65535) {
     const unsigned nb = (unsigned)std::min(65535, nops - o);
-    if (KC == 32) sweep_kernel<32><<<dim3(nb, gy), NT, smem, s>>>(d_ops + o, (int)kind, X0, X1, k);
-    else sweep_kernel<16><<<dim3(nb, gy), NT, smem, s>>>(d_ops + o, (int)kind, X0, X1, k);
+    if (mma) {
+      if (KC == 32) sweep_mma_kernel<32><<<dim3(nb, gy), NT, smem, s>>>(d_ops + o, (int)kind, X0, X1, k);
+      else sweep_mma_kernel<16><<<dim3(nb, gy), NT, smem, s>>>(d_ops + o, (int)kind, X0, X1, k);
+    } else {
+      if (KC == 32) sweep_kernel<32><<<dim3(nb, gy), NT, smem, s>>>(d_ops + o, (int)kind, X0, X1, k);
+      else sweep_kernel<16><<<dim3(nb, gy), NT, smem, s>>>(d_ops + o, (int)kind, X0, X1, k);
+    }
     count_launch();
   }
   RSF_LAUNCH_CHECK();

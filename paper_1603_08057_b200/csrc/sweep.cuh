@@ -26,7 +26,10 @@ struct BoxOp {
 
 enum SweepKind { SW_SOLVE_FWD = 0, SW_SOLVE_BWD = 1, SW_AO_UP = 2, SW_AO_DN = 3 };
 
-constexpr int SWEEP_MAX_I = 128;   // largest |I_b| handled by the fused kernel (measured: slower than the GEMM path above)
+constexpr int SWEEP_MAX_I = 128;       // largest |I_b| of the FMA fused kernel (measured: slower than the GEMM path above)
+constexpr int SWEEP_MAX_I_MMA = 256;   // ... of the DMMA fused kernel
+// largest |I_b| the fused sweeps take with the current settings (RSF_SWEEP_MMA=1: DMMA kernel)
+int sweep_max_i();
 
 // X0: the operand updated in place (solve: X'; apply-only: x'), X1: apply-only output y'.
 // ldx = k (number of right-hand sides, X' is k x n column-major).

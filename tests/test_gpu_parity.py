@@ -315,9 +315,9 @@ np.save(sys.argv[2], np.concatenate([F.solve(B.clone()).cpu().numpy(), Fi.apply(
 
 
 def test_fused_sweeps_match_batched_gemm_path(tmp_path):
-    """The fused small-box level sweeps (sweep.cu, every level of a leaf-32 tree) against the
-    batched-GEMM level steps (RSF_FUSED=0): F^-1 B and F_i B on 40 right-hand sides agree to
-    round-off (same factor, same operation order up to FMA contraction)."""
+    """The fused small-box level sweeps (sweep.cu, every level of a leaf-32 tree; FMA kernel and
+    the DMMA kernel of RSF_SWEEP_MMA=1) against the batched-GEMM level steps (RSF_FUSED=0):
+    F^-1 B and F_i B on 40 right-hand sides agree to round-off."""
     import os
     import subprocess
     import sys
@@ -325,13 +325,14 @@ def test_fused_sweeps_match_batched_gemm_path(tmp_path):
     script = tmp_path / "probe.py"
     script.write_text(_FUSED_PROBE)
     out = {}
-    for flag in ("1", "0"):
-        f = tmp_path / f"out{flag}.npy"
-        env = dict(os.environ, RSF_FUSED=flag)
+    for flag, mma in (("1", "0"), ("0", "0"), ("1", "1")):
+        f = tmp_path / f"out{flag}{mma}.npy"
+        env = dict(os.environ, RSF_FUSED=flag, RSF_SWEEP_MMA=mma)
         subprocess.run([sys.executable, str(script), root, str(f)], env=env, check=True, timeout=600)
-        out[flag] = np.load(f)
-    a, b = out["1"], out["0"]
-    assert np.linalg.norm(a - b) <= 1e-10 * np.linalg.norm(b)
+        out[flag + mma] = np.load(f)
+    b = out["00"]
+    for key in ("10", "11"):   # FMA fused kernel (|I| <= 128), DMMA fused kernel (|I| <= 256)
+        assert np.linalg.norm(out[key] - b) <= 1e-10 * np.linalg.norm(b), key
 
 
 @pytest.fixture(scope="module")
