@@ -133,15 +133,21 @@ __device__ __forceinline__ void slab_mm_mma(double* __restrict__ out, const doub
 #pragma unroll
       for (int m = 0; m < MT; ++m) { acc[u][m][0] = 0.0; acc[u][m][1] = 0.0; }
     const int jb0 = nt0 * 8 + g, jb1 = nt1 * 8 + g;
+    auto ldb = [&](int kk, int jb) -> double {
+      if (kk >= K || jb >= N) return 0.0;
+      return TR ? __ldg(Mat + jb + (long long)kk * ldm) : __ldg(Mat + kk + (long long)jb * ldm);
+    };
+    // B fragments of the next k-step are fetched before the MMAs of this one (global latency)
+    double nb0 = ldb(tq, jb0), nb1 = has1 ? ldb(tq, jb1) : 0.0;
     for (int k0 = 0; k0 < K; k0 += 4) {
       const int kk = k0 + tq;
       const bool kv = kk < K;
       double a[MT];
 #pragma unroll
       for (int m = 0; m < MT; ++m) a[m] = kv ? in[kk * KC + m * 8 + g] : 0.0;
-      double b0 = 0.0, b1 = 0.0;
-      if (kv && jb0 < N) b0 = TR ? __ldg(Mat + jb0 + (long long)kk * ldm) : __ldg(Mat + kk + (long long)jb0 * ldm);
-      if (kv && has1 && jb1 < N) b1 = TR ? __ldg(Mat + jb1 + (long long)kk * ldm) : __ldg(Mat + kk + (long long)jb1 * ldm);
+      const double b0 = nb0, b1 = nb1;
+      nb0 = ldb(kk + 4, jb0);
+      nb1 = has1 ? ldb(kk + 4, jb1) : 0.0;
 #pragma unroll
       for (int m = 0; m < MT; ++m) {
         asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
