@@ -197,9 +197,11 @@ __global__ void __launch_bounds__(NT) sketch_cpqr_kernel(const RDesc* __restrict
 // (SP x chunk each); every greedy step exchanges the CTAs' best candidates and the
 // Householder vector of the winner through distributed shared memory, so one step
 // costs two cluster barriers instead of a pass of one SM over the whole sketch in
-// global memory.  Produces the same swap list as sketch_cpqr_kernel.
+// global memory.  Same greedy rule as sketch_cpqr_kernel (the column norms are summed in a
+// different order, so near-ties may resolve differently).
 constexpr int SK_NT = 512, SK_NW = SK_NT / 32;
-constexpr int SK_MAXCOLS = 600;   // columns per CTA: SP * 600 * 8 B = 192 KB of shared memory
+constexpr int SK_MAXCOLS = 600;   // columns per CTA: (SPP + 1) * 600 * 8 B = 202 KB of shared memory
+constexpr int SPP = SP + 1;       // padded shared-memory column stride (odd: conflict-free per-thread columns)
 
 template <int CL>
 __global__ void __launch_bounds__(SK_NT) sketch_cpqr_cl_kernel(const RDesc* __restrict__ d0) {
@@ -217,18 +219,19 @@ __global__ void __launch_bounds__(SK_NT) sketch_cpqr_cl_kernel(const RDesc* __re
   const int J = d.J, cr = d.c - J, nbp = d.nbp;
   const int chunk = (cr + CL - 1) / CL;
   const int j0 = rank * chunk, nc = max(0, min(cr, j0 + chunk) - j0);
-  double* Zs = sk_sm;               // SP x chunk, column-major
-  double* zn = Zs + SP * chunk;     // squared trailing norms (-1: retired)
+  double* Zs = sk_sm;               // SP x chunk, column-major with the padded stride SPP
+  double* zn = Zs + SPP * chunk;    // squared trailing norms (-1: retired)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int e = tid; e < SP * nc; e += SK_NT) Zs[e] = d.Y[(long long)(J + j0) * SP + e];
+  for (int e = tid; e < SP * nc; e += SK_NT) {
+    const int j = e / SP, r = e - j * SP;
+    Zs[j * SPP + r] = d.Y[(long long)(J + j0) * SP + e];
+  }
   __syncthreads();
-  for (int j = warp; j < nc; j += SK_NW) {
-    const double* z = Zs + j * SP;
-    double v = (lane < SP) ? z[lane] : 0.0;
-    double s2 = v * v;
-    if (lane + 32 < SP) { const double w = z[lane + 32]; s2 += w * w; }
-    s2 = wsum(s2);
-    if (lane == 0) zn[j] = s2;
+  for (int j = tid; j < nc; j += SK_NT) {   // one thread per column
+    const double* z = Zs + j * SPP;
+    double s2 = 0.0;
+    for (int r = 0; r < SP; ++r) s2 += z[r] * z[r];
+    zn[j] = s2;
   }
   __syncthreads();
   for (int t = 0; t < nbp; ++t) {
@@ -266,7 +269,7 @@ __global__ void __launch_bounds__(SK_NT) sketch_cpqr_cl_kernel(const RDesc* __re
     const int owner = p / chunk;
     if (rank == owner && warp == 0) {
       // Householder reflector of Zs(t:SP, p): v = [1; x(t+1:)/(x_t - beta)], tau = (beta - x_t)/beta
-      double* x = Zs + (p - j0) * SP;
+      double* x = Zs + (p - j0) * SPP;
       double s2 = 0.0;
       for (int r = t + 1 + lane; r < SP; r += 32) s2 += x[r] * x[r];
       s2 = wsum(s2);
@@ -287,48 +290,24 @@ __global__ void __launch_bounds__(SK_NT) sketch_cpqr_cl_kernel(const RDesc* __re
     }
     if (rank == 0 && tid == 0) chosen[t] = p;
     cluster.sync();
-    // apply (I - tau v v^T) to the active local columns, recompute their trailing norms
-    // (U columns per warp at a time: their warp reductions interleave instead of running back
-    // to back)
+    // apply (I - tau v v^T) to the active local columns and recompute their trailing norms,
+    // one thread per column (hv is read as a broadcast; the padded stride SPP keeps the
+    // per-thread column accesses at two wavefronts per warp): a warp-per-column layout spends
+    // most of its instructions in shuffle reductions over only SP = 40 rows
     const double tau = htau;
-    const double v0 = (lane < SP) ? hv[lane] : 0.0;
-    const double v1 = (lane + 32 < SP) ? hv[lane + 32] : 0.0;
-    constexpr int U = 4;
-    for (int jb = warp; jb < nc; jb += U * SK_NW) {
-      double a0[U], a1[U], w[U];
-      bool on[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int j = jb + u * SK_NW;
-        on[u] = j < nc && zn[j] >= 0.0;
-        const double* z = Zs + j * SP;
-        a0[u] = (on[u] && lane < SP && lane >= t) ? z[lane] : 0.0;
-        a1[u] = (on[u] && lane + 32 < SP && lane + 32 >= t) ? z[lane + 32] : 0.0;
-        w[u] = a0[u] * v0 + a1[u] * v1;
+    for (int j = tid; j < nc; j += SK_NT) {
+      if (zn[j] < 0.0) continue;
+      double* z = Zs + j * SPP;
+      double dot = 0.0;
+      for (int r = t; r < SP; ++r) dot += z[r] * hv[r];
+      const double w = tau * dot;
+      double s2 = 0.0;
+      for (int r = t; r < SP; ++r) {
+        const double b = z[r] - w * hv[r];
+        z[r] = b;
+        if (r > t) s2 += b * b;
       }
-#pragma unroll
-      for (int o = 16; o; o >>= 1)
-#pragma unroll
-        for (int u = 0; u < U; ++u) w[u] += __shfl_xor_sync(0xffffffffu, w[u], o);
-      double s2[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int j = jb + u * SK_NW;
-        const double ww = tau * w[u];
-        const double b0 = a0[u] - ww * v0, b1 = a1[u] - ww * v1;
-        double* z = Zs + j * SP;
-        if (on[u] && lane < SP && lane >= t) z[lane] = b0;
-        if (on[u] && lane + 32 < SP && lane + 32 >= t) z[lane + 32] = b1;
-        s2[u] = (lane > t && lane < SP ? b0 * b0 : 0.0) + (lane + 32 > t && lane + 32 < SP ? b1 * b1 : 0.0);
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1)
-#pragma unroll
-        for (int u = 0; u < U; ++u) s2[u] += __shfl_xor_sync(0xffffffffu, s2[u], o);
-      if (lane == 0)
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (on[u]) zn[jb + u * SK_NW] = s2[u];
+      zn[j] = s2;
     }
     __syncthreads();
   }
@@ -518,13 +497,13 @@ template <int CL>
 void launch_cl(cudaStream_t s, const RDesc* dd, int na, int chunk) {
   static std::once_flag attr_once;
   std::call_once(attr_once, [&] {
-    RSF_CUDA(cudaFuncSetAttribute(sketch_cpqr_cl_kernel<CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    RSF_CUDA(cudaFuncSetAttribute(sketch_cpqr_cl_kernel<CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
     if (CL > 8) RSF_CUDA(cudaFuncSetAttribute(sketch_cpqr_cl_kernel<CL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   });
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(na * CL));
   cfg.blockDim = dim3(SK_NT);
-  cfg.dynamicSmemBytes = (size_t)(SP + 1) * chunk * sizeof(double);
+  cfg.dynamicSmemBytes = (size_t)(SPP + 1) * chunk * sizeof(double);
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
