@@ -59,7 +59,8 @@ Arena* arena_for(cudaStream_t s) {
   for (auto& a : arenas()) if (a.s == s) return &a;
   size_t fr = 0, tot = 0;
   cudaMemGetInfo(&fr, &tot);
-  size_t cap = std::min<size_t>(fr / 2, size_t(40) << 30) / (size_t(2) << 20) * (size_t(2) << 20);
+  static const size_t cap_gb = getenv("RSF_ARENA_GB") ? (size_t)atoi(getenv("RSF_ARENA_GB")) : 40;
+  size_t cap = std::min<size_t>(fr / 2, cap_gb << 30) / (size_t(2) << 20) * (size_t(2) << 20);
   Arena a;
   a.s = s;
   if (cap >= (size_t(1) << 30) && cudaMallocAsync((void**)&a.base, cap, s) == cudaSuccess) {
