@@ -52,33 +52,35 @@ struct RDesc {
   double eps;
 };
 
-// ref = max_j ||A(:, j)||, piv = identity
-__global__ void ref_kernel(const RDesc* __restrict__ d0) {
-  const RDesc d = d0[blockIdx.x];
-  __shared__ double red[NT / 32];
+// ref = max_j ||A(:, j)||, piv = identity.  Grid (column blocks, problems): warp per column,
+// the squared norms combined with an integer atomicMax (the bit patterns of non-negative
+// doubles order like the values); ref2 must be zero on entry.
+__global__ void ref_norms_kernel(const RDesc* __restrict__ d0, unsigned long long* __restrict__ ref2) {
+  const RDesc d = d0[blockIdx.y];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double mx = 0.0;
-  for (int j = warp; j < d.c; j += NT / 32) {
+  for (int j = blockIdx.x * (NT / 32) + warp; j < d.c; j += gridDim.x * (NT / 32)) {
     const double* a = d.A + (long long)j * d.lda;
     double s = 0.0;
     for (int r = lane; r < d.m; r += 32) s += a[r] * a[r];
-    s = wsum(s);
-    mx = fmax(mx, s);
+    mx = fmax(mx, wsum(s));
   }
-  for (int j = threadIdx.x; j < d.c; j += NT) d.piv[j] = j;
-  if (lane == 0) red[warp] = mx;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double v = 0.0;
-    for (int w = 0; w < NT / 32; ++w) v = fmax(v, red[w]);
-    if (d.ref_out) *d.ref_out = sqrt(v);
-    const double rf = d.ref_in ? *d.ref_in : sqrt(v);
-    *d.ref = rf;
-    // nothing to factor: an all-zero matrix, or every column already below the absolute threshold
-    d.flag[0] = (v > 0.0 && rf > 0.0 && sqrt(v) > d.eps * rf) ? 0 : 1;
-    d.flag[1] = 0;
-    d.flag[2] = 0;
-  }
+  if (lane == 0 && mx > 0.0) atomicMax(ref2 + blockIdx.y, (unsigned long long)__double_as_longlong(mx));
+  for (int j = blockIdx.x * NT + threadIdx.x; j < d.c; j += gridDim.x * NT) d.piv[j] = j;
+}
+// per problem: the reference scale and the "nothing to factor" flag
+__global__ void ref_finish_kernel(const RDesc* __restrict__ d0, const unsigned long long* __restrict__ ref2, int P) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  const RDesc d = d0[i];
+  const double v = __longlong_as_double((long long)ref2[i]);
+  if (d.ref_out) *d.ref_out = sqrt(v);
+  const double rf = d.ref_in ? *d.ref_in : sqrt(v);
+  *d.ref = rf;
+  // nothing to factor: an all-zero matrix, or every column already below the absolute threshold
+  d.flag[0] = (v > 0.0 && rf > 0.0 && sqrt(v) > d.eps * rf) ? 0 : 1;
+  d.flag[1] = 0;
+  d.flag[2] = 0;
 }
 
 __global__ void gauss_kernel(const RDesc* __restrict__ d0, unsigned seed) {
@@ -633,7 +635,17 @@ RRQRResult rrqr_batched(cudaStream_t s, const std::vector<RRQRProb>& probs, doub
     DBuf<double> G(gt, s);
     for (int i = 0; i < P; ++i) base[i].G = G.p + goff[i];
     auto db = ring_up(base, s);
-    ref_kernel<<<P, NT, 0, s>>>(db.p);
+    {
+      DBuf<unsigned long long> ref2(P, s);
+      RSF_CUDA(cudaMemsetAsync(ref2.p, 0, P * sizeof(unsigned long long), s));
+      long long cmax = 1, work = 0;
+      for (auto& p : probs) { cmax = std::max<long long>(cmax, p.c); work = std::max<long long>(work, (long long)p.m * p.c); }
+      // column blocks of 8 columns; enough CTAs per problem that ~1 MB of A goes to each
+      const long long gx = std::max<long long>(1, std::min<long long>((cmax + 7) / 8, (work + (1 << 17) - 1) >> 17));
+      ref_norms_kernel<<<dim3((unsigned)std::min<long long>(gx, 4096), P), NT, 0, s>>>(db.p, ref2.p);
+      ref_finish_kernel<<<(P + 127) / 128, 128, 0, s>>>(db.p, ref2.p, P);
+      count_launch();
+    }
     long long mx = 0;
     for (auto& p : probs) mx = std::max(mx, (long long)SP * p.m);
     gauss_kernel<<<dim3((unsigned)std::min<long long>(1024, (mx + NT - 1) / NT), P), NT, 0, s>>>(
