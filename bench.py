@@ -196,12 +196,12 @@ def cpu_baseline_sample(args, c):
                       f"n^1.6 (P:830)", "sample_seconds": t_s}
 
 
-# ncu --set full of the longest launch of the dominant kernel (profiles/r01_gemm_pipe_ncu_v3.txt)
-TRAFFIC_BYTES = 4.119e9 + 0.692e9
-TRAFFIC_NOTE = ("dram__bytes_read.sum + dram__bytes_write.sum of gemm_pipe_kernel launch #14677 (the longest "
-                "peeling-subtraction launch, 14.05 ms, 12288 CTAs, DMMA pipe 83 % busy); its compulsory "
-                "bytes are ~5.6e9 (V_i of three level-1 boxes 4.2 GB + the Y' block read and written), "
-                "so operands are not re-read from DRAM")
+# ncu --set full of the longest launch of the dominant kernel (profiles/r01_gemm_pipe_ncu_v4.txt)
+TRAFFIC_BYTES = 4.1665e9 + 0.7543e9
+TRAFFIC_NOTE = ("dram__bytes_read.sum + dram__bytes_write.sum of the longest gemm_pipe_kernel launch of an "
+                "evaluation (peeling subtraction at level 1, 13.76 ms, 12288 CTAs, DMMA pipe 85 % busy); "
+                "its compulsory bytes are ~5.6e9 (V_i of three level-1 boxes 4.2 GB + the Y' block read "
+                "and written), so operands are not re-read from DRAM")
 
 
 def main():
