@@ -1165,6 +1165,7 @@ void GemmBatch::run(cudaStream_t s, double* X0, double* X1, int ldx, int Mglob, 
       // DMMA peak, plus the workspace traffic of the deterministic reduction and its launch.
       static const int splitk_mode = getenv("RSF_SPLITK") ? atoi(getenv("RSF_SPLITK")) : 1;
       static const int small_k = getenv("RSF_GEMM_SMALLK") ? atoi(getenv("RSF_GEMM_SMALLK")) : 256;
+      static const double splitk_gain = getenv("RSF_SPLITK_GAIN") ? atof(getenv("RSF_SPLITK_GAIN")) : 0.9;
       const int force = gemm_force_splitk();
       long long ctas = 0;
       double mntot = 0;
@@ -1184,7 +1185,7 @@ void GemmBatch::run(cudaStream_t s, double* X0, double* X1, int ldx, int Mglob, 
         double best = cost(1);
         for (int S2 = 2; S2 <= 32 && maxK_ / S2 >= 256 && S2 * mntot * 8.0 <= 2e9; ++S2) {
           const double c2 = cost(S2);
-          if (c2 < 0.9 * best) { best = c2; S = S2; }
+          if (c2 < splitk_gain * best) { best = c2; S = S2; }
         }
       }
       if (force > 0 && !has_lower_) S = std::max(1, std::min(force, std::max(1, maxK_ / P_BK)));
