@@ -29,6 +29,11 @@
  *     creation; concurrent solve/apply calls on one handle must use the same
  *     context stream (calls are stream-ordered on it).
  *   - results are bitwise reproducible for a fixed (input, seed, build, GPU).
+ *   - stream ordering: the library works on its context stream.  Device inputs must be
+ *     complete before a call reads them: a caller that produced them on another stream
+ *     calls rsf_ctx_wait_stream(ctx, that_stream) first (the Python binding does this with
+ *     torch's current stream before every call).  Every call returns after its own device
+ *     work is complete, so outputs are ready for any stream on return.
  */
 #ifndef RSF_H_
 #define RSF_H_
@@ -124,6 +129,10 @@ void rsf_opts_default(rsf_opts* out);
  * nccl_comm is reserved (NULL = single GPU). */
 rsf_status rsf_ctx_create(int device, void* cuda_stream, void* nccl_comm, rsf_ctx* out);
 void rsf_ctx_destroy(rsf_ctx ctx);
+/* Order the context after the caller: everything enqueued on `stream` so far (an event recorded
+ * there) completes before the context stream runs further work.  stream = NULL is the legacy
+ * default stream.  Returns RSF_EINVAL for a NULL ctx, RSF_ECUDA on a runtime error. */
+rsf_status rsf_ctx_wait_stream(rsf_ctx ctx, void* stream);
 
 /* Build F ~ Sigma (which = -1) with ID tolerance eps (Def. id: |R'_jj| <= eps |R'_11| truncation,
  * reading R-A), leaf capacity `leaf` (n_occ), or (which = i in [0,p)) the apply-only

@@ -35,6 +35,16 @@ def kernel_launches() -> int:
     return int(lib.rsf_kernel_launches())
 
 
+def _order_after_caller(ctx_h):
+    """Stream ordering (include/rsf.h conventions): the library's context stream waits for the
+    work torch has enqueued so far on its current stream (inputs produced there, outputs
+    cloned there).  The library returns only after its own work is complete."""
+    torch = sys.modules.get("torch")
+    if torch is None or not torch.cuda.is_available() or not torch.cuda.is_initialized():
+        return
+    _check(lib.rsf_ctx_wait_stream(ctx_h, C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+
+
 def _ptr(a, dtype_ok=True):
     """(address, keepalive) of a float64 contiguous torch tensor or numpy array."""
     try:
@@ -126,6 +136,7 @@ class Factor:
         h = C.c_void_p()
         kc = kernel.c()
         oc = (opts or Opts()).c()
+        _order_after_caller(ctx.h)
         _check(lib.rsf_factor(ctx.h, p, n, C.byref(kc), -1 if which is None else which, eps, leaf,
                               C.byref(oc), C.byref(h)))
         self.h, self.ctx, self.n, self.which = h, ctx, n, which
@@ -158,6 +169,7 @@ class Factor:
         po, ko = _ptr(out)
         nrhs = 1 if b.ndim == 1 else b.shape[0]
         # (nrhs, n) row-major == column-major n x nrhs with ld = n
+        _order_after_caller(self.ctx.h)
         _check(fn(self.h, pb, po, nrhs, self.n))
         return out
 
@@ -196,6 +208,7 @@ def gp_profile_eval(ctx: Context, xy, z, kernel: Kernel, eps: float, leaf: int =
     ell = C.c_double()
     grad = (C.c_double * 4)()
     d = rsf_eval_diag()
+    _order_after_caller(ctx.h)
     _check(lib.gp_profile_eval(ctx.h, px, pz, n, C.byref(kc), eps, leaf, C.byref(oc), C.byref(ell), grad,
                                C.byref(d)))
     return EvalResult(ell.value, [grad[i] for i in range(len(kernel.theta))], d)
@@ -211,6 +224,7 @@ def gp_cond_mean(F: Factor, z, xy_new, out=None):
     pz, kz = _ptr(z)
     px, kx = _ptr(xy_new)
     po, ko = _ptr(out)
+    _order_after_caller(F.ctx.h)
     _check(lib.gp_cond_mean(F.h, pz, px, m, po))
     return out
 
@@ -240,6 +254,7 @@ def gp_mle_eval(ctx: Context, xy, z, kernel: Kernel, eps: float, leaf: int = 64,
     ell = C.c_double()
     grad = (C.c_double * 4)()
     d = rsf_eval_diag()
+    _order_after_caller(ctx.h)
     _check(lib.gp_mle_eval(ctx.h, px, pz, n, C.byref(kc), eps, leaf, C.byref(oc), C.byref(ell), grad,
                            C.byref(d)))
     return EvalResult(ell.value, [grad[i] for i in range(len(kernel.theta))], d)

@@ -186,7 +186,23 @@ void rsf_ctx_destroy(rsf_ctx ctx) {
   rsf::dev_cache_trim(ctx->ctx.stream);
   cudaStreamSynchronize(ctx->ctx.stream);
   if (ctx->ctx.own_stream) cudaStreamDestroy(ctx->ctx.stream);
+  rsf::ring_trim();
   delete ctx;
+}
+
+rsf_status rsf_ctx_wait_stream(rsf_ctx ctx, void* stream) {
+  return guard([&] {
+    RSF_REQUIRE(ctx != nullptr, rsf::ST_EINVAL, "null context");
+    RSF_CUDA(cudaSetDevice(ctx->ctx.device));
+    cudaStream_t cs = (cudaStream_t)stream;
+    if (cs == ctx->ctx.stream) return;
+    cudaEvent_t ev;
+    RSF_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    RSF_CUDA(cudaEventRecord(ev, cs));
+    const cudaError_t e = cudaStreamWaitEvent(ctx->ctx.stream, ev, 0);
+    cudaEventDestroy(ev);   // destruction is deferred by the runtime until the wait resolved
+    RSF_CUDA(e);
+  });
 }
 
 rsf_status rsf_factor(rsf_ctx ctx, const double* xy, int64_t n, const rsf_kernel* kernel, int32_t which,

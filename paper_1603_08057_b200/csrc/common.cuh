@@ -109,6 +109,7 @@ struct DBuf {
 // synchronised first, so every earlier reader has finished.  Replaces a cudaMallocAsync
 // plus a pageable (host-blocking) copy per launch.
 void* ring_upload(cudaStream_t s, const void* h, size_t bytes);
+void ring_trim();   // free the retired (outgrown) rings; waits until their last readers ran
 template <class T>
 struct RPtr { T* p; };
 template <class T>

@@ -7,6 +7,7 @@
 #include <ctime>
 #include <cstdlib>
 #include <cstring>
+#include <list>
 #include <map>
 #include <mutex>
 #include <string>
@@ -158,25 +159,63 @@ void dev_free(void* p, size_t bytes, cudaStream_t s) {
 
 // ---------------------------------------------------------------- upload ring
 namespace {
+// One ring per stream.  A ring that is outgrown is RETIRED, not freed: earlier launches may
+// still read descriptors from it (a caller can hold an RPtr across later uploads), so it is
+// released only once an event recorded at retirement has completed (checked on later
+// resizes, and at ctx destroy through ring_trim).  The global mutex only guards the list;
+// stream synchronisations happen with no lock held (each stream is driven by one host
+// thread at a time, so its ring needs no lock of its own).
 struct Ring { char* dev = nullptr; char* host = nullptr; size_t cap = 0, off = 0; };
+struct Retired { char* dev; char* host; cudaEvent_t done; };
 std::mutex& ring_mu() { static std::mutex m; return m; }
-std::vector<std::pair<cudaStream_t, Ring>>& rings() { static std::vector<std::pair<cudaStream_t, Ring>> v; return v; }
+std::list<std::pair<cudaStream_t, Ring>>& rings() { static std::list<std::pair<cudaStream_t, Ring>> v; return v; }
+std::vector<Retired>& retired() { static std::vector<Retired> v; return v; }
+void reap_retired(bool block) {   // caller holds ring_mu
+  auto& v = retired();
+  for (size_t i = 0; i < v.size();) {
+    if (block) cudaEventSynchronize(v[i].done);
+    if (cudaEventQuery(v[i].done) == cudaSuccess) {
+      cudaFree(v[i].dev);
+      cudaFreeHost(v[i].host);
+      cudaEventDestroy(v[i].done);
+      v[i] = v.back();
+      v.pop_back();
+    } else {
+      cudaGetLastError();
+      ++i;
+    }
+  }
+}
 }  // namespace
-void* ring_upload(cudaStream_t s, const void* h, size_t bytes) {
+void ring_trim() {
   std::lock_guard<std::mutex> lk(ring_mu());
+  reap_retired(true);
+}
+void* ring_upload(cudaStream_t s, const void* h, size_t bytes) {
   Ring* r = nullptr;
-  for (auto& x : rings()) if (x.first == s) { r = &x.second; break; }
-  if (!r) { rings().emplace_back(s, Ring{}); r = &rings().back().second; }
+  {
+    std::lock_guard<std::mutex> lk(ring_mu());
+    for (auto& x : rings()) if (x.first == s) { r = &x.second; break; }
+    if (!r) { rings().emplace_back(s, Ring{}); r = &rings().back().second; }   // list: stable address
+  }
   const size_t need = (std::max<size_t>(bytes, 1) + 255) / 256 * 256;
-  if (need > r->cap / 2) {   // (re)size: previous contents may still be read -> synchronise first
-    RSF_CUDA(cudaStreamSynchronize(s));
-    if (r->dev) { cudaFree(r->dev); cudaFreeHost(r->host); }
+  if (need > r->cap / 2) {   // grow: retire the old ring until the stream has passed this point
+    if (r->dev) {
+      cudaEvent_t ev;
+      RSF_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      RSF_CUDA(cudaEventRecord(ev, s));
+      std::lock_guard<std::mutex> lk(ring_mu());
+      retired().push_back(Retired{r->dev, r->host, ev});
+      reap_retired(false);
+    }
+    r->dev = nullptr;
+    r->host = nullptr;
     r->cap = std::max<size_t>(size_t(64) << 20, 4 * need);
     RSF_CUDA(cudaMalloc((void**)&r->dev, r->cap));
     RSF_CUDA(cudaMallocHost((void**)&r->host, r->cap));
     r->off = 0;
   }
-  if (r->off + need > r->cap) {   // wrap: every earlier reader must have run
+  if (r->off + need > r->cap) {   // wrap: every earlier reader of this ring must have run
     RSF_CUDA(cudaStreamSynchronize(s));
     r->off = 0;
   }
@@ -208,9 +247,20 @@ cudaEvent_t get_ev() {
   cudaEventCreate(&e);
   return e;
 }
-void drain() {
-  for (auto& r : krecs()) {
-    cudaEventSynchronize(r.b);
+// fold finished records into the totals; block = false never waits (records whose end
+// event has not completed stay queued), block = true waits for all of them
+void drain(bool block) {
+  auto& v = krecs();
+  size_t keep = 0;
+  for (size_t i = 0; i < v.size(); ++i) {
+    KRec& r = v[i];
+    if (block) {
+      cudaEventSynchronize(r.b);
+    } else if (cudaEventQuery(r.b) != cudaSuccess) {
+      cudaGetLastError();
+      v[keep++] = r;
+      continue;
+    }
     float ms = 0.f, t0 = 0.f, t1 = 0.f;
     cudaEventElapsedTime(&ms, r.a, r.b);
     cudaEventElapsedTime(&t0, k_ref, r.a);
@@ -220,7 +270,7 @@ void drain() {
     kpool().push_back(r.a);
     kpool().push_back(r.b);
   }
-  krecs().clear();
+  v.resize(keep);
 }
 // length of the union of the launch intervals: the time at least one launch was running
 // (equals the sum of the durations when launches are serial; smaller when streams overlap)
@@ -246,16 +296,16 @@ void KStats::record(cudaStream_t s, cudaEvent_t* e0, cudaEvent_t* e1) {
 void KStats::push(cudaEvent_t e0, cudaEvent_t e1, double flops, double bytes) {
   std::lock_guard<std::mutex> lk(k_mu());
   krecs().push_back(KRec{e0, e1, flops, bytes});
-  if (krecs().size() > 4096) drain();
+  if (krecs().size() > 4096) drain(false);   // never waits on the device under the lock
 }
 void KStats::collect(double out[4]) {
   std::lock_guard<std::mutex> lk(k_mu());
-  drain();
+  drain(true);
   out[0] = k_launch; out[1] = busy_seconds(); out[2] = k_flops; out[3] = k_bytes;
 }
 void KStats::reset() {
   std::lock_guard<std::mutex> lk(k_mu());
-  drain();
+  drain(true);
   k_launch = k_sec = k_flops = k_bytes = 0;
   k_iv.clear();
   if (k_ref) { cudaEventDestroy(k_ref); k_ref = nullptr; }
