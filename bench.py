@@ -103,9 +103,11 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def aggregate(t_local: float, steps: int, world: int, device=None):
-    """Max-over-ranks time and whole-job throughput (every rank evaluates `steps`
-    independent replicas).  Used by the timed region and by tests/test_multirank.py."""
+def aggregate(t_local: float, steps: int, world: int, device=None, strong: bool = False):
+    """Max-over-ranks time and whole-job throughput.  strong: the ranks share each of the
+    `steps` evaluations (probe columns split across ranks, DESIGN.md §7) -> steps / time;
+    else every rank evaluates `steps` independent replicas -> world * steps / time.
+    Used by the timed region and by tests/test_multirank.py."""
     t_all = t_local
     if world > 1:
         import torch
@@ -113,7 +115,7 @@ def aggregate(t_local: float, steps: int, world: int, device=None):
         tt = torch.tensor([t_local], dtype=torch.float64, device=device)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_all = float(tt.item())
-    return t_all, world * steps / t_all
+    return t_all, (steps if strong else world * steps) / t_all
 
 
 def workload(cid: int, n: int | None):
@@ -123,47 +125,81 @@ def workload(cid: int, n: int | None):
     return c, n, points_for(c, n), w_for(c, n)
 
 
-def run_reference(args, rank):
-    """CPU oracle (O2: serial numpy RSF + weak peeling) on a bounded sample."""
-    if rank != 0:
-        return
+# O2 sample sizes of config 3's recipe (square grids: 24^2, 32^2, 40^2); the time of one l+g
+# evaluation is fitted as t = a n^b over the measured points (least squares in log-log) and
+# extrapolated to the workload's n with the FITTED exponent b (round 1 assumed the paper's 1.6)
+REF_SIZES = (576, 1024, 1600)
+
+
+def _o2_eval_seconds(args, c, n_s):
     from oracle.kernels import Kernel as OK
     from oracle.mle import rsf_mle_eval
     from workloads import philox_normal
-    c, n_full, _, _ = workload(args.config, args.n)
-    n_s = args.ref_n
-    c_s, _, xy, w = workload(args.config, n_s)
-    _, _, xy_w, w_w = workload(args.config, 576)   # warm-up steps: a 24 x 24 sample (code paths only)
+    _, _, xy, w = workload(args.config, n_s)
     ok = OK(c.family, c.rho, c.sigma2, c.nugget, c.alpha, c.theta)
-    # z = w (a valid observation vector for timing; the time does not depend on z)
-    times = []
-    for it in range(args.warmup + args.steps):
-        t = time.perf_counter()
-        if it < args.warmup:
-            rsf_mle_eval(ok, xy_w, w_w, c.eps_fact, c.eps_peel, c.leaf, c.seed, philox_normal, block=8)
-        else:
-            rsf_mle_eval(ok, xy, w, c.eps_fact, c.eps_peel, c.leaf, c.seed, philox_normal, block=8)
-        dt = time.perf_counter() - t
-        if it >= args.warmup:
-            times.append(dt)
-        if sum(times) > args.ref_budget:
-            break
-    t_s = float(np.mean(times))
-    # extrapolation to n_full by the paper's observed n^1.6 scaling of one evaluation (P:830)
-    t_full = t_s * (n_full / n_s) ** 1.6
+    t = time.perf_counter()
+    # z = w: a valid observation vector for timing (the time does not depend on z)
+    rsf_mle_eval(ok, xy, w, c.eps_fact, c.eps_peel, c.leaf, c.seed, philox_normal, block=8)
+    return time.perf_counter() - t
+
+
+def _fit_and_extrapolate(pts, n_full):
+    """pts: [(n, seconds)].  Least-squares fit of log t = log a + b log n."""
+    ns = np.log([p[0] for p in pts])
+    ts = np.log([p[1] for p in pts])
+    if len(set(p[0] for p in pts)) >= 2:
+        b, la = np.polyfit(ns, ts, 1)
+    else:
+        b, la = 1.6, float(np.mean(ts - 1.6 * ns))   # one size only: the paper's n^1.6 (P:830)
+    return float(math.exp(la) * n_full ** b), float(b)
+
+
+def _host_info():
+    info = {"cores": len(os.sched_getaffinity(0))}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            k, _, v = ln.partition(":")
+            if k.strip() in ("Model name", "Socket(s)", "Core(s) per socket", "Thread(s) per core"):
+                info[k.strip()] = v.strip()
+    except Exception:
+        pass
+    try:
+        import numpy.__config__  # noqa: F401
+        info["blas_threads"] = os.environ.get("OMP_NUM_THREADS", "all cores (unset)")
+    except Exception:
+        pass
+    return info
+
+
+def run_reference(args, rank):
+    """CPU oracle (O2: serial numpy RSF + weak peeling), rank 0 only: every step is one full
+    l+g evaluation of config 3's recipe at a sample size (cycling through REF_SIZES; warm-up
+    steps at the smallest), the points are fitted by a power law and extrapolated."""
+    if rank != 0:
+        return
+    c, n_full, _, _ = workload(args.config, args.n)
+    for _ in range(args.warmup):
+        _o2_eval_seconds(args, c, REF_SIZES[0])
+    pts = []
+    for it in range(args.steps):
+        n_s = REF_SIZES[it % len(REF_SIZES)]
+        pts.append((n_s, _o2_eval_seconds(args, c, n_s)))
+    t_full, b = _fit_and_extrapolate(pts, n_full)
     value = 1.0 / t_full
-    cores = len(os.sched_getaffinity(0))
+    host = _host_info()
+    meas = {str(n): float(np.median([t for m, t in pts if m == n])) for n in sorted(set(m for m, _ in pts))}
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": len(times), "warmup": args.warmup, "ms_per_step": t_full * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": _config_dict(c, n_full, args),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                         "sample": f"O2 oracle (numpy RSF + weak peeling) full l+g evaluation of config "
-                                   f"{c.cid}'s recipe at n={n_s}, mean {t_s:.2f} s over {len(times)} "
-                                   f"step(s) (warm-up steps on an n=576 sample); extrapolated to "
-                                   f"n={n_full} by the paper's n^1.6 (P:830)",
-                         "sample_seconds": t_s},
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_full * 1e3,
+        "higher_is_better": True, "scaling": "strong" if args.gpus > 1 else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic", "config": _config_dict(c, n_full, args),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": host["cores"], "kind": "oracle",
+                         "sample": f"O2 oracle (numpy/scipy RSF + weak peeling, all {host['cores']} host cores "
+                                   f"through the BLAS) full l+g evaluations of config {c.cid}'s recipe at "
+                                   f"n = {', '.join(meas)} (median seconds {meas}); fitted t ~ n^{b:.2f}; "
+                                   f"value = extrapolation to n = {n_full} with the fitted exponent",
+                         "measured_points": pts, "fitted_exponent": b, "host": host},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -178,22 +214,18 @@ def _config_dict(c, n, args):
 
 
 def cpu_baseline_sample(args, c):
-    """The oracle as it stands on a bounded sample (rank 0, N=1 only)."""
-    from oracle.kernels import Kernel as OK
-    from oracle.mle import rsf_mle_eval
-    from workloads import philox_normal
-    n_s = args.ref_n
-    _, _, xy, w = workload(args.config, n_s)
-    ok = OK(c.family, c.rho, c.sigma2, c.nugget, c.alpha, c.theta)
-    t = time.perf_counter()
-    rsf_mle_eval(ok, xy, w, c.eps_fact, c.eps_peel, c.leaf, c.seed, philox_normal, block=8)
-    t_s = time.perf_counter() - t
+    """The oracle as it stands on a bounded sample (rank 0, N=1 only): one O2 evaluation at
+    each of REF_SIZES (about 20 s of CPU work), power-law fit, labeled extrapolation."""
+    pts = [(n_s, _o2_eval_seconds(args, c, n_s)) for n_s in REF_SIZES]
     n_full = args.n or c.n
-    t_full = t_s * (n_full / n_s) ** 1.6
-    return {"value": 1.0 / t_full, "unit": UNIT, "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
-            "sample": f"O2 oracle (numpy RSF + weak peeling) one full l+g evaluation of config {c.cid}'s "
-                      f"recipe at n={n_s} took {t_s:.2f} s; extrapolated to n={n_full} by the paper's "
-                      f"n^1.6 (P:830)", "sample_seconds": t_s}
+    t_full, b = _fit_and_extrapolate(pts, n_full)
+    host = _host_info()
+    return {"value": 1.0 / t_full, "unit": UNIT, "cores": host["cores"], "kind": "oracle",
+            "sample": f"O2 oracle (numpy/scipy RSF + weak peeling) one full l+g evaluation of config {c.cid}'s "
+                      f"recipe at each n in {list(REF_SIZES)}: {[round(t, 2) for _, t in pts]} s; fitted "
+                      f"t ~ n^{b:.2f}; value = extrapolation to n = {n_full} with the fitted exponent "
+                      f"(profiles/ has the 1-thread / all-core study at larger n)",
+            "measured_points": pts, "fitted_exponent": b, "host": host}
 
 
 # ncu --set full of the longest launch of the dominant kernel (profiles/r01_gemm_pipe_ncu_v4.txt)
@@ -248,10 +280,21 @@ def main():
     opts = R.Opts(eps_peel=c.eps_peel, seed=c.seed + 1000 * rank)
     xy = torch.from_numpy(xy_h).to(dev)
     w = torch.from_numpy(w_h).to(dev)
-    # z = F^{1/2} w through the CUDA path (input recipe R-V), before timing
-    F = R.Factor(ctx, xy, K, c.eps_fact, c.leaf, opts=opts)
-    z = F.sample(w)
-    F.close()
+    # z (reading R-V): config 3's frozen bytes (O2 oracle F^{1/2} w, SHA-256 checked); configs
+    # without frozen bytes sample z = F^{1/2} w through the CUDA path before timing (labeled)
+    try:
+        from workloads import frozen_z
+        z_h = frozen_z(c.cid) if args.n in (None, c.n) else None
+        z_src = "frozen (workloads/data, O2 F^{1/2} w, sha256-checked)" if z_h is not None else None
+    except (FileNotFoundError, KeyError):
+        z_h = None
+    if z_h is not None:
+        z = torch.from_numpy(z_h).to(dev)
+    else:
+        F = R.Factor(ctx, xy, K, c.eps_fact, c.leaf, opts=opts)
+        z = F.sample(w)
+        F.close()
+        z_src = "F^{1/2} w from the CUDA factor before timing (not frozen)"
     torch.cuda.synchronize()
 
     def step(xyb, zb):
@@ -267,9 +310,7 @@ def main():
     fp64_peak = R.lib.rsf_debug_fp64_peak(1, 3)
     fp64_peak_dfma = R.lib.rsf_debug_fp64_peak(0, 3)
 
-    # ---- timed region: device-resident inputs
-    R.lib.rsf_stats_reset()
-    R.lib.rsf_stats_enable(1)
+    # ---- timed region: device-resident inputs, no instrumentation
     clk = ClockSampler(local)
     clk.start()
     l0 = R.kernel_launches()
@@ -288,17 +329,27 @@ def main():
     wall = time.perf_counter() - t0
     barrier()
     clocks = clk.stop()
-    R.lib.rsf_stats_enable(0)
     launches = R.kernel_launches() - l0
-    st = (R.C if hasattr(R, "C") else __import__("ctypes")).c_double * 4
-    stats = st()
-    R.lib.rsf_stats_get(stats)
     # the library synchronises its own stream at the end of every evaluation, so the
     # wall time brackets exactly the device work; torch events on the default stream
     # see only the torch part, hence max(device-synchronised wall, event time)
     ev_ms = e0.elapsed_time(e1)
     t_local = max(wall, ev_ms / 1e3)
-    t_all, value = aggregate(t_local, args.steps, world, dev)
+    t_all, value = aggregate(t_local, args.steps, world, dev, strong=world > 1)
+
+    # ---- one more step with the GEMM statistics on (events around every batched-GEMM launch,
+    # on its own stream): the roofline numbers, kept out of the timed steps above
+    R.lib.rsf_stats_reset()
+    R.lib.rsf_stats_enable(1)
+    torch.cuda.synchronize()
+    ts0 = time.perf_counter()
+    step(xy, z)
+    torch.cuda.synchronize()
+    t_stat = time.perf_counter() - ts0
+    R.lib.rsf_stats_enable(0)
+    st = (R.C if hasattr(R, "C") else __import__("ctypes")).c_double * 4
+    stats = st()
+    R.lib.rsf_stats_get(stats)
 
     # ---- e2e: same metric through the C ABI with pinned HOST buffers (H2D inside the call)
     xy_p = torch.from_numpy(xy_h).pin_memory()
@@ -310,7 +361,7 @@ def main():
     for _ in range(e2e_steps):
         step(xy_p, z_p)
     torch.cuda.synchronize()
-    te, e2e_value = aggregate(time.perf_counter() - t0, e2e_steps, world, dev)
+    te, e2e_value = aggregate(time.perf_counter() - t0, e2e_steps, world, dev, strong=world > 1)
     e2e = {"value": e2e_value, "unit": UNIT,
            "h2d_bytes_per_step": int(xy_h.nbytes + z_p.numel() * 8),
            "d2h_bytes_per_step": int(8 * (1 + len(c.theta)))}
@@ -338,7 +389,9 @@ def main():
                 "timing": "CUDA events around every launch on its stream; kernel_seconds = length of the "
                           "union of the launch intervals (the trace jobs run on concurrent streams, so "
                           "summed durations would double-count overlap)",
-                "share_of_step": gsec / (t_local) if t_local > 0 else None,
+                "share_of_step": gsec / t_stat if t_stat > 0 else None,
+                "stats_pass": "one extra evaluation after the timed steps with rsf_stats_enable(1) "
+                              f"({t_stat:.2f} s); the timed steps ran uninstrumented",
                 "algorithmic_flops_per_launch": gfl / gl if gl else None}
     fl_factor = d.flops_factor
     line = {
@@ -350,7 +403,7 @@ def main():
         "rsf_factor_tflops": fl_factor / max(d.t_factor + d.t_compress, 1e-9) / 1e12,
         "phases_s": {"tree": d.t_tree, "factor": d.t_factor, "compress": d.t_compress,
                      "solve": d.t_solve, "peel": d.t_peel, "total": d.t_total},
-        "ell": r.ell, "grad": r.grad,
+        "ell": r.ell, "grad": r.grad, "z": z_src,
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_sample(args, c)

@@ -81,8 +81,15 @@ def dk_dalpha(family: str, r, rho: float, alpha: float = 1.0):
         raise ValueError("alpha is a parameter of the rational-quadratic family only")
     r = np.asarray(r, dtype=np.float64)
     u = r * r / (2.0 * rho * rho)
-    k = np.exp(-alpha * np.log1p(u / alpha))
-    return k * (u / (alpha + u) - np.log1p(u / alpha))
+    x = u / alpha
+    k = np.exp(-alpha * np.log1p(x))
+    # the bracket u/(alpha+u) - log1p(u/alpha) = x/(1+x) - log1p(x) cancels for small x; its
+    # Taylor series is  sum_{j>=2} (-1)^(j+1) (j-1)/j x^j
+    #   = -x^2/2 + 2x^3/3 - 3x^4/4 + ...,  used for x < 1e-3 (5 terms: truncation < 1e-18 x^2)
+    series = x * x * (-0.5 + x * (2.0 / 3.0 + x * (-0.75 + x * (0.8 + x * (-5.0 / 6.0)))))
+    with np.errstate(invalid="ignore"):
+        direct = x / (1.0 + x) - np.log1p(x)
+    return k * np.where(x < 1e-3, series, direct)
 
 
 class Kernel:

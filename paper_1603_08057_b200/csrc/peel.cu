@@ -504,8 +504,15 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
   pd.rank_max.assign(L + 1, 0);
   int prev_rank = -1;
   const int kb = std::max(16, o.probe_block);
-  const double budget = 16.0 * (1ull << 30);   // bytes of transient per-batch buffers
-  const double wcache_budget = 8.0 * (1ull << 30);   // W_i^T kept for a whole probe group
+  // bytes of transient per-batch buffers, and of W_i^T kept for a whole probe group (else the
+  // probes are regenerated per batch).  RSF_PEEL_BUDGET_MB / RSF_PEEL_WCACHE_MB shrink them
+  // (tests force the batch-split and regeneration paths at small sizes).
+  auto env_mb = [](const char* k, double d) {
+    const char* v = getenv(k);
+    return (v && atof(v) >= 0) ? atof(v) * (1 << 20) : d;
+  };
+  const double budget = env_mb("RSF_PEEL_BUDGET_MB", 16.0 * (1ull << 30));
+  const double wcache_budget = env_mb("RSF_PEEL_WCACHE_MB", 8.0 * (1ull << 30));
 
   struct SparseSub { std::vector<GemmBatch> g1, g3; std::vector<char> has1, has3; };
   auto residual = [&](const double* W, double* Y, int k, int upto, const SparseSub* sp) {

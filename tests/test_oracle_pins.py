@@ -16,8 +16,9 @@ from oracle.kernels import Kernel, k_of_r
 from oracle.mle import rsf_mle_eval
 from oracle.peel import peel_trace
 from oracle.rsf import RSF, interp_decomp, proxy_points
+from oracle.separable import SeparableSE
 from oracle.tree import QuadTree
-from workloads import config, philox4x32, philox_normal, points_for, w_for
+from workloads import config, philox4x32, philox_normal, points_for, separable_axes, w_for
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 LOG2PI = math.log(2 * math.pi)
@@ -198,46 +199,66 @@ def _separable_case(ma=24, mb=20, rho=0.15, sigma2=1.2, tau=0.05, seed=8):
     r = _rng(seed)
     a = np.sort(r.random(ma))
     b = np.sort(r.random(mb))
-    xy = np.array([(x, y) for x in a for y in b])           # index = i*mb + j
-    K = Kernel("sqexp", rho, sigma2=sigma2, nugget=tau, theta=("rho",))
-    Ka = np.exp(-(a[:, None] - a[None]) ** 2 / (2 * rho ** 2))
-    Kb = np.exp(-(b[:, None] - b[None]) ** 2 / (2 * rho ** 2))
-    Kap = Ka * (a[:, None] - a[None]) ** 2 / rho ** 3
-    Kbp = Kb * (b[:, None] - b[None]) ** 2 / rho ** 3
-    la, Qa = np.linalg.eigh(Ka)
-    lb, Qb = np.linalg.eigh(Kb)
-    lap = np.einsum("ij,ik,kj->j", Qa, Kap, Qa)
-    lbp = np.einsum("ij,ik,kj->j", Qb, Kbp, Qb)
-    ev = sigma2 * np.outer(la, lb) + tau
-    logdet = float(np.sum(np.log(ev)))
-    tr = float(np.sum(sigma2 * (np.outer(lap, lb) + np.outer(la, lbp)) / ev))
+    S = SeparableSE(a, b, rho, sigma2, tau)
+    K = Kernel("sqexp", rho, sigma2=sigma2, nugget=tau, theta=("rho", "sigma2", "nugget"))
     z = r.standard_normal(ma * mb)
-    zh = Qa.T @ z.reshape(ma, mb) @ Qb
-    quad = float(np.sum(zh ** 2 / ev))
-    return K, xy, z, logdet, tr, quad
+    return S, K, S.points(), z
 
 
 def test_P7_separable_closed_form_dense():
-    K, xy, z, logdet, tr, quad = _separable_case()
+    """oracle/separable.py (Kronecker eigen closed forms) against O1 (dense Cholesky, explicit
+    inverse): every part of l and g for rho, sigma2 and the nugget."""
+    S, K, xy, z = _separable_case()
     d = dense_eval(K, xy, z)
-    assert d["logdet"] == pytest.approx(logdet, rel=1e-12)
-    assert d["trace"][0] == pytest.approx(tr, rel=1e-10)
-    assert d["quad"] == pytest.approx(quad, rel=1e-10)
+    c = S.eval(z, K.theta)
+    assert c["logdet"] == pytest.approx(d["logdet"], rel=1e-12)
+    assert c["quad"] == pytest.approx(d["quad"], rel=1e-10)
+    assert c["ell"] == pytest.approx(d["ell"], rel=1e-11)
+    np.testing.assert_allclose(c["trace"], d["trace"], rtol=1e-10)
+    np.testing.assert_allclose(c["q"], d["q"], rtol=1e-10)
+    np.testing.assert_allclose(c["grad"], d["grad"], rtol=1e-9)
+    assert c["trace_inv"] == pytest.approx(d["trace_inv"], rel=1e-10)
+    # Sigma from the closed form's matvec equals the dense matrix
+    sig = dense_sigma(K, xy)
+    x = _rng(3).standard_normal(len(xy))
+    np.testing.assert_allclose(S.matvec(x), sig @ x, rtol=1e-12, atol=1e-12)
+
+
+def test_P7_separable_sample_has_covariance_sigma():
+    """sample(w) = A w with A A^T = Sigma: A^T Sigma^-1 A = I tested on random w, and
+    the sample's dense quadratic form z^T Sigma^-1 z = w^T w (O1 Cholesky)."""
+    S, K, xy, _ = _separable_case(ma=12, mb=10)
+    w = _rng(5).standard_normal(S.n)
+    z = S.sample(w)
+    d = dense_eval(K, xy, z)
+    assert d["quad"] == pytest.approx(float(w @ w), rel=1e-10)
+    A = np.stack([S.sample(e) for e in np.eye(S.n)], axis=1)
+    np.testing.assert_allclose(A @ A.T, dense_sigma(K, xy), rtol=1e-10, atol=1e-12)
 
 
 def test_P7_separable_closed_form_rsf_and_peel():
-    K, xy, z, logdet, tr, quad = _separable_case(ma=40, mb=36)
+    S, K, xy, z = _separable_case(ma=40, mb=36)
+    K = Kernel("sqexp", S.rho, sigma2=S.sigma2, nugget=S.tau, theta=("rho",))
     F = RSF(K, xy, 1e-11, 32)
     assert F.tree.L >= 2
-    assert F.logdet == pytest.approx(logdet, rel=1e-9)
-    assert float(z @ F.solve(z)) == pytest.approx(quad, rel=1e-6)
+    assert F.logdet == pytest.approx(S.logdet(), rel=1e-9)
+    assert float(z @ F.solve(z)) == pytest.approx(float(z @ S.solve(z)), rel=1e-6)
     Fi = RSF(K, xy, 1e-11, 32, which="rho")
 
     def G(X):
         return 0.5 * (F.solve(Fi.apply(X)) + Fi.apply(F.solve(X)))
     from oracle.mle import make_probe
     t = peel_trace(G, F.tree, 1e-8, make_probe(11, 0, philox_normal), block=16)
-    assert t == pytest.approx(tr, rel=1e-6)
+    assert t == pytest.approx(S.trace("rho"), rel=1e-6)
+
+
+def test_separable_axes_recipe():
+    a, b = separable_axes(64)
+    g = (np.arange(64) + 0.5) / 64
+    assert np.all(np.abs(a - g) <= 0.4 / 64 + 1e-15) and np.all(np.abs(b - g) <= 0.4 / 64 + 1e-15)
+    assert np.all(np.diff(a) > 0) and np.all(np.diff(b) > 0) and not np.allclose(a, b)
+    a2, _ = separable_axes(64)
+    np.testing.assert_array_equal(a, a2)
 
 
 # ------------------------------------------------------------------ P8, P9, P10
@@ -433,6 +454,35 @@ def test_P14_score_has_mean_zero_and_fisher_variance():
     sd = dense_eval(K, xy, np.zeros(n), fisher=True)["fisher_sd"][0]
     assert abs(gs.mean()) < 3 * sd / math.sqrt(len(gs))
     assert 0.75 < gs.std() / sd < 1.25
+
+
+def test_dk_dalpha_small_u_series_matches_exact_bracket():
+    """The small-u branch of d k / d alpha (series) against the bracket evaluated in exact
+    rational arithmetic: x/(1+x) - log1p(x) from 40 terms of the alternating series with
+    Fraction, at points on both sides of the x = 1e-3 switch."""
+    from oracle.kernels import dk_dalpha
+    rho, alpha = 0.1, 1.5
+    for x in (1e-9, 3e-6, 2e-4, 9.9e-4, 1.1e-3, 5e-3):
+        u = x * alpha
+        r = math.sqrt(2.0 * rho * rho * u)
+        xf = Fraction(r * r) / Fraction(2.0 * rho * rho) / Fraction(alpha)
+        br = sum(Fraction((-1) ** (j + 1) * (j - 1), j) * xf ** j for j in range(2, 40))
+        exact = float(br) * float(k_of_r("rq", r, rho, alpha))
+        assert float(dk_dalpha("rq", r, rho, alpha)) == pytest.approx(exact, rel=1e-10, abs=1e-300)
+
+
+def test_O2_sigma2_nugget_branch_matches_O1():
+    """O2's reading-R-G branch (oracle/mle.py: t_sigma2 = (n - tau Tr F^-1)/sigma2,
+    q_sigma2 = (q0 - tau u^T u)/sigma2, nugget: G = F^-1, q = u^T u) against O1, which forms
+    Sigma_sigma2 = k and Sigma_tau = I explicitly."""
+    xy = _uniform(400, 31)
+    K = Kernel("matern32", 0.15, sigma2=1.3, nugget=0.02, theta=("rho", "sigma2", "nugget"))
+    z = dense_sample(K, xy, _rng(32).standard_normal(400))
+    d = dense_eval(K, xy, z)
+    o = rsf_mle_eval(K, xy, z, 1e-12, 1e-9, 32, 77, philox_normal, block=16)
+    np.testing.assert_allclose(o["trace"], d["trace"], rtol=1e-7)
+    np.testing.assert_allclose(o["q"], d["q"], rtol=1e-8)
+    np.testing.assert_allclose(o["grad"], d["grad"], rtol=1e-5)
 
 
 # ------------------------------------------------------------------ O2 vs O1 (config 1)

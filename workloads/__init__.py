@@ -23,7 +23,8 @@ import numpy as np
 
 __all__ = [
     "philox4x32", "philox_uniform_pair", "philox_normal_pair", "philox_normal", "philox_rademacher",
-    "CONFIGS", "Config", "points_for", "w_for", "config", "paper_grid_points",
+    "CONFIGS", "Config", "points_for", "w_for", "config", "paper_grid_points", "frozen_z", "DATA_DIR",
+    "separable_axes", "SEED_SEPARABLE",
 ]
 
 _M0 = np.uint64(0xD2511F53)
@@ -196,6 +197,21 @@ def paper_grid_points(m: int) -> np.ndarray:
     return np.stack([np.repeat(g, m), np.tile(g, m)], axis=1)
 
 
+SEED_SEPARABLE = SEED_BASE + 7   # the P7 separable surrogate (R-W numbering: configs use 1..5)
+
+
+def separable_axes(m: int, seed: int = SEED_SEPARABLE):
+    """Axis coordinates of the P7 tensor-grid surrogate at config 3's size and density:
+    a_i = (i + 1/2 + 0.8 (u_i - 1/2)) / m (the +-0.4-cell jitter of R-T, applied per axis so
+    that the grid stays a tensor product), u from Philox stream 0, counters (i, 1, 0, 0) for
+    a and (i, 2, 0, 0) for b.  Point (i, j) of the grid is (a_i, b_j), index i * m + j."""
+    i = np.arange(m, dtype=np.uint64)
+    ua, _ = philox_uniform_pair(i, 1, 0, 0, seed, STREAM_POINTS)
+    ub, _ = philox_uniform_pair(i, 2, 0, 0, seed, STREAM_POINTS)
+    g = np.arange(m, dtype=np.float64) + 0.5
+    return (g + 0.8 * (ua - 0.5)) / m, (g + 0.8 * (ub - 0.5)) / m
+
+
 def points_for(cfg: Config, n: int | None = None) -> np.ndarray:
     """n x 2 float64 coordinates in [0,1)^2 (row-major), deterministic."""
     n = cfg.n if n is None else n
@@ -219,3 +235,24 @@ def w_for(cfg: Config, n: int | None = None, stream: int = STREAM_W) -> np.ndarr
     w[0::2] = n0
     w[1::2] = n1
     return w[:n].copy()
+
+
+DATA_DIR = __import__("os").path.join(__import__("os").path.dirname(__import__("os").path.abspath(__file__)), "data")
+
+
+def frozen_z(cid: int) -> np.ndarray:
+    """The frozen observation vector of config `cid` (reading R-V): bytes written once by
+    tools/make_frozen_z.py from the O2 oracle, verified against the SHA-256 in
+    data/MANIFEST.json.  Raises if the file is missing or its hash does not match."""
+    import hashlib
+    import json
+    import os
+    man = json.load(open(os.path.join(DATA_DIR, "MANIFEST.json")))[str(cid)]
+    raw = open(os.path.join(DATA_DIR, man["file"]), "rb").read()
+    h = hashlib.sha256(raw).hexdigest()
+    if h != man["sha256"]:
+        raise ValueError(f"frozen z of config {cid}: sha256 {h} != manifest {man['sha256']}")
+    z = np.frombuffer(raw, dtype="<f8").astype(np.float64)
+    if z.size != man["n"]:
+        raise ValueError(f"frozen z of config {cid}: {z.size} values, manifest says {man['n']}")
+    return z
