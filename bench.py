@@ -7,11 +7,13 @@
 A "step" is one full evaluation of Alg. 1 -- quadtree, RSF of
 Sigma, compression of each Sigma_i, solve, and the peeled traces -- at the
 largest BASELINE.json workload that fits one B200 (config 3: n = 262,144
-jittered-grid points, rational quadratic, theta = (rho, alpha)); the metric's
-own config 4 (n = 2^20, "8-GPU subdomain sharding") exceeds one GPU's memory
-(DESIGN.md §7).  Inputs are resident in HBM.  Multi-GPU (torchrun): every rank
-evaluates its own independent replica ("replicas"), the time is
-the max over ranks, value = evaluations of all ranks / time.
+jittered-grid points, rational quadratic, theta = (rho, alpha), z frozen from
+the O2 oracle); the metric's own config 4 (n = 2^20) exceeds one GPU's memory
+with replicated peeling bases.  Inputs are resident in HBM.
+Multi-GPU (torchrun): the ranks form one NCCL group and share every evaluation
+(factor replicated, peeling probe columns split, one all-gather per probe
+block) -- strong scaling, time = max over ranks, value =
+evaluations / time.
 
 --impl reference times the CPU oracle (oracle/, the only other place bench.py
 runs it) on rank 0 on a bounded sample of the same workload.
@@ -209,7 +211,9 @@ def _config_dict(c, n, args):
     return {"workload": f"config{c.cid}: n={n} {c.points} points, {c.family}, rho={c.rho}, "
                         f"nugget={c.nugget}, theta={list(c.theta)}, leaf={c.leaf}",
             "n": n, "eps": c.eps, "eps_fact": c.eps_fact, "eps_peel": c.eps_peel, "leaf": c.leaf,
-            "theta": list(c.theta), "parallelism": f"replicas x{args.gpus}",
+            "theta": list(c.theta),
+            "parallelism": (f"sharded x{args.gpus}: factor replicated, peeling probe columns split, NCCL "
+                            "all-gather per probe block" if args.gpus > 1 else "1 GPU"),
             "l2": "working set (factor + probe blocks, GBs) >> 126 MB L2; no flush"}
 
 
@@ -275,9 +279,11 @@ def main():
             dist.barrier()
 
     c, n, xy_h, w_h = workload(args.config, args.n)
-    ctx = R.Context(local)
+    # N > 1: ONE evaluation shared by the group (probe columns split, NCCL all-gather per
+    # probe block) -- strong scaling, the same inputs and seed on every rank
+    ctx = R.Context.from_process_group(local) if world > 1 else R.Context(local)
     K = R.Kernel(c.family, c.rho, c.sigma2, c.nugget, c.alpha, c.theta)
-    opts = R.Opts(eps_peel=c.eps_peel, seed=c.seed + 1000 * rank)
+    opts = R.Opts(eps_peel=c.eps_peel, seed=c.seed)
     xy = torch.from_numpy(xy_h).to(dev)
     w = torch.from_numpy(w_h).to(dev)
     # z (reading R-V): config 3's frozen bytes (O2 oracle F^{1/2} w, SHA-256 checked); configs
@@ -397,7 +403,7 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * t_all / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": _config_dict(c, n, args), "clocks": clocks, "gpu_launches": int(launches),
         "e2e": e2e, "roofline": roofline,
         "rsf_factor_tflops": fl_factor / max(d.t_factor + d.t_compress, 1e-9) / 1e12,

@@ -125,9 +125,26 @@ typedef struct {
 
 void rsf_opts_default(rsf_opts* out);
 
-/* context on CUDA device `device`; cuda_stream may be NULL (library creates a stream);
- * nccl_comm is reserved (NULL = single GPU). */
+/* context on CUDA device `device`; cuda_stream may be NULL (library creates a stream).
+ * nccl_comm: NULL = single GPU, else an ncclComm_t of the caller (not owned): this context is
+ * one rank of a group that shares every gp_mle_eval / peel_trace call (DESIGN.md §7 -- the
+ * peeling probe columns of each block are split across the ranks, and exchanged
+ * with one NCCL all-gather per block; every rank passes the same inputs and receives the
+ * same results).  Returns RSF_ENCCL when NCCL cannot be loaded or queried. */
 rsf_status rsf_ctx_create(int device, void* cuda_stream, void* nccl_comm, rsf_ctx* out);
+/* NCCL bootstrap of a rank group without a caller communicator (one process per GPU):
+ * rank 0 calls rsf_nccl_unique_id (out: 128 bytes, host), the caller distributes the bytes
+ * (e.g. torch.distributed broadcast), then every rank calls rsf_ctx_create_group with its
+ * rank in [0, world).  The context owns the communicator.  world = 1 needs no id traffic
+ * (any 128 bytes).  RSF_EINVAL on bad ranks, RSF_ENCCL on NCCL failures. */
+rsf_status rsf_nccl_unique_id(unsigned char* out);
+rsf_status rsf_ctx_create_group(int device, void* cuda_stream, const unsigned char* id, int rank, int world,
+                                rsf_ctx* out);
+/* rank and group size of a context (0 and 1 for a single-GPU context) */
+rsf_status rsf_ctx_group(rsf_ctx ctx, int* rank, int* world);
+/* column slice [lo, hi) that part `part` of `parts` owns when k probe columns are split
+ * (contiguous; sizes differ by at most one, larger first).  Host only (tests). */
+void rsf_debug_col_slice(int64_t k, int parts, int part, int64_t* lo, int64_t* hi);
 void rsf_ctx_destroy(rsf_ctx ctx);
 /* Order the context after the caller: everything enqueued on `stream` so far (an event recorded
  * there) completes before the context stream runs further work.  stream = NULL is the legacy
@@ -162,7 +179,10 @@ rsf_status peel_trace(rsf_fact F, rsf_fact Fi, double eps_peel, const rsf_opts* 
  * Fi == NULL estimates Tr(F^-1).  One solve and one apply per probe.  trace, std_err: host. */
 rsf_status hutch_trace(rsf_fact F, rsf_fact Fi, int64_t nprobe, uint64_t seed, double* trace, double* std_err);
 
-/* Alg. 1: l-hat and g-hat at theta = kernel values.  eps is the ID tolerance of every
+/* Alg. 1: l-hat and g-hat at theta = kernel values.  On a rank group (rsf_ctx_create
+ * with a communicator, rsf_ctx_create_group) every rank calls it with the same arguments; the
+ * factorizations are replicated (deterministic), the peeling columns are split, and every rank
+ * returns the same l and g.  eps is the ID tolerance of every
  * factorization (eps_fact), opts->eps_peel the peeling tolerance.  ell: host scalar; grad: host
  * array of p doubles.  xy, z device or host.  diag nullable.  The independent trace jobs (one per
  * theta component) run concurrently on streams the context creates on first use and

@@ -15,7 +15,7 @@ from . import _lib
 from ._lib import FAMILY, PARAM, rsf_eval_diag, rsf_fact_diag, rsf_kernel, rsf_opts, rsf_peel_diag
 
 __all__ = ["Context", "Kernel", "Opts", "Factor", "peel_trace", "gp_mle_eval", "RsfError", "lib",
-           "kernel_launches"]
+           "kernel_launches", "nccl_unique_id", "col_slice"]
 
 lib = _lib.load()
 
@@ -103,14 +103,58 @@ class Opts:
         return o
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id for rsf_ctx_create_group (rank 0 calls it, then distributes it)."""
+    buf = (C.c_ubyte * 128)()
+    _check(lib.rsf_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def col_slice(k: int, parts: int, part: int):
+    """[lo, hi) of the probe columns part `part` of `parts` owns (include/rsf.h)."""
+    lo, hi = C.c_int64(), C.c_int64()
+    lib.rsf_debug_col_slice(k, parts, part, C.byref(lo), C.byref(hi))
+    return lo.value, hi.value
+
+
+def group_id_from_process_group():
+    """(id_bytes, rank, world) for Context(group=...): rank 0 draws the NCCL unique id and the
+    default torch.distributed group broadcasts it (any backend; plumbing only)."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(), dist.get_world_size()
+    obj = [nccl_unique_id() if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(obj, src=0)
+    return obj[0], rank, world
+
+
 class Context:
-    def __init__(self, device: int = 0, stream=None):
+    """rsf_ctx.  group=(id_bytes, rank, world): one rank of a sharded group (NCCL, DESIGN.md §7);
+    nccl_comm: an existing ncclComm_t address of the caller instead."""
+
+    def __init__(self, device: int = 0, stream=None, group=None, nccl_comm=None):
         h = C.c_void_p()
         s = None
         if stream is not None:
             s = C.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
-        _check(lib.rsf_ctx_create(device, s, None, C.byref(h)))
+        if group is not None:
+            uid, rank, world = group
+            buf = (C.c_ubyte * 128).from_buffer_copy(bytes(uid))
+            _check(lib.rsf_ctx_create_group(device, s, buf, int(rank), int(world), C.byref(h)))
+        else:
+            _check(lib.rsf_ctx_create(device, s, C.c_void_p(nccl_comm) if nccl_comm else None, C.byref(h)))
         self.h = h
+
+    @classmethod
+    def from_process_group(cls, device: int, stream=None):
+        """Collective over the default torch.distributed group (plumbing only): rank 0 draws
+        the NCCL id, torch.distributed broadcasts it, every rank joins the group."""
+        return cls(device, stream, group=group_id_from_process_group())
+
+    def group(self):
+        r, w = C.c_int(), C.c_int()
+        _check(lib.rsf_ctx_group(self.h, C.byref(r), C.byref(w)))
+        return r.value, w.value
 
     def close(self):
         if self.h:

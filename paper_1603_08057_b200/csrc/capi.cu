@@ -158,7 +158,15 @@ rsf_status rsf_ctx_create(int device, void* cuda_stream, void* nccl_comm, rsf_ct
     RSF_CUDA(cudaSetDevice(device));
     auto* c = new rsf_ctx_s;
     c->ctx.device = device;
-    c->ctx.nccl = nccl_comm;
+    if (nccl_comm) {   // the caller's communicator: this context is one rank of a sharded group
+      try {
+        c->ctx.comm.nccl = nccl_comm;
+        rsf::nccl_query(nccl_comm, &c->ctx.comm.rank, &c->ctx.comm.world);
+      } catch (...) {
+        delete c;
+        throw;
+      }
+    }
     if (cuda_stream) {
       c->ctx.stream = (cudaStream_t)cuda_stream;
     } else {
@@ -187,7 +195,56 @@ void rsf_ctx_destroy(rsf_ctx ctx) {
   cudaStreamSynchronize(ctx->ctx.stream);
   if (ctx->ctx.own_stream) cudaStreamDestroy(ctx->ctx.stream);
   rsf::ring_trim();
+  for (auto& jc : ctx->ctx.job_comms)
+    if (jc.owned) rsf::nccl_destroy(jc.nccl);
+  if (ctx->ctx.comm.owned) rsf::nccl_destroy(ctx->ctx.comm.nccl);
   delete ctx;
+}
+
+rsf_status rsf_nccl_unique_id(unsigned char* out) {
+  return guard([&] {
+    RSF_REQUIRE(out != nullptr, rsf::ST_EINVAL, "out is NULL");
+    rsf::nccl_unique_id(out);
+  });
+}
+
+rsf_status rsf_ctx_create_group(int device, void* cuda_stream, const unsigned char* id, int rank, int world,
+                                rsf_ctx* out) {
+  return guard([&] {
+    RSF_REQUIRE(out != nullptr && id != nullptr, rsf::ST_EINVAL, "null argument");
+    RSF_REQUIRE(world >= 1 && rank >= 0 && rank < world, rsf::ST_EINVAL, "rank / world out of range");
+    rsf_ctx c = nullptr;
+    const rsf_status st = rsf_ctx_create(device, cuda_stream, nullptr, &c);
+    if (st != RSF_OK) throw rsf::Error(st, g_err);
+    if (world > 1) {
+      try {
+        RSF_CUDA(cudaSetDevice(device));
+        c->ctx.comm.nccl = rsf::nccl_init_rank(id, rank, world);
+        c->ctx.comm.owned = true;
+        c->ctx.comm.rank = rank;
+        c->ctx.comm.world = world;
+      } catch (...) {
+        rsf_ctx_destroy(c);
+        throw;
+      }
+    }
+    *out = c;
+  });
+}
+
+rsf_status rsf_ctx_group(rsf_ctx ctx, int* rank, int* world) {
+  return guard([&] {
+    RSF_REQUIRE(ctx && rank && world, rsf::ST_EINVAL, "null argument");
+    *rank = ctx->ctx.comm.rank;
+    *world = ctx->ctx.comm.world;
+  });
+}
+
+void rsf_debug_col_slice(int64_t k, int parts, int part, int64_t* lo, int64_t* hi) {
+  long long a = 0, b = 0;
+  if (parts >= 1 && part >= 0 && part < parts && k >= 0) rsf::Comm::slice(k, parts, part, &a, &b);
+  *lo = a;
+  *hi = b;
 }
 
 rsf_status rsf_ctx_wait_stream(rsf_ctx ctx, void* stream) {

@@ -487,9 +487,15 @@ double ddot(cudaStream_t s, const double* a, const double* b, long long n) {
   return r;
 }
 
-double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag* diag) {
+double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag* diag, const Comm* comm) {
   const double t0 = now_s();
   cudaStream_t s = op_stream(F);
+  Comm cm = comm ? *comm : F.ctx->comm;
+  if (cm.world == 1) {   // one-process emulation of a rank group (tests; comm.cuh)
+    const char* e = getenv("RSF_EMU_WORLD");
+    cm.emu = e ? std::max(1, atoi(e)) : 1;
+  }
+  const int NP = cm.parts();
   const Tree& t = *F.tree;
   const int n = t.n, L = t.L;
   const unsigned long long seed = o.seed;
@@ -694,13 +700,32 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
         std::vector<DBuf<int>> g1keep;
         const SparseSub g1sp = sparse_g1(hq, g, lev, g1keep);
         // equal chunks of <= kb columns (multiple of 8) instead of kb-wide chunks plus a thin tail
-        const int nch = (c + kb - 1) / kb;
-        const int kc = std::min(kb, ((c + nch - 1) / nch + 7) / 8 * 8);
-        DBuf<double> W((size_t)n * kc, s), Y((size_t)n * kc, s);
+        // (sharded: every rank owns a 1/NP slice of each chunk, so chunks are NP times wider)
+        // (capped so that the chunk and its gather buffer stay within 16 GB)
+        const int kbp = std::max(kb, std::min(kb * NP, (int)std::min<long long>(1 << 20, (16ll << 30) / (16ll * n))));
+        const int nch = (c + kbp - 1) / kbp;
+        const int kc = std::min(kbp, ((c + nch - 1) / nch + 7) / 8 * 8);
+        const long long slot = (long long)cm.kmax(kc) * n;
+        DBuf<double> W(NP > 1 ? (size_t)slot : (size_t)n * kc, s), Y((size_t)n * kc, s);
+        DBuf<double> gath(NP > 1 ? (size_t)slot * NP : 0, s);
         for (int c0 = 0; c0 < c; c0 += kc) {
           const int k = std::min(kc, c - c0);
-          gen_probes(s, W.p, k, n, t.d_perm.p, qmap.p, g, c0, lev, trace_id, seed);
-          residual(W.p, Y.p, k, lev, &g1sp);
+          if (NP == 1) {
+            gen_probes(s, W.p, k, n, t.d_perm.p, qmap.p, g, c0, lev, trace_id, seed);
+            residual(W.p, Y.p, k, lev, &g1sp);
+          } else {
+            // this rank's (or every emulated rank's) column slice, then one exchange per chunk
+            RSF_PHASE("p.exchange", s);
+            for (int r = cm.p0(); r < cm.p1(); ++r) {
+              long long lo, hi;
+              Comm::slice(k, NP, r, &lo, &hi);
+              if (hi == lo) continue;
+              gen_probes(s, W.p, (int)(hi - lo), n, t.d_perm.p, qmap.p, g, c0 + (int)lo, lev, trace_id, seed);
+              residual(W.p, gath.p + r * slot, (int)(hi - lo), lev, &g1sp);
+            }
+            cm.exchange(s, gath.p, slot);
+            cm.merge(s, gath.p, slot, k, n, Y.p);
+          }
           RSF_PHASE("p.basis", s);
           size_t x0 = 0;
           while (x0 < NA) {
@@ -869,6 +894,7 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
         }
         W.release();
         Y.release();
+        gath.release();
         // eps_peel-rank of every sibling block from its Gaussian sketch P_ij (R-N); adaptivity (R-M)
         DBuf<double> Pc(pt, s);
         DBuf<int> piv((size_t)c * NA, s);
@@ -1159,19 +1185,29 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
   RSF_PHASE("p.extract", s);
   double tr = 0.0, tra = 0.0;
   const int GB = 256;
-  for (int e0 = 0; e0 < nL; e0 += kb) {
-    const int k = std::min(kb, nL - e0);
-    DBuf<double> E((size_t)n * k, s), H((size_t)n * k, s), part(GB, s), parta(GB, s);
-    extract_probe_kernel<<<gxx((long long)n * k), NT, 0, s>>>(E.p, k, n, dlb.p, e0);
-    count_launch();
-    RSF_LAUNCH_CHECK();
-    residual(E.p, H.p, k, L + 1, nullptr);
-    extract_diag_kernel<<<GB, NT, 0, s>>>(H.p, k, n, dlb.p, e0, part.p, parta.p);
-    count_launch();
-    RSF_LAUNCH_CHECK();
-    auto hp = part.to_host(GB), ha = parta.to_host(GB);
-    for (int i = 0; i < GB; ++i) { tr += hp[i]; tra += ha[i]; }
+  // (sharded: the nL extraction columns are split over the parts; partial leaf traces are
+  // summed over the ranks in rank order)
+  double trp[2] = {0.0, 0.0};
+  for (int r = cm.p0(); r < cm.p1(); ++r) {
+    long long lo, hi;
+    Comm::slice(nL, NP, r, &lo, &hi);
+    for (int e0 = (int)lo; e0 < (int)hi; e0 += kb) {
+      const int k = std::min<int>(kb, (int)hi - e0);
+      DBuf<double> E((size_t)n * k, s), H((size_t)n * k, s), part(GB, s), parta(GB, s);
+      extract_probe_kernel<<<gxx((long long)n * k), NT, 0, s>>>(E.p, k, n, dlb.p, e0);
+      count_launch();
+      RSF_LAUNCH_CHECK();
+      residual(E.p, H.p, k, L + 1, nullptr);
+      extract_diag_kernel<<<GB, NT, 0, s>>>(H.p, k, n, dlb.p, e0, part.p, parta.p);
+      count_launch();
+      RSF_LAUNCH_CHECK();
+      auto hp = part.to_host(GB), ha = parta.to_host(GB);
+      for (int i = 0; i < GB; ++i) { trp[0] += hp[i]; trp[1] += ha[i]; }
+    }
   }
+  cm.allsum(s, trp, 2);
+  tr = trp[0];
+  tra = trp[1];
   pd.nL = nL;
   pd.cancellation = tr != 0.0 ? tra / std::fabs(tr) : INFINITY;
   pd.applies = G.columns;
@@ -1301,12 +1337,16 @@ EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KP
     f_ready.get();
     if (f_event && ctx_stream(ctx) != s) RSF_CUDA(cudaStreamWaitEvent(ctx_stream(ctx), f_event, 0));
   };
+  // sharded evaluation: one communicator per trace job, split from the group's
+  // communicator here, on the calling thread, in job order (the same on every rank)
+  auto job_comm = [&](int j) -> const Comm* { return ctx.comm.world > 1 ? &ctx.job_comms[j] : &ctx.comm; };
   std::vector<std::function<void()>> jobs;
   bool need_trinv = false;
   for (int i = 0; i < p; ++i) {
     const int w = theta[i];
     if (w == W_SIGMA2 || w == W_NUGGET) { need_trinv = true; continue; }
-    jobs.push_back([&, i, w]() {
+    const int jid = (int)jobs.size();
+    jobs.push_back([&, i, w, jid]() {
       double t1 = now_s();
       auto Fi = factor(ctx, tree, kp, w, eps, o);
       tcomp[i] = now_s() - t1;
@@ -1320,18 +1360,28 @@ EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KP
       qv[i] = ddot(s2, u.p, y.p, n);
       tsol[i] = now_s() - t1;
       t1 = now_s();
-      trv[i] = peel(*F, Fi.get(), o, i, &R.pd[i]);
+      trv[i] = peel(*F, Fi.get(), o, i, &R.pd[i], job_comm(jid));
       tpl[i] = now_s() - t1;
     });
   }
-  if (need_trinv)
-    jobs.push_back([&]() {
+  if (need_trinv) {
+    const int jid = (int)jobs.size();
+    jobs.push_back([&, jid]() {
       wait_f();
       const double t1 = now_s();
-      trinv = peel(*F, nullptr, o, 100, &pd_trinv);
+      trinv = peel(*F, nullptr, o, 100, &pd_trinv, job_comm(jid));
       utu = ddot(ctx_stream(ctx), u.p, u.p, n);
       t_trinv = now_s() - t1;
     });
+  }
+
+  if (ctx.comm.world > 1)
+    while (ctx.job_comms.size() < jobs.size()) {
+      Comm jc = ctx.comm;
+      jc.nccl = nccl_split(ctx.comm.nccl, ctx.comm.rank);
+      jc.owned = true;
+      ctx.job_comms.push_back(jc);
+    }
 
   // F ~ Sigma (solve-only), u = F^-1 z (k = 1), q0 = z^T u; profile terms (Eq. prof)
   double Qp = 0.0;

@@ -14,8 +14,10 @@ struct PeelDiag {
   double flops = 0;
 };
 
-// Tr(G) with G = 1/2 (F^-1 Fi + Fi F^-1) (Fi != null) or G = F^-1 (Fi == null).
-double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag* diag);
+// Tr(G) with G = 1/2 (F^-1 Fi + Fi F^-1) (Fi != null) or G = F^-1 (Fi == null).  comm: the rank
+// group sharing the probe columns (null: the factor context's group)
+double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag* diag,
+            const Comm* comm = nullptr);
 void fill_peel_diag(const PeelDiag& d, rsf_peel_diag* out);
 
 // Hutchinson estimate of Tr(F^-1 F_i) or Tr(F^-1): mean and standard error over q probes

@@ -4,6 +4,7 @@
 #include <memory>
 #include <unordered_map>
 
+#include "comm.cuh"
 #include "common.cuh"
 #include "covariance.cuh"
 #include "gemm.cuh"
@@ -26,7 +27,8 @@ struct Ctx {
   cudaStream_t stream = 0;
   std::vector<cudaStream_t> aux;   // streams of the concurrent trace jobs of gp_mle_eval (created lazily)
   bool own_stream = false;
-  void* nccl = nullptr;
+  Comm comm;                        // rank group of a sharded evaluation (world 1: none)
+  std::vector<Comm> job_comms;      // one split communicator per concurrent trace job
   std::string last_error;
 };
 

@@ -1,5 +1,6 @@
-"""N > 1 host logic on CPU: world_size-2 gloo process group, the bench's
-max-over-ranks aggregation and the per-rank replica seeds."""
+"""N > 1 host logic on CPU: world_size-2 gloo process groups for the bench's max-over-ranks
+aggregation (replicas and the sharded strong-scaling form) and the NCCL-id bootstrap of a
+sharded group; the probe-column partition of include/rsf.h."""
 import os
 import socket
 
@@ -23,7 +24,8 @@ def _worker(rank, world, port, q):
     import bench
     t_local = 2.0 + rank          # rank 1 is the slow one
     t_all, value = bench.aggregate(t_local, steps=3, world=world)
-    q.put((rank, t_all, value))
+    _, vs = bench.aggregate(t_local, steps=3, world=world, strong=True)
+    q.put((rank, t_all, value, vs))
     dist.destroy_process_group()
 
 
@@ -39,12 +41,56 @@ def test_aggregate_max_over_ranks_gloo():
         p.join(timeout=120)
         assert p.exitcode == 0
     res = sorted(q.get() for _ in range(world))
-    for rank, t_all, value in res:
+    for rank, t_all, value, vs in res:
         assert t_all == pytest.approx(3.0)
         assert value == pytest.approx(world * 3 / 3.0)
+        assert vs == pytest.approx(3 / 3.0)       # one shared evaluation per step
 
 
 def test_aggregate_single_rank():
     import bench
     t, v = bench.aggregate(4.0, steps=2, world=1)
     assert t == 4.0 and v == 0.5
+
+
+def _id_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_1603_08057_b200 as R
+    uid, r, w = R.group_id_from_process_group()
+    q.put((rank, r, w, uid))
+    dist.destroy_process_group()
+
+
+def test_nccl_id_bootstrap_gloo():
+    """rank 0's 128-byte NCCL id reaches every rank unchanged (the bytes rsf_ctx_create_group
+    needs); ncclGetUniqueId itself needs no GPU."""
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_id_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    res = sorted(q.get() for _ in range(world))
+    assert [x[1] for x in res] == [0, 1] and all(x[2] == world for x in res)
+    assert len(res[0][3]) == 128 and res[0][3] == res[1][3]
+
+
+def test_column_slices_partition_every_block():
+    """include/rsf.h rsf_debug_col_slice: contiguous, disjoint, covering, balanced to one
+    column, larger slices first -- for every block width the peeling uses."""
+    import paper_1603_08057_b200 as R
+    for P in (1, 2, 3, 4, 7, 8):
+        for k in list(range(0, 70)) + [512, 1000, 4096, 4103]:
+            sl = [R.col_slice(k, P, r) for r in range(P)]
+            assert sl[0][0] == 0 and sl[-1][1] == k
+            for (a, b), (c, d) in zip(sl, sl[1:]):
+                assert b == c
+            sizes = [b - a for a, b in sl]
+            assert max(sizes) - min(sizes) <= 1 and sizes == sorted(sizes, reverse=True)

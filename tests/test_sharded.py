@@ -1,0 +1,50 @@
+"""Sharded evaluation on ONE GPU: RSF_EMU_WORLD=P emulates a
+group of P ranks in one process -- every emulated rank's probe-column slice is generated,
+pushed through G and the peeled levels, written into its slot of the gather buffer (the
+layout ncclAllGather produces), merged, and the extraction columns are split the same way
+(comm.cuh).  Checked against the dense oracle O1 with the BASELINE gates and against the
+unsharded evaluation.  (Ranks that wait on one another are never run as separate launches
+on one GPU; the NCCL transport itself needs >= 2 GPUs.)"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle.dense import dense_eval, dense_sample  # noqa: E402
+from oracle.kernels import Kernel as OK  # noqa: E402
+from workloads import config, points_for, w_for  # noqa: E402
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1603_08057_b200 as R  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+def _d(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(DEV)
+
+
+@pytest.mark.parametrize("cid,n,P", [(1, 1024, 2), (1, 1024, 3), (2, 4096, 4)])
+def test_emulated_group_matches_oracle_and_unsharded(cid, n, P, monkeypatch):
+    c = config(cid)
+    xy = points_for(c, n)
+    ok = OK(c.family, c.rho, c.sigma2, c.nugget, c.alpha, c.theta)
+    z = dense_sample(ok, xy, w_for(c, n))
+    d = dense_eval(ok, xy, z)
+    ctx = R.Context(0)
+    assert ctx.group() == (0, 1)
+    K = R.Kernel(c.family, c.rho, c.sigma2, c.nugget, c.alpha, c.theta)
+    o = R.Opts(eps_peel=c.eps_peel, seed=c.seed, probe_block=64)
+    r1 = R.gp_mle_eval(ctx, _d(xy), _d(z), K, c.eps_fact, c.leaf, o)
+    monkeypatch.setenv("RSF_EMU_WORLD", str(P))
+    rP = R.gp_mle_eval(ctx, _d(xy), _d(z), K, c.eps_fact, c.leaf, o)
+    g1, gP = np.array(r1.grad), np.array(rP.grad)
+    assert rP.ell == r1.ell                        # factor, solve and l are not split
+    assert np.all(np.abs(gP - d["grad"]) <= 1e-3 * np.abs(d["grad"])), (gP, d["grad"])
+    tr1 = np.array([r1.diag.trace[i] for i in range(len(c.theta))])
+    trP = np.array([rP.diag.trace[i] for i in range(len(c.theta))])
+    np.testing.assert_allclose(trP, d["trace"], rtol=1e-5)
+    np.testing.assert_allclose(trP, tr1, rtol=1e-6)
