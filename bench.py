@@ -120,6 +120,16 @@ def aggregate(t_local: float, steps: int, world: int, device=None, strong: bool 
     return t_all, (steps if strong else world * steps) / t_all
 
 
+def _hbm_peak():
+    """(GB/s, source): MEASURED_PEAKS.json's measured copy bandwidth, else the profiling guide's
+    fallback figure."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy bandwidth)"
+    except Exception:
+        return 6540.2, "fallback: the measured B200 copy bandwidth of round 1 (MEASURED_PEAKS.json absent)"
+
+
 def workload(cid: int, n: int | None):
     from workloads import config, points_for, w_for
     c = config(cid)
@@ -357,6 +367,25 @@ def main():
     stats = st()
     R.lib.rsf_stats_get(stats)
 
+    # ---- 1-RHS solve on the HBM roofline (north star: "achieved HBM GB/s for the solves"):
+    # device time of F^-1 z sweeps of the full Sigma factor, algorithmic bytes per solve
+    solve_rl = None
+    try:
+        Fs = R.Factor(ctx, xy, K, c.eps_fact, c.leaf, opts=opts)
+        nb = __import__("ctypes").c_double()
+        t_solve = R.lib.rsf_debug_solve_bench(Fs.h, 1, 20, __import__("ctypes").byref(nb))
+        Fs.close()
+        if t_solve > 0:
+            hbm = _hbm_peak()
+            ach = nb.value / t_solve / 1e9
+            solve_rl = {"bound": "hbm", "achieved": ach, "peak": hbm[0], "unit": "GB/s", "frac": ach / hbm[0],
+                        "peak_source": hbm[1], "seconds_per_solve": t_solve, "bytes_per_solve": nb.value,
+                        "what": "one F^-1 z (k = 1) of config 3's Sigma factor, forward + backward sweeps; "
+                                "bytes = 2 x (T, E, L^-1 of every box + C^-1) + active-DOF vector traffic "
+                                "(DESIGN.md §5); CUDA events, mean of 20"}
+    except Exception as e:  # diagnostics only
+        solve_rl = {"error": str(e)}
+
     # ---- e2e: same metric through the C ABI with pinned HOST buffers (H2D inside the call)
     xy_p = torch.from_numpy(xy_h).pin_memory()
     z_p = z.cpu().pin_memory()
@@ -405,7 +434,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": 1e3 * t_all / args.steps, "higher_is_better": True,
         "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": _config_dict(c, n, args), "clocks": clocks, "gpu_launches": int(launches),
-        "e2e": e2e, "roofline": roofline,
+        "e2e": e2e, "roofline": roofline, "solve_roofline": solve_rl,
         "rsf_factor_tflops": fl_factor / max(d.t_factor + d.t_compress, 1e-9) / 1e12,
         "phases_s": {"tree": d.t_tree, "factor": d.t_factor, "compress": d.t_compress,
                      "solve": d.t_solve, "peel": d.t_peel, "total": d.t_total},

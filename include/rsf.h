@@ -237,6 +237,10 @@ double rsf_debug_gemm_bench(int M, int N, int K, int batch, int ta, int tb, int 
 int rsf_debug_gemm(int ta, int tb, int M, int N, int K, int batch, double alpha, const double* A,
                    const double* B, double beta, double* C, int splitk);
 void rsf_stats_get(double* out4);
+/* diagnostics: seconds per F^-1 X on nrhs columns of the Sigma factor f, device time
+ * (CUDA events on the context stream, mean of reps after one warm-up; no layout permutation);
+ * *bytes (nullable) = algorithmic bytes of one 1-RHS solve.  -1 on error. */
+double rsf_debug_solve_bench(rsf_fact f, int nrhs, int reps, double* bytes);
 /* diagnostics: FP64 peak (TFLOP/s) of independent DMMA.8x8x4 (dmma=1) or DFMA (dmma=0) chains on the
  * current device, best of `reps` timed launches -- the live roofline denominator of bench.py */
 double rsf_debug_fp64_peak(int dmma, int reps);

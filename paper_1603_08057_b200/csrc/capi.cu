@@ -615,6 +615,36 @@ double rsf_debug_fp64_peak(int dmma, int reps) {
   }
 }
 
+double rsf_debug_solve_bench(rsf_fact f, int nrhs, int reps, double* bytes) {
+  // diagnostics (bench.py "solve" roofline): device time of one F^-1 X sweep pair
+  // on nrhs internal-layout columns (CUDA events on the op stream, after one warm-up), and
+  // its algorithmic bytes for nrhs = 1 (FactDiag::bytes_solve)
+  try {
+    if (!f || f->F->which != rsf::W_SIGMA || nrhs < 1 || reps < 1) return -1.0;
+    const rsf::Fact& F = *f->F;
+    RSF_CUDA(cudaSetDevice(f->owner->ctx.device));
+    cudaStream_t s = rsf::op_stream(F);
+    rsf::DBuf<double> X((size_t)F.n() * nrhs, s), tmp((size_t)std::max<long long>(F.tmp_cols, 1) * nrhs, s);
+    RSF_CUDA(cudaMemsetAsync(X.p, 0, (size_t)F.n() * nrhs * sizeof(double), s));
+    rsf::solve_internal(F, X.p, nrhs, tmp.p);
+    cudaEvent_t e0, e1;
+    RSF_CUDA(cudaEventCreate(&e0));
+    RSF_CUDA(cudaEventCreate(&e1));
+    RSF_CUDA(cudaEventRecord(e0, s));
+    for (int r = 0; r < reps; ++r) rsf::solve_internal(F, X.p, nrhs, tmp.p);
+    RSF_CUDA(cudaEventRecord(e1, s));
+    RSF_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (bytes) *bytes = F.diag.bytes_solve;
+    return ms * 1e-3 / reps;
+  } catch (...) {
+    return -1.0;
+  }
+}
+
 void rsf_stats_enable(int on) { rsf::KStats::on = on != 0; }
 void rsf_stats_get(double* out4) { rsf::KStats::collect(out4); }
 void rsf_stats_reset(void) { rsf::KStats::reset(); }

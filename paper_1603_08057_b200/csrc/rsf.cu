@@ -478,6 +478,7 @@ std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams
     long long Isum = 0, Ssum = 0;
     int Imax = 0;
     for (int b = 0; b < nb; ++b) { Isum += cvec[b]; Ssum += kvec[b]; Imax = std::max(Imax, cvec[b]); }
+    if (sig) F->diag.bytes_solve += 2.0 * 8.0 * (2.0 * ttot + ltot) + 2.0 * 16.0 * (double)Isum;
     F->diag.level_I.push_back((int)Isum);
     F->diag.level_S.push_back((int)Ssum);
     F->diag.level_maxI.push_back(Imax);
@@ -622,6 +623,7 @@ std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams
         F->diag.flops_top = (double)n0 * n0 * n0 / 3.0;
       }
       F->diag.bytes_factor += 8.0 * (double)n0 * n0 * (sig && !solve_only ? 2 : 1);
+      if (sig) F->diag.bytes_solve += 2.0 * 8.0 * (double)n0 * n0;
     }
     Bp_prev.release();
     auto mk = [&](int N, int K, int selA, const int* mapA, const double* Bm, int ldb, int selC,

@@ -98,6 +98,10 @@ struct Level {
 struct FactDiag {
   double flops_id = 0, flops_elim = 0, flops_top = 0;   // algorithmic (formulas of DESIGN.md)
   double bytes_factor = 0;                              // stored factor bytes
+  // algorithmic bytes of one 1-RHS solve: the forward and the backward sweep
+  // each read T, E and L^-1 of every box once and C^-1 once, and read + write every active
+  // DOF of every level once: 2 (8 (2 sum k r + sum r^2) + 8 n0^2) + 2 * 16 sum |I|
+  double bytes_solve = 0;
   double t_tree = 0, t_factor = 0;
   std::vector<int> level_boxes, level_I, level_S, level_maxI;
 };
