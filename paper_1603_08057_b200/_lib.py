@@ -124,6 +124,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         if f not in ("rsf_ctx_destroy", "rsf_fact_destroy", "rsf_opts_default", "rsf_last_error",
                      "rsf_kernel_launches", "rsf_profile_dump", "rsf_profile_reset", "rsf_stats_enable",
                      "rsf_stats_get", "rsf_stats_reset", "rsf_debug_gemm_bench",
-                     "rsf_debug_fp64_peak", "rsf_trace_dump", "rsf_debug_gemm_log"):
+                     "rsf_debug_fp64_peak", "rsf_trace_dump", "rsf_debug_gemm_log", "rsf_debug_col_slice",
+                     "rsf_debug_solve_bench"):
             getattr(lib, f).restype = C.c_int
     return lib

@@ -635,12 +635,13 @@ double rsf_debug_solve_bench(rsf_fact f, int nrhs, int reps, double* bytes) {
     RSF_CUDA(cudaEventRecord(e1, s));
     RSF_CUDA(cudaEventSynchronize(e1));
     float ms = 0.f;
-    cudaEventElapsedTime(&ms, e0, e1);
+    RSF_CUDA(cudaEventElapsedTime(&ms, e0, e1));
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     if (bytes) *bytes = F.diag.bytes_solve;
     return ms * 1e-3 / reps;
-  } catch (...) {
+  } catch (const std::exception& e) {
+    g_err = e.what();
     return -1.0;
   }
 }

@@ -1123,6 +1123,128 @@ __global__ void splitk_reduce_kernel(const GemmDesc* __restrict__ descs, const d
   }
 }
 
+// ---------------------------------------------------------------------------
+// M = 1 (one right-hand side: the 1-RHS solve/apply sweeps of P:381-384, u = F^-1 z of Alg. 1):
+// a batched gather-GEMV instead of 128-row DMMA tiles with 127 idle rows.  The sweep is bound
+// by the HBM stream of the factor blocks (T, E, L^-1, C^-1), so the kernel is laid out for
+// coalesced streaming of op(B):
+//   !TB: op(B)(l, j) = B(l, c(j)) -- column j contiguous in l: each warp owns 8 columns of the
+//        CTA's 64-column tile, lanes stride over l, 8 independent loads in flight per lane,
+//        shuffle reduction per column;
+//   TB:  op(B)(l, j) = B(j, c(l)) -- contiguous in j: lanes over 32 consecutive j, the 8 warps
+//        split (2 j-halves) x (4 l-phases), shared-memory reduction over the phases.
+// op(A)(0, l) (gathered through mapA) is staged in shared memory per K-chunk of GV_KC.  Long K
+// with few column tiles is split over gridDim.z slices (workspace + the deterministic
+// splitk_reduce_kernel); btri restricts the K range of triangular op(B) exactly like the
+// tiled kernel.  lower / mapK batches keep the tiled path.
+constexpr int GV_TJ = 64, GV_NT = 256, GV_KC = 4096;
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(GV_NT) gemv1_kernel(const GemmDesc* __restrict__ descs, const int* __restrict__ prefix,
+                                                      int nprob, double* X0, double* X1, int ldx, double* ws,
+                                                      const long long* __restrict__ mnpre, int kchunk) {
+  __shared__ double as[GV_KC];
+  __shared__ double red[4][GV_TJ];
+  const int p = find_prob(prefix, nprob, blockIdx.x);
+  const GemmDesc& dd = descs[p];
+  const int N = dd.N, K = dd.K;
+  const int n0 = (blockIdx.x - __ldg(prefix + p)) * GV_TJ;
+  const double* A = dd.selA == 0 ? dd.A + dd.offA : (dd.selA == 1 ? X0 : X1) + dd.offA * (long long)ldx;
+  const double* B = dd.selB == 0 ? dd.B + dd.offB : (dd.selB == 1 ? X0 : X1) + dd.offB * (long long)ldx;
+  double* C = dd.selC == 0 ? dd.C + dd.offC : (dd.selC == 1 ? X0 : X1) + dd.offC * (long long)ldx;
+  const long long lda = dd.selA ? ldx : dd.lda;
+  const long long ldb = dd.selB ? ldx : dd.ldb;
+  const long long ldc = dd.selC ? ldx : dd.ldc;
+  const int* mapA = dd.mapA;
+  const int* mapB = dd.mapB;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int kz0 = ws ? blockIdx.z * kchunk : 0;
+  const int kz1 = ws ? min(K, kz0 + kchunk) : K;
+  // K range that can be nonzero for this tile of a triangular op(B)
+  int kb0 = kz0, kb1 = kz1;
+  if (dd.btri == 1) kb0 = max(kb0, n0);                       // op(B)(l, j) = 0 for l < j
+  if (dd.btri == 2) kb1 = min(kb1, n0 + GV_TJ);               // op(B)(l, j) = 0 for l > j
+  double acc[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+  const long long a0 = TA ? (mapA ? (long long)__ldg(mapA) : 0) * lda : 0;
+  for (int c0 = kb0; c0 < kb1; c0 += GV_KC) {
+    const int c1 = min(kb1, c0 + GV_KC);
+    __syncthreads();
+    for (int l = c0 + tid; l < c1; l += GV_NT)
+      as[l - c0] = TA ? A[a0 + l] : A[(mapA ? (long long)__ldg(mapA + l) : (long long)l) * lda];
+    __syncthreads();
+    if (!TB) {
+      // warp w: columns n0 + 8w .. n0 + 8w + 7
+      const double* bc[8];
+      int lmin[8], lmax[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = n0 + 8 * warp + u;
+        const long long cj = j < N ? (mapB ? (long long)__ldg(mapB + j) : (long long)j) : 0;
+        bc[u] = B + cj * ldb;
+        lmin[u] = (dd.btri == 1) ? max(c0, j) : c0;
+        lmax[u] = j < N ? ((dd.btri == 2) ? min(c1, j + 1) : c1) : c0;
+      }
+      for (int l = c0 + lane; l < c1; l += 32) {
+        const double a = as[l - c0];
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = (l >= lmin[u] && l < lmax[u]) ? __ldg(bc[u] + l) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[u] = fma(a, v[u], acc[u]);
+      }
+    } else {
+      // thread: column j = n0 + 32 (warp & 1) + lane, l-phase = warp >> 1 (of 4)
+      const int j = n0 + 32 * (warp & 1) + lane, ph = warp >> 1;
+      if (j < N) {
+        const int lo = (dd.btri == 1) ? max(c0, j) : c0;
+        const int hi = (dd.btri == 2) ? min(c1, j + 1) : c1;
+        int l = lo + ((ph - lo) % 4 + 4) % 4;   // first l >= lo with l = ph (mod 4)
+        for (; l + 12 < hi; l += 16) {
+          double v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int ll = l + 4 * u;
+            v[u] = __ldg(B + (mapB ? (long long)__ldg(mapB + ll) : (long long)ll) * ldb + j);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) acc[u] = fma(as[l + 4 * u - c0], v[u], acc[u]);
+        }
+        for (; l < hi; l += 4)
+          acc[0] = fma(as[l - c0], __ldg(B + (mapB ? (long long)__ldg(mapB + l) : (long long)l) * ldb + j), acc[0]);
+      }
+    }
+  }
+  // reduce to one value per column j of the tile
+  double out = 0.0;
+  int jo = -1;
+  if (!TB) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      double v = acc[u];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == u) { out = v; jo = n0 + 8 * warp + u; }
+    }
+  } else {
+    const double v = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    red[warp >> 1][32 * (warp & 1) + lane] = v;
+    __syncthreads();
+    if (tid < GV_TJ) {
+      out = (red[0][tid] + red[1][tid]) + (red[2][tid] + red[3][tid]);
+      jo = n0 + tid;
+    }
+  }
+  if (jo < 0 || jo >= N) return;
+  if (ws) {
+    ws[mnpre[p] * (long long)gridDim.z + (long long)blockIdx.z * N + jo] = out;   // W[z * MN + e], MN = N
+  } else {
+    const long long cc = dd.mapC ? (long long)__ldg(dd.mapC + jo) : (long long)jo;
+    double* c = C + cc * ldc;
+    *c = dd.beta != 0.0 ? fma(dd.beta, *c, dd.alpha * out) : dd.alpha * out;
+  }
+}
+
 int gemm_mode() {
   static int v = -1;
   if (v < 0) {
@@ -1194,7 +1316,41 @@ void GemmBatch::run(cudaStream_t s, double* X0, double* X1, int ldx, int Mglob, 
   if (KStats::on) KStats::record(s, &e0, nullptr);
   const bool glog = GemmLog::on();
   if (glog) KStats::record(s, &g0, nullptr);
-  if (M <= 16 && !has_mapk_) {   // (only the pipelined kernel implements mapK)
+  static const bool gemv_on = !(getenv("RSF_GEMV") && getenv("RSF_GEMV")[0] == '0');
+  if (M == 1 && gemv_on && !has_mapk_ && !has_lower_) {
+    // one right-hand side: gather-GEMV (HBM stream of op(B)); K split when the column tiles
+    // alone would leave the GPU's resident slots mostly empty
+    const size_t P = h_.size();
+    const int tiles = totalN_;   // 64-column tiles (the BN = 64 prefix)
+    int S = 1;
+    while (S < 32 && (long long)tiles * S < 4 * 148 && maxK_ / (2 * S) >= 512) S *= 2;
+    if (S > 1) {
+      std::vector<long long> mn(P + 1, 0);
+      for (size_t i = 0; i < P; ++i) mn[i + 1] = mn[i] + (h_[i].N > 0 ? h_[i].N : 0);
+      const int kc = (maxK_ + S - 1) / S;
+      const long long* dmn = static_cast<const long long*>(ring_upload(s, mn.data(), mn.size() * sizeof(long long)));
+      DBuf<double> ws((size_t)S * std::max<long long>(mn[P], 1), s);
+      const dim3 grid(tiles, 1, S);
+      if (!ta_ && !tb_) gemv1_kernel<false, false><<<grid, GV_NT, 0, s>>>(dp_, pp_, (int)P, X0, X1, ldx, ws.p, dmn, kc);
+      else if (ta_ && !tb_) gemv1_kernel<true, false><<<grid, GV_NT, 0, s>>>(dp_, pp_, (int)P, X0, X1, ldx, ws.p, dmn, kc);
+      else if (!ta_ && tb_) gemv1_kernel<false, true><<<grid, GV_NT, 0, s>>>(dp_, pp_, (int)P, X0, X1, ldx, ws.p, dmn, kc);
+      else gemv1_kernel<true, true><<<grid, GV_NT, 0, s>>>(dp_, pp_, (int)P, X0, X1, ldx, ws.p, dmn, kc);
+      count_launch();
+      long long mx = 0;
+      for (size_t i = 0; i < P; ++i) mx = std::max(mx, mn[i + 1] - mn[i]);
+      const int gx = (int)std::max<long long>(1, std::min<long long>((mx + P_NT - 1) / P_NT, 1024));
+      for (size_t o = 0; o < P; o += 65535) {
+        const unsigned ny = (unsigned)std::min<size_t>(65535, P - o);
+        splitk_reduce_kernel<<<dim3(gx, ny), P_NT, 0, s>>>(dp_, ws.p, dmn, S, (int)o, X0, X1, ldx, 1);
+      }
+    } else {
+      const dim3 grid(tiles, 1, 1);
+      if (!ta_ && !tb_) gemv1_kernel<false, false><<<grid, GV_NT, 0, s>>>(dp_, pp_, (int)P, X0, X1, ldx, nullptr, nullptr, 0);
+      else if (ta_ && !tb_) gemv1_kernel<true, false><<<grid, GV_NT, 0, s>>>(dp_, pp_, (int)P, X0, X1, ldx, nullptr, nullptr, 0);
+      else if (!ta_ && tb_) gemv1_kernel<false, true><<<grid, GV_NT, 0, s>>>(dp_, pp_, (int)P, X0, X1, ldx, nullptr, nullptr, 0);
+      else gemv1_kernel<true, true><<<grid, GV_NT, 0, s>>>(dp_, pp_, (int)P, X0, X1, ldx, nullptr, nullptr, 0);
+    }
+  } else if (M <= 16 && !has_mapk_) {   // (only the pipelined kernel implements mapK)
     dim3 grid(totalN_, ceil_div(M, 16));
     launch_variant<16, 1>(ta_, tb_, grid, s, dp_, pp_, (int)h_.size(), X0, X1, ldx, Mglob);
   } else if (gemm_mode() == 2 || has_mapk_) {

@@ -33,7 +33,11 @@ def _run(R, ta, tb, M, N, K, batch, alpha, beta, splitk, seed):
 
 @pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
 @pytest.mark.parametrize("M,N,K,batch", [(1, 1, 1, 1), (130, 70, 33, 3), (257, 31, 2049, 2), (64, 200, 5000, 1),
-                                         (7, 300, 40, 5)])
+                                         (7, 300, 40, 5),
+                                         # M = 1: the gather-GEMV path (one column tile with K split,
+                                         # many tiles, ragged tails, K beyond one shared-memory chunk)
+                                         (1, 64, 20000, 1), (1, 200, 5000, 2), (1, 5000, 700, 1), (1, 70, 33, 3),
+                                         (1, 131, 9000, 2)])
 @pytest.mark.parametrize("splitk", [1, 0, 3, 7])
 def test_batched_gemm_vs_matmul(ta, tb, M, N, K, batch, splitk):
     import paper_1603_08057_b200 as R

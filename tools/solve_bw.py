@@ -33,6 +33,9 @@ hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if o
 for k in ks:
     b = C.c_double()
     t = R.lib.rsf_debug_solve_bench(F.h, k, 20, C.byref(b))
+    if t <= 0:
+        print("error", t, R.lib.rsf_last_error().decode(), flush=True)
+        continue
     print(json.dumps({"config": cid, "nrhs": k, "seconds": t, "bytes_1rhs": b.value,
                       "GBps": b.value / t / 1e9, "frac_hbm": b.value / t / 1e9 / hbm,
                       "factor_bytes": info.factor_bytes, "levels": info.levels, "top": info.top_size}), flush=True)
