@@ -624,6 +624,7 @@ double rsf_debug_solve_bench(rsf_fact f, int nrhs, int reps, double* bytes) {
     const rsf::Fact& F = *f->F;
     RSF_CUDA(cudaSetDevice(f->owner->ctx.device));
     cudaStream_t s = rsf::op_stream(F);
+    rsf::KTrace::set_stream(s);   // (RSF_KTRACE=1: time per launch site, rsf_trace_dump)
     rsf::DBuf<double> X((size_t)F.n() * nrhs, s), tmp((size_t)std::max<long long>(F.tmp_cols, 1) * nrhs, s);
     RSF_CUDA(cudaMemsetAsync(X.p, 0, (size_t)F.n() * nrhs * sizeof(double), s));
     rsf::solve_internal(F, X.p, nrhs, tmp.p);

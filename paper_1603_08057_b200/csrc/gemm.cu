@@ -1137,17 +1137,17 @@ __global__ void splitk_reduce_kernel(const GemmDesc* __restrict__ descs, const d
 // with few column tiles is split over gridDim.z slices (workspace + the deterministic
 // splitk_reduce_kernel); btri restricts the K range of triangular op(B) exactly like the
 // tiled kernel.  lower / mapK batches keep the tiled path.
-constexpr int GV_TJ = 64, GV_NT = 256, GV_KC = 4096;
-template <bool TA, bool TB>
+constexpr int GV_TJ = 64, GV_NT = 256, GV_KC = 2048;
+template <bool TA, bool TB, bool TRI, int TJ = 64>
 __global__ void __launch_bounds__(GV_NT) gemv1_kernel(const GemmDesc* __restrict__ descs, const int* __restrict__ prefix,
                                                       int nprob, double* X0, double* X1, int ldx, double* ws,
                                                       const long long* __restrict__ mnpre, int kchunk) {
   __shared__ double as[GV_KC];
-  __shared__ double red[4][GV_TJ];
+  __shared__ double red[4][64];
   const int p = find_prob(prefix, nprob, blockIdx.x);
   const GemmDesc& dd = descs[p];
   const int N = dd.N, K = dd.K;
-  const int n0 = (blockIdx.x - __ldg(prefix + p)) * GV_TJ;
+  const int n0 = (blockIdx.x - __ldg(prefix + p)) * TJ;
   const double* A = dd.selA == 0 ? dd.A + dd.offA : (dd.selA == 1 ? X0 : X1) + dd.offA * (long long)ldx;
   const double* B = dd.selB == 0 ? dd.B + dd.offB : (dd.selB == 1 ? X0 : X1) + dd.offB * (long long)ldx;
   double* C = dd.selC == 0 ? dd.C + dd.offC : (dd.selC == 1 ? X0 : X1) + dd.offC * (long long)ldx;
@@ -1162,7 +1162,7 @@ __global__ void __launch_bounds__(GV_NT) gemv1_kernel(const GemmDesc* __restrict
   // K range that can be nonzero for this tile of a triangular op(B)
   int kb0 = kz0, kb1 = kz1;
   if (dd.btri == 1) kb0 = max(kb0, n0);                       // op(B)(l, j) = 0 for l < j
-  if (dd.btri == 2) kb1 = min(kb1, n0 + GV_TJ);               // op(B)(l, j) = 0 for l > j
+  if (dd.btri == 2) kb1 = min(kb1, n0 + TJ);                  // op(B)(l, j) = 0 for l > j
   double acc[8];
 #pragma unroll
   for (int u = 0; u < 8; ++u) acc[u] = 0.0;
@@ -1182,10 +1182,45 @@ __global__ void __launch_bounds__(GV_NT) gemv1_kernel(const GemmDesc* __restrict
         const int j = n0 + 8 * warp + u;
         const long long cj = j < N ? (mapB ? (long long)__ldg(mapB + j) : (long long)j) : 0;
         bc[u] = B + cj * ldb;
-        lmin[u] = (dd.btri == 1) ? max(c0, j) : c0;
-        lmax[u] = j < N ? ((dd.btri == 2) ? min(c1, j + 1) : c1) : c0;
+        if (TRI) {
+          lmin[u] = (dd.btri == 1) ? max(c0, j) : c0;
+          lmax[u] = j < N ? ((dd.btri == 2) ? min(c1, j + 1) : c1) : c0;
+        }
       }
-      for (int l = c0 + lane; l < c1; l += 32) {
+      if (!TRI) {   // general op(B): only the ragged column tail needs a predicate
+        const int nv = min(8, N - (n0 + 8 * warp));
+        int l = c0 + lane;
+        for (; l + 32 < c1; l += 64) {
+          const double a = as[l - c0], a2 = as[l + 32 - c0];
+          double v[8], w[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            v[u] = u < nv ? __ldg(bc[u] + l) : 0.0;
+            w[u] = u < nv ? __ldg(bc[u] + l + 32) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc[u] = fma(a2, w[u], fma(a, v[u], acc[u]));
+        }
+        for (; l < c1; l += 32) {
+          const double a = as[l - c0];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc[u] = fma(a, u < nv ? __ldg(bc[u] + l) : 0.0, acc[u]);
+        }
+        continue;
+      }
+      int l = c0 + lane;
+      for (; l + 32 < c1; l += 64) {           // two rows of 8 columns: 16 loads in flight per lane
+        const double a = as[l - c0], a2 = as[l + 32 - c0];
+        double v[8], w[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          v[u] = (l >= lmin[u] && l < lmax[u]) ? __ldg(bc[u] + l) : 0.0;
+          w[u] = (l + 32 >= lmin[u] && l + 32 < lmax[u]) ? __ldg(bc[u] + l + 32) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[u] = fma(a2, w[u], fma(a, v[u], acc[u]));
+      }
+      for (; l < c1; l += 32) {
         const double a = as[l - c0];
         double v[8];
 #pragma unroll
@@ -1200,15 +1235,15 @@ __global__ void __launch_bounds__(GV_NT) gemv1_kernel(const GemmDesc* __restrict
         const int lo = (dd.btri == 1) ? max(c0, j) : c0;
         const int hi = (dd.btri == 2) ? min(c1, j + 1) : c1;
         int l = lo + ((ph - lo) % 4 + 4) % 4;   // first l >= lo with l = ph (mod 4)
-        for (; l + 12 < hi; l += 16) {
-          double v[4];
+        for (; l + 60 < hi; l += 64) {          // 16 independent 256-byte row segments per warp
+          double v[16];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
+          for (int u = 0; u < 16; ++u) {
             const int ll = l + 4 * u;
             v[u] = __ldg(B + (mapB ? (long long)__ldg(mapB + ll) : (long long)ll) * ldb + j);
           }
 #pragma unroll
-          for (int u = 0; u < 4; ++u) acc[u] = fma(as[l + 4 * u - c0], v[u], acc[u]);
+          for (int u = 0; u < 16; ++u) acc[u & 7] = fma(as[l + 4 * u - c0], v[u], acc[u & 7]);
         }
         for (; l < hi; l += 4)
           acc[0] = fma(as[l - c0], __ldg(B + (mapB ? (long long)__ldg(mapB + l) : (long long)l) * ldb + j), acc[0]);
@@ -1227,10 +1262,10 @@ __global__ void __launch_bounds__(GV_NT) gemv1_kernel(const GemmDesc* __restrict
       if (lane == u) { out = v; jo = n0 + 8 * warp + u; }
     }
   } else {
-    const double v = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    const double v = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
     red[warp >> 1][32 * (warp & 1) + lane] = v;
     __syncthreads();
-    if (tid < GV_TJ) {
+    if (tid < TJ) {
       out = (red[0][tid] + red[1][tid]) + (red[2][tid] + red[3][tid]);
       jo = n0 + tid;
     }
@@ -1318,23 +1353,37 @@ void GemmBatch::run(cudaStream_t s, double* X0, double* X1, int ldx, int Mglob, 
   if (glog) KStats::record(s, &g0, nullptr);
   static const bool gemv_on = !(getenv("RSF_GEMV") && getenv("RSF_GEMV")[0] == '0');
   if (M == 1 && gemv_on && !has_mapk_ && !has_lower_) {
-    // one right-hand side: gather-GEMV (HBM stream of op(B)); K split when the column tiles
-    // alone would leave the GPU's resident slots mostly empty
+    // one right-hand side: gather-GEMV (HBM stream of op(B)).  Column tiles are 64 wide (128-wide
+    // tiles for op(B) = B^T measured slower); K is split (workspace +
+    // deterministic reduction) until the launch holds ~8 CTAs per SM (2 waves of the 4 resident
+    // ones) while slices keep >= 256 rows (measured best: more slices cost more in reductions)
     const size_t P = h_.size();
-    const int tiles = totalN_;   // 64-column tiles (the BN = 64 prefix)
+    const int tiles = totalN_;   // 64-column tiles
+    const int* ppv = pp_;
+    bool tri = false;
+    for (const auto& d : h_) tri = tri || d.btri != 0;
     int S = 1;
-    while (S < 32 && (long long)tiles * S < 4 * 148 && maxK_ / (2 * S) >= 512) S *= 2;
+    while (S < 32 && (long long)tiles * S < 8 * 148 && maxK_ / (2 * S) >= 256) S *= 2;
+    std::vector<long long> mn;
+    DBuf<double> ws;
+    const long long* dmn = nullptr;
+    int kc = 0;
     if (S > 1) {
-      std::vector<long long> mn(P + 1, 0);
+      mn.assign(P + 1, 0);
       for (size_t i = 0; i < P; ++i) mn[i + 1] = mn[i] + (h_[i].N > 0 ? h_[i].N : 0);
-      const int kc = (maxK_ + S - 1) / S;
-      const long long* dmn = static_cast<const long long*>(ring_upload(s, mn.data(), mn.size() * sizeof(long long)));
-      DBuf<double> ws((size_t)S * std::max<long long>(mn[P], 1), s);
-      const dim3 grid(tiles, 1, S);
-      if (!ta_ && !tb_) gemv1_kernel<false, false><<<grid, GV_NT, 0, s>>>(dp_, pp_, (int)P, X0, X1, ldx, ws.p, dmn, kc);
-      else if (ta_ && !tb_) gemv1_kernel<true, false><<<grid, GV_NT, 0, s>>>(dp_, pp_, (int)P, X0, X1, ldx, ws.p, dmn, kc);
-      else if (!ta_ && tb_) gemv1_kernel<false, true><<<grid, GV_NT, 0, s>>>(dp_, pp_, (int)P, X0, X1, ldx, ws.p, dmn, kc);
-      else gemv1_kernel<true, true><<<grid, GV_NT, 0, s>>>(dp_, pp_, (int)P, X0, X1, ldx, ws.p, dmn, kc);
+      kc = (maxK_ + S - 1) / S;
+      dmn = static_cast<const long long*>(ring_upload(s, mn.data(), mn.size() * sizeof(long long)));
+      ws.alloc((size_t)S * std::max<long long>(mn[P], 1), s);
+    }
+    const dim3 grid(tiles, 1, S);
+    double* wsp = S > 1 ? ws.p : nullptr;
+#define RSF_GV(TA, TB, TRI) gemv1_kernel<TA, TB, TRI><<<grid, GV_NT, 0, s>>>(dp_, ppv, (int)P, X0, X1, ldx, wsp, dmn, kc)
+    if (!ta_ && !tb_) { if (tri) RSF_GV(false, false, true); else RSF_GV(false, false, false); }
+    else if (ta_ && !tb_) { if (tri) RSF_GV(true, false, true); else RSF_GV(true, false, false); }
+    else if (!ta_ && tb_) { if (tri) RSF_GV(false, true, true); else RSF_GV(false, true, false); }
+    else { if (tri) RSF_GV(true, true, true); else RSF_GV(true, true, false); }
+#undef RSF_GV
+    if (S > 1) {
       count_launch();
       long long mx = 0;
       for (size_t i = 0; i < P; ++i) mx = std::max(mx, mn[i + 1] - mn[i]);
@@ -1343,12 +1392,6 @@ void GemmBatch::run(cudaStream_t s, double* X0, double* X1, int ldx, int Mglob, 
         const unsigned ny = (unsigned)std::min<size_t>(65535, P - o);
         splitk_reduce_kernel<<<dim3(gx, ny), P_NT, 0, s>>>(dp_, ws.p, dmn, S, (int)o, X0, X1, ldx, 1);
       }
-    } else {
-      const dim3 grid(tiles, 1, 1);
-      if (!ta_ && !tb_) gemv1_kernel<false, false><<<grid, GV_NT, 0, s>>>(dp_, pp_, (int)P, X0, X1, ldx, nullptr, nullptr, 0);
-      else if (ta_ && !tb_) gemv1_kernel<true, false><<<grid, GV_NT, 0, s>>>(dp_, pp_, (int)P, X0, X1, ldx, nullptr, nullptr, 0);
-      else if (!ta_ && tb_) gemv1_kernel<false, true><<<grid, GV_NT, 0, s>>>(dp_, pp_, (int)P, X0, X1, ldx, nullptr, nullptr, 0);
-      else gemv1_kernel<true, true><<<grid, GV_NT, 0, s>>>(dp_, pp_, (int)P, X0, X1, ldx, nullptr, nullptr, 0);
     }
   } else if (M <= 16 && !has_mapk_) {   // (only the pipelined kernel implements mapK)
     dim3 grid(totalN_, ceil_div(M, 16));

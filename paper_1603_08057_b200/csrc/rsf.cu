@@ -556,7 +556,8 @@ std::unique_ptr<Fact> factor(Ctx& ctx, std::shared_ptr<Tree> tree, const KParams
       LV.max_i = 0;
       for (int b = 0; b < nb; ++b) LV.max_i = std::max(LV.max_i, cvec[b]);
       LV.fused = fused_on && LV.max_i <= sweep_max_i();
-      if (LV.fused) {
+      LV.fused1 = fused_on && LV.max_i <= SWEEP1_MAX_I && (sig || !LV.stacked);
+      if (LV.fused || LV.fused1) {
         std::vector<BoxOp> ops;
         for (int b = 0; b < nb; ++b) {
           if (LV.r[b] == 0) continue;
@@ -668,7 +669,7 @@ void solve_internal(const Fact& F, double* X, int k, double* tmp) {
   for (int lev = L; lev >= 1; --lev) {
     const Level& LV = F.levels[lev];
     RSF_PHASE(lvname("sv", lev), s);
-    if (LV.fused) { sweep_level(s, LV.ops.p, LV.nops, LV.max_i, SW_SOLVE_FWD, X, nullptr, k); continue; }
+    if (LV.sweep1(k)) { sweep_level(s, LV.ops.p, LV.nops, LV.max_i, SW_SOLVE_FWD, X, nullptr, k); continue; }
     LV.fs1.run(s, X, tmp, k, k);
     LV.fs2.run(s, X, tmp, k, k);
     LV.fs3.run(s, X, tmp, k, k);
@@ -682,7 +683,7 @@ void solve_internal(const Fact& F, double* X, int k, double* tmp) {
   for (int lev = 1; lev <= L; ++lev) {
     const Level& LV = F.levels[lev];
     RSF_PHASE(lvname("sv", lev), s);
-    if (LV.fused) { sweep_level(s, LV.ops.p, LV.nops, LV.max_i, SW_SOLVE_BWD, X, nullptr, k); continue; }
+    if (LV.sweep1(k)) { sweep_level(s, LV.ops.p, LV.nops, LV.max_i, SW_SOLVE_BWD, X, nullptr, k); continue; }
     colcopy(s, tmp, X, k, k, nullptr, LV.R.p, LV.rtot);
     LV.bs2.run(s, X, tmp, k, k);
     LV.bs3.run(s, X, tmp, k, k);
@@ -698,7 +699,7 @@ void solve_half_fwd(const Fact& F, double* X, int k, double* tmp) {
   for (int lev = F.tree->L; lev >= 1; --lev) {
     const Level& LV = F.levels[lev];
     RSF_PHASE(lvname("sv", lev), s);
-    if (LV.fused) { sweep_level(s, LV.ops.p, LV.nops, LV.max_i, SW_SOLVE_FWD, X, nullptr, k); continue; }
+    if (LV.sweep1(k)) { sweep_level(s, LV.ops.p, LV.nops, LV.max_i, SW_SOLVE_FWD, X, nullptr, k); continue; }
     LV.fs1.run(s, X, tmp, k, k);
     LV.fs2.run(s, X, tmp, k, k);
     LV.fs3.run(s, X, tmp, k, k);
@@ -722,7 +723,7 @@ void solve_half_bwd(const Fact& F, double* X, int k, double* tmp) {
   for (int lev = 1; lev <= F.tree->L; ++lev) {
     const Level& LV = F.levels[lev];
     RSF_PHASE(lvname("sv", lev), s);
-    if (LV.fused) { sweep_level(s, LV.ops.p, LV.nops, LV.max_i, SW_SOLVE_BWD, X, nullptr, k); continue; }
+    if (LV.sweep1(k)) { sweep_level(s, LV.ops.p, LV.nops, LV.max_i, SW_SOLVE_BWD, X, nullptr, k); continue; }
     colcopy(s, tmp, X, k, k, nullptr, LV.R.p, LV.rtot);
     LV.bs2.run(s, X, tmp, k, k);
     LV.bs3.run(s, X, tmp, k, k);
@@ -773,7 +774,7 @@ void apply_only_internal(const Fact& F, double* X, double* Y, int k) {
   for (int lev = L; lev >= 1; --lev) {
     const Level& LV = F.levels[lev];
     RSF_PHASE(lvname("ao", lev), s);
-    if (LV.fused) { sweep_level(s, LV.ops.p, LV.nops, LV.max_i, SW_AO_UP, X, Y, k); continue; }
+    if (LV.sweep1(k)) { sweep_level(s, LV.ops.p, LV.nops, LV.max_i, SW_AO_UP, X, Y, k); continue; }
     LV.ao1.run(s, X, Y, k, k);
     LV.ao2a.run(s, X, Y, k, k);
     LV.ao2b.run(s, X, Y, k, k);
@@ -785,7 +786,7 @@ void apply_only_internal(const Fact& F, double* X, double* Y, int k) {
   for (int lev = 1; lev <= L; ++lev) {
     const Level& LV = F.levels[lev];
     RSF_PHASE(lvname("ao", lev), s);
-    if (LV.fused) { sweep_level(s, LV.ops.p, LV.nops, LV.max_i, SW_AO_DN, X, Y, k); continue; }
+    if (LV.sweep1(k)) { sweep_level(s, LV.ops.p, LV.nops, LV.max_i, SW_AO_DN, X, Y, k); continue; }
     LV.ao3.run(s, X, Y, k, k);
     LV.ao4.run(s, X, Y, k, k);
   }

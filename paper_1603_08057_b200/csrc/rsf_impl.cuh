@@ -91,7 +91,9 @@ struct Level {
   GemmBatch ao1, ao2a, ao2b, ao3, ao4;  // apply-only (Sigma_i); ao2a alone when stacked
   // fused small-box sweeps (sweep.cuh): used when every box has |I_b| <= SWEEP_MAX_I
   bool fused = false;
+  bool fused1 = false;                // ops built for the one-right-hand-side fused sweep (k = 1)
   int max_i = 0, nops = 0;
+  bool sweep1(int k) const { return fused || (k == 1 && fused1); }
   DBuf<BoxOp> ops;
 };
 

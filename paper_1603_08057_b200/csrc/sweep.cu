@@ -228,6 +228,127 @@ __global__ void __launch_bounds__(NT) sweep_mma_kernel(const BoxOp* __restrict__
   }
 }
 
+// One right-hand side (k = 1): the box's x_S, x_R live in shared memory as plain vectors and
+// every step is a GEMV laid out for coalesced reads of the box matrix (the 1-RHS sweep is
+// bound by streaming T, L, E from HBM):
+//   TR = false, out[j] = sum_kk in[kk] Mat[kk + j ldm]: a warp per output j, lanes over kk;
+//   TR = true,  out[j] = sum_kk in[kk] Mat[j + kk ldm]: a thread per output j, loop over kk.
+constexpr int NT1 = 128;
+template <bool TR>
+__device__ __forceinline__ void vec_mv(double* __restrict__ out, const double* __restrict__ in, int K, int N,
+                                       const double* __restrict__ Mat, int ldm, double alpha, double beta) {
+  if (!TR) {
+    // a warp per 4 output columns, lanes over kk: 4 (x 2 unrolled) independent loads in flight
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int j0 = 4 * warp; j0 < N; j0 += 4 * (NT1 / 32)) {
+      const double* m[4];
+      bool ok[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { ok[u] = j0 + u < N; m[u] = Mat + (long long)(ok[u] ? j0 + u : j0) * ldm; }
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      int kk = lane;
+      for (; kk + 32 < K; kk += 64) {
+        const double x0 = in[kk], x1 = in[kk + 32];
+        double v[4], w[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) { v[u] = ok[u] ? __ldg(m[u] + kk) : 0.0; w[u] = ok[u] ? __ldg(m[u] + kk + 32) : 0.0; }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[u] = fma(x1, w[u], fma(x0, v[u], acc[u]));
+      }
+      for (; kk < K; kk += 32) {
+        const double x0 = in[kk];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[u] = fma(x0, ok[u] ? __ldg(m[u] + kk) : 0.0, acc[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        double a = acc[u];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        if (lane == 0 && ok[u]) out[j0 + u] = (beta == 0.0) ? alpha * a : fma(beta, out[j0 + u], alpha * a);
+      }
+    }
+  } else {
+    // a thread per output j (coalesced across the warp), 8 rows kk in flight
+    for (int j = threadIdx.x; j < N; j += NT1) {
+      double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+      int kk = 0;
+      for (; kk + 8 <= K; kk += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldg(Mat + j + (long long)(kk + u) * ldm);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[u] = fma(in[kk + u], v[u], acc[u]);
+      }
+      for (; kk < K; ++kk) acc[0] = fma(in[kk], __ldg(Mat + j + (long long)kk * ldm), acc[0]);
+      const double a = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+      out[j] = (beta == 0.0) ? alpha * a : fma(beta, out[j], alpha * a);
+    }
+  }
+}
+
+__device__ __forceinline__ void load_vec(double* __restrict__ dst, const double* __restrict__ X, const int* __restrict__ idx,
+                                         int cnt) {
+  for (int e = threadIdx.x; e < cnt; e += NT1) dst[e] = X[__ldg(idx + e)];
+}
+__device__ __forceinline__ void store_vec(const double* __restrict__ src, double* __restrict__ X, const int* __restrict__ idx,
+                                          int cnt) {
+  for (int e = threadIdx.x; e < cnt; e += NT1) X[__ldg(idx + e)] = src[e];
+}
+
+__global__ void __launch_bounds__(NT1) sweep1_kernel(const BoxOp* __restrict__ ops, int kind, double* X0, double* X1) {
+  extern __shared__ double sm[];
+  const BoxOp op = ops[blockIdx.x];
+  const int kb = op.kb, r = op.r;
+  double* xs = sm;
+  double* xr = sm + kb;
+  double* yr = xr + r;
+  if (kind == SW_SOLVE_FWD || kind == SW_SOLVE_BWD) {
+    load_vec(xs, X0, op.S, kb);
+    load_vec(xr, X0, op.R, r);
+    __syncthreads();
+    if (kind == SW_SOLVE_FWD) {
+      if (kb) vec_mv<false>(xr, xs, kb, r, op.T, kb, -1.0, 1.0);   // x_R -= T^T x_S
+      __syncthreads();
+      vec_mv<true>(yr, xr, r, r, op.L, r, 1.0, 0.0);               // y_R = L^-1 x_R
+      __syncthreads();
+      if (kb) vec_mv<true>(xs, yr, r, kb, op.E, kb, -1.0, 1.0);    // x_S -= E y_R
+    } else {
+      if (kb) vec_mv<false>(xr, xs, kb, r, op.E, kb, -1.0, 1.0);   // x_R -= E^T x_S
+      __syncthreads();
+      vec_mv<false>(yr, xr, r, r, op.L, r, 1.0, 0.0);              // y_R = L^-T x_R
+      __syncthreads();
+      if (kb) vec_mv<true>(xs, yr, r, kb, op.T, kb, -1.0, 1.0);    // x_S -= T y_R
+    }
+    __syncthreads();
+    store_vec(xs, X0, op.S, kb);
+    store_vec(yr, X0, op.R, r);
+  } else if (kind == SW_AO_UP) {
+    load_vec(xs, X0, op.S, kb);
+    load_vec(xr, X0, op.R, r);
+    __syncthreads();
+    if (kb) vec_mv<true>(xs, xr, r, kb, op.T, kb, 1.0, 1.0);       // x_S += T x_R
+    __syncthreads();
+    if (kb) vec_mv<false>(yr, xs, kb, r, op.E, kb, 1.0, 0.0);      // y_R = X_SR^T x_S
+    __syncthreads();
+    vec_mv<false>(yr, xr, r, r, op.L, r, 1.0, kb ? 1.0 : 0.0);     //     + X_RR x_R
+    __syncthreads();
+    store_vec(xs, X0, op.S, kb);
+    store_vec(yr, X1, op.R, r);
+  } else {   // SW_AO_DN: xs holds y_S, xr holds x_R, yr holds y_R
+    load_vec(xs, X1, op.S, kb);
+    load_vec(xr, X0, op.R, r);
+    load_vec(yr, X1, op.R, r);
+    __syncthreads();
+    if (kb) vec_mv<true>(xs, xr, r, kb, op.E, kb, 1.0, 1.0);       // y_S += X_SR x_R
+    __syncthreads();
+    if (kb) vec_mv<false>(yr, xs, kb, r, op.T, kb, 1.0, 1.0);      // y_R += T^T y_S
+    __syncthreads();
+    store_vec(xs, X1, op.S, kb);
+    store_vec(yr, X1, op.R, r);
+  }
+}
+
 bool sweep_mma_on() {
   static const bool on = getenv("RSF_SWEEP_MMA") && getenv("RSF_SWEEP_MMA")[0] == '1';
   return on;
@@ -240,7 +361,8 @@ int sweep_max_i() { return sweep_mma_on() ? SWEEP_MAX_I_MMA : SWEEP_MAX_I; }
 void sweep_level(cudaStream_t s, const BoxOp* d_ops, int nops, int max_i, SweepKind kind, double* X0, double* X1,
                  int k) {
   if (nops == 0 || k <= 0) return;
-  RSF_REQUIRE(max_i <= sweep_max_i(), ST_EINVAL, "sweep_level: box too large for the fused kernel");
+  RSF_REQUIRE(max_i <= (k == 1 ? SWEEP1_MAX_I : sweep_max_i()), ST_EINVAL,
+              "sweep_level: box too large for the fused kernel");
   static std::once_flag attr_once;
   std::call_once(attr_once, [&] {
     RSF_CUDA(cudaFuncSetAttribute(sweep_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -248,6 +370,17 @@ void sweep_level(cudaStream_t s, const BoxOp* d_ops, int nops, int max_i, SweepK
     RSF_CUDA(cudaFuncSetAttribute(sweep_mma_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     RSF_CUDA(cudaFuncSetAttribute(sweep_mma_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   });
+  static const bool k1_on = !(getenv("RSF_SWEEP1") && getenv("RSF_SWEEP1")[0] == '0');
+  if (k == 1 && k1_on) {   // one right-hand side: GEMV steps (HBM stream of the box matrices)
+    const size_t smem = (size_t)2 * max_i * sizeof(double);
+    for (int o = 0; o < nops; o += 65535) {
+      const unsigned nb = (unsigned)std::min(65535, nops - o);
+      sweep1_kernel<<<nb, NT1, smem, s>>>(d_ops + o, (int)kind, X0, X1);
+      count_launch();
+    }
+    RSF_LAUNCH_CHECK();
+    return;
+  }
   // shared memory: (kb + 2 r) * KC doubles <= 2 |I| * KC
   const int KC = (max_i <= 128) ? 32 : 16;
   const size_t smem = (size_t)2 * max_i * KC * sizeof(double);

@@ -28,6 +28,7 @@ enum SweepKind { SW_SOLVE_FWD = 0, SW_SOLVE_BWD = 1, SW_AO_UP = 2, SW_AO_DN = 3 
 
 constexpr int SWEEP_MAX_I = 128;       // largest |I_b| of the FMA fused kernel (measured: slower than the GEMM path above)
 constexpr int SWEEP_MAX_I_MMA = 256;   // ... of the DMMA fused kernel
+constexpr int SWEEP1_MAX_I = 512;      // largest |I_b| of the one-right-hand-side fused kernel (k = 1)
 // largest |I_b| the fused sweeps take with the current settings (RSF_SWEEP_MMA=1: DMMA kernel)
 int sweep_max_i();
 

@@ -32,10 +32,16 @@ hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if o
     os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6540.2
 for k in ks:
     b = C.c_double()
-    t = R.lib.rsf_debug_solve_bench(F.h, k, 20, C.byref(b))
+    t = R.lib.rsf_debug_solve_bench(F.h, k, int(os.environ.get("SOLVE_REPS", "20")), C.byref(b))
     if t <= 0:
         print("error", t, R.lib.rsf_last_error().decode(), flush=True)
         continue
     print(json.dumps({"config": cid, "nrhs": k, "seconds": t, "bytes_1rhs": b.value,
                       "GBps": b.value / t / 1e9, "frac_hbm": b.value / t / 1e9 / hbm,
                       "factor_bytes": info.factor_bytes, "levels": info.levels, "top": info.top_size}), flush=True)
+    if os.environ.get("RSF_KTRACE") == "1":
+        rows = [x.rsplit("=", 1) for x in R.lib.rsf_trace_dump().decode().split(";") if "=" in x]
+        rows = sorted(((float(v.split(",")[0]), k, v) for k, v in rows), reverse=True)[:25]
+        for sec, k, v in rows:
+            print(f"   {sec * 1e3:9.3f} ms  {k}  {v}", flush=True)
+        R.lib.rsf_profile_reset()
