@@ -140,19 +140,27 @@ def workload(cid: int, n: int | None):
 # O2 sample sizes of config 3's recipe (square grids: 24^2, 32^2, 40^2); the time of one l+g
 # evaluation is fitted as t = a n^b over the measured points (least squares in log-log) and
 # extrapolated to the workload's n with the FITTED exponent b (round 1 assumed the paper's 1.6)
-REF_SIZES = (576, 1024, 1600)
+REF_SIZES = (1024, 2304, 4096)
+# BLAS threads of the oracle: 1.  Measured on the GPU box's 16-core host (profiles/
+# r02_oracle_timing.jsonl): O2 at n = 576 / 1024 / 2304 takes 0.40 / 1.1 / 6.4 s on one thread and
+# 5.6 / 7.6 / 34.6 s with the BLAS on all 16 cores (thread overhead on its small dense blocks), so
+# the single-threaded oracle is the faster baseline at every size it can run in the bench.
+REF_THREADS = 1
 
 
 def _o2_eval_seconds(args, c, n_s):
+    from threadpoolctl import threadpool_limits
+
     from oracle.kernels import Kernel as OK
     from oracle.mle import rsf_mle_eval
     from workloads import philox_normal
     _, _, xy, w = workload(args.config, n_s)
     ok = OK(c.family, c.rho, c.sigma2, c.nugget, c.alpha, c.theta)
-    t = time.perf_counter()
-    # z = w: a valid observation vector for timing (the time does not depend on z)
-    rsf_mle_eval(ok, xy, w, c.eps_fact, c.eps_peel, c.leaf, c.seed, philox_normal, block=8)
-    return time.perf_counter() - t
+    with threadpool_limits(REF_THREADS):
+        t = time.perf_counter()
+        # z = w: a valid observation vector for timing (the time does not depend on z)
+        rsf_mle_eval(ok, xy, w, c.eps_fact, c.eps_peel, c.leaf, c.seed, philox_normal, block=8)
+        return time.perf_counter() - t
 
 
 def _fit_and_extrapolate(pts, n_full):
@@ -192,7 +200,7 @@ def run_reference(args, rank):
         return
     c, n_full, _, _ = workload(args.config, args.n)
     for _ in range(args.warmup):
-        _o2_eval_seconds(args, c, REF_SIZES[0])
+        _o2_eval_seconds(args, c, 576)
     pts = []
     for it in range(args.steps):
         n_s = REF_SIZES[it % len(REF_SIZES)]
@@ -206,9 +214,10 @@ def run_reference(args, rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_full * 1e3,
         "higher_is_better": True, "scaling": "strong" if args.gpus > 1 else "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic", "config": _config_dict(c, n_full, args),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": host["cores"], "kind": "oracle",
-                         "sample": f"O2 oracle (numpy/scipy RSF + weak peeling, all {host['cores']} host cores "
-                                   f"through the BLAS) full l+g evaluations of config {c.cid}'s recipe at "
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": REF_THREADS, "kind": "oracle",
+                         "sample": f"O2 oracle (numpy/scipy RSF + weak peeling, BLAS on {REF_THREADS} thread of "
+                                   f"the {host['cores']}-core host: faster than all cores at these sizes) "
+                                   f"full l+g evaluations of config {c.cid}'s recipe at "
                                    f"n = {', '.join(meas)} (median seconds {meas}); fitted t ~ n^{b:.2f}; "
                                    f"value = extrapolation to n = {n_full} with the fitted exponent",
                          "measured_points": pts, "fitted_exponent": b, "host": host},
@@ -234,8 +243,9 @@ def cpu_baseline_sample(args, c):
     n_full = args.n or c.n
     t_full, b = _fit_and_extrapolate(pts, n_full)
     host = _host_info()
-    return {"value": 1.0 / t_full, "unit": UNIT, "cores": host["cores"], "kind": "oracle",
-            "sample": f"O2 oracle (numpy/scipy RSF + weak peeling) one full l+g evaluation of config {c.cid}'s "
+    return {"value": 1.0 / t_full, "unit": UNIT, "cores": REF_THREADS, "kind": "oracle",
+            "sample": f"O2 oracle (numpy/scipy RSF + weak peeling, BLAS on {REF_THREADS} thread of the "
+                      f"{host['cores']}-core host) one full l+g evaluation of config {c.cid}'s "
                       f"recipe at each n in {list(REF_SIZES)}: {[round(t, 2) for _, t in pts]} s; fitted "
                       f"t ~ n^{b:.2f}; value = extrapolation to n = {n_full} with the fitted exponent "
                       f"(profiles/ has the 1-thread / all-core study at larger n)",
