@@ -441,6 +441,63 @@ __global__ void __launch_bounds__(NT) rank_kernel(const RDesc* __restrict__ d0) 
   }
 }
 
+// The same rank test, parallel over columns: a warp per column j holds the panel rows J + lane
+// (coalesced), a suffix scan over the lanes gives sum_{r >= J+q} of the squares for every q at
+// once (rows r <= j only inside the panel: below the diagonal are Householder vectors), and the
+// per-q maxima over the columns go to mxb by an atomic max on the IEEE bit patterns (exact and
+// order-independent for non-negative doubles, so the result is deterministic).  rank_finish_kernel
+// applies the threshold and resets mxb for the next block.  (The one-CTA-per-problem rank_kernel
+// above kept 33 maxima in a dynamically indexed local array: 280-byte stack, uncoalesced reads.)
+__global__ void __launch_bounds__(NT) rank_cols_kernel(const RDesc* __restrict__ d0, unsigned long long* mxb) {
+  const RDesc d = d0[blockIdx.y];
+  if (d.flag[0]) return;
+  const int J = d.J, nbp = d.nbp, j1 = J + nbp;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ double red[NT / 32][QR_NB + 1];
+  double mq = 0.0, mb = 0.0;   // running max of this lane's q = lane, and of q = nbp (trailing only)
+  for (int j = J + blockIdx.x * (NT / 32) + warp; j < d.c; j += gridDim.x * (NT / 32)) {
+    const double* a = d.A + (long long)j * d.lda;
+    const int r = J + lane;
+    const double x = (lane < nbp && (j >= j1 || r <= j)) ? a[r] : 0.0;
+    double sfx = x * x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double t = __shfl_down_sync(0xffffffffu, sfx, o);
+      if (lane + o < 32) sfx += t;
+    }
+    const double base = (j >= j1) ? d.nrm2[j] : 0.0;
+    if (lane < nbp) mq = fmax(mq, base + sfx);
+    mb = fmax(mb, base);
+  }
+  red[warp][lane] = mq;
+  if (lane == 0) red[warp][QR_NB] = mb;
+  __syncthreads();
+  if (threadIdx.x <= QR_NB && threadIdx.x <= nbp) {
+    const int q = threadIdx.x == nbp ? QR_NB : threadIdx.x;
+    double v = 0.0;
+    for (int w = 0; w < NT / 32; ++w) v = fmax(v, red[w][q]);
+    atomicMax(mxb + (long long)d.id * (QR_NB + 1) + q, (unsigned long long)__double_as_longlong(v));
+  }
+}
+
+__global__ void rank_finish_kernel(const RDesc* __restrict__ d0, unsigned long long* mxb) {
+  const RDesc d = d0[blockIdx.x];
+  unsigned long long* m = mxb + (long long)d.id * (QR_NB + 1);
+  if (threadIdx.x == 0 && !d.flag[0]) {
+    const int J = d.J, nbp = d.nbp, j1 = J + nbp;
+    const double thr = d.eps * (*d.ref);
+    int k = -1;
+    for (int q = 0; q <= nbp; ++q) {
+      const double v = __longlong_as_double((long long)m[q == nbp ? QR_NB : q]);
+      if (sqrt(v) <= thr) { k = J + q; break; }
+    }
+    if (k < 0 && j1 >= min(d.m, d.c)) k = j1;
+    if (k >= 0) { d.flag[0] = 1; d.flag[1] = k; d.flag[2] = j1; }
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q <= QR_NB; q += blockDim.x) m[q] = 0ull;
+}
+
 // inverse of the upper-triangular block R(J:j1, J:j1) -> R11i (ld QR_NB)
 __global__ void r11_inv_kernel(const RDesc* __restrict__ d0) {
   const RDesc d = d0[blockIdx.x];
@@ -619,6 +676,8 @@ RRQRResult rrqr_batched(cudaStream_t s, const std::vector<RRQRProb>& probs, doub
   DBuf<double> Y(yt, s), Z(yt, s), zn(ct, s), nrm2(ct, s), V(vt, s), W(wt, s), W2(wt, s), Wt(wt, s);
   DBuf<double> Tsc((size_t)P * QR_NB * QR_NB, s), R11i((size_t)P * QR_NB * QR_NB, s), ref(P, s);
   DBuf<int> sw((size_t)P * QR_NB, s), flag((size_t)3 * P, s);
+  DBuf<unsigned long long> mxb((size_t)P * (QR_NB + 1), s);   // per-problem maxima of the rank test
+  RSF_CUDA(cudaMemsetAsync(mxb.p, 0, (size_t)P * (QR_NB + 1) * sizeof(unsigned long long), s));
   std::vector<RDesc> base(P);
   for (int i = 0; i < P; ++i) {
     const auto& p = probs[i];
@@ -724,8 +783,19 @@ RRQRResult rrqr_batched(cudaStream_t s, const std::vector<RRQRProb>& probs, doub
       trail_norm_kernel<<<dim3((unsigned)std::min(256, (maxc + 7) / 8), na), NT, 0, s>>>(dd.p);
       count_launch();
     }
-    rank_kernel<<<na, NT, 0, s>>>(dd.p);
-    count_launch();
+    {
+      static const bool old_rank = getenv("RSF_RANK_OLD") && getenv("RSF_RANK_OLD")[0] == '1';
+      if (old_rank) {
+        rank_kernel<<<na, NT, 0, s>>>(dd.p);
+        count_launch();
+      } else {
+        int cmax = 0;
+        for (auto& d : dv) cmax = std::max(cmax, d.c - d.J);
+        rank_cols_kernel<<<dim3((unsigned)std::max(1, std::min(512, (cmax + 7) / 8)), na), NT, 0, s>>>(dd.p, mxb.p);
+        rank_finish_kernel<<<na, 64, 0, s>>>(dd.p, mxb.p);
+        count_launch(2);
+      }
+    }
     RSF_LAUNCH_CHECK();
     bool last = false;
     for (size_t a = 0; a < dv.size(); ++a) last |= (J + dv[a].nbp >= std::min(dv[a].m, dv[a].c));
