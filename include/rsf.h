@@ -145,6 +145,10 @@ rsf_status rsf_ctx_group(rsf_ctx ctx, int* rank, int* world);
 /* column slice [lo, hi) that part `part` of `parts` owns when k probe columns are split
  * (contiguous; sizes differ by at most one, larger first).  Host only (tests). */
 void rsf_debug_col_slice(int64_t k, int parts, int part, int64_t* lo, int64_t* hi);
+/* 1 if rank `rank` of a `world`-rank group runs trace job `job` of an evaluation with `njobs` jobs
+ * (jobs dealt to min(njobs, world) rank groups), 0 if not, -1 on bad arguments.
+ * Host only (tests). */
+int rsf_debug_job_runs(int njobs, int world, int rank, int job);
 void rsf_ctx_destroy(rsf_ctx ctx);
 /* Order the context after the caller: everything enqueued on `stream` so far (an event recorded
  * there) completes before the context stream runs further work.  stream = NULL is the legacy

@@ -240,6 +240,12 @@ rsf_status rsf_ctx_group(rsf_ctx ctx, int* rank, int* world) {
   });
 }
 
+int rsf_debug_job_runs(int njobs, int world, int rank, int job) {
+  if (njobs < 1 || world < 1 || rank < 0 || rank >= world || job < 0 || job >= njobs) return -1;
+  const int G = rsf::Comm::job_groups(njobs, world);
+  return (world == 1 || job % G == rank % G) ? 1 : 0;
+}
+
 void rsf_debug_col_slice(int64_t k, int parts, int part, int64_t* lo, int64_t* hi) {
   long long a = 0, b = 0;
   if (parts >= 1 && part >= 0 && part < parts && k >= 0) rsf::Comm::slice(k, parts, part, &a, &b);

@@ -101,6 +101,19 @@ void Comm::allsum(cudaStream_t s, double* v, int cnt) const {
   }
 }
 
+void Comm::allgather_host(cudaStream_t s, const double* in, int cnt, double* out) const {
+  if (world <= 1) {
+    std::copy(in, in + cnt, out);
+    return;
+  }
+  DBuf<double> g((size_t)cnt * world, s);
+  RSF_CUDA(cudaMemcpyAsync(g.p + (size_t)rank * cnt, in, cnt * sizeof(double), cudaMemcpyHostToDevice, s));
+  check(api().all_gather(g.p + (size_t)rank * cnt, g.p, (size_t)cnt, ncclDouble, (ncclComm_t)nccl, s),
+        "ncclAllGather");
+  const std::vector<double> h = g.to_host((size_t)cnt * world);
+  std::copy(h.begin(), h.end(), out);
+}
+
 void nccl_unique_id(unsigned char out[128]) {
   ncclUniqueId id;
   check(api().get_unique_id(&id), "ncclGetUniqueId");
@@ -125,6 +138,12 @@ void* nccl_split(void* comm, int rank) {
   ncclComm_t c = nullptr;
   check(api().split((ncclComm_t)comm, 0, rank, &c, nullptr), "ncclCommSplit");
   return c;
+}
+
+void* nccl_split_color(void* comm, int color, int key) {
+  ncclComm_t c = nullptr;
+  check(api().split((ncclComm_t)comm, color < 0 ? NCCL_SPLIT_NOCOLOR : color, key, &c, nullptr), "ncclCommSplit");
+  return color < 0 ? nullptr : c;
 }
 
 void nccl_destroy(void* comm) {

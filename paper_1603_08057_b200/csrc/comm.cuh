@@ -14,6 +14,7 @@
 // gather layout (each emulated rank's slice is computed in turn and copied into its slot of
 // the gather buffer) -- the test of the partition and exchange layout on one GPU.
 #pragma once
+#include <algorithm>
 #include <mutex>
 #include <vector>
 
@@ -49,6 +50,11 @@ struct Comm {
   void merge(cudaStream_t s, const double* gath, long long slot, long long k, int n, double* Y) const;
   // sum of cnt host doubles over the ranks, added in rank order (deterministic)
   void allsum(cudaStream_t s, double* v, int cnt) const;
+  // every rank's cnt host doubles, rank-ordered into out (world * cnt)
+  void allgather_host(cudaStream_t s, const double* in, int cnt, double* out) const;
+  // trace jobs of one evaluation over the ranks: G = min(njobs, world) groups,
+  // rank r in group r mod G, job j run by group j mod G (its ranks split the job's probe columns)
+  static int job_groups(int njobs, int world) { return std::max(1, std::min(njobs, world)); }
 };
 
 // NCCL entry points (dlopen'd): 128-byte unique id, communicator from (id, rank, world) or
@@ -57,6 +63,8 @@ void nccl_unique_id(unsigned char out[128]);
 void* nccl_init_rank(const unsigned char id[128], int rank, int world);
 void nccl_query(void* comm, int* rank, int* world);
 void* nccl_split(void* comm, int rank);
+// split with a color (< 0: this rank joins no new communicator and gets nullptr)
+void* nccl_split_color(void* comm, int color, int key);
 void nccl_destroy(void* comm);
 
 }  // namespace rsf

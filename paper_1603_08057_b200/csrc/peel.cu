@@ -1337,15 +1337,19 @@ EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KP
     f_ready.get();
     if (f_event && ctx_stream(ctx) != s) RSF_CUDA(cudaStreamWaitEvent(ctx_stream(ctx), f_event, 0));
   };
-  // sharded evaluation: one communicator per trace job, split from the group's
-  // communicator here, on the calling thread, in job order (the same on every rank)
+  // sharded evaluation: the jobs are dealt to G = min(jobs, ranks) rank groups
+  // (job j to group j mod G, rank r in group r mod G); a job's communicator holds its group's
+  // ranks, which split its probe columns.  Communicators are split from the group's communicator
+  // on the calling thread, in job order (the same on every rank).
   auto job_comm = [&](int j) -> const Comm* { return ctx.comm.world > 1 ? &ctx.job_comms[j] : &ctx.comm; };
   std::vector<std::function<void()>> jobs;
+  std::vector<int> job_theta;   // theta index of a general job, -1 for the Tr(F^-1) job
   bool need_trinv = false;
   for (int i = 0; i < p; ++i) {
     const int w = theta[i];
     if (w == W_SIGMA2 || w == W_NUGGET) { need_trinv = true; continue; }
     const int jid = (int)jobs.size();
+    job_theta.push_back(i);
     jobs.push_back([&, i, w, jid]() {
       double t1 = now_s();
       auto Fi = factor(ctx, tree, kp, w, eps, o);
@@ -1366,6 +1370,7 @@ EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KP
   }
   if (need_trinv) {
     const int jid = (int)jobs.size();
+    job_theta.push_back(-1);
     jobs.push_back([&, jid]() {
       wait_f();
       const double t1 = now_s();
@@ -1375,13 +1380,31 @@ EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KP
     });
   }
 
-  if (ctx.comm.world > 1)
-    while (ctx.job_comms.size() < jobs.size()) {
-      Comm jc = ctx.comm;
-      jc.nccl = nccl_split(ctx.comm.nccl, ctx.comm.rank);
+  const int njobs = (int)jobs.size();
+  const int NG = Comm::job_groups(njobs, ctx.comm.world);
+  const int my_group = ctx.comm.rank % NG;
+  auto mine = [&](int j) { return ctx.comm.world == 1 || j % NG == my_group; };
+  if (ctx.comm.world > 1 && ctx.job_comms_njobs != njobs) {
+    for (auto& jc : ctx.job_comms)
+      if (jc.owned) nccl_destroy(jc.nccl);
+    ctx.job_comms.assign(njobs, Comm{});
+    for (int j = 0; j < njobs; ++j) {
+      void* c = nccl_split_color(ctx.comm.nccl, mine(j) ? j % NG : -1, ctx.comm.rank);
+      if (!c) continue;
+      Comm jc;
+      jc.nccl = c;
       jc.owned = true;
-      ctx.job_comms.push_back(jc);
+      nccl_query(c, &jc.rank, &jc.world);
+      ctx.job_comms[j] = jc;
     }
+    ctx.job_comms_njobs = njobs;
+  }
+  {   // this rank runs the jobs of its group only
+    std::vector<std::function<void()>> run;
+    for (int j = 0; j < njobs; ++j)
+      if (mine(j)) run.push_back(jobs[j]);
+    jobs.swap(run);
+  }
 
   // F ~ Sigma (solve-only), u = F^-1 z (k = 1), q0 = z^T u; profile terms (Eq. prof)
   double Qp = 0.0;
@@ -1484,7 +1507,8 @@ EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KP
     };
     bool oom = is_oom(main_err);
     for (auto& e : err) oom = oom || is_oom(e);
-    if (oom) {
+    // (on a rank group a one-rank rerun would leave its peers' collectives unmatched: report)
+    if (oom && ctx.comm.world == 1) {
       for (size_t j = 0; j < jobs.size(); ++j) {
         cudaStreamSynchronize(ctx.aux[j]);
         dev_cache_trim(ctx.aux[j]);
@@ -1500,6 +1524,43 @@ EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KP
       if (main_err) std::rethrow_exception(main_err);
       for (auto& e : err)
         if (e) std::rethrow_exception(e);
+    }
+  }
+  if (ctx.comm.world > 1 && njobs > 0) {
+    // every job's results from the lowest rank of the group that ran it (all members hold the
+    // same values): one all-gather of fixed-size records over the whole group
+    constexpr int RS = 12 + 2 * 32;
+    std::vector<double> rec((size_t)njobs * RS, 0.0), all((size_t)ctx.comm.world * njobs * RS);
+    for (int j = 0; j < njobs; ++j) {
+      if (!mine(j)) continue;
+      double* r = rec.data() + (size_t)j * RS;
+      const int i = job_theta[j];
+      const PeelDiag& pd = i >= 0 ? R.pd[i] : pd_trinv;
+      r[0] = 1.0;
+      r[1] = i >= 0 ? qv[i] : utu;
+      r[2] = i >= 0 ? trv[i] : trinv;
+      r[3] = i >= 0 ? tcomp[i] : 0.0;
+      r[4] = i >= 0 ? tsol[i] : 0.0;
+      r[5] = i >= 0 ? tpl[i] : t_trinv;
+      r[6] = i >= 0 ? ffl[i] : 0.0;
+      r[7] = pd.nL; r[8] = pd.cancellation; r[9] = pd.applies; r[10] = pd.seconds; r[11] = pd.flops;
+      for (size_t l = 0; l < pd.cols.size() && l < 32; ++l) { r[12 + l] = pd.cols[l]; r[44 + l] = pd.rank_max[l]; }
+    }
+    ctx.comm.allgather_host(s, rec.data(), njobs * RS, all.data());
+    for (int j = 0; j < njobs; ++j) {
+      const double* r = nullptr;
+      for (int rk = 0; rk < ctx.comm.world && !r; ++rk)
+        if (all[((size_t)rk * njobs + j) * RS] == 1.0) r = all.data() + ((size_t)rk * njobs + j) * RS;
+      RSF_REQUIRE(r != nullptr, ST_ENCCL, "sharded evaluation: a trace job ran on no rank");
+      const int i = job_theta[j];
+      PeelDiag& pd = i >= 0 ? R.pd[i] : pd_trinv;
+      if (i >= 0) { qv[i] = r[1]; trv[i] = r[2]; tcomp[i] = r[3]; tsol[i] = r[4]; tpl[i] = r[5]; ffl[i] = r[6]; }
+      else { utu = r[1]; trinv = r[2]; t_trinv = r[5]; }
+      pd.nL = (int)r[7]; pd.cancellation = r[8]; pd.applies = r[9]; pd.seconds = r[10]; pd.flops = r[11];
+      const int nl = std::min(32, tree->L + 1);
+      pd.cols.assign(nl, 0);
+      pd.rank_max.assign(nl, 0);
+      for (int l = 0; l < nl; ++l) { pd.cols[l] = (int)r[12 + l]; pd.rank_max[l] = (int)r[44 + l]; }
     }
   }
   R.t_peel += t_trinv;

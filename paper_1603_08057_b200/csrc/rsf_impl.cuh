@@ -28,7 +28,8 @@ struct Ctx {
   std::vector<cudaStream_t> aux;   // streams of the concurrent trace jobs of gp_mle_eval (created lazily)
   bool own_stream = false;
   Comm comm;                        // rank group of a sharded evaluation (world 1: none)
-  std::vector<Comm> job_comms;      // one split communicator per concurrent trace job
+  std::vector<Comm> job_comms;      // one split communicator per trace job (its group's ranks)
+  int job_comms_njobs = -1;         // number of jobs job_comms was built for
   std::string last_error;
 };
 

@@ -94,3 +94,26 @@ def test_column_slices_partition_every_block():
                 assert b == c
             sizes = [b - a for a, b in sl]
             assert max(sizes) - min(sizes) <= 1 and sizes == sorted(sizes, reverse=True)
+
+
+def test_trace_jobs_dealt_to_rank_groups():
+    """include/rsf.h rsf_debug_job_runs: with J jobs on W ranks there are G = min(J, W) groups;
+    every job runs on at least one rank, the groups partition the ranks (sizes differ by at most
+    one), and every rank of a group runs the same jobs."""
+    import paper_1603_08057_b200 as R
+    for J in (1, 2, 3, 4):
+        for W in (1, 2, 3, 4, 5, 8):
+            runs = [[R.lib.rsf_debug_job_runs(J, W, r, j) for j in range(J)] for r in range(W)]
+            assert all(v in (0, 1) for row in runs for v in row)
+            for j in range(J):
+                assert sum(runs[r][j] for r in range(W)) >= 1
+            G = min(J, W)
+            groups = {}
+            for r in range(W):
+                groups.setdefault(tuple(runs[r]), []).append(r)
+            assert len(groups) == G
+            sizes = [len(v) for v in groups.values()]
+            assert max(sizes) - min(sizes) <= 1
+            if W >= J:
+                assert all(sum(row) == 1 for row in runs)   # one job per rank group
+    assert R.lib.rsf_debug_job_runs(0, 2, 0, 0) == -1
