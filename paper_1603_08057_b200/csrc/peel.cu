@@ -629,7 +629,8 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
     // per-level state (reset when the width grows)
     std::vector<int> rb(nb, 0);                   // basis size r_i
     std::vector<DBuf<double>> Vb(nb), Ab(nb);     // V_i (n_i x r_i, ld n_i), A_i = W_i^T V_i (c x r_i, ld c)
-    std::vector<int> vcap(nb, 0);                 // allocated columns of V_i / A_i
+    std::vector<int> vcap(nb, 0);                 // allocated columns of V_i / A_i (grown exactly)
+    std::vector<int> vmax(nb, 0);                 // most columns V_i can take: min(n_i, c per sibling group)
     // per ordered pair (index: b * 4 + position of the sibling in the family)
     struct PairData { int k = 0, rz = 0; double *Z = nullptr, *X = nullptr, *Lm = nullptr, *Gi = nullptr; };
     std::vector<PairData> pdat((size_t)nb * 4);
@@ -640,14 +641,27 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
       for (auto& v : Vb) v.release();
       for (auto& v : Ab) v.release();
       // fixed capacity per box: every probe group adds at most c directions (no regrowth)
+      // V_i and A_i grow to exactly the columns they take (reallocated as the chunks add
+      // directions) instead of being reserved at their upper bound min(n_i, 3c): at config 4
+      // the bound reserved ~50 GB per level at levels 1-3 against 17-35 GB of final bases
+      // (the upper bound is still reserved up front when it is small -- <= 16 GB for the level:
+      // fewer, fixed-size allocations; config 3 reserves 6 GB at level 1)
       std::fill(vcap.begin(), vcap.end(), 0);
+      double vres = 0;
       for (int b = 0; b < nb; ++b) {
         const int ng = bx[b].fam1 - bx[b].fam0 - 1;
-        if (ng <= 0) continue;
-        vcap[b] = std::min(bx[b].ni, ng * c);
-        Vb[b].alloc((size_t)bx[b].ni * vcap[b], s);
-        Ab[b].alloc((size_t)c * vcap[b], s);
+        vmax[b] = ng <= 0 ? 0 : std::min(bx[b].ni, ng * c);
+        vres += 8.0 * bx[b].ni * (double)vmax[b];
       }
+      static const double vres_max = getenv("RSF_VRESERVE_GB") ? atof(getenv("RSF_VRESERVE_GB")) * (1ull << 30)
+                                                               : 16.0 * (1ull << 30);
+      if (vres <= vres_max)
+        for (int b = 0; b < nb; ++b) {
+          if (vmax[b] == 0) continue;
+          vcap[b] = vmax[b];
+          Vb[b].alloc((size_t)bx[b].ni * vcap[b], s);
+          Ab[b].alloc((size_t)c * vcap[b], s);
+        }
       arenas.clear();
       for (auto& q : pdat) q = PairData{};
       bool fail = false;
@@ -807,9 +821,22 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
             std::vector<long long> qo(B), ro(B);
             for (size_t x = 0; x < B; ++x) {
               const int i = act[x0 + x];
-              qq[x] = std::min<int>(qq[x], std::min<int>((int)(cccap[x0 + x] - rb[i]), vcap[i] - rb[i]));
+              qq[x] = std::min<int>(qq[x], std::min<int>((int)(cccap[x0 + x] - rb[i]), vmax[i] - rb[i]));
               qo[x] = qt; qt += (long long)bx[i].ni * qq[x];
               ro[x] = rt; rt += (long long)qq[x] * qq[x];
+              if (rb[i] + qq[x] > vcap[i]) {   // grow V_i (n_i x r, ld n_i) and A_i (c x r, ld c)
+                const int nc = rb[i] + qq[x];
+                DBuf<double> nv((size_t)bx[i].ni * nc, s), na((size_t)c * nc, s);
+                if (rb[i] > 0) {
+                  RSF_CUDA(cudaMemcpyAsync(nv.p, Vb[i].p, (size_t)bx[i].ni * rb[i] * sizeof(double),
+                                           cudaMemcpyDeviceToDevice, s));
+                  RSF_CUDA(cudaMemcpyAsync(na.p, Ab[i].p, (size_t)c * rb[i] * sizeof(double),
+                                           cudaMemcpyDeviceToDevice, s));
+                }
+                Vb[i] = std::move(nv);
+                Ab[i] = std::move(na);
+                vcap[i] = nc;
+              }
             }
             DBuf<double> Q0(std::max<long long>(qt, 1), s), Ri(std::max<long long>(rt, 1), s);
             // the new directions are formed in place in the free columns of V_i
@@ -1106,10 +1133,11 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
     // ---- subtraction batches of G^(lev)
     PL.V.clear();
     PL.V.resize(nb);
-    {
+    {   // exactly sized buffers move over; reserved ones are copied to their size box by box
       std::vector<CopyProb> cpv;
       for (int b = 0; b < nb; ++b) {
         if (rb[b] == 0) continue;
+        if (vcap[b] == rb[b]) { PL.V[b] = std::move(Vb[b]); continue; }
         PL.V[b].alloc((size_t)bx[b].ni * rb[b], s);
         cpv.push_back(CopyProb{Vb[b].p, bx[b].ni, PL.V[b].p, bx[b].ni, bx[b].ni, rb[b], 1.0});
       }
