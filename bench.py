@@ -456,7 +456,16 @@ def main():
         "config": _config_dict(c, n, args), "clocks": clocks, "gpu_launches": int(launches),
         "e2e": e2e, "roofline": roofline, "solve_roofline": solve_rl, "factor_roofline": factor_rl,
         "phases_s": {"tree": d.t_tree, "factor": d.t_factor, "compress": d.t_compress,
-                     "solve": d.t_solve, "peel": d.t_peel, "total": d.t_total},
+                     "solve": d.t_solve, "peel": d.t_peel, "jobs_wall": d.t_jobs_wall, "total": d.t_total,
+                     "note": f"compress/solve/peel are sums over the {d.jobs} trace jobs, which ran "
+                             f"{'concurrently' if d.concurrent else 'serially'} (jobs_wall: their wall time)"},
+        "peel_levels": [{"theta": c.theta[i],
+                         "cols": [d.peel[i].cols[l] for l in range(1, d.peel[i].levels + 1)],
+                         "rank_min": [d.peel[i].rank_min[l] for l in range(1, d.peel[i].levels + 1)],
+                         "rank_med": [d.peel[i].rank_med[l] for l in range(1, d.peel[i].levels + 1)],
+                         "rank_max": [d.peel[i].rank_max[l] for l in range(1, d.peel[i].levels + 1)],
+                         "stored_GB": d.peel[i].stored_bytes / 1e9} for i in range(len(c.theta))],
+        "serial_fallback": int(d.serial_fallback),
         "ell": r.ell, "grad": r.grad, "z": z_src,
     }
     if world == 1 and not args.no_cpu_baseline:

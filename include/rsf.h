@@ -111,6 +111,9 @@ typedef struct {
   double cancellation;       /* sum |diag(H)| / |Tr| (P:597-599 diagnostic) */
   double applies;            /* operator columns applied (G X column count) */
   double seconds;
+  int32_t rank_min[32];      /* min / median eps_peel-rank of the sibling blocks at level l */
+  int32_t rank_med[32];
+  double stored_bytes;       /* bytes of the peeled representation (bases V_i + cores) */
 } rsf_peel_diag;
 
 typedef struct {
@@ -121,6 +124,13 @@ typedef struct {
   double kernel_launches;    /* CUDA kernels launched by the call */
   rsf_fact_diag fact;        /* the Sigma factor */
   rsf_peel_diag peel[4];     /* per theta component (sigma2/nugget share the F^-1 peel) */
+  /* t_compress, t_solve and t_peel above are SUMS over the trace jobs, which may run concurrently
+   * (and then exceed t_total); t_jobs_wall is the wall time of the job section itself */
+  double t_jobs_wall;
+  int32_t jobs;              /* trace jobs of the evaluation (one per general theta_i, + Tr(F^-1)) */
+  int32_t concurrent;        /* 1: the jobs ran concurrently on their own streams */
+  int32_t serial_fallback;   /* 1: out of memory side by side, the evaluation was redone serially */
+  int32_t groups;            /* rank sub-groups the jobs were dealt to (1 on a single GPU) */
 } rsf_eval_diag;
 
 void rsf_opts_default(rsf_opts* out);

@@ -39,7 +39,8 @@ class rsf_fact_diag(C.Structure):
 class rsf_peel_diag(C.Structure):
     _fields_ = [("levels", C.c_int32), ("cols", C.c_int32 * 32), ("rank_max", C.c_int32 * 32),
                 ("nL", C.c_int32), ("cancellation", C.c_double), ("applies", C.c_double),
-                ("seconds", C.c_double)]
+                ("seconds", C.c_double), ("rank_min", C.c_int32 * 32), ("rank_med", C.c_int32 * 32),
+                ("stored_bytes", C.c_double)]
 
 
 class rsf_eval_diag(C.Structure):
@@ -48,7 +49,8 @@ class rsf_eval_diag(C.Structure):
                 ("t_compress", C.c_double), ("t_solve", C.c_double), ("t_peel", C.c_double),
                 ("t_total", C.c_double), ("flops_factor", C.c_double),
                 ("kernel_launches", C.c_double), ("fact", rsf_fact_diag),
-                ("peel", rsf_peel_diag * 4)]
+                ("peel", rsf_peel_diag * 4), ("t_jobs_wall", C.c_double), ("jobs", C.c_int32),
+                ("concurrent", C.c_int32), ("serial_fallback", C.c_int32), ("groups", C.c_int32)]
 
 
 EXPORTS = ["rsf_opts_default", "rsf_ctx_create", "rsf_ctx_destroy", "rsf_factor", "rsf_fact_destroy",

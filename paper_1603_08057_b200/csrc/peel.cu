@@ -508,6 +508,9 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
   dfail.zero();
   pd.cols.assign(L + 1, 0);
   pd.rank_max.assign(L + 1, 0);
+  pd.rank_min.assign(L + 1, 0);
+  pd.rank_med.assign(L + 1, 0);
+  std::vector<int> lev_ranks;
   int prev_rank = -1;
   const int kb = std::max(16, o.probe_block);
   // bytes of transient per-batch buffers, and of W_i^T kept for a whole probe group (else the
@@ -666,6 +669,7 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
       for (auto& q : pdat) q = PairData{};
       bool fail = false;
       mr = 0;
+      lev_ranks.clear();
       for (int g : gorder) {
         if (gcount[g] == 0) continue;
         // boxes i with a sibling j in quadrant g (at most one per family)
@@ -936,6 +940,7 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
         }
         for (size_t x = 0; x < NA; ++x) mr = std::max(mr, kk[x]);
         if (mr > c - o.oversample && c < cmax) { fail = true; break; }
+        lev_ranks.insert(lev_ranks.end(), kk.begin(), kk.end());
         // per-pair basis Z_ij = orth(C_ij(:, piv[0:k])) in the coordinates of V_i
         // (U_ij = V_i Z_ij = orth(Y_ij), R-N) and the left core factor
         //   X_ij = W_i^T U_ij,  Lm_ij = X_ij^+ (W_i^T Y_ij)       (Eq. lowrankapprox)
@@ -1051,6 +1056,11 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
     }
     pd.cols[lev] = c;
     pd.rank_max[lev] = mr;
+    if (!lev_ranks.empty()) {
+      std::sort(lev_ranks.begin(), lev_ranks.end());
+      pd.rank_min[lev] = lev_ranks.front();
+      pd.rank_med[lev] = lev_ranks[lev_ranks.size() / 2];
+    }
     prev_rank = mr;
     for (auto& v : Ab) v.release();
 
@@ -1146,6 +1156,7 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
     }
     double vbytes = 0;
     for (auto& v : PL.V) vbytes += 8.0 * v.n;
+    pd.stored_bytes += vbytes + 8.0 * PL.Brow.n;
     PL.g1.reset(false, false);
     PL.g2.reset(false, true);
     PL.g3.reset(false, true);
@@ -1314,11 +1325,13 @@ void fill_peel_diag(const PeelDiag& d, rsf_peel_diag* out) {
   for (size_t l = 0; l < d.cols.size() && l < 32; ++l) {
     out->cols[l] = d.cols[l];
     out->rank_max[l] = d.rank_max[l];
+    if (l < d.rank_min.size()) { out->rank_min[l] = d.rank_min[l]; out->rank_med[l] = d.rank_med[l]; }
   }
   out->nL = d.nL;
   out->cancellation = d.cancellation;
   out->applies = d.applies;
   out->seconds = d.seconds;
+  out->stored_bytes = d.stored_bytes;
 }
 
 // ----------------------------------------------------------------- Alg. 1
@@ -1475,12 +1488,18 @@ EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KP
   };
 
   static const bool par_on = !(getenv("RSF_PAR_TRACES") && getenv("RSF_PAR_TRACES")[0] == '0');
+  R.jobs = njobs;
+  R.groups = NG;
+  double tj0 = 0.0;
   // (the profiler and the launch trace synchronise one stream at a time: serial then)
   if (!par_on || jobs.size() < 2 || Prof::enabled() || KTrace::on()) {
     main_part();
     f_promise.set_value();
+    tj0 = now_s();
     for (auto& j : jobs) j();
   } else {
+    R.concurrent = 1;
+    tj0 = now_s();
     while (ctx.aux.size() < jobs.size()) {
       cudaStream_t a2;
       RSF_CUDA(cudaStreamCreateWithFlags(&a2, cudaStreamNonBlocking));
@@ -1546,6 +1565,7 @@ EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KP
       u.release();
       wait_f = []() {};
       R.flops_factor = 0;
+      R.serial_fallback = 1;
       main_part();
       for (auto& j : jobs) j();
     } else {
@@ -1554,10 +1574,12 @@ EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KP
         if (e) std::rethrow_exception(e);
     }
   }
+  RSF_CUDA(cudaStreamSynchronize(s));
+  R.t_jobs_wall = now_s() - tj0;
   if (ctx.comm.world > 1 && njobs > 0) {
     // every job's results from the lowest rank of the group that ran it (all members hold the
     // same values): one all-gather of fixed-size records over the whole group
-    constexpr int RS = 12 + 2 * 32;
+    constexpr int RS = 13 + 4 * 32;
     std::vector<double> rec((size_t)njobs * RS, 0.0), all((size_t)ctx.comm.world * njobs * RS);
     for (int j = 0; j < njobs; ++j) {
       if (!mine(j)) continue;
@@ -1572,7 +1594,11 @@ EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KP
       r[5] = i >= 0 ? tpl[i] : t_trinv;
       r[6] = i >= 0 ? ffl[i] : 0.0;
       r[7] = pd.nL; r[8] = pd.cancellation; r[9] = pd.applies; r[10] = pd.seconds; r[11] = pd.flops;
-      for (size_t l = 0; l < pd.cols.size() && l < 32; ++l) { r[12 + l] = pd.cols[l]; r[44 + l] = pd.rank_max[l]; }
+      r[12] = pd.stored_bytes;
+      for (size_t l = 0; l < pd.cols.size() && l < 32; ++l) {
+        r[13 + l] = pd.cols[l]; r[45 + l] = pd.rank_max[l];
+        r[77 + l] = l < pd.rank_min.size() ? pd.rank_min[l] : 0; r[109 + l] = l < pd.rank_med.size() ? pd.rank_med[l] : 0;
+      }
     }
     ctx.comm.allgather_host(s, rec.data(), njobs * RS, all.data());
     for (int j = 0; j < njobs; ++j) {
@@ -1586,9 +1612,15 @@ EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KP
       else { utu = r[1]; trinv = r[2]; t_trinv = r[5]; }
       pd.nL = (int)r[7]; pd.cancellation = r[8]; pd.applies = r[9]; pd.seconds = r[10]; pd.flops = r[11];
       const int nl = std::min(32, tree->L + 1);
+      pd.stored_bytes = r[12];
       pd.cols.assign(nl, 0);
       pd.rank_max.assign(nl, 0);
-      for (int l = 0; l < nl; ++l) { pd.cols[l] = (int)r[12 + l]; pd.rank_max[l] = (int)r[44 + l]; }
+      pd.rank_min.assign(nl, 0);
+      pd.rank_med.assign(nl, 0);
+      for (int l = 0; l < nl; ++l) {
+        pd.cols[l] = (int)r[13 + l]; pd.rank_max[l] = (int)r[45 + l];
+        pd.rank_min[l] = (int)r[77 + l]; pd.rank_med[l] = (int)r[109 + l];
+      }
     }
   }
   R.t_peel += t_trinv;
@@ -1630,6 +1662,11 @@ void fill_eval_diag(const EvalResult& r, rsf_eval_diag* out) {
   out->t_total = r.t_total;
   out->flops_factor = r.flops_factor;
   out->kernel_launches = (double)r.launches;
+  out->t_jobs_wall = r.t_jobs_wall;
+  out->jobs = r.jobs;
+  out->concurrent = r.concurrent;
+  out->serial_fallback = r.serial_fallback;
+  out->groups = r.groups;
   out->fact.levels = r.L;
   out->fact.top_size = r.n0;
   const auto& d = r.fdiag;

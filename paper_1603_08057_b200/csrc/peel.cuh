@@ -7,6 +7,8 @@ namespace rsf {
 
 struct PeelDiag {
   std::vector<int> cols, rank_max;   // per level (index = level)
+  std::vector<int> rank_min, rank_med;   // per level: min / median eps_peel-rank over the sibling blocks
+  double stored_bytes = 0;           // bytes of the peeled representation (bases V_i + cores Brow_i)
   int nL = 0;
   double cancellation = 0;
   double applies = 0;
@@ -32,6 +34,8 @@ struct EvalResult {
   FactDiag fdiag;
   int L = 0, n0 = 0;
   PeelDiag pd[4];
+  double t_jobs_wall = 0;            // wall time from the start of the trace jobs to the last one's end
+  int jobs = 0, concurrent = 0, serial_fallback = 0, groups = 1;
 };
 
 // profile = true: the log profile likelihood of Eq. prof and its gradient; quad holds

@@ -31,5 +31,7 @@ if os.environ.get("RSF_GEMMLOG") == "1":
         f = v.split(",")
         rows.append((float(f[0]), float(f[1]), k, v))
     rows.sort(reverse=True)
+    import json as _json
+    _json.dump([[sec, fl, k, v] for sec, fl, k, v in rows], open(os.path.join("gpurun_out", "gemmlog_rows.json"), "w"))
     for sec, fl, k, v in rows[:40]:
         print(f"{sec:8.3f} s {fl / max(sec, 1e-12) / 1e12:6.1f} TF/s  {k}  {v}")
