@@ -86,6 +86,9 @@ typedef struct {
   double r_near;       /* near radius / box half-width (R-C). default 1.8 */
   double r_in, r_out;  /* proxy annulus radii / half-width (R-C; 4 rings x 64 angles, n_prox=256). 1.75, 2.45 */
   uint64_t seed;       /* Philox4x32-10 key of the peeling probes (stream 3). default 1603080570 */
+  int32_t strong;      /* peeling admissibility (next row f4): 0 weak (default);
+                          1 strong -- interaction-list blocks, 36 probe classes per level, 9 extraction
+                          classes; needs a perfect quadtree (every leaf at depth L), else RSF_EINVAL */
 } rsf_opts;            /* pass NULL for all defaults; rsf_opts_default() fills the defaults */
 
 typedef struct rsf_ctx_s* rsf_ctx;     /* device, stream, optional NCCL communicator */

@@ -95,6 +95,7 @@ class Opts:
     r_in: float = 1.75
     r_out: float = 2.45
     seed: int = 1603080570
+    strong: int = 0        # 1: strong-admissibility peeling (perfect quadtrees)
 
     def c(self) -> rsf_opts:
         o = rsf_opts()

@@ -61,6 +61,7 @@ rsf::Opts make_opts(const rsf_opts* o) {
   if (o->r_in > 0) r.r_in = o->r_in;
   if (o->r_out > 0) r.r_out = o->r_out;
   r.seed = o->seed;
+  r.strong = o->strong != 0;
   return r;
 }
 
@@ -147,6 +148,7 @@ void rsf_opts_default(rsf_opts* o) {
   o->r_in = d.r_in;
   o->r_out = d.r_out;
   o->seed = d.seed;
+  o->strong = d.strong;
 }
 
 rsf_status rsf_ctx_create(int device, void* cuda_stream, void* nccl_comm, rsf_ctx* out) {

@@ -20,6 +20,7 @@
 #include <exception>
 #include <thread>
 #include <functional>
+#include <unordered_map>
 #include <future>
 
 #include "dense.cuh"
@@ -122,23 +123,25 @@ __global__ void eye_kernel(const EyeDesc* __restrict__ descs) {
   }
 }
 
-// E' (k x n): 1 where t - leafbegin[t] == e0 + j
-__global__ void extract_probe_kernel(double* X, int k, int n, const int* __restrict__ lb, int e0) {
+// E' (k x n): 1 where t - leafbegin[t] == e0 + j (and, with a class map, cls[t] == kappa)
+__global__ void extract_probe_kernel(double* X, int k, int n, const int* __restrict__ lb, int e0,
+                                     const int* __restrict__ cls = nullptr, int kappa = 0) {
   const long long tot = (long long)n * k;
   for (long long e = blockIdx.x * (long long)NT + threadIdx.x; e < tot; e += (long long)gridDim.x * NT) {
     const int t = (int)(e / k), j = (int)(e % k);
-    X[e] = (t - lb[t] == e0 + j) ? 1.0 : 0.0;
+    X[e] = (t - lb[t] == e0 + j && (!cls || cls[t] == kappa)) ? 1.0 : 0.0;
   }
 }
 
 // per-block partial sums of diag entries H'(t - lb[t] - e0, t) and of their magnitudes
 __global__ void extract_diag_kernel(const double* H, int k, int n, const int* __restrict__ lb, int e0,
-                                    double* part, double* parta) {
+                                    double* part, double* parta, const int* __restrict__ cls = nullptr,
+                                    int kappa = 0) {
   __shared__ double s1[NT], s2[NT];
   double a = 0.0, b = 0.0;
   for (int t = blockIdx.x * NT + threadIdx.x; t < n; t += gridDim.x * NT) {
     const int j = t - lb[t] - e0;
-    if (j >= 0 && j < k) {
+    if (j >= 0 && j < k && (!cls || cls[t] == kappa)) {
       const double v = H[(long long)t * k + j];
       a += v;
       b += fabs(v);
@@ -312,6 +315,7 @@ struct PeelLevel {
     (g3x ? *g3x : g3).run(s, Y, tmp, k, k);         // Y'(:, I_i) -= S'_i V_i^T
   }
   std::vector<long long> soff;           // S' column offsets
+  DBuf<int> mapk;                        // strong admissibility: T' columns of IL(b), per box
 };
 
 // out (rows x q, ld rows) = transpose of rows piv[0:q] of src (c x rows, ld lds)
@@ -586,7 +590,17 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
 
   static const int verbose = getenv("RSF_VERBOSE") ? atoi(getenv("RSF_VERBOSE")) : 0;
   static const int max_lev = getenv("RSF_PEEL_LEVELS") ? atoi(getenv("RSF_PEEL_LEVELS")) : 1 << 30;
-  for (int lev = 1; lev <= std::min(L, max_lev); ++lev) {
+  // admissibility (next row f4): weak -- partners of a box are its siblings,
+  // probe groups the 4 quadrants; strong -- partners are the interaction list
+  // IL(b) = children of the parent's 3 x 3 neighbourhood not adjacent to b, probe groups the 36
+  // classes (ix mod 6, iy mod 6) (each 6 x 6 window of a parent neighbourhood holds one box per
+  // class), levels 2..L of a perfect quadtree
+  const bool strong = o.strong != 0;
+  if (strong)
+    for (int l = 0; l <= L; ++l)
+      RSF_REQUIRE((long long)t.levels[l].size() == (1ll << (2 * l)), ST_EINVAL,
+                  "strong-admissibility peeling needs a perfect quadtree (every leaf at depth L)");
+  for (int lev = strong ? 2 : 1; lev <= std::min(L, max_lev); ++lev) {
     const std::vector<int>& nodes = t.levels[lev];
     const int nb = (int)nodes.size();
     // boxes and families (siblings are consecutive in Morton order; Def. sibs)
@@ -605,15 +619,55 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
       npairs += (e - b) * (e - b - 1);
       b = e;
     }
+    // part[b]: partner boxes (ascending); rowset[b]: the boxes whose cores form b's row of
+    // Brow (weak: the whole family, b's own zero block included; strong: IL(b)); grp[b]: group
+    const int NGRP = strong ? 36 : 4;
+    std::vector<std::vector<int>> part(nb), rowset(nb);
+    std::vector<int> grp(nb);
+    if (!strong) {
+      for (int b = 0; b < nb; ++b) {
+        grp[b] = bx[b].quad;
+        for (int x = bx[b].fam0; x < bx[b].fam1; ++x) {
+          rowset[b].push_back(x);
+          if (x != b) part[b].push_back(x);
+        }
+      }
+    } else {
+      std::unordered_map<long long, int> at;
+      for (int b = 0; b < nb; ++b) at[(long long)t.ix[nodes[b]] * (1ll << 31) + t.iy[nodes[b]]] = b;
+      npairs = 0;
+      for (int b = 0; b < nb; ++b) {
+        const int x = t.ix[nodes[b]], y = t.iy[nodes[b]];
+        grp[b] = (x % 6) * 6 + (y % 6);
+        const int px = x / 2, py = y / 2;
+        for (int cx = 2 * px - 2; cx < 2 * px + 4; ++cx)
+          for (int cy = 2 * py - 2; cy < 2 * py + 4; ++cy) {
+            if (std::max(std::abs(cx - x), std::abs(cy - y)) <= 1) continue;
+            auto it = at.find((long long)cx * (1ll << 31) + cy);
+            if (it != at.end()) part[b].push_back(it->second);
+          }
+        std::sort(part[b].begin(), part[b].end());
+        rowset[b] = part[b];
+        npairs += (int)part[b].size();
+      }
+    }
     if (npairs == 0) continue;
-    // probe groups: W_g on the boxes with quadrant g (R-R), largest groups first
-    std::vector<int> gcount(4, 0);
-    for (auto& b : bx) if (b.fam1 - b.fam0 > 1) gcount[b.quad]++;
-    std::vector<int> gorder = {0, 1, 2, 3};
+    // pair slots: (b, position of the partner in part[b])
+    std::vector<long long> pslot0(nb + 1, 0);
+    for (int b = 0; b < nb; ++b) pslot0[b + 1] = pslot0[b] + (long long)part[b].size();
+    auto pslot = [&](int b, int x) -> size_t {
+      const auto& v = part[b];
+      return (size_t)(pslot0[b] + (std::lower_bound(v.begin(), v.end(), x) - v.begin()));
+    };
+    // probe groups: W_g on the boxes of group g (quadrant R-R, or class), largest groups first
+    std::vector<int> gcount(NGRP, 0);
+    for (int b = 0; b < nb; ++b) if (!part[b].empty()) gcount[grp[b]]++;
+    std::vector<int> gorder(NGRP);
+    for (int g = 0; g < NGRP; ++g) gorder[g] = g;
     std::stable_sort(gorder.begin(), gorder.end(), [&](int a2, int b2) { return gcount[a2] > gcount[b2]; });
     std::vector<int> hq(n, -1);
-    for (auto& b : bx)
-      for (int x = b.ib; x < b.ib + b.ni; ++x) hq[x] = b.quad;
+    for (int b = 0; b < nb; ++b)
+      for (int x = bx[b].ib; x < bx[b].ib + bx[b].ni; ++x) hq[x] = grp[b];
     DBuf<int> qmap = up(hq, s);
     const int cmax = ((maxni + o.oversample) + 7) / 8 * 8;
     // initial width (R-M): level 1 from the factor's level-1 skeleton sizes, deeper levels
@@ -624,7 +678,7 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
     // (0.6: the eps_peel-rank a sketch reveals grows with its width, so a wide first guess is
     // accepted at a higher rank and inflates every later level; measured at config 3: 0.6 with one
     // restart 25.1 s per evaluation, 0.75 without restarts 27.8 s)
-    int c = (prev_rank < 0) ? (int)std::ceil(0.6 * hint) : prev_rank + o.oversample;
+    int c = (prev_rank < 0) ? (strong ? o.peel_start : (int)std::ceil(0.6 * hint)) : prev_rank + o.oversample;
     int restarts = 0;
     c = std::min(std::max(c, o.oversample + 8), cmax);
     c = (c + 7) / 8 * 8;
@@ -634,9 +688,9 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
     std::vector<DBuf<double>> Vb(nb), Ab(nb);     // V_i (n_i x r_i, ld n_i), A_i = W_i^T V_i (c x r_i, ld c)
     std::vector<int> vcap(nb, 0);                 // allocated columns of V_i / A_i (grown exactly)
     std::vector<int> vmax(nb, 0);                 // most columns V_i can take: min(n_i, c per sibling group)
-    // per ordered pair (index: b * 4 + position of the sibling in the family)
+    // per ordered pair (index: pslot(b, partner))
     struct PairData { int k = 0, rz = 0; double *Z = nullptr, *X = nullptr, *Lm = nullptr, *Gi = nullptr; };
-    std::vector<PairData> pdat((size_t)nb * 4);
+    std::vector<PairData> pdat((size_t)std::max<long long>(pslot0[nb], 1));
     std::vector<DBuf<double>> arenas;
     int mr = 0;
     while (true) {
@@ -652,7 +706,7 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
       std::fill(vcap.begin(), vcap.end(), 0);
       double vres = 0;
       for (int b = 0; b < nb; ++b) {
-        const int ng = bx[b].fam1 - bx[b].fam0 - 1;
+        const int ng = (int)part[b].size();
         vmax[b] = ng <= 0 ? 0 : std::min(bx[b].ni, ng * c);
         vres += 8.0 * bx[b].ni * (double)vmax[b];
       }
@@ -672,12 +726,13 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
       lev_ranks.clear();
       for (int g : gorder) {
         if (gcount[g] == 0) continue;
-        // boxes i with a sibling j in quadrant g (at most one per family)
+        // boxes i with a partner j in group g (at most one: one sibling per quadrant, one box per
+        // class in a parent neighbourhood)
         std::vector<int> act, partner;
         for (int b = 0; b < nb; ++b) {
-          if (bx[b].quad == g) continue;
-          for (int x = bx[b].fam0; x < bx[b].fam1; ++x)
-            if (bx[x].quad == g) { act.push_back(b); partner.push_back(x); break; }
+          if (grp[b] == g) continue;
+          for (int x : part[b])
+            if (grp[x] == g) { act.push_back(b); partner.push_back(x); break; }
         }
         if (act.empty()) continue;
         const size_t NA = act.size();
@@ -1041,7 +1096,7 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
           for (size_t x = 0; x < B; ++x) {
             const size_t xa = x0 + x;
             const int i = act[xa], j = partner[xa];
-            PairData& q = pdat[(size_t)i * 4 + (j - bx[i].fam0)];
+            PairData& q = pdat[pslot(i, j)];
             q.k = kk[xa]; q.rz = rb[i];
             q.Z = arena.p + zo[x]; q.X = arena.p + xo[x]; q.Lm = arena.p + lo[x]; q.Gi = arena.p + go[x];
           }
@@ -1069,9 +1124,15 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
     PeelLevel& PL = peeled[lev];
     std::vector<long long> fo(nb), bo(nb);     // column offset of box b inside its family row; Brow offsets
     long long brt = 0;
+    // column offset of box x inside b's row of cores: sum of r_y over y in rowset[b], y < x
+    auto fo_of = [&](int b, int x) -> long long {
+      long long off = 0;
+      for (int y : rowset[b]) { if (y >= x) break; off += rb[y]; }
+      return off;
+    };
     for (int b = 0; b < nb; ++b) {
       long long off = 0, tot = 0;
-      for (int x = bx[b].fam0; x < bx[b].fam1; ++x) { if (x < b) off += rb[x]; tot += rb[x]; }
+      for (int x : rowset[b]) { if (x < b) off += rb[x]; tot += rb[x]; }
       fo[b] = off;
       bo[b] = brt; brt += (long long)rb[b] * tot;
     }
@@ -1083,10 +1144,10 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
       std::vector<std::array<long long, 3>> mo;
       std::vector<std::pair<int, int>> pl;
       for (int i = 0; i < nb; ++i)
-        for (int j = bx[i].fam0; j < bx[i].fam1; ++j) {
+        for (int j : part[i]) {
           if (j <= i) continue;
-          const PairData& a = pdat[(size_t)i * 4 + (j - bx[i].fam0)];
-          const PairData& b2 = pdat[(size_t)j * 4 + (i - bx[j].fam0)];
+          const PairData& a = pdat[pslot(i, j)];
+          const PairData& b2 = pdat[pslot(j, i)];
           if (a.k == 0 || b2.k == 0) continue;
           std::array<long long, 3> m{};
           m[0] = mt; mt += (long long)a.k * b2.k;                 // T1, then M
@@ -1100,8 +1161,8 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
           m6(false, true), m7(false, true);
       for (size_t q = 0; q < pl.size(); ++q) {
         const int i = pl[q].first, j = pl[q].second;
-        const PairData& a = pdat[(size_t)i * 4 + (j - bx[i].fam0)];
-        const PairData& b2 = pdat[(size_t)j * 4 + (i - bx[j].fam0)];
+        const PairData& a = pdat[pslot(i, j)];
+        const PairData& b2 = pdat[pslot(j, i)];
         const int k1 = a.k, k2 = b2.k;
         double* T1p = Mw.p + mo[q][0];
         double* T2p = Mw.p + mo[q][1];
@@ -1121,14 +1182,14 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
         m4.add(d4);
         GemmDesc d5 = gdesc(a.rz, b2.rz, k2);   // B_ij = T3 Z_ji^T  -> Brow_i
         d5.A = T3p; d5.lda = a.rz; d5.B = b2.Z; d5.ldb = b2.rz;
-        d5.C = PL.Brow.p + bo[i] + (long long)rb[i] * fo[j]; d5.ldc = rb[i];
+        d5.C = PL.Brow.p + bo[i] + (long long)rb[i] * fo_of(i, j); d5.ldc = rb[i];
         m5.add(d5);
         GemmDesc d6 = gdesc(b2.rz, k1, k2);     // T4 = Z_ji M^T
         d6.A = b2.Z; d6.lda = b2.rz; d6.B = T1p; d6.ldb = k1; d6.C = T4p; d6.ldc = b2.rz;
         m6.add(d6);
         GemmDesc d7 = gdesc(b2.rz, a.rz, k1);   // B_ji = T4 Z_ij^T  -> Brow_j
         d7.A = T4p; d7.lda = b2.rz; d7.B = a.Z; d7.ldb = a.rz;
-        d7.C = PL.Brow.p + bo[j] + (long long)rb[j] * fo[i]; d7.ldc = rb[j];
+        d7.C = PL.Brow.p + bo[j] + (long long)rb[j] * fo_of(j, i); d7.ldc = rb[j];
         m7.add(d7);
         pd.flops += 2.0 * k1 * (double)k2 * c + 2.0 * a.rz * (double)b2.rz * (k1 + k2);
       }
@@ -1164,17 +1225,31 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
     std::vector<long long> toff(nb), soff(nb);
     for (int b = 0; b < nb; ++b) { toff[b] = tc; tc += rb[b]; }
     for (int b = 0; b < nb; ++b) { soff[b] = tc; tc += rb[b]; }
+    // strong: the T' columns of IL(b) are not contiguous -> a K-gather list per box
+    std::vector<long long> moff(nb, 0);
+    if (strong) {
+      std::vector<int> hm;
+      for (int b = 0; b < nb; ++b) {
+        moff[b] = (long long)hm.size();
+        for (int x : rowset[b])
+          for (int q = 0; q < rb[x]; ++q) hm.push_back((int)(toff[x] + q));
+      }
+      PL.mapk = up(hm, s);
+    }
     for (int b = 0; b < nb; ++b) {
       if (rb[b] == 0) continue;
       long long tot = 0;
-      for (int x = bx[b].fam0; x < bx[b].fam1; ++x) tot += rb[x];
+      for (int x : rowset[b]) tot += rb[x];
       GemmDesc a = gdesc(-1, rb[b], bx[b].ni);            // T'_b = X'(:, I_b) V_b
       a.selA = 1; a.offA = bx[b].ib; a.B = PL.V[b].p; a.ldb = bx[b].ni; a.selC = 2; a.offC = toff[b];
       PL.g1.add(a);
       PL.ib.push_back(bx[b].ib); PL.ni.push_back(bx[b].ni); PL.r.push_back(rb[b]); PL.bidx.push_back(b);
       PL.toff.push_back(toff[b]); PL.soff.push_back(soff[b]);
-      GemmDesc d = gdesc(-1, rb[b], (int)tot);            // S'_b = T'_fam Brow_b^T
-      d.selA = 2; d.offA = toff[bx[b].fam0]; d.B = PL.Brow.p + bo[b]; d.ldb = rb[b]; d.selC = 2; d.offC = soff[b];
+      GemmDesc d = gdesc(-1, rb[b], (int)tot);            // S'_b = T'_row Brow_b^T
+      d.selA = 2; d.offA = strong ? 0 : toff[bx[b].fam0]; d.B = PL.Brow.p + bo[b]; d.ldb = rb[b];
+      d.selC = 2; d.offC = soff[b];
+      if (strong) d.mapA = PL.mapk.p + moff[b];
+      if (tot == 0) continue;                              // (strong: no partner has a basis)
       PL.g2.add(d);
       GemmDesc e = gdesc(-1, bx[b].ni, rb[b]);            // Y'(:, I_b) -= S'_b V_b^T
       e.selA = 2; e.offA = soff[b]; e.B = PL.V[b].p; e.ldb = bx[b].ni; e.selC = 1; e.offC = bx[b].ib;
@@ -1226,24 +1301,34 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
   const int GB = 256;
   // (sharded: the nL extraction columns are split over the parts; partial leaf traces are
   // summed over the ranks in rank order)
+  // (strong: the leaf near field remains in the residual, so the identity probes go to the 9
+  // leaf classes (ix mod 3, iy mod 3) in turn -- one box per class in every 3 x 3 neighbourhood)
   double trp[2] = {0.0, 0.0};
-  for (int r = cm.p0(); r < cm.p1(); ++r) {
-    long long lo, hi;
-    Comm::slice(nL, NP, r, &lo, &hi);
-    for (int e0 = (int)lo; e0 < (int)hi; e0 += kb) {
-      const int k = std::min<int>(kb, (int)hi - e0);
-      DBuf<double> E((size_t)n * k, s), H((size_t)n * k, s), part(GB, s), parta(GB, s);
-      extract_probe_kernel<<<gxx((long long)n * k), NT, 0, s>>>(E.p, k, n, dlb.p, e0);
-      count_launch();
-      RSF_LAUNCH_CHECK();
-      residual(E.p, H.p, k, L + 1, nullptr);
-      extract_diag_kernel<<<GB, NT, 0, s>>>(H.p, k, n, dlb.p, e0, part.p, parta.p);
-      count_launch();
-      RSF_LAUNCH_CHECK();
-      auto hp = part.to_host(GB), ha = parta.to_host(GB);
-      for (int i = 0; i < GB; ++i) { trp[0] += hp[i]; trp[1] += ha[i]; }
-    }
+  DBuf<int> dcls;
+  if (strong) {
+    std::vector<int> hc(n, 0);
+    for (int nd : t.levels[L])
+      for (int x = t.begin[nd]; x < t.end[nd]; ++x) hc[x] = (t.ix[nd] % 3) * 3 + (t.iy[nd] % 3);
+    dcls = up(hc, s);
   }
+  for (int kap = 0; kap < (strong ? 9 : 1); ++kap)
+    for (int r = cm.p0(); r < cm.p1(); ++r) {
+      long long lo, hi;
+      Comm::slice(nL, NP, r, &lo, &hi);
+      for (int e0 = (int)lo; e0 < (int)hi; e0 += kb) {
+        const int k = std::min<int>(kb, (int)hi - e0);
+        DBuf<double> E((size_t)n * k, s), H((size_t)n * k, s), part(GB, s), parta(GB, s);
+        extract_probe_kernel<<<gxx((long long)n * k), NT, 0, s>>>(E.p, k, n, dlb.p, e0, dcls.p, kap);
+        count_launch();
+        RSF_LAUNCH_CHECK();
+        residual(E.p, H.p, k, L + 1, nullptr);
+        extract_diag_kernel<<<GB, NT, 0, s>>>(H.p, k, n, dlb.p, e0, part.p, parta.p, dcls.p, kap);
+        count_launch();
+        RSF_LAUNCH_CHECK();
+        auto hp = part.to_host(GB), ha = parta.to_host(GB);
+        for (int i = 0; i < GB; ++i) { trp[0] += hp[i]; trp[1] += ha[i]; }
+      }
+    }
   cm.allsum(s, trp, 2);
   tr = trp[0];
   tra = trp[1];

@@ -20,6 +20,7 @@ struct Opts {
   int max_depth = 30;
   double r_near = 1.8, r_in = 1.75, r_out = 2.45;   // R-C (in units of the box half-width)
   unsigned long long seed = 1603080570ull;
+  int strong = 0;            // peeling admissibility: 0 weak, 1 strong (next row f4)
 };
 
 struct Ctx {
