@@ -48,3 +48,27 @@ if which in ("both", "p7"):
                           "grad_rel_err": [abs(r.grad[i] - ref["grad"][i]) / abs(ref["grad"][i]) for i in range(3)],
                           "cols": [[d.peel[i].cols[l] for l in range(1, d.peel[i].levels + 1)] for i in (0, 1)],
                           "stored_GB": [d.peel[i].stored_bytes / 1e9 for i in (0, 1)]}), flush=True)
+if which == "m12":
+    # Matern 1/2 (config 4's kernel, rho = 0.01, nugget 1e-3, theta = (rho, sigma2)) on a perfect
+    # jittered m x m grid: weak vs strong peeling (P:760 -- strong should scale better for Matern)
+    m = int(os.environ.get("M12M", "512"))
+    c3 = config(3)
+    xy = torch.from_numpy(points_for(c3, m * m)).to(dev)
+    K = R.Kernel("matern12", 0.01, 1.0, 1e-3, 1.0, ("rho", "sigma2"))
+    w = torch.from_numpy(np.random.default_rng(5).standard_normal(m * m)).to(dev)
+    F = R.Factor(ctx, xy, K, 1e-8, 64)
+    z = F.sample(w)
+    F.close()
+    order = [int(x) for x in os.environ.get("M12ORDER", "1,0").split(",")]
+    for strong in order:
+        t = time.time()
+        try:
+            r = R.gp_mle_eval(ctx, xy, z, K, 1e-8, 64, R.Opts(eps_peel=1e-6, strong=strong))
+            d = r.diag
+            print(json.dumps({"m12_m": m, "strong": strong, "t": time.time() - t, "grad": r.grad,
+                              "trace": [d.trace[0], d.trace[1]],
+                              "cols": [[d.peel[i].cols[l] for l in range(1, d.peel[i].levels + 1)] for i in (0, 1)],
+                              "rank_max": [[d.peel[i].rank_max[l] for l in range(1, d.peel[i].levels + 1)] for i in (0, 1)],
+                              "stored_GB": [d.peel[i].stored_bytes / 1e9 for i in (0, 1)]}), flush=True)
+        except Exception as e:
+            print(json.dumps({"m12_m": m, "strong": strong, "t": time.time() - t, "error": str(e)[:300]}), flush=True)
