@@ -450,7 +450,12 @@ def main():
                               f"({t_stat:.2f} s); the timed steps ran uninstrumented",
                 "algorithmic_flops_per_launch": gfl / gl if gl else None}
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": METRIC,
+        "metric_note": ("BASELINE.json quotes this metric at n = 2^20 (config 4); config 4 does not fit one "
+                        "B200's memory with weak peeling (DESIGN.md §7), so per the task's rule `value` is "
+                        "measured on the largest single-GPU config, named in config.workload"
+                        if (args.n or c.n) != 1048576 else "config 4 (n = 2^20)"),
+        "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * t_all / args.steps, "higher_is_better": True,
         "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": _config_dict(c, n, args), "clocks": clocks, "gpu_launches": int(launches),

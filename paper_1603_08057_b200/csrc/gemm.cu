@@ -1363,7 +1363,20 @@ void GemmBatch::run(cudaStream_t s, double* X0, double* X1, int ldx, int Mglob, 
     bool tri = false;
     for (const auto& d : h_) tri = tri || d.btri != 0;
     int S = 1;
-    while (S < 32 && (long long)tiles * S < 8 * 148 && maxK_ / (2 * S) >= 256) S *= 2;
+    static const int gv_model = getenv("RSF_GEMV_SPLIT") ? atoi(getenv("RSF_GEMV_SPLIT")) : 1;
+    if (gv_model == 0) {
+      while (S < 32 && (long long)tiles * S < 8 * 148 && maxK_ / (2 * S) >= 256) S *= 2;
+    } else {
+      // waves x (rows per CTA + a fixed per-CTA cost): resident CTAs per SM from the kernels'
+      // register use (op(B) = B^T: 64 registers -> 4; op(B) = B: 95-128 -> 2)
+      const double slots = 148.0 * (tb_ ? 4 : 2), c0 = 128.0;
+      double best = 1e300;
+      for (int S2 = 1; S2 <= 32; S2 *= 2) {
+        if (S2 > 1 && maxK_ / S2 < 128) break;
+        const double cost = std::ceil((double)tiles * S2 / slots) * ((double)maxK_ / S2 + c0) + (S2 > 1 ? c0 : 0.0);
+        if (cost < best) { best = cost; S = S2; }
+      }
+    }
     std::vector<long long> mn;
     DBuf<double> ws;
     const long long* dmn = nullptr;
