@@ -1576,8 +1576,11 @@ EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KP
   R.jobs = njobs;
   R.groups = NG;
   double tj0 = 0.0;
+  // memory plan: a shape that ran out of memory with its jobs side by side runs them serially
+  bool planned_serial = false;
+  for (auto& sh : ctx.serial_shapes) planned_serial = planned_serial || (sh.first == n && sh.second == njobs);
   // (the profiler and the launch trace synchronise one stream at a time: serial then)
-  if (!par_on || jobs.size() < 2 || Prof::enabled() || KTrace::on()) {
+  if (!par_on || jobs.size() < 2 || Prof::enabled() || KTrace::on() || planned_serial) {
     main_part();
     f_promise.set_value();
     tj0 = now_s();
@@ -1651,6 +1654,7 @@ EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KP
       wait_f = []() {};
       R.flops_factor = 0;
       R.serial_fallback = 1;
+      ctx.serial_shapes.emplace_back((long long)n, njobs);
       main_part();
       for (auto& j : jobs) j();
     } else {

@@ -31,6 +31,9 @@ struct Ctx {
   Comm comm;                        // rank group of a sharded evaluation (world 1: none)
   std::vector<Comm> job_comms;      // one split communicator per trace job (its group's ranks)
   int job_comms_njobs = -1;         // number of jobs job_comms was built for
+  // memory plan of gp_mle_eval: (n, jobs) shapes whose trace jobs did not fit side by side; later
+  // evaluations of such a shape run them in the serial order directly (no OOM-and-redo)
+  std::vector<std::pair<long long, int>> serial_shapes;
   std::string last_error;
 };
 

@@ -394,7 +394,11 @@ z = torch.from_numpy(w_for(c, n)).cuda()
 ctx = R.Context(0)
 K = R.Kernel(c.family, c.rho, c.sigma2, c.nugget, c.alpha, ("rho", "alpha", "nugget"))
 r = R.gp_mle_eval(ctx, xy, z, K, 1e-9, c.leaf, R.Opts(eps_peel=c.eps_peel, seed=c.seed))
-json.dump({"ell": r.ell, "grad": list(r.grad), "trace": list(r.diag.trace)[:3]}, open(sys.argv[2], "w"))
+r2 = R.gp_mle_eval(ctx, xy, z, K, 1e-9, c.leaf, R.Opts(eps_peel=c.eps_peel, seed=c.seed))
+json.dump({"ell": r.ell, "grad": list(r.grad), "trace": list(r.diag.trace)[:3],
+           "same2": r2.ell == r.ell and list(r2.grad) == list(r.grad),
+           "flags": [[x.diag.jobs, x.diag.concurrent, x.diag.serial_fallback] for x in (r, r2)]},
+          open(sys.argv[2], "w"))
 """
 
 
@@ -416,7 +420,13 @@ def test_concurrent_trace_jobs_equal_serial_order(tmp_path):
         env = dict(os.environ, RSF_PAR_TRACES=flag, RSF_TEST_PAR_OOM=oom)
         subprocess.run([sys.executable, str(script), root, str(f)], env=env, check=True, timeout=600)
         out[flag + oom] = json.load(open(f))
-    assert out["10"] == out["00"]
-    # out of memory in a concurrent job: everything is redone in the serial order
-    assert out["11"] == out["00"]
+    res = {k: {kk: v[kk] for kk in ("ell", "grad", "trace")} for k, v in out.items()}
+    assert res["10"] == res["00"]
+    # out of memory in a concurrent job: everything is redone in the serial order, and the
+    # context's memory plan runs the next evaluation of the same shape serially from the start
+    assert res["11"] == res["00"]
     assert all(np.isfinite(out["10"]["grad"]))
+    assert all(v["same2"] for v in out.values())
+    assert out["10"]["flags"] == [[3, 1, 0], [3, 1, 0]]
+    assert out["00"]["flags"] == [[3, 0, 0], [3, 0, 0]]
+    assert out["11"]["flags"] == [[3, 1, 1], [3, 0, 0]]
