@@ -98,15 +98,26 @@ def cfg3(ctx):
     return c, _d(xy), _d(z), z
 
 
-def _ell_at(ctx, c, xy, z, n, **kw):
+def _ell_at(ctx, c, xy, z, n, logdet_only=False, **kw):
     """l(theta) from the Sigma factor alone: log|F| and z^T F^-1 z."""
-    K = R.Kernel(c.family, kw.get("rho", c.rho), c.sigma2, c.nugget, kw.get("alpha", c.alpha), theta=())
+    K = R.Kernel(c.family, kw.get("rho", c.rho), kw.get("sigma2", c.sigma2), kw.get("nugget", c.nugget),
+                 kw.get("alpha", c.alpha), theta=())
     F = R.Factor(ctx, xy, K, c.eps_fact, c.leaf)
+    ld = F.logdet()
+    if logdet_only:
+        F.close()
+        return ld
     u = F.solve(z)
     quad = float(torch.dot(z, u))
-    ld = F.logdet()
     F.close()
     return -0.5 * quad - 0.5 * ld - 0.5 * n * math.log(2 * math.pi)
+
+
+def _richardson(f, v, rel=1e-2):
+    h = rel * v
+    d1 = (f(v + h) - f(v - h)) / (2 * h)
+    d2 = (f(v + 2 * h) - f(v - 2 * h)) / (4 * h)
+    return (4 * d1 - d2) / 3
 
 
 def test_cfg3_frozen_z_reproducible_and_gradient_vs_fd(ctx, cfg3):
@@ -140,10 +151,44 @@ def test_cfg3_frozen_z_reproducible_and_gradient_vs_fd(ctx, cfg3):
         d2 = (ell(v + 2 * h) - ell(v - 2 * h)) / (4 * h)
         fd.append((4 * d1 - d2) / 3)                            # Richardson: O(h^4)
     err = [abs(r1.grad[i] - fd[i]) / abs(fd[i]) for i in range(2)]
+    # P8 at full size: the peeled traces alone against d log|Sigma| / d theta_i
+    tfd = [_richardson(lambda x, nm=nm: _ell_at(ctx, c, xy, z, n, logdet_only=True, **{nm: x}), v)
+           for nm, v in (("rho", c.rho), ("alpha", c.alpha))]
+    terr = [abs(r1.diag.trace[i] - tfd[i]) / abs(tfd[i]) for i in range(2)]
     _record("cfg3_frozen_z", {"n": n, "ell": r1.ell, "grad": list(r1.grad), "grad_fd": fd, "rel_err": err,
                               "q": [r1.diag.q[i] for i in range(2)], "trace": [r1.diag.trace[i] for i in range(2)],
-                              "t_total": r1.diag.t_total})
+                              "trace_fd_logdet": tfd, "trace_rel_err": terr, "t_total": r1.diag.t_total})
     assert max(err) <= 1e-3, (r1.grad, fd, err)
+    assert max(terr) <= 1e-5, (terr,)
+
+
+def test_cfg5_recipe_quarter_million_vs_finite_differences(ctx):
+    """Config 5's recipe (Matern 5/2, theta = (rho, sigma2, nugget), leaf 128, eps_fact 1e-9) at
+    n = 2^18 (the full n = 2^22 exceeds one GPU): every g_i against Richardson differences of l,
+    every trace against differences of log|Sigma| (P8), and the sigma2 / nugget identities (P9)."""
+    c = config(5)
+    n = 1 << 18
+    xy = _d(points_for(c, n))
+    K = R.Kernel(c.family, c.rho, c.sigma2, c.nugget, c.alpha, c.theta)
+    F = R.Factor(ctx, xy, K, c.eps_fact, c.leaf)
+    z = F.sample(_d(w_for(c, n)))
+    F.close()
+    r = R.gp_mle_eval(ctx, xy, z, K, c.eps_fact, c.leaf, R.Opts(eps_peel=c.eps_peel, seed=c.seed))
+    names = list(c.theta)
+    vals = {"rho": c.rho, "sigma2": c.sigma2, "nugget": c.nugget}
+    gfd = [_richardson(lambda x, nm=nm: _ell_at(ctx, c, xy, z, n, **{nm: x}), vals[nm]) for nm in names]
+    tfd = [_richardson(lambda x, nm=nm: _ell_at(ctx, c, xy, z, n, logdet_only=True, **{nm: x}), vals[nm])
+           for nm in names]
+    gerr = [abs(r.grad[i] - gfd[i]) / abs(gfd[i]) for i in range(3)]
+    terr = [abs(r.diag.trace[i] - tfd[i]) / abs(tfd[i]) for i in range(3)]
+    _record("cfg5_recipe_n262144", {"grad": list(r.grad), "grad_fd": gfd, "rel_err": gerr,
+                                     "trace": [r.diag.trace[i] for i in range(3)], "trace_fd_logdet": tfd,
+                                     "trace_rel_err": terr, "t_total": r.diag.t_total})
+    # P9: sigma2 g_sigma2 + tau g_tau = 1/2 z^T Sigma^-1 z - n/2 (exact identity of the model)
+    lhs = c.sigma2 * r.grad[1] + c.nugget * r.grad[2]
+    assert abs(lhs - (0.5 * r.diag.quad - 0.5 * n)) <= 1e-8 * (0.5 * n)
+    assert max(terr) <= 1e-5, terr
+    assert max(gerr) <= 1e-3, (r.grad, gfd, gerr)
 
 
 def test_multichunk_batch_split_peeling_vs_O1(ctx, monkeypatch):
