@@ -48,3 +48,27 @@ def test_emulated_group_matches_oracle_and_unsharded(cid, n, P, monkeypatch):
     trP = np.array([rP.diag.trace[i] for i in range(len(c.theta))])
     np.testing.assert_allclose(trP, d["trace"], rtol=1e-5)
     np.testing.assert_allclose(trP, tr1, rtol=1e-6)
+
+
+def test_job_result_exchange_round_trip(monkeypatch):
+    """The fixed-size job-result records of a rank group (one all-gather after the trace jobs,
+    DESIGN.md §7) carry every q_i, trace and peeling diagnostic unchanged: a single-GPU
+    evaluation routed through the same pack / gather / unpack path is bit-identical."""
+    c = config(2)
+    n = 4096
+    xy = points_for(c, n)
+    ok = OK(c.family, c.rho, c.sigma2, c.nugget, c.alpha, c.theta)
+    z = dense_sample(ok, xy, w_for(c, n))
+    ctx = R.Context(0)
+    K = R.Kernel(c.family, c.rho, c.sigma2, c.nugget, c.alpha, c.theta)
+    o = R.Opts(eps_peel=c.eps_peel, seed=c.seed)
+    r1 = R.gp_mle_eval(ctx, _d(xy), _d(z), K, c.eps_fact, c.leaf, o)
+    monkeypatch.setenv("RSF_EMU_EXCHANGE", "1")
+    r2 = R.gp_mle_eval(ctx, _d(xy), _d(z), K, c.eps_fact, c.leaf, o)
+    assert r2.ell == r1.ell and list(r2.grad) == list(r1.grad)
+    for i in range(2):
+        a, b = r1.diag.peel[i], r2.diag.peel[i]
+        assert list(a.cols) == list(b.cols) and list(a.rank_max) == list(b.rank_max)
+        assert list(a.rank_min) == list(b.rank_min) and list(a.rank_med) == list(b.rank_med)
+        assert a.stored_bytes == b.stored_bytes and a.nL == b.nL and a.applies == b.applies
+        assert r1.diag.q[i] == r2.diag.q[i] and r1.diag.trace[i] == r2.diag.trace[i]
