@@ -1666,7 +1666,7 @@ EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KP
   RSF_CUDA(cudaStreamSynchronize(s));
   R.t_jobs_wall = now_s() - tj0;
   // (RSF_EMU_EXCHANGE=1 routes a single-GPU evaluation through the same record exchange: tests)
-  static const bool emu_exchange = getenv("RSF_EMU_EXCHANGE") && getenv("RSF_EMU_EXCHANGE")[0] == '1';
+  const bool emu_exchange = getenv("RSF_EMU_EXCHANGE") && getenv("RSF_EMU_EXCHANGE")[0] == '1';
   if ((ctx.comm.world > 1 || emu_exchange) && njobs > 0) {
     // every job's results from the lowest rank of the group that ran it (all members hold the
     // same values): one all-gather of fixed-size records over the whole group
