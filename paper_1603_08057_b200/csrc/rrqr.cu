@@ -377,6 +377,67 @@ __global__ void apply_swaps_kernel(const RDesc* __restrict__ d0) {
     }
 }
 
+// The same column swaps with the sequence composed first: thread 0 lists the affected columns
+// (the block's positions J..J+nbp-1 and their swap targets, <= 2 QR_NB) and which original
+// column ends up in each; every CTA then moves its 64-row slab of those columns through shared
+// memory -- coalesced column reads, all loads in flight at once -- instead of nbp dependent
+// read-modify-write swaps per row.  The sketch columns and pivots are swapped as before.
+constexpr int SW_ROWS = 64;
+__global__ void __launch_bounds__(NT) apply_swaps_rows_kernel(const RDesc* __restrict__ d0) {
+  const RDesc d = d0[blockIdx.y];
+  __shared__ int cols[2 * QR_NB], cur[2 * QR_NB], ncol_s;
+  __shared__ double buf[2 * QR_NB][SW_ROWS + 1];
+  if (threadIdx.x == 0) {
+    int nc = 0;
+    for (int t = 0; t < d.nbp; ++t) cols[nc++] = d.J + t;
+    for (int t = 0; t < d.nbp; ++t) {
+      const int b = d.J + d.sw[t];
+      bool have = false;
+      for (int q = 0; q < nc; ++q) have = have || cols[q] == b;
+      if (!have) cols[nc++] = b;
+    }
+    for (int q = 0; q < nc; ++q) cur[q] = cols[q];
+    for (int t = 0; t < d.nbp; ++t) {
+      const int a = d.J + t, b = d.J + d.sw[t];
+      if (a == b) continue;
+      int pa = 0, pb = 0;
+      for (int q = 0; q < nc; ++q) { if (cols[q] == a) pa = q; if (cols[q] == b) pb = q; }
+      const int v = cur[pa]; cur[pa] = cur[pb]; cur[pb] = v;
+    }
+    ncol_s = nc;
+  }
+  __syncthreads();
+  const int nc = ncol_s;
+  for (long long r0 = (long long)blockIdx.x * SW_ROWS; r0 < d.m; r0 += (long long)gridDim.x * SW_ROWS) {
+    const int rows = (int)min((long long)SW_ROWS, d.m - r0);
+    for (int e = threadIdx.x; e < nc * SW_ROWS; e += NT) {
+      const int rr = e % SW_ROWS, q = e / SW_ROWS;
+      if (rr < rows && cur[q] != cols[q]) buf[q][rr] = d.A[(long long)cur[q] * d.lda + r0 + rr];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < nc * SW_ROWS; e += NT) {
+      const int rr = e % SW_ROWS, q = e / SW_ROWS;
+      if (rr < rows && cur[q] != cols[q]) d.A[(long long)cols[q] * d.lda + r0 + rr] = buf[q][rr];
+    }
+    __syncthreads();
+  }
+  if (blockIdx.x != 0) return;
+  for (int r = threadIdx.x; r < SP; r += NT)
+    for (int t = 0; t < d.nbp; ++t) {
+      const int a = d.J + t, b = d.J + d.sw[t];
+      if (a != b) {
+        double* ya = d.Y + (long long)a * SP + r;
+        double* yb = d.Y + (long long)b * SP + r;
+        const double v = *ya; *ya = *yb; *yb = v;
+      }
+    }
+  if (threadIdx.x == 0)
+    for (int t = 0; t < d.nbp; ++t) {
+      const int a = d.J + t, b = d.J + d.sw[t];
+      if (a != b) { const int v = d.piv[a]; d.piv[a] = d.piv[b]; d.piv[b] = v; }
+    }
+}
+
 // squared norms of the trailing columns A(j1:m, j) for j >= j1 (warp per column, many CTAs)
 __global__ void trail_norm_kernel(const RDesc* __restrict__ d0) {
   const RDesc d = d0[blockIdx.y];
@@ -760,7 +821,12 @@ RRQRResult rrqr_batched(cudaStream_t s, const std::vector<RRQRProb>& probs, doub
     {
       int mmax = 0;
       for (auto& d : dv) mmax = std::max(mmax, d.m);
-      apply_swaps_kernel<<<dim3((unsigned)std::max(1, std::min(64, (mmax + NT - 1) / NT)), na), NT, 0, s>>>(dd.p);
+      static const bool old_swaps = getenv("RSF_SWAPS_OLD") && getenv("RSF_SWAPS_OLD")[0] == '1';
+      if (old_swaps)
+        apply_swaps_kernel<<<dim3((unsigned)std::max(1, std::min(64, (mmax + NT - 1) / NT)), na), NT, 0, s>>>(dd.p);
+      else
+        apply_swaps_rows_kernel<<<dim3((unsigned)std::max(1, std::min(512, (mmax + SW_ROWS - 1) / SW_ROWS)), na), NT, 0,
+                                  s>>>(dd.p);
       count_launch();
     }
     RSF_LAUNCH_CHECK();
