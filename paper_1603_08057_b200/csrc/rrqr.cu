@@ -385,39 +385,46 @@ __global__ void apply_swaps_kernel(const RDesc* __restrict__ d0) {
 constexpr int SW_ROWS = 64;
 __global__ void __launch_bounds__(NT) apply_swaps_rows_kernel(const RDesc* __restrict__ d0) {
   const RDesc d = d0[blockIdx.y];
-  __shared__ int cols[2 * QR_NB], cur[2 * QR_NB], ncol_s;
+  // cols[q]: original column of slot q; cur[q]: the column it moves to.  Slots 0..nbp-1 are the
+  // block positions J+q, slots QR_NB+t the swap targets outside the block (first occurrence);
+  // every slot replays the swap sequence on its own position (no serial composition)
+  __shared__ int cols[2 * QR_NB], cur[2 * QR_NB];
   __shared__ double buf[2 * QR_NB][SW_ROWS + 1];
-  if (threadIdx.x == 0) {
-    int nc = 0;
-    for (int t = 0; t < d.nbp; ++t) cols[nc++] = d.J + t;
-    for (int t = 0; t < d.nbp; ++t) {
-      const int b = d.J + d.sw[t];
-      bool have = false;
-      for (int q = 0; q < nc; ++q) have = have || cols[q] == b;
-      if (!have) cols[nc++] = b;
+  if (threadIdx.x < 2 * QR_NB) {
+    const int q = threadIdx.x, J = d.J, nbp = d.nbp;
+    int col = -1;
+    if (q < QR_NB) {
+      if (q < nbp) col = J + q;
+    } else {
+      const int t = q - QR_NB;
+      if (t < nbp) {
+        const int b = J + d.sw[t];
+        bool first = b >= J + nbp;
+        for (int t2 = 0; t2 < t && first; ++t2) first = (J + d.sw[t2]) != b;
+        if (first) col = b;
+      }
     }
-    for (int q = 0; q < nc; ++q) cur[q] = cols[q];
-    for (int t = 0; t < d.nbp; ++t) {
-      const int a = d.J + t, b = d.J + d.sw[t];
-      if (a == b) continue;
-      int pa = 0, pb = 0;
-      for (int q = 0; q < nc; ++q) { if (cols[q] == a) pa = q; if (cols[q] == b) pb = q; }
-      const int v = cur[pa]; cur[pa] = cur[pb]; cur[pb] = v;
-    }
-    ncol_s = nc;
+    int pos = col;
+    if (col >= 0)
+      for (int t = 0; t < nbp; ++t) {
+        const int a = J + t, b = J + d.sw[t];
+        if (pos == a) pos = b; else if (pos == b) pos = a;
+      }
+    cols[q] = col;      // data of original column col ...
+    cur[q] = pos;       // ... ends up in column pos
   }
   __syncthreads();
-  const int nc = ncol_s;
+  const int nc = 2 * QR_NB;
   for (long long r0 = (long long)blockIdx.x * SW_ROWS; r0 < d.m; r0 += (long long)gridDim.x * SW_ROWS) {
     const int rows = (int)min((long long)SW_ROWS, d.m - r0);
     for (int e = threadIdx.x; e < nc * SW_ROWS; e += NT) {
       const int rr = e % SW_ROWS, q = e / SW_ROWS;
-      if (rr < rows && cur[q] != cols[q]) buf[q][rr] = d.A[(long long)cur[q] * d.lda + r0 + rr];
+      if (rr < rows && cols[q] >= 0 && cur[q] != cols[q]) buf[q][rr] = d.A[(long long)cols[q] * d.lda + r0 + rr];
     }
     __syncthreads();
     for (int e = threadIdx.x; e < nc * SW_ROWS; e += NT) {
       const int rr = e % SW_ROWS, q = e / SW_ROWS;
-      if (rr < rows && cur[q] != cols[q]) d.A[(long long)cols[q] * d.lda + r0 + rr] = buf[q][rr];
+      if (rr < rows && cols[q] >= 0 && cur[q] != cols[q]) d.A[(long long)cur[q] * d.lda + r0 + rr] = buf[q][rr];
     }
     __syncthreads();
   }
