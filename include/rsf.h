@@ -225,6 +225,18 @@ rsf_status gp_profile_eval(rsf_ctx ctx, const double* xy, const double* z, int64
  * out: m.  Device or host buffers.  Direct O(m n) cross product (FP64). */
 rsf_status gp_cond_mean(rsf_fact F, const double* z, const double* xy_new, int64_t m, double* out);
 
+/* Conditional sampling (Remark conditional): with F ~ Sigma of the joint covariance of
+ * [x_new; x_data] (the m new points FIRST, then the n2 data points, as passed to rsf_factor) and
+ * F22 ~ Sigma_22 of the data points alone,
+ *   out = Sigma_12 F22^-1 z + [I, -Sigma_12 F22^-1] F^{1/2} w
+ *       = y_1 + Sigma_12 F22^-1 (z - y_2),   y = F^{1/2} w,
+ * Sigma_12 applied as the first m rows of F [0; v] (the paper's "appropriate padding").  For w ~ N(0, I)
+ * out ~ N(Sigma_12 Sigma_22^-1 z, Sigma_11 - Sigma_12 Sigma_22^-1 Sigma_12^T) up to the factorizations'
+ * accuracy.  z: n2 data values; w: (m + n2) x nrhs (ld m + n2), joint order; out: m x nrhs (ld m);
+ * device or host.  F must be a full factor from rsf_factor.  RSF_EINVAL on shape mismatch. */
+rsf_status gp_cond_sample(rsf_fact F, rsf_fact F22, int64_t m, const double* z, const double* w, double* out,
+                          int64_t nrhs);
+
 /* message of the last failing call on this thread ("" if none) */
 const char* rsf_last_error(void);
 /* number of CUDA kernels launched by this thread so far (diagnostics) */

@@ -44,3 +44,14 @@ def dense_cond_mean(kern: Kernel, xy: np.ndarray, z: np.ndarray, xy_new: np.ndar
     """Sigma_12 Sigma_22^-1 z; Sigma_12 = sigma2 k(x', x) (distinct observations: no nugget)."""
     S = dense_sigma(kern, xy)
     return kern.sigma_points(xy_new, xy) @ np.linalg.solve(S, z)
+
+
+def dense_cond_cov(kern: Kernel, xy: np.ndarray, xy_new: np.ndarray) -> np.ndarray:
+    """Sigma_11 - Sigma_12 Sigma_22^-1 Sigma_12^T (Remark conditional): the covariance of
+    z' | z, where [z'; z] follows the GP with the new points first (nugget on every observation's
+    own diagonal, reading R-I), plain definition with a dense solve."""
+    joint = np.vstack([xy_new, xy])
+    S = dense_sigma(kern, joint)
+    m = len(xy_new)
+    S11, S12, S22 = S[:m, :m], S[:m, m:], S[m:, m:]
+    return S11 - S12 @ np.linalg.solve(S22, S12.T)

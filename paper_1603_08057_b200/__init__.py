@@ -274,6 +274,25 @@ def gp_cond_mean(F: Factor, z, xy_new, out=None):
     return out
 
 
+def gp_cond_sample(F: Factor, F22: Factor, z, w, out=None):
+    """Conditional samples (Remark conditional).  F: full factor of the joint points
+    [x_new; x_data] (new first), F22: factor of the data points, z: (n2,) data values, w:
+    (nrhs, m + n2) standard normal rows -> (nrhs, m) samples of z' | z."""
+    m = F.n - F22.n
+    nrhs = 1 if w.ndim == 1 else w.shape[0]
+    if out is None:
+        if hasattr(w, "new_empty"):
+            out = w.new_empty((nrhs, m)) if w.ndim > 1 else w.new_empty((m,))
+        else:
+            out = __import__("numpy").empty((nrhs, m) if w.ndim > 1 else (m,))
+    pz, kz = _ptr(z)
+    pw, kw = _ptr(w)
+    po, ko = _ptr(out)
+    _order_after_caller(F.ctx.h)
+    _check(lib.gp_cond_sample(F.h, F22.h, m, pz, pw, po, nrhs))
+    return out
+
+
 def hutch_trace(F: Factor, Fi: Factor | None, nprobe: int = 64, seed: int = 1603080570):
     """Hutchinson estimate of Tr(F^-1 F_i) (Fi None: Tr(F^-1)) -> (trace, standard error)."""
     t = C.c_double()

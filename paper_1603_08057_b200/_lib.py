@@ -60,7 +60,7 @@ EXPORTS = ["rsf_opts_default", "rsf_ctx_create", "rsf_ctx_destroy", "rsf_factor"
            "rsf_debug_gemm_bench", "rsf_debug_fp64_peak", "rsf_trace_dump", "rsf_debug_gemm_log",
            "rsf_debug_gemm", "rsf_ctx_wait_stream", "rsf_nccl_unique_id", "rsf_ctx_create_group",
            "rsf_ctx_group", "rsf_debug_col_slice", "rsf_debug_solve_bench",
-           "rsf_debug_job_runs"]
+           "rsf_debug_job_runs", "gp_cond_sample"]
 
 
 def load(path: str = LIB_PATH) -> C.CDLL:
@@ -97,6 +97,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
     lib.gp_profile_eval.argtypes = [vp, vp, vp, i64, C.POINTER(rsf_kernel), C.c_double, i32,
                                     C.POINTER(rsf_opts), dp, dp, C.POINTER(rsf_eval_diag)]
     lib.gp_cond_mean.argtypes = [vp, vp, vp, i64, vp]
+    lib.gp_cond_sample.argtypes = [vp, vp, i64, vp, vp, vp, i64]
     lib.gp_mle_eval.argtypes = [vp, vp, vp, i64, C.POINTER(rsf_kernel), C.c_double, i32,
                                 C.POINTER(rsf_opts), dp, dp, C.POINTER(rsf_eval_diag)]
     lib.rsf_last_error.argtypes = []

@@ -132,6 +132,33 @@ void blocked_op(const rsf::Fact& F, const double* in, double* out, int64_t nrhs,
   RSF_CUDA(cudaStreamSynchronize(s));
 }
 
+// conditional sampling helpers (gp_cond_sample): column-major blocks, k columns
+__global__ void cs_diff_kernel(double* d, const double* z, const double* Y, int m, int n2, int N, int k) {
+  // d(:, j) = z - Y(m:, j)   (d: n2 x k, Y: N x k)
+  const long long tot = (long long)n2 * k;
+  for (long long e = blockIdx.x * 256ll + threadIdx.x; e < tot; e += (long long)gridDim.x * 256) {
+    const long long j = e / n2, i = e - j * n2;
+    d[e] = z[i] - Y[j * N + m + i];
+  }
+}
+__global__ void cs_pad_kernel(double* g, const double* e, int m, int n2, int N, int k) {
+  // g(:, j) = [0_m; e(:, j)]
+  const long long tot = (long long)N * k;
+  for (long long x = blockIdx.x * 256ll + threadIdx.x; x < tot; x += (long long)gridDim.x * 256) {
+    const long long j = x / N, i = x - j * N;
+    g[x] = i < m ? 0.0 : e[j * n2 + (i - m)];
+  }
+}
+__global__ void cs_out_kernel(double* out, long long ldo, const double* Y, const double* f, int m, int N, int k) {
+  // out(:, j) = Y(0:m, j) + f(0:m, j)
+  const long long tot = (long long)m * k;
+  for (long long x = blockIdx.x * 256ll + threadIdx.x; x < tot; x += (long long)gridDim.x * 256) {
+    const long long j = x / m, i = x - j * m;
+    out[j * ldo + i] = Y[j * N + i] + f[j * N + i];
+  }
+}
+int cs_grid(long long tot) { return (int)std::max<long long>(1, std::min<long long>((tot + 255) / 256, 4096)); }
+
 }  // namespace
 
 extern "C" {
@@ -469,6 +496,68 @@ rsf_status gp_cond_mean(rsf_fact F, const double* z, const double* xy_new, int64
     if (host_out) { od.alloc((size_t)m, s); dout = od.p; }
     rsf::cond_mean(f, dz, dx, m, dout);
     if (host_out) RSF_CUDA(cudaMemcpyAsync(out, od.p, (size_t)m * sizeof(double), cudaMemcpyDeviceToHost, s));
+    RSF_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+rsf_status gp_cond_sample(rsf_fact F, rsf_fact F22, int64_t m, const double* z, const double* w, double* out,
+                          int64_t nrhs) {
+  return guard([&] {
+    RSF_REQUIRE(F && F22 && z && w && out, rsf::ST_EINVAL, "null argument");
+    RSF_REQUIRE(F->F->which == rsf::W_SIGMA && F22->F->which == rsf::W_SIGMA, rsf::ST_EINVAL,
+                "F and F22 must be Sigma factors");
+    RSF_REQUIRE(!F->F->solve_only, rsf::ST_EINVAL, "F must be a full factor (rsf_factor)");
+    RSF_REQUIRE(m >= 1 && F->F->n() == m + F22->F->n(), rsf::ST_EINVAL,
+                "F must factor the m new points followed by the n2 data points of F22");
+    RSF_REQUIRE(nrhs >= 0, rsf::ST_EINVAL, "nrhs < 0");
+    RSF_CUDA(cudaSetDevice(F->owner->ctx.device));
+    const rsf::Fact& fj = *F->F;
+    const rsf::Fact& fd = *F22->F;
+    cudaStream_t s = fj.ctx->stream;
+    const int N = fj.n(), n2 = fd.n();
+    if (nrhs == 0) return;
+    rsf::DBuf<double> zd;
+    const double* dz = z;
+    if (!is_device_ptr(z)) { zd.alloc(n2, s); zd.upload(z, n2); dz = zd.p; }
+    const bool dw = is_device_ptr(w), dout = is_device_ptr(out);
+    const int kmax = 256;
+    for (int64_t j0 = 0; j0 < nrhs; j0 += kmax) {
+      const int k = (int)std::min<int64_t>(kmax, nrhs - j0);
+      // y = F^{1/2} w (joint order: new points first)
+      rsf::DBuf<double> wst, Y((size_t)N * k, s), X((size_t)N * k, s),
+          tmpj((size_t)std::max<long long>(fj.tmp_cols, 1) * k, s), tmpd((size_t)std::max<long long>(fd.tmp_cols, 1) * k, s);
+      const double* src = w + j0 * (int64_t)N;
+      if (!dw) { wst.alloc((size_t)N * k, s); wst.upload(src, (size_t)N * k); src = wst.p; }
+      rsf::to_internal(s, *fj.tree, src, N, k, X.p);
+      rsf::sqrt_internal(fj, X.p, k, tmpj.p);
+      rsf::to_external(s, *fj.tree, X.p, k, Y.p, N);
+      // e = F22^-1 (z - y_2)
+      rsf::DBuf<double> D((size_t)n2 * k, s), Xd((size_t)n2 * k, s);
+      cs_diff_kernel<<<cs_grid((long long)n2 * k), 256, 0, s>>>(D.p, dz, Y.p, (int)m, n2, N, k);
+      count_launch();
+      rsf::to_internal(s, *fd.tree, D.p, n2, k, Xd.p);
+      rsf::solve_internal(fd, Xd.p, k, tmpd.p);
+      rsf::to_external(s, *fd.tree, Xd.p, k, D.p, n2);
+      // f = F [0; e]  (its first m rows apply Sigma_12 e, "through appropriate padding")
+      rsf::DBuf<double> G((size_t)N * k, s);
+      cs_pad_kernel<<<cs_grid((long long)N * k), 256, 0, s>>>(G.p, D.p, (int)m, n2, N, k);
+      count_launch();
+      rsf::to_internal(s, *fj.tree, G.p, N, k, X.p);
+      rsf::apply_internal(fj, X.p, k, tmpj.p);
+      rsf::to_external(s, *fj.tree, X.p, k, G.p, N);
+      // out = y_1 + f_1 = mu + [I, -Sigma_12 F22^-1] F^{1/2} w
+      if (dout) {
+        cs_out_kernel<<<cs_grid((long long)m * k), 256, 0, s>>>(out + j0 * m, m, Y.p, G.p, (int)m, N, k);
+        count_launch();
+      } else {
+        rsf::DBuf<double> O((size_t)m * k, s);
+        cs_out_kernel<<<cs_grid((long long)m * k), 256, 0, s>>>(O.p, m, Y.p, G.p, (int)m, N, k);
+        count_launch();
+        RSF_CUDA(cudaMemcpyAsync(out + j0 * m, O.p, (size_t)m * k * sizeof(double), cudaMemcpyDeviceToHost, s));
+        RSF_CUDA(cudaStreamSynchronize(s));
+      }
+      RSF_LAUNCH_CHECK();
+    }
     RSF_CUDA(cudaStreamSynchronize(s));
   });
 }

@@ -101,3 +101,53 @@ def test_gpu_profile_and_cond_mean_vs_dense():
     assert np.linalg.norm(got - want) <= bound, (np.linalg.norm(got - want), bound)
     got_h = R.gp_cond_mean(F, np.ascontiguousarray(z), np.ascontiguousarray(xn), np.empty(300))
     assert np.array_equal(got_h, got)
+
+
+def test_cond_cov_closed_forms():
+    """dense_cond_cov against (a) one data point at the new location: sigma2 + tau -
+    sigma2^2 / (sigma2 + tau); (b) the Schur-complement identity S^-1 = [(Sigma_joint)^-1]_11."""
+    from oracle.profile import dense_cond_cov
+    from oracle.dense import dense_sigma
+    k = Kernel("matern32", 0.2, 1.3, 0.05, 1.0, ("rho",))
+    x = np.array([[0.3, 0.4]])
+    S = dense_cond_cov(k, x, x.copy())
+    assert S[0, 0] == pytest.approx(1.3 + 0.05 - 1.3 ** 2 / 1.35, rel=1e-12)
+    r = np.random.default_rng(12)
+    xd, xn = r.random((60, 2)), r.random((7, 2))
+    S = dense_cond_cov(k, xd, xn)
+    J = np.linalg.inv(dense_sigma(k, np.vstack([xn, xd])))
+    np.testing.assert_allclose(np.linalg.inv(S), J[:7, :7], rtol=1e-9)
+
+
+@pytest.mark.gpu
+def test_gpu_cond_sample_mean_and_covariance():
+    """gp_cond_sample (Remark conditional, P:680-690): with w = 0 it returns the conditional mean;
+    its linear map B (columns: out(w = e_j) - out(0) over all m + n2 joint coordinates) satisfies
+    B B^T = Sigma_11 - Sigma_12 Sigma_22^-1 Sigma_12^T (dense oracle)."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_1603_08057_b200 as R
+    from oracle.profile import dense_cond_cov
+    dev = torch.device("cuda:0")
+    r = np.random.default_rng(13)
+    n2, m = 1500, 120
+    xd, xn = r.random((n2, 2)), r.random((m, 2))
+    ok = Kernel("matern32", 0.1, 1.0, 1e-2, 1.0, ("rho",))
+    rk = R.Kernel("matern32", 0.1, 1.0, 1e-2, 1.0, ("rho",))
+    z = r.standard_normal(n2)
+    ctx = R.Context(0)
+    F = R.Factor(ctx, torch.from_numpy(np.vstack([xn, xd])).to(dev), rk, 1e-11, 64)
+    F22 = R.Factor(ctx, torch.from_numpy(xd).to(dev), rk, 1e-11, 64)
+    N = n2 + m
+    W = torch.zeros((N + 1, N), dtype=torch.float64, device=dev)
+    W[1:] = torch.eye(N, dtype=torch.float64, device=dev)
+    out = R.gp_cond_sample(F, F22, torch.from_numpy(z).to(dev), W).cpu().numpy()
+    mu = dense_cond_mean(ok, xd, z, xn)
+    assert np.linalg.norm(out[0] - mu) <= 1e-6 * np.linalg.norm(mu)
+    B = (out[1:] - out[0]).T            # m x N
+    S = dense_cond_cov(ok, xd, xn)
+    assert np.linalg.norm(B @ B.T - S) <= 1e-6 * np.linalg.norm(S)
+    # host buffers give the same result
+    oh = R.gp_cond_sample(F, F22, z.copy(), np.ascontiguousarray(W[:3].cpu().numpy()))
+    np.testing.assert_allclose(oh, out[:3], rtol=1e-12, atol=1e-14)
