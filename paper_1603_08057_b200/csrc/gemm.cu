@@ -1141,8 +1141,7 @@ constexpr int GV_TJ = 64, GV_NT = 256, GV_KC = 2048;
 template <bool TA, bool TB, bool TRI, int TJ = 64>
 __global__ void __launch_bounds__(GV_NT) gemv1_kernel(const GemmDesc* __restrict__ descs, const int* __restrict__ prefix,
                                                       int nprob, double* X0, double* X1, int ldx, double* ws,
-                                                      const long long* __restrict__ mnpre, int kchunk,
-                                                      int* __restrict__ tilecnt) {
+                                                      const long long* __restrict__ mnpre, int kchunk) {
   __shared__ double as[GV_KC];
   __shared__ double red[4][64];
   const int p = find_prob(prefix, nprob, blockIdx.x);
@@ -1271,59 +1270,14 @@ __global__ void __launch_bounds__(GV_NT) gemv1_kernel(const GemmDesc* __restrict
       jo = n0 + tid;
     }
   }
-  if (!ws) {
-    if (jo < 0 || jo >= N) return;
+  if (jo < 0 || jo >= N) return;
+  if (ws) {
+    ws[mnpre[p] * (long long)gridDim.z + (long long)blockIdx.z * N + jo] = out;   // W[z * MN + e], MN = N
+  } else {
     const long long cc = dd.mapC ? (long long)__ldg(dd.mapC + jo) : (long long)jo;
     double* c = C + cc * ldc;
     *c = dd.beta != 0.0 ? fma(dd.beta, *c, dd.alpha * out) : dd.alpha * out;
-    return;
   }
-  // K split: partial to the workspace; the last slice of this column tile to finish adds the S
-  // partials in slice order (deterministic whichever CTA is last) and writes C, then re-arms the
-  // tile's counter -- no separate reduction launch
-  const long long wbase = mnpre[p] * (long long)gridDim.z;
-  if (jo >= 0 && jo < N) ws[wbase + (long long)blockIdx.z * N + jo] = out;   // W[z * MN + e], MN = N
-  __threadfence();
-  __syncthreads();
-  __shared__ int is_last;
-  if (tid == 0) is_last = atomicAdd(tilecnt + blockIdx.x, 1) == (int)gridDim.z - 1;
-  __syncthreads();
-  if (!is_last) return;
-  __threadfence();
-  for (int jj = tid; jj < TJ; jj += GV_NT) {
-    const int j = n0 + jj;
-    if (j >= N) break;
-    double v = 0.0;
-    for (int z = 0; z < (int)gridDim.z; ++z) v += __ldcg(ws + wbase + (long long)z * N + j);
-    const long long cc = dd.mapC ? (long long)__ldg(dd.mapC + j) : (long long)j;
-    double* c = C + cc * ldc;
-    *c = dd.beta != 0.0 ? fma(dd.beta, *c, dd.alpha * v) : dd.alpha * v;
-  }
-  if (tid == 0) tilecnt[blockIdx.x] = 0;
-}
-
-// per-stream tile counters of the K-split GEMV (kept zero between launches by the kernels)
-int* gemv_tile_counters(cudaStream_t s, int tiles) {
-  static std::mutex mu;
-  static std::vector<std::pair<cudaStream_t, std::pair<int*, int>>> v;
-  std::lock_guard<std::mutex> lk(mu);
-  for (auto& x : v)
-    if (x.first == s) {
-      if (x.second.second >= tiles) return x.second.first;
-      RSF_CUDA(cudaStreamSynchronize(s));
-      cudaFree(x.second.first);
-      const int cap = std::max(tiles, 2 * x.second.second);
-      RSF_CUDA(cudaMalloc((void**)&x.second.first, cap * sizeof(int)));
-      RSF_CUDA(cudaMemset(x.second.first, 0, cap * sizeof(int)));
-      x.second.second = cap;
-      return x.second.first;
-    }
-  int* p = nullptr;
-  const int cap = std::max(tiles, 1 << 16);
-  RSF_CUDA(cudaMalloc((void**)&p, cap * sizeof(int)));
-  RSF_CUDA(cudaMemset(p, 0, cap * sizeof(int)));
-  v.emplace_back(s, std::make_pair(p, cap));
-  return p;
 }
 
 int gemm_mode() {
@@ -1436,14 +1390,22 @@ void GemmBatch::run(cudaStream_t s, double* X0, double* X1, int ldx, int Mglob, 
     }
     const dim3 grid(tiles, 1, S);
     double* wsp = S > 1 ? ws.p : nullptr;
-    int* tcnt = S > 1 ? gemv_tile_counters(s, tiles) : nullptr;
-#define RSF_GV(TA, TB, TRI) gemv1_kernel<TA, TB, TRI><<<grid, GV_NT, 0, s>>>(dp_, ppv, (int)P, X0, X1, ldx, wsp, dmn, kc, tcnt)
+#define RSF_GV(TA, TB, TRI) gemv1_kernel<TA, TB, TRI><<<grid, GV_NT, 0, s>>>(dp_, ppv, (int)P, X0, X1, ldx, wsp, dmn, kc)
     if (!ta_ && !tb_) { if (tri) RSF_GV(false, false, true); else RSF_GV(false, false, false); }
     else if (ta_ && !tb_) { if (tri) RSF_GV(true, false, true); else RSF_GV(true, false, false); }
     else if (!ta_ && tb_) { if (tri) RSF_GV(false, true, true); else RSF_GV(false, true, false); }
     else { if (tri) RSF_GV(true, true, true); else RSF_GV(true, true, false); }
 #undef RSF_GV
-
+    if (S > 1) {
+      count_launch();
+      long long mx = 0;
+      for (size_t i = 0; i < P; ++i) mx = std::max(mx, mn[i + 1] - mn[i]);
+      const int gx = (int)std::max<long long>(1, std::min<long long>((mx + P_NT - 1) / P_NT, 1024));
+      for (size_t o = 0; o < P; o += 65535) {
+        const unsigned ny = (unsigned)std::min<size_t>(65535, P - o);
+        splitk_reduce_kernel<<<dim3(gx, ny), P_NT, 0, s>>>(dp_, ws.p, dmn, S, (int)o, X0, X1, ldx, 1);
+      }
+    }
   } else if (M <= 16 && !has_mapk_) {   // (only the pipelined kernel implements mapK)
     dim3 grid(totalN_, ceil_div(M, 16));
     launch_variant<16, 1>(ta_, tb_, grid, s, dp_, pp_, (int)h_.size(), X0, X1, ldx, Mglob);
