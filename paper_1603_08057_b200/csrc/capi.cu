@@ -510,10 +510,20 @@ rsf_status gp_cond_sample(rsf_fact F, rsf_fact F22, int64_t m, const double* z, 
     RSF_REQUIRE(m >= 1 && F->F->n() == m + F22->F->n(), rsf::ST_EINVAL,
                 "F must factor the m new points followed by the n2 data points of F22");
     RSF_REQUIRE(nrhs >= 0, rsf::ST_EINVAL, "nrhs < 0");
+    RSF_REQUIRE(F->owner->ctx.device == F22->owner->ctx.device, rsf::ST_EINVAL, "F and F22 on different devices");
     RSF_CUDA(cudaSetDevice(F->owner->ctx.device));
     const rsf::Fact& fj = *F->F;
     const rsf::Fact& fd = *F22->F;
     cudaStream_t s = fj.ctx->stream;
+    // every operator below runs on F's stream (F22 may belong to another context / stream)
+    if (F22->owner->ctx.stream != s) {
+      cudaEvent_t ev;
+      RSF_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      RSF_CUDA(cudaEventRecord(ev, F22->owner->ctx.stream));
+      RSF_CUDA(cudaStreamWaitEvent(s, ev, 0));
+      cudaEventDestroy(ev);
+    }
+    rsf::StreamScope scope(s);
     const int N = fj.n(), n2 = fd.n();
     if (nrhs == 0) return;
     rsf::DBuf<double> zd;
