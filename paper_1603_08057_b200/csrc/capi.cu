@@ -159,6 +159,17 @@ __global__ void cs_out_kernel(double* out, long long ldo, const double* Y, const
 }
 int cs_grid(long long tot) { return (int)std::max<long long>(1, std::min<long long>((tot + 255) / 256, 4096)); }
 
+// operators of a second handle (F_i) on the first handle's stream: order after F_i's context
+// stream, then redirect (StreamScope) every operator of the call to F's stream
+void join_stream(cudaStream_t s, rsf_fact other) {
+  if (!other || other->owner->ctx.stream == s) return;
+  cudaEvent_t ev;
+  RSF_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  RSF_CUDA(cudaEventRecord(ev, other->owner->ctx.stream));
+  RSF_CUDA(cudaStreamWaitEvent(s, ev, 0));
+  cudaEventDestroy(ev);
+}
+
 }  // namespace
 
 extern "C" {
@@ -416,6 +427,8 @@ rsf_status hutch_trace(rsf_fact F, rsf_fact Fi, int64_t nprobe, uint64_t seed, d
     RSF_REQUIRE(!Fi || Fi->F->n() == F->F->n(), rsf::ST_EINVAL, "dimension mismatch");
     RSF_REQUIRE(nprobe >= 1, rsf::ST_EINVAL, "nprobe must be >= 1");
     RSF_CUDA(cudaSetDevice(F->owner->ctx.device));
+    join_stream(F->owner->ctx.stream, Fi);
+    rsf::StreamScope scope(F->owner->ctx.stream);
     rsf::hutch(*F->F, Fi ? Fi->F.get() : nullptr, nprobe, seed, trace, std_err);
   });
 }
@@ -429,6 +442,8 @@ rsf_status peel_trace(rsf_fact F, rsf_fact Fi, double eps_peel, const rsf_opts* 
     RSF_REQUIRE(!Fi || Fi->F->n() == F->F->n(), rsf::ST_EINVAL, "dimension mismatch");
     RSF_REQUIRE(eps_peel > 0, rsf::ST_EINVAL, "eps_peel must be > 0");
     RSF_CUDA(cudaSetDevice(F->owner->ctx.device));
+    join_stream(F->owner->ctx.stream, Fi);
+    rsf::StreamScope scope(F->owner->ctx.stream);
     rsf::Opts o = opts ? make_opts(opts) : F->F->opts;
     o.eps_peel = eps_peel;
     rsf::PeelDiag pd;
