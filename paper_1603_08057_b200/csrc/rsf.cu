@@ -30,7 +30,9 @@ namespace {
 
 constexpr int N_RINGS = 4, N_ANGLES = 64;   // n_prox = 256, R-C
 constexpr long long CHUNK_ELEMS = 1ll << 28; // max doubles of ID matrices per launch group
-constexpr int SMALL_C = 128;                 // |I| <= SMALL_C: exact greedy CPQR in shared memory
+// |I| <= SMALL_C: exact greedy CPQR, one CTA per box (shared memory, global workspace when the
+// block does not fit); larger boxes: the blocked randomized RRQR (RSF_SMALL_C overrides)
+static const int SMALL_C = getenv("RSF_SMALL_C") ? atoi(getenv("RSF_SMALL_C")) : 128;
 
 double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();

@@ -41,6 +41,48 @@ __device__ __forceinline__ void slab_mm(double* __restrict__ out, const double* 
   }
 }
 
+// KC = 32, register-blocked: thread (rp, cg) with rp = tid % 16, cg = tid / 16 owns the outputs
+// (j, rho) for rho in {rp, rp + 16} and j = cg + 16 u, u < 4: per K step 2 shared loads + 4
+// (warp-pairwise uniform) matrix loads feed 8 FMAs (slab_mm: 1 + 4 loads for 4 FMAs)
+template <bool TR>
+__device__ __forceinline__ void slab_mm32(double* __restrict__ out, const double* __restrict__ in, int K, int N,
+                                          const double* __restrict__ Mat, int ldm, double alpha, double beta) {
+  constexpr int KC = 32;
+  const int rp = threadIdx.x & 15, cg = threadIdx.x >> 4;   // 16 x 16
+  for (int j0 = cg; j0 < N; j0 += 64) {
+    double a0[4] = {0.0, 0.0, 0.0, 0.0}, a1[4] = {0.0, 0.0, 0.0, 0.0};
+    int jj[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) jj[u] = min(j0 + 16 * u, N - 1);
+    for (int kk = 0; kk < K; ++kk) {
+      const double x0 = in[kk * KC + rp], x1 = in[kk * KC + rp + 16];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double m = TR ? __ldg(Mat + jj[u] + (long long)kk * ldm) : __ldg(Mat + kk + (long long)jj[u] * ldm);
+        a0[u] = fma(x0, m, a0[u]);
+        a1[u] = fma(x1, m, a1[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = j0 + 16 * u;
+      if (j < N) {
+        double* o0 = out + j * KC + rp;
+        double* o1 = o0 + 16;
+        *o0 = (beta == 0.0) ? alpha * a0[u] : fma(beta, *o0, alpha * a0[u]);
+        *o1 = (beta == 0.0) ? alpha * a1[u] : fma(beta, *o1, alpha * a1[u]);
+      }
+    }
+  }
+}
+
+template <int KC, bool TR>
+__device__ __forceinline__ void slab_mm_any(double* __restrict__ out, const double* __restrict__ in, int K, int N,
+                                            const double* __restrict__ Mat, int ldm, double alpha, double beta) {
+  if constexpr (KC == 32) slab_mm32<TR>(out, in, K, N, Mat, ldm, alpha, beta);
+  else slab_mm<KC, TR>(out, in, K, N, Mat, ldm, alpha, beta);
+}
+
 template <int KC>
 __device__ __forceinline__ void load_cols(double* __restrict__ dst, const double* __restrict__ X, const int* __restrict__ idx,
                                           int cnt, int ldx, int r0, int k) {
@@ -73,17 +115,17 @@ __global__ void __launch_bounds__(NT) sweep_kernel(const BoxOp* __restrict__ ops
     load_cols<KC>(xr, X0, op.R, r, k, r0, k);
     __syncthreads();
     if (kind == SW_SOLVE_FWD) {
-      if (kb) slab_mm<KC, false>(xr, xs, kb, r, op.T, kb, -1.0, 1.0);   // x_R -= T^T x_S
+      if (kb) slab_mm_any<KC, false>(xr, xs, kb, r, op.T, kb, -1.0, 1.0);   // x_R -= T^T x_S
       __syncthreads();
-      slab_mm<KC, true>(yr, xr, r, r, op.L, r, 1.0, 0.0);               // y_R = L^-1 x_R
+      slab_mm_any<KC, true>(yr, xr, r, r, op.L, r, 1.0, 0.0);               // y_R = L^-1 x_R
       __syncthreads();
-      if (kb) slab_mm<KC, true>(xs, yr, r, kb, op.E, kb, -1.0, 1.0);    // x_S -= E y_R
+      if (kb) slab_mm_any<KC, true>(xs, yr, r, kb, op.E, kb, -1.0, 1.0);    // x_S -= E y_R
     } else {
-      if (kb) slab_mm<KC, false>(xr, xs, kb, r, op.E, kb, -1.0, 1.0);   // x_R -= E^T x_S
+      if (kb) slab_mm_any<KC, false>(xr, xs, kb, r, op.E, kb, -1.0, 1.0);   // x_R -= E^T x_S
       __syncthreads();
-      slab_mm<KC, false>(yr, xr, r, r, op.L, r, 1.0, 0.0);              // y_R = L^-T x_R
+      slab_mm_any<KC, false>(yr, xr, r, r, op.L, r, 1.0, 0.0);              // y_R = L^-T x_R
       __syncthreads();
-      if (kb) slab_mm<KC, true>(xs, yr, r, kb, op.T, kb, -1.0, 1.0);    // x_S -= T y_R
+      if (kb) slab_mm_any<KC, true>(xs, yr, r, kb, op.T, kb, -1.0, 1.0);    // x_S -= T y_R
     }
     __syncthreads();
     store_cols<KC>(xs, X0, op.S, kb, k, r0, k);
@@ -92,10 +134,10 @@ __global__ void __launch_bounds__(NT) sweep_kernel(const BoxOp* __restrict__ ops
     load_cols<KC>(xs, X0, op.S, kb, k, r0, k);
     load_cols<KC>(xr, X0, op.R, r, k, r0, k);
     __syncthreads();
-    if (kb) slab_mm<KC, true>(xs, xr, r, kb, op.T, kb, 1.0, 1.0);       // x_S += T x_R
+    if (kb) slab_mm_any<KC, true>(xs, xr, r, kb, op.T, kb, 1.0, 1.0);       // x_S += T x_R
     __syncthreads();
-    if (kb) slab_mm<KC, false>(yr, xs, kb, r, op.E, kb, 1.0, 0.0);      // y_R = X_SR^T x_S
-    slab_mm<KC, false>(yr, xr, r, r, op.L, r, 1.0, kb ? 1.0 : 0.0);     //     + X_RR x_R (same thread owns y_R(j, rho))
+    if (kb) slab_mm_any<KC, false>(yr, xs, kb, r, op.E, kb, 1.0, 0.0);      // y_R = X_SR^T x_S
+    slab_mm_any<KC, false>(yr, xr, r, r, op.L, r, 1.0, kb ? 1.0 : 0.0);     //     + X_RR x_R (same thread owns y_R(j, rho))
     __syncthreads();
     store_cols<KC>(xs, X0, op.S, kb, k, r0, k);
     store_cols<KC>(yr, X1, op.R, r, k, r0, k);
@@ -104,9 +146,9 @@ __global__ void __launch_bounds__(NT) sweep_kernel(const BoxOp* __restrict__ ops
     load_cols<KC>(xr, X0, op.R, r, k, r0, k);
     load_cols<KC>(yr, X1, op.R, r, k, r0, k);
     __syncthreads();
-    if (kb) slab_mm<KC, true>(xs, xr, r, kb, op.E, kb, 1.0, 1.0);       // y_S += X_SR x_R
+    if (kb) slab_mm_any<KC, true>(xs, xr, r, kb, op.E, kb, 1.0, 1.0);       // y_S += X_SR x_R
     __syncthreads();
-    if (kb) slab_mm<KC, false>(yr, xs, kb, r, op.T, kb, 1.0, 1.0);      // y_R += T^T y_S
+    if (kb) slab_mm_any<KC, false>(yr, xs, kb, r, op.T, kb, 1.0, 1.0);      // y_R += T^T y_S
     __syncthreads();
     store_cols<KC>(xs, X1, op.S, kb, k, r0, k);
     store_cols<KC>(yr, X1, op.R, r, k, r0, k);
