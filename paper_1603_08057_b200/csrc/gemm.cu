@@ -823,14 +823,14 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 constexpr int P_BM = 128, P_BK = 16, P_ST = 4, P_NT = 256;
 constexpr int P_LDA = P_BM + 4;   // row stride = 8 banks mod 32: conflict-free fragment loads
 template <int BN> constexpr int p_ldb() { return BN + 4; }
-template <int BN, int BM = P_BM, int ST = P_ST>
-constexpr size_t p_smem() { return (size_t)ST * P_BK * (BM + 4 + p_ldb<BN>()) * sizeof(double); }
+template <int BN, int BM = P_BM, int ST = P_ST, int BK = P_BK>
+constexpr size_t p_smem() { return (size_t)ST * BK * (BM + 4 + p_ldb<BN>()) * sizeof(double); }
 
 // CTA tile BM x BN (BM = 128: BN = 32, 64, 128, 8 warps as 4 (M) x 2 (N), 4 stages; BM = 64:
 // BN = 64, 4 warps as 2 x 2, 3 stages, 4 CTAs per SM -- for short K, where the prologue and the
 // epilogue of a CTA dominate and more resident CTAs overlap them), warp tile 32 x BN/2
 // (4 x BN/16 DMMA.8x8x4 tiles).
-template <bool TA, bool TB, int BN, int BM, int ST>
+template <bool TA, bool TB, int BN, int BM, int ST, int BK = P_BK>
 __global__ void __launch_bounds__(2 * BM, (BN >= 128 ? 1 : (BM == 64 ? 4 : 2))) gemm_pipe_kernel(const GemmDesc* __restrict__ descs,
                                                             const int* __restrict__ prefix, int nprob,
                                                             double* X0, double* X1, int ldx, int Mglob,
@@ -838,6 +838,7 @@ __global__ void __launch_bounds__(2 * BM, (BN >= 128 ? 1 : (BM == 64 ? 4 : 2))) 
                                                             int kchunk, int mtiles, int smem_epi) {
   constexpr int LDB = p_ldb<BN>(), NI = BN / 16, WN = BN / 2;
   constexpr int P_BM = BM, P_NT = 2 * BM, P_LDA = BM + 4, P_ST = ST, WMN = BM / 32;   // warps: WMN (M) x 2 (N)
+  constexpr int P_BK = BK;
   static_assert(BN * P_LDA <= P_ST * P_BK * (P_LDA + p_ldb<BN>()), "C tile must fit in the pipeline buffers");
   extern __shared__ __align__(16) double psm[];
   double* As = psm;                              // [ST][BK][LDA]
@@ -1079,27 +1080,27 @@ __global__ void __launch_bounds__(2 * BM, (BN >= 128 ? 1 : (BM == 64 ? 4 : 2))) 
   }
 }
 
-template <int BN, int BM = P_BM, int ST = P_ST>
+template <int BN, int BM = P_BM, int ST = P_ST, int BK = P_BK>
 void launch_pipe(bool ta, bool tb, dim3 grid, cudaStream_t s, const GemmDesc* d, const int* pre, int np,
                  double* X0, double* X1, int ldx, int Mg, double* ws = nullptr, const long long* mnpre = nullptr,
                  int kchunk = 0) {
   static std::once_flag attr_once;
-  constexpr size_t SM = p_smem<BN, BM, ST>();
+  constexpr size_t SM = p_smem<BN, BM, ST, BK>();
   std::call_once(attr_once, [&] {
-    cudaFuncSetAttribute(gemm_pipe_kernel<false, false, BN, BM, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
-    cudaFuncSetAttribute(gemm_pipe_kernel<true, false, BN, BM, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
-    cudaFuncSetAttribute(gemm_pipe_kernel<false, true, BN, BM, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
-    cudaFuncSetAttribute(gemm_pipe_kernel<true, true, BN, BM, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
+    cudaFuncSetAttribute(gemm_pipe_kernel<false, false, BN, BM, ST, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
+    cudaFuncSetAttribute(gemm_pipe_kernel<true, false, BN, BM, ST, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
+    cudaFuncSetAttribute(gemm_pipe_kernel<false, true, BN, BM, ST, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
+    cudaFuncSetAttribute(gemm_pipe_kernel<true, true, BN, BM, ST, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
   });
   ++g_pipe_launches;
   static const int epi = getenv("RSF_GEMM_EPI") ? atoi(getenv("RSF_GEMM_EPI")) : 1;
   const int mt = (int)grid.y;
   const dim3 g1((unsigned)((long long)grid.x * grid.y), 1, grid.z);   // 1-D over (N-tile, M-tile)
   constexpr int NTH = 2 * BM;
-  if (!ta && !tb) gemm_pipe_kernel<false, false, BN, BM, ST><<<g1, NTH, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk, mt, epi);
-  else if (ta && !tb) gemm_pipe_kernel<true, false, BN, BM, ST><<<g1, NTH, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk, mt, epi);
-  else if (!ta && tb) gemm_pipe_kernel<false, true, BN, BM, ST><<<g1, NTH, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk, mt, epi);
-  else gemm_pipe_kernel<true, true, BN, BM, ST><<<g1, NTH, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk, mt, epi);
+  if (!ta && !tb) gemm_pipe_kernel<false, false, BN, BM, ST, BK><<<g1, NTH, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk, mt, epi);
+  else if (ta && !tb) gemm_pipe_kernel<true, false, BN, BM, ST, BK><<<g1, NTH, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk, mt, epi);
+  else if (!ta && tb) gemm_pipe_kernel<false, true, BN, BM, ST, BK><<<g1, NTH, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk, mt, epi);
+  else gemm_pipe_kernel<true, true, BN, BM, ST, BK><<<g1, NTH, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk, mt, epi);
 }
 
 // split-K reduction: C = alpha * sum_z W_z + beta * C (fixed summation order: deterministic)
@@ -1415,6 +1416,7 @@ void GemmBatch::run(cudaStream_t s, double* X0, double* X1, int ldx, int Mglob, 
     static const bool wide = getenv("RSF_GEMM_BN128") && getenv("RSF_GEMM_BN128")[0] == '1';
     if (maxN_ <= 32) {
       dim3 grid(totalN32_, ceil_div(M, P_BM));
+      // (32-deep K tiles measured equal or slower for these N <= 32 products: tools/gemm_variants.py)
       launch_pipe<32>(ta_, tb_, grid, s, dp_, pp_ + (P + 1), (int)P, X0, X1, ldx, Mglob);
     } else if (wide && maxN_ >= 512) {
       dim3 grid(totalN128_, ceil_div(M, P_BM));
@@ -1462,7 +1464,11 @@ void GemmBatch::run(cudaStream_t s, double* X0, double* X1, int ldx, int Mglob, 
         const long long* dmn = static_cast<const long long*>(ring_upload(s, mn.data(), mn.size() * sizeof(long long)));
         DBuf<double> ws((size_t)S * std::max<long long>(mn[P], 1), s);
         dim3 grid(totalN_, ceil_div(M, P_BM), S);
-        launch_pipe<64>(ta_, tb_, grid, s, dp_, pp_, (int)P, X0, X1, ldx, Mglob, ws.p, dmn, kc);
+        static const int variant_sk = getenv("RSF_GEMM_VARIANT") ? atoi(getenv("RSF_GEMM_VARIANT")) : -1;
+        if (variant_sk == 1 || (variant_sk < 0 && !tb_))
+          launch_pipe<64, 128, 2, 32>(ta_, tb_, grid, s, dp_, pp_, (int)P, X0, X1, ldx, Mglob, ws.p, dmn, kc);
+        else
+          launch_pipe<64>(ta_, tb_, grid, s, dp_, pp_, (int)P, X0, X1, ldx, Mglob, ws.p, dmn, kc);
         long long mx = 0;
         for (size_t i = 0; i < P; ++i) mx = std::max(mx, mn[i + 1] - mn[i]);
         const int gx = (int)std::max<long long>(1, std::min<long long>((mx + P_NT - 1) / P_NT, 1024));
@@ -1474,10 +1480,18 @@ void GemmBatch::run(cudaStream_t s, double* X0, double* X1, int ldx, int Mglob, 
       } else if (maxK_ <= small_k) {
         // short K: 64 x 64 tiles, 4 resident CTAs per SM (their prologues/epilogues overlap)
         dim3 grid(totalN_, ceil_div(M, 64));
+        // (32-deep K tiles here measured 10-22 % slower: tools/gemm_variants_smallk.py)
         launch_pipe<64, 64, 3>(ta_, tb_, grid, s, dp_, pp_, (int)P, X0, X1, ldx, Mglob);
       } else {
         dim3 grid(totalN_, ceil_div(M, P_BM));
-        launch_pipe<64>(ta_, tb_, grid, s, dp_, pp_, (int)P, X0, X1, ldx, Mglob);
+        // op(B) = B: 32-deep K tiles, 2 stages (same 104 KB, half the barriers; the B tile is
+        // staged with 8-byte copies there) measured +6-8 % on the sweep / subtraction shapes of
+        // config 3 (tools/gemm_variants.py); op(B) = B^T keeps 16-deep tiles, 4 stages (equal)
+        static const int variant = getenv("RSF_GEMM_VARIANT") ? atoi(getenv("RSF_GEMM_VARIANT")) : -1;
+        if (variant == 1 || (variant < 0 && !tb_)) launch_pipe<64, 128, 2, 32>(ta_, tb_, grid, s, dp_, pp_, (int)P, X0, X1, ldx, Mglob);
+        else if (variant == 2) launch_pipe<64, 128, 3, 32>(ta_, tb_, grid, s, dp_, pp_, (int)P, X0, X1, ldx, Mglob);
+        else if (variant == 3) launch_pipe<64, 128, 3>(ta_, tb_, grid, s, dp_, pp_, (int)P, X0, X1, ldx, Mglob);
+        else launch_pipe<64>(ta_, tb_, grid, s, dp_, pp_, (int)P, X0, X1, ldx, Mglob);
       }
     }
   } else if (gemm_mode() == 1) {
