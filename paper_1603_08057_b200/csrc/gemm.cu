@@ -1413,13 +1413,14 @@ void GemmBatch::run(cudaStream_t s, double* X0, double* X1, int ldx, int Mglob, 
   } else if (gemm_mode() == 2 || has_mapk_) {
     // N-tile width by the widest problem of the batch (prefix sums for each width)
     const size_t P = h_.size();
-    static const bool wide = getenv("RSF_GEMM_BN128") && getenv("RSF_GEMM_BN128")[0] == '1';
+    static const int wide = getenv("RSF_GEMM_BN128") ? atoi(getenv("RSF_GEMM_BN128")) : 0;
     if (maxN_ <= 32) {
       dim3 grid(totalN32_, ceil_div(M, P_BM));
       // (32-deep K tiles measured equal or slower for these N <= 32 products: tools/gemm_variants.py)
       launch_pipe<32>(ta_, tb_, grid, s, dp_, pp_ + (P + 1), (int)P, X0, X1, ldx, Mglob);
     } else if (wide && maxN_ >= 512) {
       dim3 grid(totalN128_, ceil_div(M, P_BM));
+      // (opt-in; measured 20-25 % slower than the 64-wide tiles on the config-3 shapes)
       launch_pipe<128>(ta_, tb_, grid, s, dp_, pp_ + 2 * (P + 1), (int)P, X0, X1, ldx, Mglob);
     } else {
       // split-K when the output tiles fill the GPU's resident slots badly and K is long
