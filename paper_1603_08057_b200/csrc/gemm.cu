@@ -1490,8 +1490,8 @@ void GemmBatch::run(cudaStream_t s, double* X0, double* X1, int ldx, int Mglob, 
         // config 3 (tools/gemm_variants.py); op(B) = B^T keeps 16-deep tiles, 4 stages (equal)
         static const int variant = getenv("RSF_GEMM_VARIANT") ? atoi(getenv("RSF_GEMM_VARIANT")) : -1;
         if (variant == 1 || (variant < 0 && !tb_)) launch_pipe<64, 128, 2, 32>(ta_, tb_, grid, s, dp_, pp_, (int)P, X0, X1, ldx, Mglob);
-        else if (variant == 2) launch_pipe<64, 128, 3, 32>(ta_, tb_, grid, s, dp_, pp_, (int)P, X0, X1, ldx, Mglob);
-        else if (variant == 3) launch_pipe<64, 128, 3>(ta_, tb_, grid, s, dp_, pp_, (int)P, X0, X1, ldx, Mglob);
+        // (measured equal or slower: 32-deep tiles in 3 stages at 1 CTA/SM, 16-deep in 3 stages,
+        // 64 x 64 tiles in 4 stages for op(B) = B^T)
         else launch_pipe<64>(ta_, tb_, grid, s, dp_, pp_, (int)P, X0, X1, ldx, Mglob);
       }
     }
