@@ -430,3 +430,30 @@ def test_concurrent_trace_jobs_equal_serial_order(tmp_path):
     assert out["10"]["flags"] == [[3, 1, 0], [3, 1, 0]]
     assert out["00"]["flags"] == [[3, 0, 0], [3, 0, 0]]
     assert out["11"]["flags"] == [[3, 1, 1], [3, 0, 0]]
+
+
+@pytest.mark.parametrize("cid,n", [(1, 1024), (2, 2304)])
+def test_cuda_vs_O2_same_algorithm(ctx, cid, n):
+    """The two independent implementations of the same algorithm -- the CUDA path and the serial
+    oracle O2 (oracle/rsf.py, oracle/peel.py, oracle/mle.py) -- on the same inputs and the same
+    Philox probe counters: log|F| and z^T F^-1 z agree to the factorizations'
+    accuracy (both approximate Sigma at eps_fact), the peeled traces to eps_peel scale, g to 1e-3;
+    and both meet the gates against the dense O1."""
+    from threadpoolctl import threadpool_limits
+    from oracle.mle import rsf_mle_eval
+    from workloads import philox_normal
+    c = config(cid)
+    xy = points_for(c, n)
+    ok, rk = _kern(c)
+    z = dense_sample(ok, xy, w_for(c, n))
+    d = dense_eval(ok, xy, z)
+    with threadpool_limits(1):
+        o2 = rsf_mle_eval(ok, xy, z, c.eps_fact, c.eps_peel, c.leaf, c.seed, philox_normal, block=8)
+    r = R.gp_mle_eval(ctx, _d(xy), _d(z), rk, c.eps_fact, c.leaf, R.Opts(eps_peel=c.eps_peel, seed=c.seed))
+    p = len(c.theta)
+    assert abs(r.diag.logdet - o2["logdet"]) <= 10 * c.eps * abs(d["logdet"])
+    assert abs(r.diag.quad - o2["quad"]) <= 10 * c.eps * abs(d["quad"])
+    tr = np.array([r.diag.trace[i] for i in range(p)])
+    np.testing.assert_allclose(tr, o2["trace"], rtol=1e-5)
+    np.testing.assert_allclose(np.array(r.grad), o2["grad"], rtol=1e-3)
+    assert np.all(np.abs(o2["grad"] - d["grad"]) <= 1e-3 * np.abs(d["grad"]))
