@@ -233,7 +233,9 @@ def _config_dict(c, n, args):
             "theta": list(c.theta),
             "parallelism": (f"sharded x{args.gpus}: factor replicated, peeling probe columns split, NCCL "
                             "all-gather per probe block" if args.gpus > 1 else "1 GPU"),
-            "l2": "working set (factor + probe blocks, GBs) >> 126 MB L2; no flush"}
+            "l2": "working set (factor + probe blocks, GBs) >> 126 MB L2; no flush",
+            "peel_storage": ("fp32 (memory-saving mode: peeled bases and cores stored in FP32, FP64 arithmetic; "
+                             "serial trace jobs; DESIGN.md §7g)" if getattr(args, "_peel_f32", 0) else "fp64")}
 
 
 def cpu_baseline_sample(args, c):
@@ -274,6 +276,9 @@ def main():
     ap.add_argument("--ref-n", type=int, default=2304)   # 48 x 48 (config 3's grid needs a square)
     ap.add_argument("--ref-budget", type=float, default=120.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    # memory-saving mode (FP32-stored peeled levels, serial trace jobs): the default
+    # for config 4 (n = 2^20), whose FP64 peeled representation exceeds one B200's 180 GB
+    ap.add_argument("--peel-f32", type=int, default=None)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -303,7 +308,9 @@ def main():
     # probe block) -- strong scaling, the same inputs and seed on every rank
     ctx = R.Context.from_process_group(local) if world > 1 else R.Context(local)
     K = R.Kernel(c.family, c.rho, c.sigma2, c.nugget, c.alpha, c.theta)
-    opts = R.Opts(eps_peel=c.eps_peel, seed=c.seed)
+    peel_f32 = args.peel_f32 if args.peel_f32 is not None else int((args.n or c.n) >= (1 << 20))
+    opts = R.Opts(eps_peel=c.eps_peel, seed=c.seed, peel_f32=peel_f32)
+    args._peel_f32 = peel_f32
     xy = torch.from_numpy(xy_h).to(dev)
     w = torch.from_numpy(w_h).to(dev)
     # z (reading R-V): config 3's frozen bytes (O2 oracle F^{1/2} w, SHA-256 checked); configs

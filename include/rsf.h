@@ -89,6 +89,11 @@ typedef struct {
   int32_t strong;      /* peeling admissibility (next row f4): 0 weak (default);
                           1 strong -- interaction-list blocks, 36 probe classes per level, 9 extraction
                           classes; needs a perfect quadtree (every leaf at depth L), else RSF_EINVAL */
+  int32_t peel_f32;    /* memory-saving mode.  1: store the peeled levels G^(m) (row bases V_i, cores
+                          Brow_i) in FP32 -- every product still runs and accumulates in FP64 -- and run
+                          gp_mle_eval's trace jobs one after the other (halves the
+                          O(n s_1) peeling storage of P:615 so that config 4, n = 2^20, fits one GPU).
+                          default 0 */
 } rsf_opts;            /* pass NULL for all defaults; rsf_opts_default() fills the defaults */
 
 typedef struct rsf_ctx_s* rsf_ctx;     /* device, stream, optional NCCL communicator */

@@ -96,6 +96,7 @@ class Opts:
     r_out: float = 2.45
     seed: int = 1603080570
     strong: int = 0        # 1: strong-admissibility peeling (perfect quadtrees)
+    peel_f32: int = 0      # 1: peeled levels stored in FP32, FP64 arithmetic
 
     def c(self) -> rsf_opts:
         o = rsf_opts()

@@ -25,7 +25,8 @@ class rsf_kernel(C.Structure):
 class rsf_opts(C.Structure):
     _fields_ = [("eps_peel", C.c_double), ("oversample", C.c_int32), ("probe_block", C.c_int32),
                 ("peel_start", C.c_int32), ("max_depth", C.c_int32), ("r_near", C.c_double),
-                ("r_in", C.c_double), ("r_out", C.c_double), ("seed", C.c_uint64), ("strong", C.c_int32)]
+                ("r_in", C.c_double), ("r_out", C.c_double), ("seed", C.c_uint64), ("strong", C.c_int32),
+                ("peel_f32", C.c_int32)]
 
 
 class rsf_fact_diag(C.Structure):

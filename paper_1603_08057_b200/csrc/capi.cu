@@ -62,6 +62,7 @@ rsf::Opts make_opts(const rsf_opts* o) {
   if (o->r_out > 0) r.r_out = o->r_out;
   r.seed = o->seed;
   r.strong = o->strong != 0;
+  r.peel_f32 = o->peel_f32 != 0;
   return r;
 }
 
@@ -187,6 +188,7 @@ void rsf_opts_default(rsf_opts* o) {
   o->r_out = d.r_out;
   o->seed = d.seed;
   o->strong = d.strong;
+  o->peel_f32 = d.peel_f32;
 }
 
 rsf_status rsf_ctx_create(int device, void* cuda_stream, void* nccl_comm, rsf_ctx* out) {

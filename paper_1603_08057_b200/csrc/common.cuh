@@ -46,6 +46,8 @@ extern long long g_n_alloc;
 void* dev_alloc(size_t bytes, cudaStream_t s);
 void dev_free(void* p, size_t bytes, cudaStream_t s);
 void dev_cache_trim(cudaStream_t s);   // release the cached blocks of a stream
+void dev_cache_trim_bins(cudaStream_t s);   // release only the cached small (power-of-two bin) blocks
+double dev_cache_bytes();                    // bytes held in the bin caches of all streams (diagnostics)
 
 // Stream-ordered device buffer (cudaMallocAsync on the context stream; the
 // default memory pool keeps freed blocks cached for the next evaluation).

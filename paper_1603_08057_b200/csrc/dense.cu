@@ -621,6 +621,179 @@ void launch_panel_cl(cudaStream_t s, const PanelDesc* d, int np, int chunk) {
   count_launch();
 }
 
+// Register-resident panel factorization (round 2): every thread of the cluster holds ONE row
+// of the panel (QR_NB doubles in registers), rows distributed over the CL CTAs (<= 512 each).
+// A Householder step needs the column norm below the diagonal and the dot products with the
+// later columns: each thread forms its 32 products, a warp "transpose reduction" (31 shuffles,
+// lane c ends with the warp's sum for column c) and a 16-way sum in shared memory give the
+// CTA's partials, which go to every CTA of the cluster through DSMEM (double-buffered by step
+// parity) -- one cluster barrier and two CTA barriers per column, no serial per-thread loops.
+// Sums over warps and ranks are taken in a fixed order (deterministic).  The WY factor T comes
+// from the Gram matrix of the reflectors, reduced the same way.
+constexpr int PR_NT = 512, PR_NW = PR_NT / 32;
+
+// Warp "transpose reduction" of 32 per-lane values f(c), c = 0..31: on return lane c holds the
+// sum over the warp's lanes of f(c).  31 shuffles; the first stage forms the values on the fly
+// (only 16 live at a time).
+template <class F>
+__device__ __forceinline__ double transpose_reduce32(F f, int lane) {
+  double v[16];
+  {
+    const bool up = (lane & 16) != 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const double lo = f(i), hi = f(i + 16);
+      v[i] = (up ? hi : lo) + __shfl_xor_sync(0xffffffffu, up ? lo : hi, 16);
+    }
+  }
+#pragma unroll
+  for (int h = 8; h >= 1; h >>= 1) {
+    const bool up = (lane & h) != 0;
+#pragma unroll
+    for (int i = 0; i < h; ++i) {
+      const double lo = v[i], hi = v[i + h];
+      v[i] = (up ? hi : lo) + __shfl_xor_sync(0xffffffffu, up ? lo : hi, h);
+    }
+  }
+  return v[0];
+}
+
+template <int CL>
+__global__ void __launch_bounds__(PR_NT, 1) qr_panel_reg_kernel(const PanelDesc* __restrict__ descs) {
+  static_assert(QR_NB == 32, "one warp lane per panel column");
+  __shared__ double red[PR_NW][QR_NB];
+  __shared__ double xch[2][CL][QR_NB];      // per-rank partial sums (slot j: sigma)
+  __shared__ double xrow[2][QR_NB];         // row j of the panel (rank 0)
+  __shared__ double wv[QR_NB], taus[QR_NB], scal[4];
+  __shared__ double G[QR_NB * QR_NB], Ts[QR_NB * QR_NB];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const PanelDesc d = descs[blockIdx.x / CL];
+  const int rows = d.rows, ncol = d.ncol;
+  const int chunk = max((rows + CL - 1) / CL, QR_NB);
+  const int r0 = rank * chunk, nr = max(0, min(rows, r0 + chunk) - r0);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = r0 + tid;                   // this thread's global panel row
+  const bool mine = tid < nr;
+  double a[QR_NB];
+#pragma unroll
+  for (int c = 0; c < QR_NB; ++c) a[c] = (mine && c < ncol) ? d.A[(long long)c * d.lda + g] : 0.0;
+  // (the step index j stays a loop variable -- a fully unrolled loop of 32 steps measured ~25k
+  // instructions of code, thrashing the instruction cache; a[j] is read with a 32-way select)
+  auto pick = [&](int j) {
+    double v = 0.0;
+#pragma unroll
+    for (int c = 0; c < QR_NB; ++c) v = (c == j) ? a[c] : v;
+    return v;
+  };
+  // One transpose reduction per step gives, for the rows below the diagonal, x . a_c for EVERY
+  // column c: c > j the dot products of the update, c == j the norm sigma, and c < j (a_c already
+  // holds the reflector v_c) the Gram entries v_c . v_j of the WY factor T once scaled -- no
+  // separate Gram pass after the panel.
+#pragma unroll 1
+  for (int j = 0; j < ncol; ++j) {
+    const int buf = j & 1;
+    const double aj = pick(j);
+    const double x = (mine && g > j) ? aj : 0.0;
+    const double ps = transpose_reduce32([&](int c) { return x * a[c]; }, lane);
+    red[warp][lane] = ps;
+    if (rank == 0 && tid == j) {
+#pragma unroll
+      for (int c = 0; c < QR_NB; ++c) xrow[buf][c] = a[c];
+    }
+    __syncthreads();
+    if (tid < QR_NB) {
+      double sacc = 0.0;
+      for (int w = 0; w < PR_NW; ++w) sacc += red[w][tid];
+      const double rv = xrow[buf][tid];
+#pragma unroll 1
+      for (int q = 0; q < CL; ++q) {
+        cluster.map_shared_rank(&xch[0][0][0], q)[(buf * CL + rank) * QR_NB + tid] = sacc;
+        if (rank == 0 && q > 0) cluster.map_shared_rank(&xrow[0][0], q)[buf * QR_NB + tid] = rv;
+      }
+    }
+    cluster.sync();
+    if (tid < QR_NB) {
+      double sigma = 0.0, dot = 0.0;
+      for (int r = 0; r < CL; ++r) { sigma += xch[buf][r][j]; dot += xch[buf][r][tid]; }
+      const double alpha = xrow[buf][j];
+      double tau = 0.0, beta = alpha, scale = 0.0;
+      if (sigma != 0.0) {
+        const double mu = sqrt(alpha * alpha + sigma);
+        beta = (alpha >= 0.0) ? -mu : mu;
+        tau = (beta - alpha) / beta;
+        scale = 1.0 / (alpha - beta);
+      }
+      wv[tid] = (tid > j) ? tau * (xrow[buf][tid] + scale * dot) : 0.0;
+      if (tid < j) G[tid * QR_NB + j] = xrow[buf][tid] + scale * dot;   // v_tid(j) + v_tid . v_j below row j
+      if (tid == 0) { scal[0] = tau; scal[1] = beta; scal[2] = scale; taus[j] = tau; }
+    }
+    __syncthreads();
+    if (mine && g > j) {
+      const double v = aj * scal[2];
+#pragma unroll
+      for (int c = 0; c < QR_NB; ++c) a[c] = (c == j) ? v : fma(-wv[c], v, a[c]);   // wv = 0 for c <= j
+    } else if (mine && g == j) {
+      const double beta = scal[1];
+#pragma unroll
+      for (int c = 0; c < QR_NB; ++c) a[c] = (c == j) ? beta : a[c] - wv[c];
+    }
+  }
+  // write back R (rows < ncol of rank 0) and the reflectors; explicit unit-lower V
+  if (mine) {
+#pragma unroll
+    for (int c = 0; c < QR_NB; ++c) {
+      if (c >= ncol) break;
+      d.A[(long long)c * d.lda + g] = a[c];
+      d.V[(long long)c * rows + g] = (g < c) ? 0.0 : (g == c ? 1.0 : a[c]);
+    }
+  }
+  if (rank != 0) return;
+  __syncthreads();
+  if (warp == 0) {
+    for (int i = 0; i < ncol; ++i) {
+      double v = 0.0;
+      if (lane < i)
+        for (int l2 = lane; l2 < i; ++l2) v += Ts[lane + l2 * QR_NB] * G[l2 * QR_NB + i];
+      __syncwarp();
+      if (lane < i) Ts[lane + i * QR_NB] = -taus[i] * v;
+      for (int r = i + 1 + lane; r < QR_NB; r += 32) Ts[r + i * QR_NB] = 0.0;
+      if (lane == 0) Ts[i + i * QR_NB] = taus[i];
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < QR_NB * QR_NB; e += PR_NT) {
+    const int r = e % QR_NB, c = e / QR_NB;
+    d.T[e] = (r < ncol && c < ncol) ? Ts[e] : 0.0;
+  }
+  if (d.tau)
+    for (int e = tid; e < ncol; e += PR_NT) d.tau[e] = taus[e];
+}
+
+template <int CL>
+void launch_panel_reg(cudaStream_t s, const PanelDesc* d, int np) {
+  static std::once_flag attr_once;
+  const size_t smem = 0;
+  std::call_once(attr_once, [&] {
+    if (CL > 8) RSF_CUDA(cudaFuncSetAttribute(qr_panel_reg_kernel<CL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  });
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(np * CL));
+  cfg.blockDim = dim3(PR_NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  RSF_CUDA(cudaLaunchKernelEx(&cfg, qr_panel_reg_kernel<CL>, d));
+  count_launch();
+}
+
 // panels in global memory (too tall for shared memory) are latency bound: give them
 // 1024 threads (one warp per remaining panel column, 4x the loads in flight)
 void launch_panels(cudaStream_t s, const std::vector<PanelDesc>& pd, const PanelDesc* d, size_t smem_need) {
@@ -632,6 +805,20 @@ void launch_panels(cudaStream_t s, const std::vector<PanelDesc>& pd, const Panel
   bool tall = false;
   int maxrows = 0;
   for (auto& p : pd) { tall |= (p.smem == 0); maxrows = std::max(maxrows, p.rows); }
+  static const bool reg_on = !(getenv("RSF_PANEL_REG") && getenv("RSF_PANEL_REG")[0] == '0');
+  if (reg_on && maxrows <= 16 * PR_NT && pd.size() <= 65535) {
+    int CL = 1;
+    while ((maxrows + CL - 1) / CL > PR_NT) CL *= 2;
+    switch (CL) {
+      case 1: launch_panel_reg<1>(s, d, (int)pd.size()); break;
+      case 2: launch_panel_reg<2>(s, d, (int)pd.size()); break;
+      case 4: launch_panel_reg<4>(s, d, (int)pd.size()); break;
+      case 8: launch_panel_reg<8>(s, d, (int)pd.size()); break;
+      default: launch_panel_reg<16>(s, d, (int)pd.size()); break;
+    }
+    RSF_LAUNCH_CHECK();
+    return;
+  }
   static const bool cl_on = !(getenv("RSF_PANEL_CLUSTER") && getenv("RSF_PANEL_CLUSTER")[0] == '0');
   if (tall && cl_on && maxrows <= 16 * PC_MAXROWS && pd.size() <= 65535) {
     int CL = 2;

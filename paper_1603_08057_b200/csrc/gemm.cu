@@ -139,6 +139,17 @@ void dev_cache_trim(cudaStream_t s) {
     else ++i;
   }
 }
+double dev_cache_bytes() {
+  std::lock_guard<std::mutex> lk(cache_mu());
+  double b = 0;
+  for (auto& f : cache()) b += (double)f.blocks.size() * (double)(size_t(1) << f.bin);
+  return b;
+}
+void dev_cache_trim_bins(cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(cache_mu());
+  for (auto& f : cache())
+    if (f.s == s) { for (void* p : f.blocks) cudaFreeAsync(p, s); f.blocks.clear(); }
+}
 void dev_free(void* p, size_t bytes, cudaStream_t s) {
   if (!p) return;
   if (bytes > CACHE_MAX) {
@@ -454,6 +465,18 @@ void gdrain() {
     if (i == a.size()) a.emplace_back(key, GAgg{});
     GAgg& g = a[i].second;
     g.sec += ms * 1e-3; g.flops += r.flops; g.cnt += 1;
+    {   // histogram over (waves of 296 resident CTAs, K) buckets: where the efficiency is lost
+      auto bucket = [](double v, const double* edges, int ne) { int b = 0; while (b < ne && v > edges[b]) ++b; return b; };
+      static const double we[] = {0.5, 1, 2, 4, 8, 16, 32}, ke[] = {32, 64, 128, 256, 512, 1024, 2048};
+      const std::string hk = "H|w" + std::to_string(bucket(r.ctas / 296.0, we, 7)) + "|k" + std::to_string(bucket(r.maxK, ke, 7));
+      size_t j = 0;
+      for (; j < a.size(); ++j) if (a[j].first == hk) break;
+      if (j == a.size()) a.emplace_back(hk, GAgg{});
+      GAgg& h = a[j].second;
+      h.sec += ms * 1e-3; h.flops += r.flops; h.cnt += 1;
+      h.ctas_min = std::min(h.ctas_min, r.ctas); h.ctas_max = std::max(h.ctas_max, r.ctas);
+      h.kmin = std::min(h.kmin, r.maxK); h.kmax = std::max(h.kmax, r.maxK);
+    }
     g.ctas_min = std::min(g.ctas_min, r.ctas); g.ctas_max = std::max(g.ctas_max, r.ctas);
     g.kmin = std::min(g.kmin, r.maxK); g.kmax = std::max(g.kmax, r.maxK);
     if (ms * 1e-3 > g.tmax) { g.tmax = ms * 1e-3; g.ord_max = r.ord; }
@@ -526,6 +549,7 @@ __global__ void __launch_bounds__(NT) gemm_vb_kernel(const GemmDesc* __restrict_
   // per-call operands: offsets count columns of X0/X1 (ld = ldx)
   const double* A = dd.selA == 0 ? dd.A + dd.offA : (dd.selA == 1 ? X0 : X1) + dd.offA * (long long)ldx;
   const double* B = dd.selB == 0 ? dd.B + dd.offB : (dd.selB == 1 ? X0 : X1) + dd.offB * (long long)ldx;
+  const float* Bf = reinterpret_cast<const float*>(dd.B) + dd.offB;   // BF: absolute FP32 operand
   double* C = dd.selC == 0 ? dd.C + dd.offC : (dd.selC == 1 ? X0 : X1) + dd.offC * (long long)ldx;
   const long long lda = dd.selA ? ldx : dd.lda;
   const long long ldb = dd.selB ? ldx : dd.ldb;
@@ -693,6 +717,7 @@ __global__ void __launch_bounds__(128) gemm_dmma_kernel(const GemmDesc* __restri
   if (dd.lower && n0 >= m0 + BM) return;
   const double* A = dd.selA == 0 ? dd.A + dd.offA : (dd.selA == 1 ? X0 : X1) + dd.offA * (long long)ldx;
   const double* B = dd.selB == 0 ? dd.B + dd.offB : (dd.selB == 1 ? X0 : X1) + dd.offB * (long long)ldx;
+  const float* Bf = reinterpret_cast<const float*>(dd.B) + dd.offB;   // BF: absolute FP32 operand
   double* C = dd.selC == 0 ? dd.C + dd.offC : (dd.selC == 1 ? X0 : X1) + dd.offC * (long long)ldx;
   const long long lda = dd.selA ? ldx : dd.lda;
   const long long ldb = dd.selB ? ldx : dd.ldb;
@@ -816,6 +841,12 @@ __device__ __forceinline__ void cp_async16(double* smem, const double* gmem, int
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(bytes));
 }
+// 4-byte variant (an FP32-stored operand element; converted to FP64 at the fragment load)
+__device__ __forceinline__ void cp_async4(float* smem, const float* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = valid ? 4 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
@@ -830,7 +861,10 @@ constexpr size_t p_smem() { return (size_t)ST * BK * (BM + 4 + p_ldb<BN>()) * si
 // BN = 64, 4 warps as 2 x 2, 3 stages, 4 CTAs per SM -- for short K, where the prologue and the
 // epilogue of a CTA dominate and more resident CTAs overlap them), warp tile 32 x BN/2
 // (4 x BN/16 DMMA.8x8x4 tiles).
-template <bool TA, bool TB, int BN, int BM, int ST, int BK = P_BK>
+// BF: op(B) is stored in FP32 (GemmDesc::bf32; the peeled bases of an FP32-stored peeling level,
+// DESIGN.md §7g) -- staged as floats with 4-byte copies and widened to FP64 at the fragment
+// load; the products and accumulators stay FP64.
+template <bool TA, bool TB, int BN, int BM, int ST, int BK = P_BK, bool BF = false>
 __global__ void __launch_bounds__(2 * BM, (BN >= 128 ? 1 : (BM == 64 ? 4 : 2))) gemm_pipe_kernel(const GemmDesc* __restrict__ descs,
                                                             const int* __restrict__ prefix, int nprob,
                                                             double* X0, double* X1, int ldx, int Mglob,
@@ -855,6 +889,7 @@ __global__ void __launch_bounds__(2 * BM, (BN >= 128 ? 1 : (BM == 64 ? 4 : 2))) 
   if (dd.lower && n0 >= m0 + P_BM) return;
   const double* A = dd.selA == 0 ? dd.A + dd.offA : (dd.selA == 1 ? X0 : X1) + dd.offA * (long long)ldx;
   const double* B = dd.selB == 0 ? dd.B + dd.offB : (dd.selB == 1 ? X0 : X1) + dd.offB * (long long)ldx;
+  const float* Bf = reinterpret_cast<const float*>(dd.B) + dd.offB;   // BF: absolute FP32 operand
   double* C = dd.selC == 0 ? dd.C + dd.offC : (dd.selC == 1 ? X0 : X1) + dd.offC * (long long)ldx;
   const long long lda = dd.selA ? ldx : dd.lda;
   const long long ldb = dd.selB ? ldx : dd.ldb;
@@ -870,7 +905,7 @@ __global__ void __launch_bounds__(2 * BM, (BN >= 128 ? 1 : (BM == 64 ? 4 : 2))) 
   // 16-byte copies where the contiguous dimension of global and shared memory agree
   // (A not transposed, B transposed) and the operand is 16-byte aligned with an even ld
   const bool vecA = !TA && ((reinterpret_cast<unsigned long long>(A) & 15ull) == 0) && ((lda & 1) == 0);
-  const bool vecB = TB && ((reinterpret_cast<unsigned long long>(B) & 15ull) == 0) && ((ldb & 1) == 0);
+  const bool vecB = !BF && TB && ((reinterpret_cast<unsigned long long>(B) & 15ull) == 0) && ((ldb & 1) == 0);
 
   // K range of the nonzero rows of op(B) for this N tile (triangular B: TRMM-style skipping)
   int kbeg = dd.btri == 1 ? min(n0, K) : 0;
@@ -933,6 +968,24 @@ __global__ void __launch_bounds__(2 * BM, (BN >= 128 ? 1 : (BM == 64 ? 4 : 2))) 
       }
       return;
     }
+    if (BF) {
+      float* bsf = reinterpret_cast<float*>(bs);
+#pragma unroll
+      for (int r = 0; r < (P_BK * BN) / P_NT; ++r) {
+        const int e = tid + r * P_NT;
+        int l, j;
+        if (!TB) { l = e % P_BK; j = e / P_BK; } else { j = e % BN; l = e / BN; }
+        const int gj = n0 + j, c = kB[st][l];
+        const bool v = c >= 0 && gj < N;
+        const float* src = Bf;
+        if (v) {
+          if (!TB) { const long long cj = mapB ? __ldg(mapB + gj) : gj; src = Bf + cj * ldb + c; }
+          else src = Bf + (long long)c * ldb + gj;
+        }
+        cp_async4(bsf + l * LDB + j, src, v);
+      }
+      return;
+    }
 #pragma unroll
     for (int r = 0; r < (P_BK * BN) / P_NT; ++r) {
       const int e = tid + r * P_NT;
@@ -986,7 +1039,9 @@ __global__ void __launch_bounds__(2 * BM, (BN >= 128 ? 1 : (BM == 64 ? 4 : 2))) 
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi) af[mi] = as[(kk + tq) * P_LDA + wm * 32 + mi * 8 + g];
 #pragma unroll
-      for (int ni = 0; ni < NI; ++ni) bf[ni] = bs[(kk + tq) * LDB + wn * WN + ni * 8 + g];
+      for (int ni = 0; ni < NI; ++ni)
+        bf[ni] = BF ? (double)reinterpret_cast<const float*>(bs)[(kk + tq) * LDB + wn * WN + ni * 8 + g]
+                    : bs[(kk + tq) * LDB + wn * WN + ni * 8 + g];
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
@@ -1080,27 +1135,37 @@ __global__ void __launch_bounds__(2 * BM, (BN >= 128 ? 1 : (BM == 64 ? 4 : 2))) 
   }
 }
 
-template <int BN, int BM = P_BM, int ST = P_ST, int BK = P_BK>
-void launch_pipe(bool ta, bool tb, dim3 grid, cudaStream_t s, const GemmDesc* d, const int* pre, int np,
-                 double* X0, double* X1, int ldx, int Mg, double* ws = nullptr, const long long* mnpre = nullptr,
-                 int kchunk = 0) {
+template <int BN, int BM, int ST, int BK, bool BF>
+void launch_pipe_t(bool ta, bool tb, dim3 grid, cudaStream_t s, const GemmDesc* d, const int* pre, int np,
+                   double* X0, double* X1, int ldx, int Mg, double* ws, const long long* mnpre, int kchunk) {
   static std::once_flag attr_once;
   constexpr size_t SM = p_smem<BN, BM, ST, BK>();
   std::call_once(attr_once, [&] {
-    cudaFuncSetAttribute(gemm_pipe_kernel<false, false, BN, BM, ST, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
-    cudaFuncSetAttribute(gemm_pipe_kernel<true, false, BN, BM, ST, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
-    cudaFuncSetAttribute(gemm_pipe_kernel<false, true, BN, BM, ST, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
-    cudaFuncSetAttribute(gemm_pipe_kernel<true, true, BN, BM, ST, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
+    cudaFuncSetAttribute(gemm_pipe_kernel<false, false, BN, BM, ST, BK, BF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
+    cudaFuncSetAttribute(gemm_pipe_kernel<true, false, BN, BM, ST, BK, BF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
+    cudaFuncSetAttribute(gemm_pipe_kernel<false, true, BN, BM, ST, BK, BF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
+    cudaFuncSetAttribute(gemm_pipe_kernel<true, true, BN, BM, ST, BK, BF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
   });
   ++g_pipe_launches;
   static const int epi = getenv("RSF_GEMM_EPI") ? atoi(getenv("RSF_GEMM_EPI")) : 1;
   const int mt = (int)grid.y;
   const dim3 g1((unsigned)((long long)grid.x * grid.y), 1, grid.z);   // 1-D over (N-tile, M-tile)
   constexpr int NTH = 2 * BM;
-  if (!ta && !tb) gemm_pipe_kernel<false, false, BN, BM, ST, BK><<<g1, NTH, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk, mt, epi);
-  else if (ta && !tb) gemm_pipe_kernel<true, false, BN, BM, ST, BK><<<g1, NTH, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk, mt, epi);
-  else if (!ta && tb) gemm_pipe_kernel<false, true, BN, BM, ST, BK><<<g1, NTH, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk, mt, epi);
-  else gemm_pipe_kernel<true, true, BN, BM, ST, BK><<<g1, NTH, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk, mt, epi);
+  if (!ta && !tb) gemm_pipe_kernel<false, false, BN, BM, ST, BK, BF><<<g1, NTH, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk, mt, epi);
+  else if (ta && !tb) gemm_pipe_kernel<true, false, BN, BM, ST, BK, BF><<<g1, NTH, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk, mt, epi);
+  else if (!ta && tb) gemm_pipe_kernel<false, true, BN, BM, ST, BK, BF><<<g1, NTH, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk, mt, epi);
+  else gemm_pipe_kernel<true, true, BN, BM, ST, BK, BF><<<g1, NTH, SM, s>>>(d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk, mt, epi);
+}
+
+// the batch being launched stores op(B) in FP32 (set by GemmBatch::run around its launches)
+thread_local bool g_launch_bf = false;
+
+template <int BN, int BM = P_BM, int ST = P_ST, int BK = P_BK>
+void launch_pipe(bool ta, bool tb, dim3 grid, cudaStream_t s, const GemmDesc* d, const int* pre, int np,
+                 double* X0, double* X1, int ldx, int Mg, double* ws = nullptr, const long long* mnpre = nullptr,
+                 int kchunk = 0) {
+  if (g_launch_bf) launch_pipe_t<BN, BM, ST, BK, true>(ta, tb, grid, s, d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk);
+  else launch_pipe_t<BN, BM, ST, BK, false>(ta, tb, grid, s, d, pre, np, X0, X1, ldx, Mg, ws, mnpre, kchunk);
 }
 
 // split-K reduction: C = alpha * sum_z W_z + beta * C (fixed summation order: deterministic)
@@ -1151,6 +1216,7 @@ __global__ void __launch_bounds__(GV_NT) gemv1_kernel(const GemmDesc* __restrict
   const int n0 = (blockIdx.x - __ldg(prefix + p)) * TJ;
   const double* A = dd.selA == 0 ? dd.A + dd.offA : (dd.selA == 1 ? X0 : X1) + dd.offA * (long long)ldx;
   const double* B = dd.selB == 0 ? dd.B + dd.offB : (dd.selB == 1 ? X0 : X1) + dd.offB * (long long)ldx;
+  const float* Bf = reinterpret_cast<const float*>(dd.B) + dd.offB;   // BF: absolute FP32 operand
   double* C = dd.selC == 0 ? dd.C + dd.offC : (dd.selC == 1 ? X0 : X1) + dd.offC * (long long)ldx;
   const long long lda = dd.selA ? ldx : dd.lda;
   const long long ldb = dd.selB ? ldx : dd.ldb;
@@ -1319,6 +1385,7 @@ void GemmBatch::finalize_meta() const {
   maxK_ = 0;
   has_lower_ = false;
   has_mapk_ = false;
+  has_bf_ = false;
   glob_ = false;
   const int bns[3] = {64, 32, 128};
   for (size_t i = 0; i < P; ++i) {
@@ -1332,6 +1399,7 @@ void GemmBatch::finalize_meta() const {
     maxK_ = std::max(maxK_, d.K);
     has_lower_ = has_lower_ || d.lower;
     has_mapk_ = has_mapk_ || d.mapK;
+    has_bf_ = has_bf_ || d.bf32;
   }
   totalN_ = pre[P];
   totalN32_ = pre[(P + 1) + P];
@@ -1353,7 +1421,8 @@ void GemmBatch::run(cudaStream_t s, double* X0, double* X1, int ldx, int Mglob, 
   const bool glog = GemmLog::on();
   if (glog) KStats::record(s, &g0, nullptr);
   static const bool gemv_on = !(getenv("RSF_GEMV") && getenv("RSF_GEMV")[0] == '0');
-  if (M == 1 && gemv_on && !has_mapk_ && !has_lower_) {
+  g_launch_bf = has_bf_;   // FP32-stored op(B): only the pipelined kernel reads it
+  if (M == 1 && gemv_on && !has_mapk_ && !has_lower_ && !has_bf_) {
     // one right-hand side: gather-GEMV (HBM stream of op(B)).  Column tiles are 64 wide (128-wide
     // tiles for op(B) = B^T measured slower); K is split (workspace +
     // deterministic reduction) until the launch holds ~8 CTAs per SM (2 waves of the 4 resident
@@ -1407,10 +1476,10 @@ void GemmBatch::run(cudaStream_t s, double* X0, double* X1, int ldx, int Mglob, 
         splitk_reduce_kernel<<<dim3(gx, ny), P_NT, 0, s>>>(dp_, ws.p, dmn, S, (int)o, X0, X1, ldx, 1);
       }
     }
-  } else if (M <= 16 && !has_mapk_) {   // (only the pipelined kernel implements mapK)
+  } else if (M <= 16 && !has_mapk_ && !has_bf_) {   // (only the pipelined kernel implements mapK)
     dim3 grid(totalN_, ceil_div(M, 16));
     launch_variant<16, 1>(ta_, tb_, grid, s, dp_, pp_, (int)h_.size(), X0, X1, ldx, Mglob);
-  } else if (gemm_mode() == 2 || has_mapk_) {
+  } else if (gemm_mode() == 2 || has_mapk_ || has_bf_) {
     // N-tile width by the widest problem of the batch (prefix sums for each width)
     const size_t P = h_.size();
     static const int wide = getenv("RSF_GEMM_BN128") ? atoi(getenv("RSF_GEMM_BN128")) : 0;
@@ -1502,6 +1571,7 @@ void GemmBatch::run(cudaStream_t s, double* X0, double* X1, int ldx, int Mglob, 
     dim3 grid(totalN_, ceil_div(M, 64));
     launch_variant<64, 4>(ta_, tb_, grid, s, dp_, pp_, (int)h_.size(), X0, X1, ldx, Mglob);
   }
+  g_launch_bf = false;
   if (glog) {
     KStats::record(s, nullptr, &g1);
     long long ctas = 0;

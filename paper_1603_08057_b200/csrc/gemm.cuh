@@ -25,6 +25,7 @@ struct GemmDesc {
   const int* mapK;             // optional K-index gather applied to both operands (sparse right-hand sides)
   int btri;                    // op(B) triangular (TRMM-style K range): 1 lower (op(B)(l,j) = 0 for l < j),
                                // 2 upper (op(B)(l,j) = 0 for l > j); 0 general
+  int bf32;                    // B (absolute pointer, selB = 0) holds FP32 values: (const float*)B, ldb in floats
 };
 
 inline GemmDesc gdesc(int M, int N, int K) {
@@ -78,7 +79,7 @@ class GemmBatch {
   mutable const int* pp_ = nullptr;
   void finalize_meta() const;
   mutable int totalN_ = 0, totalN32_ = 0, totalN128_ = 0, maxM_ = 0, maxN_ = 0, maxK_ = 0;
-  mutable bool has_lower_ = false, has_mapk_ = false;
+  mutable bool has_lower_ = false, has_mapk_ = false, has_bf_ = false;
   mutable bool glob_ = false;
 };
 

@@ -288,6 +288,10 @@ struct GOp {
   }
 };
 
+__global__ void d2f_kernel(const double* __restrict__ a, float* __restrict__ b, long long n) {
+  for (long long e = blockIdx.x * (long long)NT + threadIdx.x; e < n; e += (long long)gridDim.x * NT) b[e] = (float)a[e];
+}
+
 // ----------------------------------------------------------------- G^(m): shared row bases
 // The peeled level-m operator G^(m) is stored with one
 // orthonormal row basis per box:  G^(m)_ij ~= V_i B_ij V_j^T for every ordered
@@ -299,6 +303,12 @@ struct GOp {
 struct PeelLevel {
   std::vector<DBuf<double>> V;   // per box: V_i (n_i x r_i, ld n_i)
   DBuf<double> Brow;
+  // FP32 storage of the same (opts.peel_f32): the subtraction GEMMs read them as an
+  // FP32 op(B) and compute in FP64
+  bool f32 = false;
+  std::vector<DBuf<float>> Vf;
+  DBuf<float> Browf;
+  const void* vptr(int b) const { return f32 ? (const void*)Vf[b].p : (const void*)V[b].p; }
   long long tcols = 0;   // tmp columns per probe column: sum r (T') + sum r (S')
   GemmBatch g1, g2, g3;
   std::vector<int> ib, ni, r, bidx;      // boxes with r > 0: range, basis size, level box index
@@ -524,8 +534,9 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
     const char* v = getenv(k);
     return (v && atof(v) >= 0) ? atof(v) * (1 << 20) : d;
   };
-  const double budget = env_mb("RSF_PEEL_BUDGET_MB", 16.0 * (1ull << 30));
-  const double wcache_budget = env_mb("RSF_PEEL_WCACHE_MB", 8.0 * (1ull << 30));
+  // (memory-saving mode, opts.peel_f32: 4 GB / 2 GB -- DESIGN.md §7g)
+  const double budget = env_mb("RSF_PEEL_BUDGET_MB", (o.peel_f32 ? 4.0 : 16.0) * (1ull << 30));
+  const double wcache_budget = env_mb("RSF_PEEL_WCACHE_MB", (o.peel_f32 ? 2.0 : 8.0) * (1ull << 30));
 
   struct SparseSub { std::vector<GemmBatch> g1, g3; std::vector<char> has1, has3; };
   auto residual = [&](const double* W, double* Y, int k, int upto, const SparseSub* sp) {
@@ -561,7 +572,8 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
       out[m].reset(false, false);
       for (size_t b = 0; b < P.ib.size(); ++b) {
         GemmDesc a = gdesc(-1, P.r[b], (int)(off[b + 1] - off[b]));
-        a.selA = 1; a.offA = P.ib[b]; a.B = P.V[P.bidx[b]].p; a.ldb = P.ni[b]; a.selC = 2; a.offC = P.toff[b];
+        a.selA = 1; a.offA = P.ib[b]; a.B = (const double*)P.vptr(P.bidx[b]); a.bf32 = P.f32; a.ldb = P.ni[b];
+        a.selC = 2; a.offC = P.toff[b];
         a.mapK = dk + off[b];
         out[m].add(a);
       }
@@ -576,7 +588,8 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
           int e = t + 1;
           while (e < P.ni[b] && hq[P.ib[b] + e] >= 0 && hq[P.ib[b] + e] != g) ++e;
           GemmDesc d = gdesc(-1, e - t, P.r[b]);
-          d.selA = 2; d.offA = P.soff[b]; d.B = P.V[P.bidx[b]].p + t; d.ldb = P.ni[b];
+          d.selA = 2; d.offA = P.soff[b]; d.B = (const double*)P.vptr(P.bidx[b]); d.offB = t; d.bf32 = P.f32;
+          d.ldb = P.ni[b];
           d.selC = 1; d.offC = P.ib[b] + t; d.alpha = -1.0; d.beta = 1.0;
           sp.g3[m].add(d);
           t = e;
@@ -692,6 +705,7 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
     struct PairData { int k = 0, rz = 0; double *Z = nullptr, *X = nullptr, *Lm = nullptr, *Gi = nullptr; };
     std::vector<PairData> pdat((size_t)std::max<long long>(pslot0[nb], 1));
     std::vector<DBuf<double>> arenas;
+    double pair_bytes = 0;   // per-pair data of the level (diagnostics)
     int mr = 0;
     while (true) {
       std::fill(rb.begin(), rb.end(), 0);
@@ -720,6 +734,7 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
           Ab[b].alloc((size_t)c * vcap[b], s);
         }
       arenas.clear();
+      pair_bytes = 0;
       for (auto& q : pdat) q = PairData{};
       bool fail = false;
       mr = 0;
@@ -1100,6 +1115,7 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
             q.k = kk[xa]; q.rz = rb[i];
             q.Z = arena.p + zo[x]; q.X = arena.p + xo[x]; q.Lm = arena.p + lo[x]; q.Gi = arena.p + go[x];
           }
+          pair_bytes += 8.0 * arena.n;
           arenas.push_back(std::move(arena));
           x0 = x1;
         }
@@ -1217,7 +1233,27 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
     }
     double vbytes = 0;
     for (auto& v : PL.V) vbytes += 8.0 * v.n;
-    pd.stored_bytes += vbytes + 8.0 * PL.Brow.n;
+    double browbytes = 8.0 * PL.Brow.n;
+    if (o.peel_f32) {   // FP32 storage of G^(lev), box by box
+      PL.f32 = true;
+      PL.Vf.clear();
+      PL.Vf.resize(nb);
+      for (int b = 0; b < nb; ++b) {
+        if (!PL.V[b].p) continue;
+        PL.Vf[b].alloc(PL.V[b].n, s);
+        d2f_kernel<<<gxx((long long)PL.V[b].n), NT, 0, s>>>(PL.V[b].p, PL.Vf[b].p, (long long)PL.V[b].n);
+        count_launch();
+        PL.V[b].release();
+      }
+      PL.Browf.alloc(std::max<size_t>(PL.Brow.n, 1), s);
+      d2f_kernel<<<gxx((long long)PL.Brow.n), NT, 0, s>>>(PL.Brow.p, PL.Browf.p, (long long)PL.Brow.n);
+      count_launch();
+      RSF_LAUNCH_CHECK();
+      PL.Brow.release();
+      vbytes *= 0.5;
+      browbytes *= 0.5;
+    }
+    pd.stored_bytes += vbytes + browbytes;
     PL.g1.reset(false, false);
     PL.g2.reset(false, true);
     PL.g3.reset(false, true);
@@ -1241,18 +1277,21 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
       long long tot = 0;
       for (int x : rowset[b]) tot += rb[x];
       GemmDesc a = gdesc(-1, rb[b], bx[b].ni);            // T'_b = X'(:, I_b) V_b
-      a.selA = 1; a.offA = bx[b].ib; a.B = PL.V[b].p; a.ldb = bx[b].ni; a.selC = 2; a.offC = toff[b];
+      a.selA = 1; a.offA = bx[b].ib; a.B = (const double*)PL.vptr(b); a.bf32 = PL.f32; a.ldb = bx[b].ni;
+      a.selC = 2; a.offC = toff[b];
       PL.g1.add(a);
       PL.ib.push_back(bx[b].ib); PL.ni.push_back(bx[b].ni); PL.r.push_back(rb[b]); PL.bidx.push_back(b);
       PL.toff.push_back(toff[b]); PL.soff.push_back(soff[b]);
       GemmDesc d = gdesc(-1, rb[b], (int)tot);            // S'_b = T'_row Brow_b^T
-      d.selA = 2; d.offA = strong ? 0 : toff[bx[b].fam0]; d.B = PL.Brow.p + bo[b]; d.ldb = rb[b];
+      d.selA = 2; d.offA = strong ? 0 : toff[bx[b].fam0]; d.ldb = rb[b];
+      if (PL.f32) { d.B = (const double*)PL.Browf.p; d.offB = bo[b]; d.bf32 = 1; } else d.B = PL.Brow.p + bo[b];
       d.selC = 2; d.offC = soff[b];
       if (strong) d.mapA = PL.mapk.p + moff[b];
       if (tot == 0) continue;                              // (strong: no partner has a basis)
       PL.g2.add(d);
       GemmDesc e = gdesc(-1, bx[b].ni, rb[b]);            // Y'(:, I_b) -= S'_b V_b^T
-      e.selA = 2; e.offA = soff[b]; e.B = PL.V[b].p; e.ldb = bx[b].ni; e.selC = 1; e.offC = bx[b].ib;
+      e.selA = 2; e.offA = soff[b]; e.B = (const double*)PL.vptr(b); e.bf32 = PL.f32; e.ldb = bx[b].ni;
+      e.selC = 1; e.offC = bx[b].ib;
       e.alpha = -1.0; e.beta = 1.0;
       PL.g3.add(e);
     }
@@ -1260,6 +1299,9 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
     max_tcols = std::max(max_tcols, tc);
     for (GemmBatch* g : {&PL.g1, &PL.g2, &PL.g3})
       if (!g->empty()) g->finalize(s);
+    // memory-saving mode: the per-box blocks of this level (<= 64 MB, power-of-two bins) go back to
+    // the stream-ordered pool instead of waiting in the bin cache for sizes the next level never asks
+    if (o.peel_f32) dev_cache_trim_bins(s);
     if (verbose) {
       RSF_CUDA(cudaStreamSynchronize(s));
       size_t fr = 0, tot = 0;
@@ -1269,9 +1311,21 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
       for (int b = 0; b < nb; ++b) { rsum += rb[b]; rmax = std::max(rmax, rb[b]); }
       fprintf(stderr, "[peel tr%d] level %d boxes %d pairs %d cols %d rank_max %d restarts %d basis sum %lld max %d "
                       "V %.2f GB Brow %.2f GB dev_used %.2f GB t %.2f s\n",
-              trace_id, lev, nb, npairs, c, mr, restarts, rsum, rmax, 1e-9 * vbytes, 8e-9 * PL.Brow.n,
+              trace_id, lev, nb, npairs, c, mr, restarts, rsum, rmax, 1e-9 * vbytes, 1e-9 * browbytes,
               1e-9 * (tot - fr), now_s() - t0);
-      if (verbose > 1) {
+      {
+        cudaMemPool_t pool;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        unsigned long long res = 0, used = 0;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+          cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res);
+          cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+        }
+        fprintf(stderr, "    memory: pool reserved %.2f GB used %.2f GB, bin caches %.2f GB, pair data of the level %.2f GB\n",
+                1e-9 * res, 1e-9 * used, 1e-9 * dev_cache_bytes(), 1e-9 * pair_bytes);
+      }
+      if (verbose > 1 && !PL.f32) {
         DBuf<unsigned long long> cnt(4, s);
         RSF_CUDA(cudaMemsetAsync(cnt.p, 0, 4 * sizeof(unsigned long long), s));
         long long rows = 0;
@@ -1580,7 +1634,9 @@ EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KP
   bool planned_serial = false;
   for (auto& sh : ctx.serial_shapes) planned_serial = planned_serial || (sh.first == n && sh.second == njobs);
   // (the profiler and the launch trace synchronise one stream at a time: serial then)
-  if (!par_on || jobs.size() < 2 || Prof::enabled() || KTrace::on() || planned_serial) {
+  // (opts.peel_f32 is the memory-saving mode: the trace jobs also run one after the other, so one
+  // peeled representation is resident at a time -- DESIGN.md §7g)
+  if (!par_on || jobs.size() < 2 || Prof::enabled() || KTrace::on() || planned_serial || o.peel_f32) {
     main_part();
     f_promise.set_value();
     tj0 = now_s();

@@ -342,6 +342,207 @@ __global__ void __launch_bounds__(SK_NT) sketch_cpqr_cl_kernel(const RDesc* __re
   }
 }
 
+// Swap list of a block from the chosen original columns (positions relative to J), composed by
+// one warp: a table of the (<= 2 QR_NB) positions the swaps touched, searched with a ballot per
+// step, instead of one thread's linear scans over local-memory arrays.  sw[t]: the position
+// swapped with t at step t (swap positions t and sw[t], t = 0..nbp-1, in order).
+__device__ void compose_swaps_warp(const int* chosen, int nbp, int* sw, int* posv, int* origv, int lane) {
+  int n = 0;   // table entries (uniform across the warp)
+  auto find = [&](const int* keys, int key) -> int {   // entry index holding key, -1 if none
+    int f = -1;
+    for (int b = 0; b < n; b += 32) {
+      const int e = b + lane;
+      const unsigned m = __ballot_sync(0xffffffffu, e < n && keys[e] == key);
+      if (m) { f = b + __ffs(m) - 1; break; }
+    }
+    return f;
+  };
+  for (int t = 0; t < nbp; ++t) {
+    const int o = chosen[t];
+    const int eo = find(origv, o);
+    const int q = eo >= 0 ? posv[eo] : o;
+    if (lane == 0) sw[t] = q;
+    if (q != t) {
+      const int et = find(posv, t);
+      const int ot = et >= 0 ? origv[et] : t;
+      // position t now holds o, position q holds ot
+      if (lane == 0) {
+        if (et >= 0) origv[et] = o; else { posv[n] = t; origv[n] = o; }
+      }
+      const int n1 = n + (et >= 0 ? 0 : 1);
+      __syncwarp();
+      const int eq = (eo >= 0) ? eo : -1;   // the entry of position q is the one that held o
+      if (lane == 0) {
+        if (eq >= 0) origv[eq] = ot; else { posv[n1] = q; origv[n1] = ot; }
+      }
+      n = n1 + (eq >= 0 ? 0 : 1);
+      __syncwarp();
+    }
+  }
+}
+
+// Register-resident pivot selection (round 2): one sketch column (SP doubles) per thread in
+// registers, columns over the CL CTAs of a cluster (<= 512 each).  Each step every CTA finds
+// its best trailing norm, publishes the candidate COLUMN itself (not only its index) to every
+// CTA through DSMEM, and after ONE cluster barrier every thread knows the winner and builds the
+// Householder vector from the published column -- no second barrier to broadcast it.  Same
+// greedy rule as sketch_cpqr_cl_kernel (largest trailing norm, ties to the lowest index).
+constexpr int SR_NT = 512, SR_NW = SR_NT / 32;
+template <int CL>
+__global__ void __launch_bounds__(SR_NT, 1) sketch_cpqr_reg_kernel(const RDesc* __restrict__ d0) {
+  __shared__ double xc[2][CL][SP];     // candidate columns, by rank
+  __shared__ double xv[2][CL];         // candidate trailing norms (-2: none)
+  __shared__ int xi[2][CL];            // candidate indices (block-relative)
+  __shared__ double redv[SR_NW];
+  __shared__ int redi[SR_NW];
+  __shared__ double colbuf[SP];
+  __shared__ int chosen[QR_NB], posv[2 * QR_NB], origv[2 * QR_NB];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const RDesc d = d0[blockIdx.x / CL];
+  const int J = d.J, cr = d.c - J, nbp = d.nbp;
+  const int chunk = (cr + CL - 1) / CL;
+  const int j0 = rank * chunk, nc = max(0, min(cr, j0 + chunk) - j0);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool mine = tid < nc;
+  const int myc = j0 + tid;
+  double z[SP];
+  double zn = -2.0;
+  if (mine) {
+    const double* src = d.Y + (long long)(J + myc) * SP;
+    zn = 0.0;
+#pragma unroll
+    for (int r = 0; r < SP; ++r) { z[r] = src[r]; zn += z[r] * z[r]; }
+  } else {
+#pragma unroll
+    for (int r = 0; r < SP; ++r) z[r] = 0.0;
+  }
+  auto better = [](double ov, int oi, double bv, int bi) { return ov > bv || (ov == bv && oi < bi); };
+  for (int t = 0; t < nbp; ++t) {
+    const int buf = t & 1;
+    // local candidate: largest trailing norm, ties -> lowest index (warp shuffles, then every warp
+    // reduces the 16 warp results itself: one CTA barrier per step)
+    double bv = (mine && zn > -1.0) ? zn : -2.0;
+    int bi = (mine && zn > -1.0) ? myc : INT_MAX;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (better(ov, oi, bv, bi)) { bv = ov; bi = oi; }
+    }
+    if (lane == 0) { redv[warp] = bv; redi[warp] = bi; }
+    __syncthreads();
+    bv = lane < SR_NW ? redv[lane] : -2.0;
+    bi = lane < SR_NW ? redi[lane] : INT_MAX;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (better(ov, oi, bv, bi)) { bv = ov; bi = oi; }
+    }
+    // the warp holding the CTA's candidate (warp 0 when the CTA has none) publishes (norm, index,
+    // column) to every rank
+    const int ow = (bi == INT_MAX) ? 0 : (bi - j0) / 32;
+    if (warp == ow) {
+      if (bi != INT_MAX && myc == bi) {
+#pragma unroll
+        for (int r = 0; r < SP; ++r) colbuf[r] = z[r];
+      }
+      __syncwarp();
+      for (int e = lane; e < CL * (SP + 1); e += 32) {
+        const int q = e / (SP + 1), r = e - q * (SP + 1);
+        if (r < SP) {
+          cluster.map_shared_rank(&xc[0][0][0], q)[(buf * CL + rank) * SP + r] = colbuf[r];
+        } else {
+          cluster.map_shared_rank(&xv[0][0], q)[buf * CL + rank] = bv;
+          cluster.map_shared_rank(&xi[0][0], q)[buf * CL + rank] = bi;
+        }
+      }
+    }
+    cluster.sync();
+    double pv = xv[buf][0];
+    int p = xi[buf][0], wr = 0;
+#pragma unroll
+    for (int r = 1; r < CL; ++r)
+      if (better(xv[buf][r], xi[buf][r], pv, p)) { pv = xv[buf][r]; p = xi[buf][r]; wr = r; }
+    if (p >= cr || pv < -1.0) p = t;   // degenerate (no active column): keep the order
+    if (rank == 0 && tid == 0) chosen[t] = p;
+    if (pv < -1.0) continue;           // nothing left to reflect (uniform over the cluster)
+    // Householder reflector of the winner's rows t..SP-1 (every thread, from the published copy):
+    // its trailing norm^2 is the published pv (rows >= t), so mu = sqrt(pv)
+    const double* xw = &xc[buf][wr][0];
+    const double alpha = xw[t];
+    double tau = 0.0, scale = 0.0;
+    if (pv > alpha * alpha) {
+      const double mu = sqrt(pv);
+      const double beta = (alpha >= 0.0) ? -mu : mu;
+      tau = (beta - alpha) / beta;
+      scale = 1.0 / (alpha - beta);
+    }
+    if (mine && myc == p) zn = -2.0;   // retired
+    if (mine && zn > -1.0) {
+      double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+      for (int r = 0; r < SP; ++r) {
+        if (r < t) continue;
+        const double hv = (r == t) ? 1.0 : xw[r] * scale;
+        if (r & 1) d1 += z[r] * hv; else d0 += z[r] * hv;
+      }
+      const double w = tau * (d0 + d1);
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int r = 0; r < SP; ++r) {
+        if (r < t) continue;
+        const double hv = (r == t) ? 1.0 : xw[r] * scale;
+        z[r] -= w * hv;
+        if (r > t) { if (r & 1) s1 += z[r] * z[r]; else s0 += z[r] * z[r]; }
+      }
+      zn = s0 + s1;
+    }
+  }
+  if (rank != 0) return;
+  __syncthreads();
+  if (warp == 0) compose_swaps_warp(chosen, nbp, d.sw, posv, origv, lane);
+}
+
+template <int CL>
+void launch_sk_reg(cudaStream_t s, const RDesc* dd, int na) {
+  static std::once_flag attr_once;
+  std::call_once(attr_once, [&] {
+    if (CL > 8) RSF_CUDA(cudaFuncSetAttribute(sketch_cpqr_reg_kernel<CL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  });
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(na * CL));
+  cfg.blockDim = dim3(SR_NT);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  RSF_CUDA(cudaLaunchKernelEx(&cfg, sketch_cpqr_reg_kernel<CL>, dd));
+  count_launch();
+}
+
+// register pivot selection when the widest trailing sketch fits in <= 16 CTAs x 512 columns
+bool launch_sketch_reg(cudaStream_t s, const RDesc* dd, int na, int crmax) {
+  static const bool on = !(getenv("RSF_SKETCH_REG") && getenv("RSF_SKETCH_REG")[0] == '0');
+  if (!on || crmax <= 0 || crmax > 16 * SR_NT) return false;
+  int CL = 1;
+  while ((crmax + CL - 1) / CL > SR_NT) CL *= 2;
+  switch (CL) {
+    case 1: launch_sk_reg<1>(s, dd, na); break;
+    case 2: launch_sk_reg<2>(s, dd, na); break;
+    case 4: launch_sk_reg<4>(s, dd, na); break;
+    case 8: launch_sk_reg<8>(s, dd, na); break;
+    default: launch_sk_reg<16>(s, dd, na); break;
+  }
+  return true;
+}
+
 // apply the swap list to A (m rows), Y (SP rows) and piv
 // The block's column swaps (positions J + t and J + sw[t], t = 0..nbp-1, in order).  Rows are
 // independent: every thread applies the whole swap sequence to its rows of A, so the CTAs of
@@ -821,7 +1022,7 @@ RRQRResult rrqr_batched(cudaStream_t s, const std::vector<RRQRProb>& probs, doub
     const unsigned na = (unsigned)dv.size();
     int crmax = 0;
     for (auto& d : dv) crmax = std::max(crmax, d.c - d.J);
-    if (!launch_sketch_cluster(s, dd.p, (int)na, crmax)) {
+    if (!launch_sketch_reg(s, dd.p, (int)na, crmax) && !launch_sketch_cluster(s, dd.p, (int)na, crmax)) {
       sketch_cpqr_kernel<<<na, NT, 0, s>>>(dd.p);
       count_launch();
     }

@@ -21,6 +21,7 @@ struct Opts {
   double r_near = 1.8, r_in = 1.75, r_out = 2.45;   // R-C (in units of the box half-width)
   unsigned long long seed = 1603080570ull;
   int strong = 0;            // peeling admissibility: 0 weak, 1 strong (next row f4)
+  int peel_f32 = 0;          // peeled levels stored in FP32 (FP64 arithmetic), DESIGN.md §7g
 };
 
 struct Ctx {

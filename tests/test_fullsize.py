@@ -102,7 +102,9 @@ def _ell_at(ctx, c, xy, z, n, logdet_only=False, **kw):
     """l(theta) from the Sigma factor alone: log|F| and z^T F^-1 z."""
     K = R.Kernel(c.family, kw.get("rho", c.rho), kw.get("sigma2", c.sigma2), kw.get("nugget", c.nugget),
                  kw.get("alpha", c.alpha), theta=())
-    F = R.Factor(ctx, xy, K, c.eps_fact, c.leaf)
+    # the evaluation's own seed: the RRQR sketches (and through them the skeletons) of the
+    # standalone factor are then those of the factor inside gp_mle_eval
+    F = R.Factor(ctx, xy, K, c.eps_fact, c.leaf, opts=R.Opts(eps_peel=c.eps_peel, seed=c.seed))
     ld = F.logdet()
     if logdet_only:
         F.close()

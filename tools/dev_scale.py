@@ -29,7 +29,7 @@ free, tot = torch.cuda.mem_get_info(); print('mem free/total GB', free / 1e9, to
 for rep in range(reps):
     R.lib.rsf_profile_reset()
     t = time.time()
-    r = R.gp_mle_eval(ctx, xy, z, K, c.eps_fact, c.leaf, R.Opts(eps_peel=c.eps_peel, seed=c.seed, probe_block=int(__import__('os').environ.get('PROBE_BLOCK', '512'))))
+    r = R.gp_mle_eval(ctx, xy, z, K, c.eps_fact, c.leaf, R.Opts(eps_peel=c.eps_peel, seed=c.seed, probe_block=int(__import__('os').environ.get('PROBE_BLOCK', '512')), peel_f32=int(__import__('os').environ.get('PEEL_F32', '0'))))
     el = time.time() - t
     d = r.diag
     if __import__('os').environ.get('RSF_KTRACE') == '1':
