@@ -3,6 +3,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <stdexcept>
@@ -47,7 +48,14 @@ void* dev_alloc(size_t bytes, cudaStream_t s);
 void dev_free(void* p, size_t bytes, cudaStream_t s);
 void dev_cache_trim(cudaStream_t s);   // release the cached blocks of a stream
 void dev_cache_trim_bins(cudaStream_t s);   // release only the cached small (power-of-two bin) blocks
-double dev_cache_bytes();                    // bytes held in the bin caches of all streams (diagnostics)
+double dev_cache_bytes();
+extern std::atomic<int> g_big_sync;          // > 0: large blocks via cudaMalloc/cudaFree (memory-saving mode)
+void pool_trim();                            // return the stream-ordered pool's unused pages to the driver
+struct BigSyncScope {                        // RAII: memory-saving mode for the scope when on
+  bool on;
+  explicit BigSyncScope(bool o) : on(o) { if (on && g_big_sync++ == 0) pool_trim(); }
+  ~BigSyncScope() { if (on) --g_big_sync; }
+};                    // bytes held in the bin caches of all streams (diagnostics)
 
 // Stream-ordered device buffer (cudaMallocAsync on the context stream; the
 // default memory pool keeps freed blocks cached for the next evaluation).

@@ -10,6 +10,8 @@
 #include <list>
 #include <map>
 #include <mutex>
+#include <unordered_set>
+#include <atomic>
 #include <string>
 
 #include "gemm.cuh"
@@ -100,8 +102,22 @@ bool arena_free(cudaStream_t s, void* p, size_t bytes) {
   }
   return false;
 }
+// Memory-saving mode (opts.peel_f32): large blocks come from cudaMalloc / cudaFree directly -- the
+// stream-ordered pool measured 67 GB of its 176 GB reservation unused but unreleasable (fragmented by
+// long-lived per-level storage between transients) at level 5 of config 4; cudaFree returns the
+// pages at once (it synchronises the device; the trace jobs run one after the other in this mode).
+std::atomic<int> g_big_sync{0};
+std::unordered_set<void*>& sync_blocks() { static std::unordered_set<void*> v; return v; }
 void* dev_alloc(size_t bytes, cudaStream_t s) {
   void* p = nullptr;
+  if (bytes > CACHE_MAX && g_big_sync.load() > 0) {
+    const double t0 = wall();
+    RSF_CUDA(cudaMalloc(&p, bytes));
+    g_amiss_large += wall() - t0; ++g_nmiss_large;
+    std::lock_guard<std::mutex> lk(cache_mu());
+    sync_blocks().insert(p);
+    return p;
+  }
   if (bytes > CACHE_MAX) {
     const size_t rb = (bytes + (size_t(2) << 20) - 1) / (size_t(2) << 20) * (size_t(2) << 20);
     {
@@ -139,6 +155,24 @@ void dev_cache_trim(cudaStream_t s) {
     else ++i;
   }
 }
+void pool_trim() {
+  int dev = 0;
+  cudaMemPool_t pool;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
+  {   // the per-stream arenas and bin caches go back to the pool (recreated on demand outside the mode)
+    std::lock_guard<std::mutex> lk(cache_mu());
+    for (auto& f : cache()) { for (void* p : f.blocks) cudaFreeAsync(p, f.s); f.blocks.clear(); }
+    auto& A = arenas();   // only arenas with nothing allocated in them (a live handle may own blocks)
+    for (size_t i = 0; i < A.size();) {
+      const bool empty = !A[i].base || (A[i].free_.size() == 1 && A[i].free_.begin()->first == 0 &&
+                                        A[i].free_.begin()->second == A[i].cap);
+      if (empty) { if (A[i].base) cudaFreeAsync(A[i].base, A[i].s); A.erase(A.begin() + i); }
+      else ++i;
+    }
+  }
+  cudaDeviceSynchronize();
+  cudaMemPoolTrimTo(pool, 0);
+}
 double dev_cache_bytes() {
   std::lock_guard<std::mutex> lk(cache_mu());
   double b = 0;
@@ -153,6 +187,13 @@ void dev_cache_trim_bins(cudaStream_t s) {
 void dev_free(void* p, size_t bytes, cudaStream_t s) {
   if (!p) return;
   if (bytes > CACHE_MAX) {
+    bool sync = false;
+    {
+      std::lock_guard<std::mutex> lk(cache_mu());
+      auto it = sync_blocks().find(p);
+      if (it != sync_blocks().end()) { sync_blocks().erase(it); sync = true; }
+    }
+    if (sync) { RSF_CUDA(cudaFree(p)); return; }
     const size_t rb = (bytes + (size_t(2) << 20) - 1) / (size_t(2) << 20) * (size_t(2) << 20);
     {
       std::lock_guard<std::mutex> lk(cache_mu());

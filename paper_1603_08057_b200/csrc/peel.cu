@@ -306,9 +306,11 @@ struct PeelLevel {
   // FP32 storage of the same (opts.peel_f32): the subtraction GEMMs read them as an
   // FP32 op(B) and compute in FP64
   bool f32 = false;
-  std::vector<DBuf<float>> Vf;
-  DBuf<float> Browf;
-  const void* vptr(int b) const { return f32 ? (const void*)Vf[b].p : (const void*)V[b].p; }
+  DBuf<float> store;                 // every V_i and Brow of the level in one allocation (no bin rounding,
+  std::vector<size_t> vfo;           // one long-lived block per level in the pool): V_i at vfo[i],
+  size_t browf_off = 0;              // Brow at browf_off
+  const void* vptr(int b) const { return f32 ? (const void*)(store.p + vfo[b]) : (const void*)V[b].p; }
+  const float* browf() const { return store.p + browf_off; }
   long long tcols = 0;   // tmp columns per probe column: sum r (T') + sum r (S')
   GemmBatch g1, g2, g3;
   std::vector<int> ib, ni, r, bidx;      // boxes with r > 0: range, basis size, level box index
@@ -502,6 +504,7 @@ double ddot(cudaStream_t s, const double* a, const double* b, long long n) {
 }
 
 double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag* diag, const Comm* comm) {
+  BigSyncScope big_sync(o.peel_f32 != 0);
   const double t0 = now_s();
   cudaStream_t s = op_stream(F);
   Comm cm = comm ? *comm : F.ctx->comm;
@@ -702,10 +705,96 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
     std::vector<int> vcap(nb, 0);                 // allocated columns of V_i / A_i (grown exactly)
     std::vector<int> vmax(nb, 0);                 // most columns V_i can take: min(n_i, c per sibling group)
     // per ordered pair (index: pslot(b, partner))
-    struct PairData { int k = 0, rz = 0; double *Z = nullptr, *X = nullptr, *Lm = nullptr, *Gi = nullptr; };
+    struct PairData { int k = 0, rz = 0, arena = -1; double *Z = nullptr, *X = nullptr, *Lm = nullptr, *Gi = nullptr; };
     std::vector<PairData> pdat((size_t)std::max<long long>(pslot0[nb], 1));
+    // The per-pair data live in arenas, one per (pair-core batch, group of the act boxes); an arena is
+    // released as soon as every pair it holds has its core (a pair {i, j} is complete once the groups of
+    // i and of j have both been sketched), so at most ~7/12 of a level's pair data are resident at once
+    // (was: all of it until the level end -- 23 GB at level 5 of config 4)
     std::vector<DBuf<double>> arenas;
-    double pair_bytes = 0;   // per-pair data of the level (diagnostics)
+    std::vector<int> arena_uses;
+    double pair_bytes = 0, pair_peak = 0;   // per-pair data of the level: resident now / peak (diagnostics)
+    // finished cores: B_ij blocks (rz_i x rz_j, ld rz_i) until Brow's layout (final r's) is known
+    struct CBlock { int i, j; const double* p; int ri, rj; };
+    std::vector<CBlock> cblocks;
+    std::vector<DBuf<double>> cbufs;
+    std::vector<char> gdone(NGRP, 0);
+    // cores of complete pairs {i < j}: M_ij = Lm_ij (X_ji^T)^+ = Lm_ij X_ji (X_ji^T X_ji)^-1,
+    // B_ij = Z_ij M_ij Z_ji^T, B_ji = B_ij^T -> blocks in cbufs; the pairs' arenas are
+    // released when their last pair is done
+    auto compute_cores = [&](const std::vector<std::pair<int, int>>& cand) {
+      RSF_PHASE("p.cores", s);
+      long long mt = 0, bt = 0;
+      std::vector<std::array<long long, 4>> mo;
+      std::vector<std::pair<int, int>> pl;
+      for (const auto& ij : cand) {
+        const int i = ij.first, j = ij.second;
+        const PairData& a = pdat[pslot(i, j)];
+        const PairData& b2 = pdat[pslot(j, i)];
+        if (a.k == 0 || b2.k == 0) continue;
+        std::array<long long, 4> m{};
+        m[0] = mt; mt += (long long)a.k * b2.k;                 // T1, then M
+        m[1] = mt; mt += (long long)a.k * b2.k;                 // T2
+        m[2] = mt; mt += (long long)std::max(a.rz, b2.rz) * std::max(a.k, b2.k) * 2;  // T3 / T4
+        m[3] = bt; bt += 2ll * a.rz * b2.rz;                    // B_ij, B_ji
+        mo.push_back(m);
+        pl.emplace_back(i, j);
+      }
+      if (!pl.empty()) {
+        DBuf<double> Mw(std::max<long long>(mt, 1), s);
+        cbufs.emplace_back(DBuf<double>((size_t)std::max<long long>(bt, 1), s));
+        double* Bb = cbufs.back().p;
+        GemmBatch m1(false, false), m2(false, true), m3(false, false), m4(false, false), m5(false, true),
+            m6(false, true), m7(false, true);
+        for (size_t q = 0; q < pl.size(); ++q) {
+          const int i = pl[q].first, j = pl[q].second;
+          const PairData& a = pdat[pslot(i, j)];
+          const PairData& b2 = pdat[pslot(j, i)];
+          const int k1 = a.k, k2 = b2.k;
+          double* T1p = Mw.p + mo[q][0];
+          double* T2p = Mw.p + mo[q][1];
+          double* T3p = Mw.p + mo[q][2];
+          double* T4p = T3p + (long long)std::max(a.rz, b2.rz) * std::max(k1, k2);
+          double* Bij = Bb + mo[q][3];
+          double* Bji = Bij + (long long)a.rz * b2.rz;
+          GemmDesc d1 = gdesc(k1, k2, c);     // T1 = Lm_ij X_ji
+          d1.A = a.Lm; d1.lda = k1; d1.B = b2.X; d1.ldb = c; d1.C = T1p; d1.ldc = k1;
+          m1.add(d1);
+          GemmDesc d2 = gdesc(k1, k2, k2);    // T2 = T1 Gi_ji^T
+          d2.A = T1p; d2.lda = k1; d2.B = b2.Gi; d2.ldb = k2; d2.C = T2p; d2.ldc = k1;
+          m2.add(d2);
+          GemmDesc d3 = gdesc(k1, k2, k2);    // M = T2 Gi_ji   (into T1)
+          d3.A = T2p; d3.lda = k1; d3.B = b2.Gi; d3.ldb = k2; d3.C = T1p; d3.ldc = k1;
+          m3.add(d3);
+          GemmDesc d4 = gdesc(a.rz, k2, k1);  // T3 = Z_ij M
+          d4.A = a.Z; d4.lda = a.rz; d4.B = T1p; d4.ldb = k1; d4.C = T3p; d4.ldc = a.rz;
+          m4.add(d4);
+          GemmDesc d5 = gdesc(a.rz, b2.rz, k2);   // B_ij = T3 Z_ji^T
+          d5.A = T3p; d5.lda = a.rz; d5.B = b2.Z; d5.ldb = b2.rz; d5.C = Bij; d5.ldc = a.rz;
+          m5.add(d5);
+          GemmDesc d6 = gdesc(b2.rz, k1, k2);     // T4 = Z_ji M^T
+          d6.A = b2.Z; d6.lda = b2.rz; d6.B = T1p; d6.ldb = k1; d6.C = T4p; d6.ldc = b2.rz;
+          m6.add(d6);
+          GemmDesc d7 = gdesc(b2.rz, a.rz, k1);   // B_ji = T4 Z_ij^T
+          d7.A = T4p; d7.lda = b2.rz; d7.B = a.Z; d7.ldb = a.rz; d7.C = Bji; d7.ldc = b2.rz;
+          m7.add(d7);
+          pd.flops += 2.0 * k1 * (double)k2 * c + 2.0 * a.rz * (double)b2.rz * (k1 + k2);
+          cblocks.push_back(CBlock{i, j, Bij, a.rz, b2.rz});
+          cblocks.push_back(CBlock{j, i, Bji, b2.rz, a.rz});
+        }
+        m1.run(s); m2.run(s); m3.run(s); m4.run(s); m5.run(s); m6.run(s); m7.run(s);
+      }
+      // release the pair data of the candidates (stream-ordered: after the GEMMs above)
+      for (const auto& ij : cand)
+        for (int side = 0; side < 2; ++side) {
+          PairData& q = side ? pdat[pslot(ij.second, ij.first)] : pdat[pslot(ij.first, ij.second)];
+          if (q.arena >= 0 && --arena_uses[q.arena] == 0) {
+            pair_bytes -= 8.0 * arenas[q.arena].n;
+            arenas[q.arena].release();
+          }
+          q.arena = -1;
+        }
+    };
     int mr = 0;
     while (true) {
       std::fill(rb.begin(), rb.end(), 0);
@@ -734,7 +823,12 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
           Ab[b].alloc((size_t)c * vcap[b], s);
         }
       arenas.clear();
+      arena_uses.clear();
+      cblocks.clear();
+      cbufs.clear();
+      std::fill(gdone.begin(), gdone.end(), 0);
       pair_bytes = 0;
+      pair_peak = 0;
       for (auto& q : pdat) q = PairData{};
       bool fail = false;
       mr = 0;
@@ -743,12 +837,32 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
         if (gcount[g] == 0) continue;
         // boxes i with a partner j in group g (at most one: one sibling per quadrant, one box per
         // class in a parent neighbourhood)
-        std::vector<int> act, partner;
+        std::vector<int> act_all, partner_all;
         for (int b = 0; b < nb; ++b) {
           if (grp[b] == g) continue;
           for (int x : part[b])
-            if (grp[x] == g) { act.push_back(b); partner.push_back(x); break; }
+            if (grp[x] == g) { act_all.push_back(b); partner_all.push_back(x); break; }
         }
+        if (act_all.empty()) continue;
+        // memory-saving mode: when the group's per-box sketch products (P_ij: c x c, C_ij: c x (r_i + c)
+        // per act box -- 53 GB at level 6 of config 4) exceed a third of the free memory, the act boxes
+        // are taken in subsets, each re-running the G applies of the group (same probes, same
+        // residual; only the boxes whose sketches are kept differ)
+        int nsub = 1;
+        if (o.peel_f32) {
+          double need = 0;
+          for (int b : act_all) need += 8.0 * c * ((double)c + std::min<double>(bx[b].ni, rb[b] + c));
+          size_t fr = 0, tot = 0;
+          cudaMemGetInfo(&fr, &tot);
+          const double avail = std::max(4.0 * (1ull << 30), 0.33 * (double)fr);
+          nsub = std::max(1, (int)std::ceil(need / avail));
+          if (verbose && nsub > 1)
+            fprintf(stderr, "    level %d group %d: %zu act boxes in %d subsets (%.1f GB of sketch products, %.1f GB free)\n",
+                    lev, g, act_all.size(), nsub, 1e-9 * need, 1e-9 * fr);
+        }
+        for (int sub = 0; sub < nsub && !fail; ++sub) {
+        const size_t a0 = act_all.size() * sub / nsub, a1 = act_all.size() * (sub + 1) / nsub;
+        std::vector<int> act(act_all.begin() + a0, act_all.begin() + a1), partner(partner_all.begin() + a0, partner_all.begin() + a1);
         if (act.empty()) continue;
         const size_t NA = act.size();
         // per act box, for the whole group: P_ij = W_i^T Y_ij (c x c), C_ij' = Y_ij^T [V_i ...]
@@ -762,6 +876,12 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
           cco[x] = cct; cct += (long long)c * cccap[x];
         }
         DBuf<double> P(pt, s), CC(std::max<long long>(cct, 1), s), ref(NA, s);
+        if (verbose > 1) {
+          size_t fr = 0, tot = 0;
+          cudaMemGetInfo(&fr, &tot);
+          fprintf(stderr, "    level %d group %d: act %zu width %d  P %.2f GB CC %.2f GB  free %.2f GB\n", lev, g, NA, c,
+                  8e-9 * pt, 8e-9 * cct, 1e-9 * fr);
+        }
         ref.zero();
         CC.zero();
         // W_i^T of every act box for the whole group when it fits (else regenerated per batch)
@@ -997,16 +1117,41 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
         Y.release();
         gath.release();
         // eps_peel-rank of every sibling block from its Gaussian sketch P_ij (R-N); adaptivity (R-M)
-        DBuf<double> Pc(pt, s);
         DBuf<int> piv((size_t)c * NA, s);
-        std::vector<int> kk;
+        std::vector<int> kk(NA, 0);
+        // R11 of every box's pivoted QR (k x k, ld k), kept for the pair cores; the c x c copies the
+        // RRQR works on exist one budget-sized batch of boxes at a time (one batch -- the whole
+        // group -- unless the copies exceed the budget: at level 6 of config 4 they were 22 GB)
+        std::vector<DBuf<double>> r11buf;
+        std::vector<const double*> r11p(NA, nullptr);
+        std::vector<int> r11ld(NA, 1);
         {
           RSF_PHASE("p.sketch_rank", s);
-          RSF_CUDA(cudaMemcpyAsync(Pc.p, P.p, pt * sizeof(double), cudaMemcpyDeviceToDevice, s));
-          std::vector<RRQRProb> rp;
-          for (size_t x = 0; x < NA; ++x)
-            rp.push_back(RRQRProb{Pc.p + po[x], c, c, c, piv.p + (long long)x * c, nullptr, nullptr, 0});
-          kk = rrqr_batched(s, rp, o.eps_peel, seed ^ (0xD1B54A32D192ED03ull * (unsigned long long)(lev + 64 * (trace_id + 1)))).k;
+          size_t y0 = 0;
+          while (y0 < NA) {
+            size_t y1 = y0;
+            while (y1 < NA && (y1 == y0 || 8.0 * (po[y1] + (long long)c * c - po[y0]) <= budget)) ++y1;
+            const long long pb = (long long)(y1 - y0) * c * c;
+            DBuf<double> Pc(pb, s);
+            RSF_CUDA(cudaMemcpyAsync(Pc.p, P.p + po[y0], pb * sizeof(double), cudaMemcpyDeviceToDevice, s));
+            std::vector<RRQRProb> rp;
+            for (size_t x = y0; x < y1; ++x)
+              rp.push_back(RRQRProb{Pc.p + (po[x] - po[y0]), c, c, c, piv.p + (long long)x * c, nullptr, nullptr, 0});
+            std::vector<int> kb = rrqr_batched(s, rp, o.eps_peel, seed ^ (0xD1B54A32D192ED03ull * (unsigned long long)(lev + 64 * (trace_id + 1)))).k;
+            long long rt = 0;
+            for (size_t x = y0; x < y1; ++x) { kk[x] = kb[x - y0]; rt += (long long)kk[x] * kk[x]; }
+            r11buf.emplace_back(DBuf<double>((size_t)std::max<long long>(rt, 1), s));
+            std::vector<CopyProb> cr;
+            long long ro = 0;
+            for (size_t x = y0; x < y1; ++x) {
+              r11p[x] = r11buf.back().p + ro;
+              r11ld[x] = std::max(1, kk[x]);
+              if (kk[x] > 0) cr.push_back(CopyProb{Pc.p + (po[x] - po[y0]), c, r11buf.back().p + ro, kk[x], kk[x], kk[x], 1.0});
+              ro += (long long)kk[x] * kk[x];
+            }
+            copy_batched(s, cr);
+            y0 = y1;
+          }
         }
         for (size_t x = 0; x < NA; ++x) mr = std::max(mr, kk[x]);
         if (mr > c - o.oversample && c < cmax) { fail = true; break; }
@@ -1038,7 +1183,34 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
             lo[x] = zt; zt += k * c;
             go[x] = zt; zt += k * k;
           }
-          DBuf<double> arena(std::max<long long>(zt, 1), s);
+          // persistent blocks [Z | X | Lm | Gi] of every act box in the arena of its own group
+          std::vector<double*> ga(B, nullptr);
+          std::vector<int> gai(B, -1);
+          {
+            std::vector<long long> gsz(NGRP, 0), gb(B, 0);
+            for (size_t x = 0; x < B; ++x) {
+              const int q = grp[act[x0 + x]];
+              const long long k = kk[x0 + x];
+              gb[x] = gsz[q];
+              gsz[q] += (long long)rb[act[x0 + x]] * k + 2ll * c * k + k * k;
+            }
+            std::vector<int> gidx(NGRP, -1);
+            for (int q = 0; q < NGRP; ++q)
+              if (gsz[q] > 0) {
+                gidx[q] = (int)arenas.size();
+                arenas.emplace_back(DBuf<double>((size_t)gsz[q], s));
+                arena_uses.push_back(0);
+                pair_bytes += 8.0 * gsz[q];
+              }
+            pair_peak = std::max(pair_peak, pair_bytes);
+            for (size_t x = 0; x < B; ++x) {
+              const int q = grp[act[x0 + x]];
+              if (gidx[q] < 0) continue;
+              gai[x] = gidx[q];
+              ga[x] = arenas[gidx[q]].p + gb[x];
+            }
+          }
+          auto AP = [&](size_t x, long long off) { return ga[x] + (off - zo[x]); };
           DBuf<double> Z0(std::max<long long>(zt, 1), s), Ri2(std::max<long long>(zt, 1), s), T1(std::max<long long>(zt, 1), s);
           std::vector<GatherTDesc> gz;
           std::vector<EyeDesc> ez;
@@ -1051,7 +1223,7 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
             if (k == 0) continue;
             gz.push_back(GatherTDesc{CC.p + cco[xa], c, piv.p + (long long)xa * c, Z0.p + zo[x], rb[i], k});
             ez.push_back(EyeDesc{Ri2.p + go[x], k, k});
-            tz.push_back(TrsmProb{Pc.p + po[xa], c, Ri2.p + go[x], k, k, k});
+            tz.push_back(TrsmProb{r11p[xa], r11ld[xa], Ri2.p + go[x], k, k, k});
             mz = std::max(mz, (long long)rb[i] * k);
           }
           PhaseSeq cseq(s);
@@ -1067,9 +1239,9 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
             const int k = kk[xa];
             if (k == 0) continue;
             GemmDesc d = gdesc(rb[i], k, k);
-            d.A = Z0.p + zo[x]; d.lda = rb[i]; d.B = Ri2.p + go[x]; d.ldb = k; d.C = arena.p + zo[x]; d.ldc = rb[i];
+            d.A = Z0.p + zo[x]; d.lda = rb[i]; d.B = Ri2.p + go[x]; d.ldb = k; d.C = AP(x, zo[x]); d.ldc = rb[i];
             gz1.add(d);
-            cz.push_back(CQProb{arena.p + zo[x], rb[i], k});
+            cz.push_back(CQProb{AP(x, zo[x]), rb[i], k});
           }
           gz1.run(s);
           cholqr2_batched(s, cz, lev, &pd.flops, dfail.p);
@@ -1081,20 +1253,20 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
             const int k = kk[xa];
             if (k == 0) continue;
             GemmDesc a = gdesc(c, k, rb[i]);               // X = A_i Z
-            a.A = Ab[i].p; a.lda = c; a.B = arena.p + zo[x]; a.ldb = rb[i]; a.C = arena.p + xo[x]; a.ldc = c;
+            a.A = Ab[i].p; a.lda = c; a.B = AP(x, zo[x]); a.ldb = rb[i]; a.C = AP(x, xo[x]); a.ldc = c;
             gx.add(a);
             GemmDesc d = gdesc(k, k, c);                   // X^T X
-            d.A = arena.p + xo[x]; d.lda = c; d.B = arena.p + xo[x]; d.ldb = c; d.C = T1.p + go[x]; d.ldc = k;
+            d.A = AP(x, xo[x]); d.lda = c; d.B = AP(x, xo[x]); d.ldb = c; d.C = T1.p + go[x]; d.ldc = k;
             gg.add(d);
-            pp.push_back(PotrfProb{T1.p + go[x], k, k, arena.p + go[x], k});
+            pp.push_back(PotrfProb{T1.p + go[x], k, k, AP(x, go[x]), k});
             GemmDesc e = gdesc(k, c, c);                   // X^T P
-            e.A = arena.p + xo[x]; e.lda = c; e.B = P.p + po[xa]; e.ldb = c; e.C = Z0.p + lo[x]; e.ldc = k;
+            e.A = AP(x, xo[x]); e.lda = c; e.B = P.p + po[xa]; e.ldb = c; e.C = Z0.p + lo[x]; e.ldc = k;
             gt1.add(e);
             GemmDesc f = gdesc(k, c, k);                   // L^-1 (X^T P)
-            f.A = arena.p + go[x]; f.lda = k; f.B = Z0.p + lo[x]; f.ldb = k; f.C = Ri2.p + lo[x]; f.ldc = k;
+            f.A = AP(x, go[x]); f.lda = k; f.B = Z0.p + lo[x]; f.ldb = k; f.C = Ri2.p + lo[x]; f.ldc = k;
             gt2.add(f);
             GemmDesc h = gdesc(k, c, k);                   // Lm = L^-T L^-1 X^T P
-            h.A = arena.p + go[x]; h.lda = k; h.B = Ri2.p + lo[x]; h.ldb = k; h.C = arena.p + lo[x]; h.ldc = k;
+            h.A = AP(x, go[x]); h.lda = k; h.B = Ri2.p + lo[x]; h.ldb = k; h.C = AP(x, lo[x]); h.ldc = k;
             gt3.add(h);
             pd.flops += 2.0 * c * (double)k * rb[i] + 4.0 * k * (double)c * c;
           }
@@ -1113,12 +1285,22 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
             const int i = act[xa], j = partner[xa];
             PairData& q = pdat[pslot(i, j)];
             q.k = kk[xa]; q.rz = rb[i];
-            q.Z = arena.p + zo[x]; q.X = arena.p + xo[x]; q.Lm = arena.p + lo[x]; q.Gi = arena.p + go[x];
+            if (gai[x] < 0) continue;   // k = 0: no block
+            q.Z = AP(x, zo[x]); q.X = AP(x, xo[x]); q.Lm = AP(x, lo[x]); q.Gi = AP(x, go[x]);
+            q.arena = gai[x];
+            ++arena_uses[gai[x]];
           }
-          pair_bytes += 8.0 * arena.n;
-          arenas.push_back(std::move(arena));
           x0 = x1;
         }
+        // cores of the pairs completed by this group: (i, j in g) whose other side (j, i) came with
+        // the group of i, sketched earlier
+        std::vector<std::pair<int, int>> done;
+        for (size_t x = 0; x < NA; ++x)
+          if (gdone[grp[act[x]]]) done.emplace_back(std::min(act[x], partner[x]), std::max(act[x], partner[x]));
+        compute_cores(done);
+        }   // subsets
+        if (fail) break;
+        gdone[g] = 1;
       }
       if (!fail) break;
       ++restarts;
@@ -1154,68 +1336,21 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
     }
     PL.Brow.alloc(std::max<long long>(brt, 1), s);
     PL.Brow.zero();
-    {
-      RSF_PHASE("p.cores", s);
-      long long mt = 0;
-      std::vector<std::array<long long, 3>> mo;
-      std::vector<std::pair<int, int>> pl;
-      for (int i = 0; i < nb; ++i)
-        for (int j : part[i]) {
-          if (j <= i) continue;
-          const PairData& a = pdat[pslot(i, j)];
-          const PairData& b2 = pdat[pslot(j, i)];
-          if (a.k == 0 || b2.k == 0) continue;
-          std::array<long long, 3> m{};
-          m[0] = mt; mt += (long long)a.k * b2.k;                 // T1, then M
-          m[1] = mt; mt += (long long)a.k * b2.k;                 // T2
-          m[2] = mt; mt += (long long)std::max(a.rz, b2.rz) * std::max(a.k, b2.k) * 2;  // T3 / T4
-          mo.push_back(m);
-          pl.emplace_back(i, j);
-        }
-      DBuf<double> Mw(std::max<long long>(mt, 1), s);
-      GemmBatch m1(false, false), m2(false, true), m3(false, false), m4(false, false), m5(false, true),
-          m6(false, true), m7(false, true);
-      for (size_t q = 0; q < pl.size(); ++q) {
-        const int i = pl[q].first, j = pl[q].second;
-        const PairData& a = pdat[pslot(i, j)];
-        const PairData& b2 = pdat[pslot(j, i)];
-        const int k1 = a.k, k2 = b2.k;
-        double* T1p = Mw.p + mo[q][0];
-        double* T2p = Mw.p + mo[q][1];
-        double* T3p = Mw.p + mo[q][2];
-        double* T4p = T3p + (long long)std::max(a.rz, b2.rz) * std::max(k1, k2);
-        GemmDesc d1 = gdesc(k1, k2, c);     // T1 = Lm_ij X_ji
-        d1.A = a.Lm; d1.lda = k1; d1.B = b2.X; d1.ldb = c; d1.C = T1p; d1.ldc = k1;
-        m1.add(d1);
-        GemmDesc d2 = gdesc(k1, k2, k2);    // T2 = T1 Gi_ji^T
-        d2.A = T1p; d2.lda = k1; d2.B = b2.Gi; d2.ldb = k2; d2.C = T2p; d2.ldc = k1;
-        m2.add(d2);
-        GemmDesc d3 = gdesc(k1, k2, k2);    // M = T2 Gi_ji   (into T1)
-        d3.A = T2p; d3.lda = k1; d3.B = b2.Gi; d3.ldb = k2; d3.C = T1p; d3.ldc = k1;
-        m3.add(d3);
-        GemmDesc d4 = gdesc(a.rz, k2, k1);  // T3 = Z_ij M
-        d4.A = a.Z; d4.lda = a.rz; d4.B = T1p; d4.ldb = k1; d4.C = T3p; d4.ldc = a.rz;
-        m4.add(d4);
-        GemmDesc d5 = gdesc(a.rz, b2.rz, k2);   // B_ij = T3 Z_ji^T  -> Brow_i
-        d5.A = T3p; d5.lda = a.rz; d5.B = b2.Z; d5.ldb = b2.rz;
-        d5.C = PL.Brow.p + bo[i] + (long long)rb[i] * fo_of(i, j); d5.ldc = rb[i];
-        m5.add(d5);
-        GemmDesc d6 = gdesc(b2.rz, k1, k2);     // T4 = Z_ji M^T
-        d6.A = b2.Z; d6.lda = b2.rz; d6.B = T1p; d6.ldb = k1; d6.C = T4p; d6.ldc = b2.rz;
-        m6.add(d6);
-        GemmDesc d7 = gdesc(b2.rz, a.rz, k1);   // B_ji = T4 Z_ij^T  -> Brow_j
-        d7.A = T4p; d7.lda = b2.rz; d7.B = a.Z; d7.ldb = a.rz;
-        d7.C = PL.Brow.p + bo[j] + (long long)rb[j] * fo_of(j, i); d7.ldc = rb[j];
-        m7.add(d7);
-        pd.flops += 2.0 * k1 * (double)k2 * c + 2.0 * a.rz * (double)b2.rz * (k1 + k2);
-      }
-      m1.run(s); m2.run(s); m3.run(s); m4.run(s); m5.run(s); m6.run(s); m7.run(s);
-      if (dfail.to_host(1)[0])
-        throw Error(ST_ENUMERIC, "peeling: Cholesky of a sketch basis or core Gram matrix failed at level " +
-                                     std::to_string(lev));
+    {   // the finished B_ij blocks into their places in Brow (zero rows/columns past rz)
+      std::vector<CopyProb> cp;
+      for (const CBlock& q : cblocks)
+        cp.push_back(CopyProb{q.p, q.ri, PL.Brow.p + bo[q.i] + (long long)rb[q.i] * fo_of(q.i, q.j), rb[q.i],
+                              q.ri, q.rj, 1.0});
+      copy_batched(s, cp);
+      cblocks.clear();
+      cbufs.clear();
     }
     arenas.clear();
+    arena_uses.clear();
     for (auto& q : pdat) q = PairData{};
+    if (dfail.to_host(1)[0])
+      throw Error(ST_ENUMERIC, "peeling: Cholesky of a sketch basis or core Gram matrix failed at level " +
+                                   std::to_string(lev));
 
     // ---- subtraction batches of G^(lev)
     PL.V.clear();
@@ -1236,17 +1371,19 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
     double browbytes = 8.0 * PL.Brow.n;
     if (o.peel_f32) {   // FP32 storage of G^(lev), box by box
       PL.f32 = true;
-      PL.Vf.clear();
-      PL.Vf.resize(nb);
+      PL.vfo.assign(nb, 0);
+      size_t tot = 0;
+      for (int b = 0; b < nb; ++b) { PL.vfo[b] = tot; tot += (PL.V[b].n + 3) & ~(size_t)3; }   // 16-byte aligned
+      PL.browf_off = tot;
+      tot += PL.Brow.n;
+      PL.store.alloc(std::max<size_t>(tot, 1), s);
       for (int b = 0; b < nb; ++b) {
         if (!PL.V[b].p) continue;
-        PL.Vf[b].alloc(PL.V[b].n, s);
-        d2f_kernel<<<gxx((long long)PL.V[b].n), NT, 0, s>>>(PL.V[b].p, PL.Vf[b].p, (long long)PL.V[b].n);
+        d2f_kernel<<<gxx((long long)PL.V[b].n), NT, 0, s>>>(PL.V[b].p, PL.store.p + PL.vfo[b], (long long)PL.V[b].n);
         count_launch();
         PL.V[b].release();
       }
-      PL.Browf.alloc(std::max<size_t>(PL.Brow.n, 1), s);
-      d2f_kernel<<<gxx((long long)PL.Brow.n), NT, 0, s>>>(PL.Brow.p, PL.Browf.p, (long long)PL.Brow.n);
+      d2f_kernel<<<gxx((long long)PL.Brow.n), NT, 0, s>>>(PL.Brow.p, PL.store.p + PL.browf_off, (long long)PL.Brow.n);
       count_launch();
       RSF_LAUNCH_CHECK();
       PL.Brow.release();
@@ -1284,7 +1421,7 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
       PL.toff.push_back(toff[b]); PL.soff.push_back(soff[b]);
       GemmDesc d = gdesc(-1, rb[b], (int)tot);            // S'_b = T'_row Brow_b^T
       d.selA = 2; d.offA = strong ? 0 : toff[bx[b].fam0]; d.ldb = rb[b];
-      if (PL.f32) { d.B = (const double*)PL.Browf.p; d.offB = bo[b]; d.bf32 = 1; } else d.B = PL.Brow.p + bo[b];
+      if (PL.f32) { d.B = (const double*)PL.browf(); d.offB = bo[b]; d.bf32 = 1; } else d.B = PL.Brow.p + bo[b];
       d.selC = 2; d.offC = soff[b];
       if (strong) d.mapA = PL.mapk.p + moff[b];
       if (tot == 0) continue;                              // (strong: no partner has a basis)
@@ -1301,7 +1438,7 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
       if (!g->empty()) g->finalize(s);
     // memory-saving mode: the per-box blocks of this level (<= 64 MB, power-of-two bins) go back to
     // the stream-ordered pool instead of waiting in the bin cache for sizes the next level never asks
-    if (o.peel_f32) dev_cache_trim_bins(s);
+    if (o.peel_f32) { dev_cache_trim_bins(s); pool_trim(); }
     if (verbose) {
       RSF_CUDA(cudaStreamSynchronize(s));
       size_t fr = 0, tot = 0;
@@ -1322,8 +1459,8 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
           cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res);
           cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
         }
-        fprintf(stderr, "    memory: pool reserved %.2f GB used %.2f GB, bin caches %.2f GB, pair data of the level %.2f GB\n",
-                1e-9 * res, 1e-9 * used, 1e-9 * dev_cache_bytes(), 1e-9 * pair_bytes);
+        fprintf(stderr, "    memory: pool reserved %.2f GB used %.2f GB, bin caches %.2f GB, pair data of the level (peak) %.2f GB\n",
+                1e-9 * res, 1e-9 * used, 1e-9 * dev_cache_bytes(), 1e-9 * pair_peak);
       }
       if (verbose > 1 && !PL.f32) {
         DBuf<unsigned long long> cnt(4, s);
@@ -1476,6 +1613,7 @@ void fill_peel_diag(const PeelDiag& d, rsf_peel_diag* out) {
 // ----------------------------------------------------------------- Alg. 1
 EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KParams& kp, int p,
                     const int* theta, double eps, int leaf, const Opts& o, bool profile) {
+  BigSyncScope big_sync(o.peel_f32 != 0);   // memory-saving mode: large blocks via cudaMalloc/cudaFree
   EvalResult R;
   const long long l0 = g_launches;
   const double T0 = now_s();
