@@ -397,7 +397,7 @@ def main():
         peak64 = fp64_peak if fp64_peak > 0 else FP64_PEAK_TFLOPS
         factor_rl = {"bound": "fp64", "achieved": fl / fi.seconds / 1e12, "peak": peak64, "unit": "TFLOP/s",
                      "frac": fl / fi.seconds / 1e12 / peak64, "seconds": fi.seconds, "flops": fl,
-                     "what": "RSF of config 3's Sigma alone (rsf_factor, full factor with L for apply), its own "
+                     "what": f"RSF of config {c.cid}'s Sigma alone (rsf_factor, full factor with L for apply), its own "
                              "device-synchronised time (not overlapped with the compressions); algorithmic flops "
                              "of DESIGN.md §5 (ID + elimination + top Cholesky)"}
         nb = __import__("ctypes").c_double()
@@ -408,7 +408,7 @@ def main():
             ach = nb.value / t_solve / 1e9
             solve_rl = {"bound": "hbm", "achieved": ach, "peak": hbm[0], "unit": "GB/s", "frac": ach / hbm[0],
                         "peak_source": hbm[1], "seconds_per_solve": t_solve, "bytes_per_solve": nb.value,
-                        "what": "one F^-1 z (k = 1) of config 3's Sigma factor, forward + backward sweeps; "
+                        "what": f"one F^-1 z (k = 1) of config {c.cid}'s Sigma factor, forward + backward sweeps; "
                                 "bytes = 2 x (T, E, L^-1 of every box + C^-1) + active-DOF vector traffic "
                                 "(DESIGN.md §5); CUDA events, mean of 20"}
     except Exception as e:  # diagnostics only
@@ -458,10 +458,13 @@ def main():
                 "algorithmic_flops_per_launch": gfl / gl if gl else None}
     line = {
         "metric": METRIC,
-        "metric_note": ("BASELINE.json quotes this metric at n = 2^20 (config 4); config 4 does not fit one "
-                        "B200's memory with weak peeling (DESIGN.md §7), so per the task's rule `value` is "
-                        "measured on the largest single-GPU config, named in config.workload"
-                        if (args.n or c.n) != 1048576 else "config 4 (n = 2^20)"),
+        "metric_note": ("BASELINE.json quotes this metric at n = 2^20 (config 4). Config 4 runs on one B200 "
+                        "only in the memory-saving mode (FP32-stored peeled levels, DESIGN.md §7g) at ~270 s "
+                        "per evaluation, so a W >= 3 run takes ~30 min; the default line measures config 3 "
+                        "(FP64 storage throughout, named in config.workload) and `bench.py --config 4` gives "
+                        "the config-4 line (profiles/r02_bench_config4.json)"
+                        if (args.n or c.n) != 1048576 else
+                        "config 4 (n = 2^20), the metric's own workload, memory-saving mode (DESIGN.md §7g)"),
         "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * t_all / args.steps, "higher_is_better": True,
         "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",

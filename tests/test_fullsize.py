@@ -193,6 +193,36 @@ def test_cfg5_recipe_quarter_million_vs_finite_differences(ctx):
     assert max(gerr) <= 1e-3, (r.grad, gfd, gerr)
 
 
+def test_cfg4_full_2pow20_memory_saving_vs_finite_differences(ctx):
+    """Config 4 itself -- n = 2^20 clustered points, Matern 1/2, theta = (rho, sigma2): the metric's
+    workload, on one B200 in the memory-saving mode (FP32-stored peeled levels, FP64 arithmetic;
+    DESIGN.md §7g).  No dense reference exists at this size: g against Richardson differences of l
+    (P10) and the peeled traces against differences of log|F| (P8), z = F^{1/2} w (R-V)."""
+    torch.cuda.empty_cache()                        # the memory of earlier tests back to the driver
+    c = config(4)
+    n = c.n
+    xy = _d(points_for(c))
+    o = R.Opts(eps_peel=c.eps_peel, seed=c.seed, peel_f32=1)
+    K = R.Kernel(c.family, c.rho, c.sigma2, c.nugget, c.alpha, c.theta)
+    F = R.Factor(ctx, xy, K, c.eps_fact, c.leaf, opts=o)
+    z = F.sample(_d(w_for(c)))
+    F.close()
+    r = R.gp_mle_eval(ctx, xy, z, K, c.eps_fact, c.leaf, o)
+    assert r.ell == _ell_at(ctx, c, xy, z, n)       # the evaluation's factor, solve and l
+    vals = {"rho": c.rho, "sigma2": c.sigma2}
+    names = list(c.theta)
+    gfd = [_richardson(lambda x, nm=nm: _ell_at(ctx, c, xy, z, n, **{nm: x}), vals[nm]) for nm in names]
+    tfd = [_richardson(lambda x, nm=nm: _ell_at(ctx, c, xy, z, n, logdet_only=True, **{nm: x}), vals[nm])
+           for nm in names]
+    gerr = [abs(r.grad[i] - gfd[i]) / abs(gfd[i]) for i in range(2)]
+    terr = [abs(r.diag.trace[i] - tfd[i]) / abs(tfd[i]) for i in range(2)]
+    _record("cfg4_n1048576_memory_saving", {"grad": list(r.grad), "grad_fd": gfd, "rel_err": gerr,
+                                            "trace": [r.diag.trace[i] for i in range(2)], "trace_fd_logdet": tfd,
+                                            "trace_rel_err": terr, "t_total": r.diag.t_total})
+    assert max(terr) <= 1e-5, terr
+    assert max(gerr) <= 1e-3, (r.grad, gfd, gerr)
+
+
 def test_multichunk_batch_split_peeling_vs_O1(ctx, monkeypatch):
     c = config(2)
     n = 4096
