@@ -167,6 +167,12 @@ void rsf_debug_col_slice(int64_t k, int parts, int part, int64_t* lo, int64_t* h
  * (jobs dealt to min(njobs, world) rank groups), 0 if not, -1 on bad arguments.
  * Host only (tests). */
 int rsf_debug_job_runs(int njobs, int world, int rank, int job);
+/* group (0..ngroups-1) of rank `rank` of a `world`-rank group when the ngroups trace-job groups carry
+ * the estimated work gw[0..ngroups-1] (gp_mle_eval: 3 per general theta_i job, 1 for the Tr(F^-1)
+ * job): ranks 0..ngroups-1 seed one group each, every further rank joins the group
+ * with the largest current work per rank; equal weights give rank r -> group r mod ngroups.
+ * -1 on bad arguments.  Host only (tests). */
+int rsf_debug_job_group(int ngroups, const double* gw, int world, int rank);
 void rsf_ctx_destroy(rsf_ctx ctx);
 /* Order the context after the caller: everything enqueued on `stream` so far (an event recorded
  * there) completes before the context stream runs further work.  stream = NULL is the legacy

@@ -61,7 +61,7 @@ EXPORTS = ["rsf_opts_default", "rsf_ctx_create", "rsf_ctx_destroy", "rsf_factor"
            "rsf_debug_gemm_bench", "rsf_debug_fp64_peak", "rsf_trace_dump", "rsf_debug_gemm_log",
            "rsf_debug_gemm", "rsf_ctx_wait_stream", "rsf_nccl_unique_id", "rsf_ctx_create_group",
            "rsf_ctx_group", "rsf_debug_col_slice", "rsf_debug_solve_bench",
-           "rsf_debug_job_runs", "gp_cond_sample"]
+           "rsf_debug_job_runs", "gp_cond_sample", "rsf_debug_job_group"]
 
 
 def load(path: str = LIB_PATH) -> C.CDLL:
@@ -83,6 +83,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
     lib.rsf_debug_solve_bench.argtypes = [vp, C.c_int, C.c_int, dp]
     lib.rsf_debug_solve_bench.restype = C.c_double
     lib.rsf_debug_job_runs.argtypes = [C.c_int] * 4
+    lib.rsf_debug_job_group.argtypes = [C.c_int, C.POINTER(C.c_double), C.c_int, C.c_int]
     lib.rsf_ctx_destroy.argtypes = [vp]
     lib.rsf_ctx_destroy.restype = None
     lib.rsf_factor.argtypes = [vp, vp, i64, C.POINTER(rsf_kernel), i32, C.c_double, i32,

@@ -285,7 +285,12 @@ rsf_status rsf_ctx_group(rsf_ctx ctx, int* rank, int* world) {
 int rsf_debug_job_runs(int njobs, int world, int rank, int job) {
   if (njobs < 1 || world < 1 || rank < 0 || rank >= world || job < 0 || job >= njobs) return -1;
   const int G = rsf::Comm::job_groups(njobs, world);
-  return (world == 1 || job % G == rank % G) ? 1 : 0;
+  return (world == 1 || job % G == rank % G) ? 1 : 0;   // (equal job weights: rank r in group r mod G)
+}
+
+int rsf_debug_job_group(int ngroups, const double* gw, int world, int rank) {
+  if (ngroups < 1 || !gw || world < ngroups || rank < 0 || rank >= world) return -1;
+  return rsf::Comm::group_of_rank(std::vector<double>(gw, gw + ngroups), world, rank);
 }
 
 void rsf_debug_col_slice(int64_t k, int parts, int part, int64_t* lo, int64_t* hi) {

@@ -55,6 +55,25 @@ struct Comm {
   // trace jobs of one evaluation over the ranks: G = min(njobs, world) groups,
   // rank r in group r mod G, job j run by group j mod G (its ranks split the job's probe columns)
   static int job_groups(int njobs, int world) { return std::max(1, std::min(njobs, world)); }
+  // group of `rank` when the G groups carry the estimated work gw[g] (the jobs dealt to them): ranks
+  // 0..G-1 seed one group each, every further rank joins the group with the largest current work per
+  // rank (ties: lowest group; this greedy minimises the largest work per rank) -- equal weights give
+  // rank r -> group r mod G
+  static int group_of_rank(const std::vector<double>& gw, int world, int rank) {
+    const int G = (int)gw.size();
+    if (G <= 1) return 0;
+    if (rank < G) return rank;
+    std::vector<int> cnt(G, 1);
+    int g_of = 0;
+    for (int r = G; r <= rank; ++r) {
+      int best = 0;
+      for (int g = 1; g < G; ++g)
+        if (gw[g] / cnt[g] > gw[best] / cnt[best]) best = g;
+      ++cnt[best];
+      g_of = best;
+    }
+    return g_of;
+  }
 };
 
 // NCCL entry points (dlopen'd): 128-byte unique id, communicator from (id, rank, world) or

@@ -912,6 +912,7 @@ __global__ void __launch_bounds__(2 * BM, (BN >= 128 ? 1 : (BM == 64 ? 4 : 2))) 
                                                             double* ws, const long long* __restrict__ mnpre,
                                                             int kchunk, int mtiles, int smem_epi) {
   constexpr int LDB = p_ldb<BN>(), NI = BN / 16, WN = BN / 2;
+  constexpr int LDBF = BN + 8;   // FP32 B tile row stride (floats): 8 banks apart per tq, conflict-free
   constexpr int P_BM = BM, P_NT = 2 * BM, P_LDA = BM + 4, P_ST = ST, WMN = BM / 32;   // warps: WMN (M) x 2 (N)
   constexpr int P_BK = BK;
   static_assert(BN * P_LDA <= P_ST * P_BK * (P_LDA + p_ldb<BN>()), "C tile must fit in the pipeline buffers");
@@ -1023,7 +1024,7 @@ __global__ void __launch_bounds__(2 * BM, (BN >= 128 ? 1 : (BM == 64 ? 4 : 2))) 
           if (!TB) { const long long cj = mapB ? __ldg(mapB + gj) : gj; src = Bf + cj * ldb + c; }
           else src = Bf + (long long)c * ldb + gj;
         }
-        cp_async4(bsf + l * LDB + j, src, v);
+        cp_async4(bsf + l * LDBF + j, src, v);
       }
       return;
     }
@@ -1081,7 +1082,7 @@ __global__ void __launch_bounds__(2 * BM, (BN >= 128 ? 1 : (BM == 64 ? 4 : 2))) 
       for (int mi = 0; mi < 4; ++mi) af[mi] = as[(kk + tq) * P_LDA + wm * 32 + mi * 8 + g];
 #pragma unroll
       for (int ni = 0; ni < NI; ++ni)
-        bf[ni] = BF ? (double)reinterpret_cast<const float*>(bs)[(kk + tq) * LDB + wn * WN + ni * 8 + g]
+        bf[ni] = BF ? (double)reinterpret_cast<const float*>(bs)[(kk + tq) * LDBF + wn * WN + ni * 8 + g]
                     : bs[(kk + tq) * LDB + wn * WN + ni * 8 + g];
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi)

@@ -117,3 +117,36 @@ def test_trace_jobs_dealt_to_rank_groups():
             if W >= J:
                 assert all(sum(row) == 1 for row in runs)   # one job per rank group
     assert R.lib.rsf_debug_job_runs(0, 2, 0, 0) == -1
+
+
+def test_weighted_job_groups():
+    """include/rsf.h rsf_debug_job_group: ranks per trace-job group by estimated work (config 4:
+    the rho job weighs 3, the Tr(F^-1) job 1).  Every group gets a rank, equal weights give
+    r mod G, and the work per rank is balanced as well as whole ranks allow (no move of one rank
+    to another group lowers the largest work per rank)."""
+    import ctypes as C
+    import paper_1603_08057_b200 as R
+
+    def groups(gw, W):
+        a = (C.c_double * len(gw))(*gw)
+        return [R.lib.rsf_debug_job_group(len(gw), a, W, r) for r in range(W)]
+
+    for G in (1, 2, 3):
+        for W in range(G, 9):
+            assert groups([1.0] * G, W) == [r % G for r in range(W)]
+    assert groups([3.0, 1.0], 4) == [0, 1, 0, 0]
+    assert groups([3.0, 1.0], 8) == [0, 1, 0, 0, 0, 1, 0, 0]   # 6 ranks : 2 ranks
+    for gw in ([3.0, 1.0], [3.0, 3.0, 1.0], [5.0, 1.0, 2.0]):
+        for W in range(len(gw), 9):
+            g = groups(gw, W)
+            cnt = [g.count(i) for i in range(len(gw))]
+            assert min(cnt) >= 1 and sum(cnt) == W
+            worst = max(gw[i] / cnt[i] for i in range(len(gw)))
+            for a in range(len(gw)):          # moving one rank from a to b never helps
+                for b in range(len(gw)):
+                    if a == b or cnt[a] == 1:
+                        continue
+                    c2 = list(cnt); c2[a] -= 1; c2[b] += 1
+                    assert max(gw[i] / c2[i] for i in range(len(gw))) >= worst - 1e-12
+    a = (C.c_double * 2)(3.0, 1.0)
+    assert R.lib.rsf_debug_job_group(2, a, 1, 0) == -1

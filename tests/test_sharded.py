@@ -27,8 +27,8 @@ def _d(a):
     return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(DEV)
 
 
-@pytest.mark.parametrize("cid,n,P", [(1, 1024, 2), (1, 1024, 3), (2, 4096, 4)])
-def test_emulated_group_matches_oracle_and_unsharded(cid, n, P, monkeypatch):
+@pytest.mark.parametrize("cid,n,P,f32", [(1, 1024, 2, 0), (1, 1024, 3, 0), (2, 4096, 4, 0), (2, 4096, 2, 1)])
+def test_emulated_group_matches_oracle_and_unsharded(cid, n, P, f32, monkeypatch):
     c = config(cid)
     xy = points_for(c, n)
     ok = OK(c.family, c.rho, c.sigma2, c.nugget, c.alpha, c.theta)
@@ -37,7 +37,8 @@ def test_emulated_group_matches_oracle_and_unsharded(cid, n, P, monkeypatch):
     ctx = R.Context(0)
     assert ctx.group() == (0, 1)
     K = R.Kernel(c.family, c.rho, c.sigma2, c.nugget, c.alpha, c.theta)
-    o = R.Opts(eps_peel=c.eps_peel, seed=c.seed, probe_block=64)
+    # (f32: the memory-saving mode of DESIGN.md §7g through the same emulated group)
+    o = R.Opts(eps_peel=c.eps_peel, seed=c.seed, probe_block=64, peel_f32=f32)
     r1 = R.gp_mle_eval(ctx, _d(xy), _d(z), K, c.eps_fact, c.leaf, o)
     monkeypatch.setenv("RSF_EMU_WORLD", str(P))
     rP = R.gp_mle_eval(ctx, _d(xy), _d(z), K, c.eps_fact, c.leaf, o)
