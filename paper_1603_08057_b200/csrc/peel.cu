@@ -504,7 +504,7 @@ double ddot(cudaStream_t s, const double* a, const double* b, long long n) {
 }
 
 double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag* diag, const Comm* comm) {
-  BigSyncScope big_sync(o.peel_f32 != 0);
+  NoArenaScope no_arena(o.peel_f32 != 0);   // memory-saving mode: no arenas, a trimmed pool
   const double t0 = now_s();
   cudaStream_t s = op_stream(F);
   Comm cm = comm ? *comm : F.ctx->comm;
@@ -1382,7 +1382,11 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
       for (int b = 0; b < nb; ++b) { PL.vfo[b] = tot; tot += (PL.V[b].n + 3) & ~(size_t)3; }   // 16-byte aligned
       PL.browf_off = tot;
       tot += PL.Brow.n;
-      PL.store.alloc(std::max<size_t>(tot, 1), s);
+      {   // the level's long-lived storage outside the stream-ordered pool (cudaMalloc): interleaved with
+          // the transients it fragmented the pool; transients stay stream-ordered
+        BigSyncScope big_sync(true);
+        PL.store.alloc(std::max<size_t>(tot, 1), s);
+      }
       for (int b = 0; b < nb; ++b) {
         if (!PL.V[b].p) continue;
         d2f_kernel<<<gxx((long long)PL.V[b].n), NT, 0, s>>>(PL.V[b].p, PL.store.p + PL.vfo[b], (long long)PL.V[b].n);
@@ -1619,7 +1623,7 @@ void fill_peel_diag(const PeelDiag& d, rsf_peel_diag* out) {
 // ----------------------------------------------------------------- Alg. 1
 EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KParams& kp, int p,
                     const int* theta, double eps, int leaf, const Opts& o, bool profile) {
-  BigSyncScope big_sync(o.peel_f32 != 0);   // memory-saving mode: large blocks via cudaMalloc/cudaFree
+  NoArenaScope no_arena(o.peel_f32 != 0);   // memory-saving mode: no arenas, a trimmed pool
   EvalResult R;
   const long long l0 = g_launches;
   const double T0 = now_s();
