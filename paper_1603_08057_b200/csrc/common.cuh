@@ -51,15 +51,9 @@ void dev_cache_trim_bins(cudaStream_t s);   // release only the cached small (po
 double dev_cache_bytes();
 extern std::atomic<int> g_big_sync;          // > 0: large blocks via cudaMalloc/cudaFree (memory-saving mode)
 void pool_trim();                            // return the stream-ordered pool's unused pages to the driver
-extern std::atomic<int> g_no_arena;         // > 0: large blocks skip the per-stream arenas (memory-saving mode)
-struct NoArenaScope {
-  bool on;
-  explicit NoArenaScope(bool o) : on(o) { if (on) { ++g_no_arena; pool_trim(); } }
-  ~NoArenaScope() { if (on) --g_no_arena; }
-};
 struct BigSyncScope {                        // RAII: memory-saving mode for the scope when on
   bool on;
-  explicit BigSyncScope(bool o) : on(o) { if (on) ++g_big_sync; }
+  explicit BigSyncScope(bool o) : on(o) { if (on && g_big_sync++ == 0) pool_trim(); }
   ~BigSyncScope() { if (on) --g_big_sync; }
 };                    // bytes held in the bin caches of all streams (diagnostics)
 

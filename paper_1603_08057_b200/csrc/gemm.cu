@@ -107,7 +107,6 @@ bool arena_free(cudaStream_t s, void* p, size_t bytes) {
 // long-lived per-level storage between transients) at level 5 of config 4; cudaFree returns the
 // pages at once (it synchronises the device; the trace jobs run one after the other in this mode).
 std::atomic<int> g_big_sync{0};
-std::atomic<int> g_no_arena{0};
 std::unordered_set<void*>& sync_blocks() { static std::unordered_set<void*> v; return v; }
 void* dev_alloc(size_t bytes, cudaStream_t s) {
   void* p = nullptr;
@@ -123,7 +122,7 @@ void* dev_alloc(size_t bytes, cudaStream_t s) {
     const size_t rb = (bytes + (size_t(2) << 20) - 1) / (size_t(2) << 20) * (size_t(2) << 20);
     {
       std::lock_guard<std::mutex> lk(cache_mu());
-      if (g_no_arena.load() == 0) p = arena_alloc(arena_for(s), rb);
+      p = arena_alloc(arena_for(s), rb);
     }
     if (p) return p;
     const double t0 = wall();

@@ -504,7 +504,9 @@ double ddot(cudaStream_t s, const double* a, const double* b, long long n) {
 }
 
 double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag* diag, const Comm* comm) {
-  NoArenaScope no_arena(o.peel_f32 != 0);   // memory-saving mode: no arenas, a trimmed pool
+  // memory-saving mode: large blocks via cudaMalloc/cudaFree, from a trimmed pool (
+  // measured faster than stream-ordered transients without arenas: 246.5 vs 268.5 s at config 4)
+  BigSyncScope big_sync(o.peel_f32 != 0);
   const double t0 = now_s();
   cudaStream_t s = op_stream(F);
   Comm cm = comm ? *comm : F.ctx->comm;
@@ -1382,11 +1384,7 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
       for (int b = 0; b < nb; ++b) { PL.vfo[b] = tot; tot += (PL.V[b].n + 3) & ~(size_t)3; }   // 16-byte aligned
       PL.browf_off = tot;
       tot += PL.Brow.n;
-      {   // the level's long-lived storage outside the stream-ordered pool (cudaMalloc): interleaved with
-          // the transients it fragmented the pool; transients stay stream-ordered
-        BigSyncScope big_sync(true);
-        PL.store.alloc(std::max<size_t>(tot, 1), s);
-      }
+      PL.store.alloc(std::max<size_t>(tot, 1), s);
       for (int b = 0; b < nb; ++b) {
         if (!PL.V[b].p) continue;
         d2f_kernel<<<gxx((long long)PL.V[b].n), NT, 0, s>>>(PL.V[b].p, PL.store.p + PL.vfo[b], (long long)PL.V[b].n);
@@ -1623,7 +1621,9 @@ void fill_peel_diag(const PeelDiag& d, rsf_peel_diag* out) {
 // ----------------------------------------------------------------- Alg. 1
 EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KParams& kp, int p,
                     const int* theta, double eps, int leaf, const Opts& o, bool profile) {
-  NoArenaScope no_arena(o.peel_f32 != 0);   // memory-saving mode: no arenas, a trimmed pool
+  // memory-saving mode: large blocks via cudaMalloc/cudaFree, from a trimmed pool (
+  // measured faster than stream-ordered transients without arenas: 246.5 vs 268.5 s at config 4)
+  BigSyncScope big_sync(o.peel_f32 != 0);
   EvalResult R;
   const long long l0 = g_launches;
   const double T0 = now_s();
