@@ -1786,10 +1786,11 @@ EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KP
   // memory plan: a shape that ran out of memory with its jobs side by side runs them serially
   bool planned_serial = false;
   for (auto& sh : ctx.serial_shapes) planned_serial = planned_serial || (sh.first == n && sh.second == njobs);
-  // (the profiler and the launch trace synchronise one stream at a time: serial then)
+  // (the profiler and the launch trace synchronise one stream at a time, and the per-site GEMM
+  // log would time launches that share the GPU with another job's: serial then)
   // (opts.peel_f32 is the memory-saving mode: the trace jobs also run one after the other, so one
   // peeled representation is resident at a time -- DESIGN.md §7g)
-  if (!par_on || jobs.size() < 2 || Prof::enabled() || KTrace::on() || planned_serial || o.peel_f32) {
+  if (!par_on || jobs.size() < 2 || Prof::enabled() || KTrace::on() || GemmLog::on() || planned_serial || o.peel_f32) {
     main_part();
     f_promise.set_value();
     tj0 = now_s();
