@@ -398,6 +398,13 @@ __global__ void __launch_bounds__(NT) potrf_diag_kernel(const DiagDesc* __restri
 }
 
 struct ZDesc { double* A; long long lda; int n; };
+struct RDesc { double* A; long long lda; int m, n; };
+__global__ void zero_rect_kernel(const RDesc* __restrict__ descs) {
+  const RDesc d = descs[blockIdx.y];
+  const long long tot = (long long)d.m * d.n;
+  for (long long e = blockIdx.x * (long long)NT + threadIdx.x; e < tot; e += (long long)gridDim.x * NT)
+    d.A[(e / d.m) * d.lda + (e % d.m)] = 0.0;
+}
 __global__ void zero_upper_kernel(const ZDesc* __restrict__ descs) {
   const ZDesc d = descs[blockIdx.y];
   const long long tot = (long long)d.n * d.n;
@@ -1136,6 +1143,47 @@ void potrf_batched(cudaStream_t s, const std::vector<PotrfProb>& probs, double* 
   bool want_inv = false;
   for (auto& p : probs) want_inv |= (p.Linv != nullptr);
   if (!want_inv) return;
+  static const bool rec_inv = !(getenv("RSF_TRINV_REC") && getenv("RSF_TRINV_REC")[0] == '0');
+  if (rec_inv) {
+    // Linv holds the inverses of the CH_NB x CH_NB diagonal blocks (potrf_diag_kernel).  Merge
+    // neighbouring inverted diagonal blocks of size sb into blocks of size 2 sb, all problems and
+    // all pairs of a size in one batch (2 GEMMs + 1 zeroing launch per doubling instead of 2 GEMMs
+    // per 64-row block row):
+    //   [L11 0; L21 L22]^-1 = [X11 0; -X22 L21 X11  X22]
+    // T^T = (L21 X11)^T = X11^T L21^T is parked in the (zero) strict upper triangle at rows of
+    // block 1, columns of block 2, then X21 = -X22 (T^T)^T, then the parked block is zeroed
+    // again (the next doubling reads X11 / X22 as full blocks with zero upper triangles).
+    for (int sb = CH_NB; sb < maxn; sb *= 2) {
+      GemmBatch g1(true, true), g2(false, true);
+      std::vector<RDesc> zr;
+      long long mz = 0;
+      for (int i = 0; i < P; ++i) {
+        const PotrfProb& p = probs[i];
+        if (!p.Linv) continue;
+        for (int a = 0; a + sb < p.n; a += 2 * sb) {
+          const int b = a + sb, s2 = std::min(sb, p.n - b);
+          double* Tt = p.Linv + (long long)b * p.ldi + a;        // sb x s2 (upper triangle)
+          GemmDesc d1 = gdesc(sb, s2, sb);                        // T^T = X11^T L21^T
+          d1.A = p.Linv + (long long)a * p.ldi + a; d1.lda = (int)p.ldi;
+          d1.B = p.A + (long long)a * p.lda + b; d1.ldb = (int)p.lda;
+          d1.C = Tt; d1.ldc = (int)p.ldi;
+          g1.add(d1);
+          GemmDesc d2 = gdesc(s2, sb, s2);                        // X21 = -X22 T
+          d2.A = p.Linv + (long long)b * p.ldi + b; d2.lda = (int)p.ldi;
+          d2.B = Tt; d2.ldb = (int)p.ldi;
+          d2.C = p.Linv + (long long)a * p.ldi + b; d2.ldc = (int)p.ldi;
+          d2.alpha = -1.0;
+          g2.add(d2);
+          zr.push_back(RDesc{Tt, p.ldi, sb, s2});
+          mz = std::max(mz, (long long)sb * s2);
+        }
+      }
+      g1.run(s);
+      g2.run(s);
+      launch_y(s, zr, mz, zero_rect_kernel);
+    }
+    return;
+  }
   DBuf<double> tmp(wtot, s);
   for (int r0 = CH_NB; r0 < maxn; r0 += CH_NB) {
     GemmBatch g1(false, false), g2(false, false);
