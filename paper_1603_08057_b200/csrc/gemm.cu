@@ -1481,10 +1481,15 @@ void GemmBatch::run(cudaStream_t s, double* X0, double* X1, int ldx, int Mglob, 
     } else {
       // waves x (rows per CTA + a fixed per-CTA cost): resident CTAs per SM from the kernels'
       // register use (op(B) = B^T: 64 registers -> 4; op(B) = B: 95-128 -> 2)
-      const double slots = 148.0 * (tb_ ? 4 : 2), c0 = 128.0;
+      // (RSF_GEMV_C0 / RSF_GEMV_SMAX / RSF_GEMV_MINK: the fixed per-CTA cost in rows, the
+      // largest split and the shortest slice -- knobs for the measured sweep in DESIGN.md §5)
+      static const double c0 = getenv("RSF_GEMV_C0") ? atof(getenv("RSF_GEMV_C0")) : 128.0;
+      static const int smax = getenv("RSF_GEMV_SMAX") ? atoi(getenv("RSF_GEMV_SMAX")) : 32;
+      static const int mink = getenv("RSF_GEMV_MINK") ? atoi(getenv("RSF_GEMV_MINK")) : 128;
+      const double slots = 148.0 * (tb_ ? 4 : 2);
       double best = 1e300;
-      for (int S2 = 1; S2 <= 32; S2 *= 2) {
-        if (S2 > 1 && maxK_ / S2 < 128) break;
+      for (int S2 = 1; S2 <= smax; S2 *= 2) {
+        if (S2 > 1 && maxK_ / S2 < mink) break;
         const double cost = std::ceil((double)tiles * S2 / slots) * ((double)maxK_ / S2 + c0) + (S2 > 1 ? c0 : 0.0);
         if (cost < best) { best = cost; S = S2; }
       }
