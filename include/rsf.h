@@ -173,6 +173,12 @@ int rsf_debug_job_runs(int njobs, int world, int rank, int job);
  * with the largest current work per rank; equal weights give rank r -> group r mod ngroups.
  * -1 on bad arguments.  Host only (tests). */
 int rsf_debug_job_group(int ngroups, const double* gw, int world, int rank);
+/* Number of NCCL collectives (all-gathers of probe-block slices, job results, memory agreements,
+ * trace partial sums) this process has issued so far.  A single-GPU context issues none; with
+ * RSF_NCCL_FORCE=1 in the environment a world = 1 group made by rsf_ctx_create_group keeps its
+ * one-rank NCCL communicator and routes every collective of the sharded path through it (the
+ * transport test on one GPU; results are unchanged).  Host only (tests). */
+int64_t rsf_debug_nccl_calls(void);
 void rsf_ctx_destroy(rsf_ctx ctx);
 /* Order the context after the caller: everything enqueued on `stream` so far (an event recorded
  * there) completes before the context stream runs further work.  stream = NULL is the legacy

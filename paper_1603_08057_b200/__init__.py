@@ -15,7 +15,7 @@ from . import _lib
 from ._lib import FAMILY, PARAM, rsf_eval_diag, rsf_fact_diag, rsf_kernel, rsf_opts, rsf_peel_diag
 
 __all__ = ["Context", "Kernel", "Opts", "Factor", "peel_trace", "gp_mle_eval", "RsfError", "lib",
-           "kernel_launches", "nccl_unique_id", "col_slice"]
+           "kernel_launches", "nccl_unique_id", "nccl_calls", "col_slice"]
 
 lib = _lib.load()
 
@@ -110,6 +110,11 @@ def nccl_unique_id() -> bytes:
     buf = (C.c_ubyte * 128)()
     _check(lib.rsf_nccl_unique_id(buf))
     return bytes(buf)
+
+
+def nccl_calls() -> int:
+    """NCCL collectives this process has issued so far (include/rsf.h; tests)."""
+    return int(lib.rsf_debug_nccl_calls())
 
 
 def col_slice(k: int, parts: int, part: int):

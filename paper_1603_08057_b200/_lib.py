@@ -61,7 +61,7 @@ EXPORTS = ["rsf_opts_default", "rsf_ctx_create", "rsf_ctx_destroy", "rsf_factor"
            "rsf_debug_gemm_bench", "rsf_debug_fp64_peak", "rsf_trace_dump", "rsf_debug_gemm_log",
            "rsf_debug_gemm", "rsf_ctx_wait_stream", "rsf_nccl_unique_id", "rsf_ctx_create_group",
            "rsf_ctx_group", "rsf_debug_col_slice", "rsf_debug_solve_bench",
-           "rsf_debug_job_runs", "gp_cond_sample", "rsf_debug_job_group"]
+           "rsf_debug_job_runs", "gp_cond_sample", "rsf_debug_job_group", "rsf_debug_nccl_calls"]
 
 
 def load(path: str = LIB_PATH) -> C.CDLL:
@@ -106,6 +106,8 @@ def load(path: str = LIB_PATH) -> C.CDLL:
     lib.rsf_last_error.restype = C.c_char_p
     lib.rsf_kernel_launches.argtypes = []
     lib.rsf_kernel_launches.restype = C.c_int64
+    lib.rsf_debug_nccl_calls.argtypes = []
+    lib.rsf_debug_nccl_calls.restype = C.c_int64
     lib.rsf_profile_dump.argtypes = []
     lib.rsf_profile_dump.restype = C.c_char_p
     lib.rsf_trace_dump.argtypes = []
@@ -132,6 +134,6 @@ def load(path: str = LIB_PATH) -> C.CDLL:
                      "rsf_kernel_launches", "rsf_profile_dump", "rsf_profile_reset", "rsf_stats_enable",
                      "rsf_stats_get", "rsf_stats_reset", "rsf_debug_gemm_bench",
                      "rsf_debug_fp64_peak", "rsf_trace_dump", "rsf_debug_gemm_log", "rsf_debug_col_slice",
-                     "rsf_debug_solve_bench"):
+                     "rsf_debug_solve_bench", "rsf_debug_nccl_calls"):
             getattr(lib, f).restype = C.c_int
     return lib

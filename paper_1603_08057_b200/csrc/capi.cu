@@ -258,13 +258,18 @@ rsf_status rsf_ctx_create_group(int device, void* cuda_stream, const unsigned ch
     rsf_ctx c = nullptr;
     const rsf_status st = rsf_ctx_create(device, cuda_stream, nullptr, &c);
     if (st != RSF_OK) throw rsf::Error(st, g_err);
-    if (world > 1) {
+    // (RSF_NCCL_FORCE=1: a one-rank group keeps its NCCL communicator and issues every collective
+    // of the sharded path through it -- the transport test on one GPU, comm.cuh)
+    const char* fe = getenv("RSF_NCCL_FORCE");
+    const bool force = world == 1 && fe && fe[0] == '1';
+    if (world > 1 || force) {
       try {
         RSF_CUDA(cudaSetDevice(device));
         c->ctx.comm.nccl = rsf::nccl_init_rank(id, rank, world);
         c->ctx.comm.owned = true;
         c->ctx.comm.rank = rank;
         c->ctx.comm.world = world;
+        c->ctx.comm.force = force;
       } catch (...) {
         rsf_ctx_destroy(c);
         throw;
@@ -287,6 +292,8 @@ int rsf_debug_job_runs(int njobs, int world, int rank, int job) {
   const int G = rsf::Comm::job_groups(njobs, world);
   return (world == 1 || job % G == rank % G) ? 1 : 0;   // (equal job weights: rank r in group r mod G)
 }
+
+int64_t rsf_debug_nccl_calls(void) { return (int64_t)rsf::nccl_calls(); }
 
 int rsf_debug_job_group(int ngroups, const double* gw, int world, int rank) {
   if (ngroups < 1 || !gw || world < ngroups || rank < 0 || rank >= world) return -1;

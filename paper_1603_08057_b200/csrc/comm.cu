@@ -3,6 +3,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <string>
 
@@ -49,6 +50,8 @@ const NcclApi& api() {
   return a;
 }
 
+std::atomic<long long> g_calls{0};
+
 void check(ncclResult_t r, const char* what) {
   if (r != ncclSuccess) throw Error(ST_ENCCL, std::string(what) + ": " + api().err(r));
 }
@@ -73,9 +76,10 @@ __global__ void merge_kernel(const double* __restrict__ gath, long long slot, lo
 }  // namespace
 
 void Comm::exchange(cudaStream_t s, double* gath, long long slot) const {
-  if (world <= 1) return;
+  if (!use_nccl()) return;
   check(api().all_gather(gath + (long long)rank * slot, gath, (size_t)slot, ncclDouble, (ncclComm_t)nccl, s),
         "ncclAllGather");
+  ++g_calls;
 }
 
 void Comm::merge(cudaStream_t s, const double* gath, long long slot, long long k, int n, double* Y) const {
@@ -87,12 +91,13 @@ void Comm::merge(cudaStream_t s, const double* gath, long long slot, long long k
 }
 
 void Comm::allsum(cudaStream_t s, double* v, int cnt) const {
-  if (world <= 1) return;
+  if (!use_nccl()) return;
   // gather every rank's values, then add them in rank order on the host (deterministic)
   DBuf<double> g((size_t)cnt * world, s);
   RSF_CUDA(cudaMemcpyAsync(g.p + (size_t)rank * cnt, v, cnt * sizeof(double), cudaMemcpyHostToDevice, s));
   check(api().all_gather(g.p + (size_t)rank * cnt, g.p, (size_t)cnt, ncclDouble, (ncclComm_t)nccl, s),
         "ncclAllGather");
+  ++g_calls;
   const std::vector<double> h = g.to_host((size_t)cnt * world);
   for (int i = 0; i < cnt; ++i) {
     double a = 0.0;
@@ -102,7 +107,7 @@ void Comm::allsum(cudaStream_t s, double* v, int cnt) const {
 }
 
 void Comm::allgather_host(cudaStream_t s, const double* in, int cnt, double* out) const {
-  if (world <= 1) {
+  if (!use_nccl()) {
     std::copy(in, in + cnt, out);
     return;
   }
@@ -110,6 +115,7 @@ void Comm::allgather_host(cudaStream_t s, const double* in, int cnt, double* out
   RSF_CUDA(cudaMemcpyAsync(g.p + (size_t)rank * cnt, in, cnt * sizeof(double), cudaMemcpyHostToDevice, s));
   check(api().all_gather(g.p + (size_t)rank * cnt, g.p, (size_t)cnt, ncclDouble, (ncclComm_t)nccl, s),
         "ncclAllGather");
+  ++g_calls;
   const std::vector<double> h = g.to_host((size_t)cnt * world);
   std::copy(h.begin(), h.end(), out);
 }
@@ -145,6 +151,8 @@ void* nccl_split_color(void* comm, int color, int key) {
   check(api().split((ncclComm_t)comm, color < 0 ? NCCL_SPLIT_NOCOLOR : color, key, &c, nullptr), "ncclCommSplit");
   return color < 0 ? nullptr : c;
 }
+
+long long nccl_calls() { return g_calls.load(); }
 
 void nccl_destroy(void* comm) {
   if (comm) api().destroy((ncclComm_t)comm);

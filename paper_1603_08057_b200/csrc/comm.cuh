@@ -27,6 +27,11 @@ struct Comm {
   void* nccl = nullptr;   // ncclComm_t
   int emu = 1;            // emulated ranks (world == 1 only)
   bool owned = false;     // nccl was created by the library (destroyed with the context)
+  // a one-rank group that still issues its collectives through NCCL (RSF_NCCL_FORCE=1 at
+  // rsf_ctx_create_group: the single-GPU test of the transport -- dlopen'd entry points,
+  // communicator splits per trace job, in-place all-gathers, host staging)
+  bool force = false;
+  bool use_nccl() const { return world > 1 || (force && nccl != nullptr); }
 
   int parts() const { return world > 1 ? world : emu; }
   bool emulated() const { return world == 1 && emu > 1; }
@@ -85,5 +90,7 @@ void* nccl_split(void* comm, int rank);
 // split with a color (< 0: this rank joins no new communicator and gets nullptr)
 void* nccl_split_color(void* comm, int color, int key);
 void nccl_destroy(void* comm);
+// NCCL collectives issued by this process so far (tests)
+long long nccl_calls();
 
 }  // namespace rsf

@@ -856,7 +856,7 @@ double peel(const Fact& F, const Fact* Fi, const Opts& o, int trace_id, PeelDiag
           for (int b : act_all) need += 8.0 * c * ((double)c + std::min<double>(bx[b].ni, rb[b] + c));
           size_t fr = 0, tot = 0;
           cudaMemGetInfo(&fr, &tot);
-          if (cm.world > 1) {   // the same subsets on every rank of the group (their collectives pair up)
+          if (cm.use_nccl()) {   // the same subsets on every rank of the group (their collectives pair up)
             std::vector<double> all((size_t)cm.world);
             double mine = (double)fr;
             cm.allgather_host(s, &mine, 1, all.data());
@@ -1669,7 +1669,7 @@ EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KP
   // (job j to group j mod G, rank r in group r mod G); a job's communicator holds its group's
   // ranks, which split its probe columns.  Communicators are split from the group's communicator
   // on the calling thread, in job order (the same on every rank).
-  auto job_comm = [&](int j) -> const Comm* { return ctx.comm.world > 1 ? &ctx.job_comms[j] : &ctx.comm; };
+  auto job_comm = [&](int j) -> const Comm* { return ctx.comm.use_nccl() ? &ctx.job_comms[j] : &ctx.comm; };
   std::vector<std::function<void()>> jobs;
   std::vector<int> job_theta;   // theta index of a general job, -1 for the Tr(F^-1) job
   bool need_trinv = false;
@@ -1717,7 +1717,7 @@ EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KP
   for (int j = 0; j < njobs; ++j) gw[j % NG] += job_theta[j] >= 0 ? 3.0 : 1.0;
   const int my_group = Comm::group_of_rank(gw, ctx.comm.world, ctx.comm.rank);
   auto mine = [&](int j) { return ctx.comm.world == 1 || j % NG == my_group; };
-  if (ctx.comm.world > 1 && ctx.job_comms_njobs != njobs) {
+  if (ctx.comm.use_nccl() && ctx.job_comms_njobs != njobs) {
     for (auto& jc : ctx.job_comms)
       if (jc.owned) nccl_destroy(jc.nccl);
     ctx.job_comms.assign(njobs, Comm{});
@@ -1727,6 +1727,7 @@ EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KP
       Comm jc;
       jc.nccl = c;
       jc.owned = true;
+      jc.force = ctx.comm.force;
       nccl_query(c, &jc.rank, &jc.world);
       ctx.job_comms[j] = jc;
     }
@@ -1877,7 +1878,7 @@ EvalResult mle_eval(Ctx& ctx, const double* xy, const double* z, int n, const KP
   R.t_jobs_wall = now_s() - tj0;
   // (RSF_EMU_EXCHANGE=1 routes a single-GPU evaluation through the same record exchange: tests)
   const bool emu_exchange = getenv("RSF_EMU_EXCHANGE") && getenv("RSF_EMU_EXCHANGE")[0] == '1';
-  if ((ctx.comm.world > 1 || emu_exchange) && njobs > 0) {
+  if ((ctx.comm.use_nccl() || emu_exchange) && njobs > 0) {
     // every job's results from the lowest rank of the group that ran it (all members hold the
     // same values): one all-gather of fixed-size records over the whole group
     constexpr int RS = 13 + 4 * 32;

@@ -73,3 +73,40 @@ def test_job_result_exchange_round_trip(monkeypatch):
         assert list(a.rank_min) == list(b.rank_min) and list(a.rank_med) == list(b.rank_med)
         assert a.stored_bytes == b.stored_bytes and a.nL == b.nL and a.applies == b.applies
         assert r1.diag.q[i] == r2.diag.q[i] and r1.diag.trace[i] == r2.diag.trace[i]
+
+
+@pytest.mark.parametrize("cid,n,P", [(1, 1024, 2), (2, 4096, 3)])
+def test_nccl_transport_one_rank_group(cid, n, P, monkeypatch):
+    """The NCCL transport on ONE GPU: RSF_NCCL_FORCE=1 makes a world = 1 group keep its one-rank
+    communicator (ncclCommInitRank through the dlopen'd entry points, one ncclCommSplit per trace
+    job) and issue every collective of the sharded path through it -- the in-place all-gather of
+    each probe chunk's slot buffer, the trace partial sums, the job-result records -- while the
+    column slices of the P emulated parts fill the slots.  One rank waits on no other, so nothing
+    here can hang; the results must equal the emulated group's without NCCL bit for bit."""
+    c = config(cid)
+    xy = points_for(c, n)
+    ok = OK(c.family, c.rho, c.sigma2, c.nugget, c.alpha, c.theta)
+    z = dense_sample(ok, xy, w_for(c, n))
+    K = R.Kernel(c.family, c.rho, c.sigma2, c.nugget, c.alpha, c.theta)
+    o = R.Opts(eps_peel=c.eps_peel, seed=c.seed, probe_block=64)
+    monkeypatch.setenv("RSF_EMU_WORLD", str(P))
+    ctx0 = R.Context(0)
+    n0 = R.nccl_calls()
+    r0 = R.gp_mle_eval(ctx0, _d(xy), _d(z), K, c.eps_fact, c.leaf, o)
+    assert R.nccl_calls() == n0                    # a single-GPU context issues no collective
+    monkeypatch.setenv("RSF_NCCL_FORCE", "1")
+    ctx1 = R.Context(0, group=(R.nccl_unique_id(), 0, 1))
+    assert ctx1.group() == (0, 1)
+    r1 = R.gp_mle_eval(ctx1, _d(xy), _d(z), K, c.eps_fact, c.leaf, o)
+    calls = R.nccl_calls() - n0
+    # at least one all-gather per peeled level and trace job, plus the result exchange
+    assert calls >= len(c.theta) * 2 + 1, calls
+    assert r1.ell == r0.ell and list(r1.grad) == list(r0.grad)
+    for i in range(len(c.theta)):
+        assert r1.diag.trace[i] == r0.diag.trace[i] and r1.diag.q[i] == r0.diag.q[i]
+        assert list(r1.diag.peel[i].cols) == list(r0.diag.peel[i].cols)
+    # a second evaluation reuses the per-job communicators
+    r2 = R.gp_mle_eval(ctx1, _d(xy), _d(z), K, c.eps_fact, c.leaf, o)
+    assert list(r2.grad) == list(r0.grad)
+    ctx1.close()
+    ctx0.close()
