@@ -75,8 +75,8 @@ def test_job_result_exchange_round_trip(monkeypatch):
         assert r1.diag.q[i] == r2.diag.q[i] and r1.diag.trace[i] == r2.diag.trace[i]
 
 
-@pytest.mark.parametrize("cid,n,P", [(1, 1024, 2), (2, 4096, 3)])
-def test_nccl_transport_one_rank_group(cid, n, P, monkeypatch):
+@pytest.mark.parametrize("cid,n,P,f32", [(1, 1024, 2, 0), (2, 4096, 3, 0), (2, 4096, 2, 1)])
+def test_nccl_transport_one_rank_group(cid, n, P, f32, monkeypatch):
     """The NCCL transport on ONE GPU: RSF_NCCL_FORCE=1 makes a world = 1 group keep its one-rank
     communicator (ncclCommInitRank through the dlopen'd entry points, one ncclCommSplit per trace
     job) and issue every collective of the sharded path through it -- the in-place all-gather of
@@ -88,7 +88,9 @@ def test_nccl_transport_one_rank_group(cid, n, P, monkeypatch):
     ok = OK(c.family, c.rho, c.sigma2, c.nugget, c.alpha, c.theta)
     z = dense_sample(ok, xy, w_for(c, n))
     K = R.Kernel(c.family, c.rho, c.sigma2, c.nugget, c.alpha, c.theta)
-    o = R.Opts(eps_peel=c.eps_peel, seed=c.seed, probe_block=64)
+    # (f32: the memory-saving mode also agrees on the free memory across the group, one more
+    # host-staged all-gather per probe group)
+    o = R.Opts(eps_peel=c.eps_peel, seed=c.seed, probe_block=64, peel_f32=f32)
     monkeypatch.setenv("RSF_EMU_WORLD", str(P))
     ctx0 = R.Context(0)
     n0 = R.nccl_calls()
