@@ -8,8 +8,10 @@ A "step" is one full evaluation of Alg. 1 -- quadtree, RSF of
 Sigma, compression of each Sigma_i, solve, and the peeled traces -- at the
 largest BASELINE.json workload that fits one B200 (config 3: n = 262,144
 jittered-grid points, rational quadratic, theta = (rho, alpha), z frozen from
-the O2 oracle); the metric's own config 4 (n = 2^20) exceeds one GPU's memory
-with replicated peeling bases.  Inputs are resident in HBM.
+the O2 oracle); the metric's own config 4 (n = 2^20) fits one GPU only in the
+memory-saving mode at ~230 s per evaluation (`--config 4`, DESIGN.md §7g;
+profiles/r02_bench_config4_v2.json), too long for a default W >= 3 run.  Inputs
+are resident in HBM.
 Multi-GPU (torchrun): the ranks form one NCCL group and share every evaluation
 (factor replicated, peeling probe columns split, one all-gather per probe
 block) -- strong scaling, time = max over ranks, value =
@@ -459,10 +461,10 @@ def main():
     line = {
         "metric": METRIC,
         "metric_note": ("BASELINE.json quotes this metric at n = 2^20 (config 4). Config 4 runs on one B200 "
-                        "only in the memory-saving mode (FP32-stored peeled levels, DESIGN.md §7g) at ~270 s "
-                        "per evaluation, so a W >= 3 run takes ~30 min; the default line measures config 3 "
+                        "only in the memory-saving mode (FP32-stored peeled levels, DESIGN.md §7g) at ~230 s "
+                        "per evaluation, so a W >= 3 run takes ~25 min; the default line measures config 3 "
                         "(FP64 storage throughout, named in config.workload) and `bench.py --config 4` gives "
-                        "the config-4 line (profiles/r02_bench_config4.json)"
+                        "the config-4 line (profiles/r02_bench_config4_v2.json: 0.00438 evals/s)"
                         if (args.n or c.n) != 1048576 else
                         "config 4 (n = 2^20), the metric's own workload, memory-saving mode (DESIGN.md §7g)"),
         "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
